@@ -1,0 +1,79 @@
+"""ctypes front-end of oracle/native/liboracle.so (TEST INFRASTRUCTURE ONLY).
+
+Plain-C CPU restatements of the periodic neighbour list, tabulated EAM and
+fp64 SNAP (see the .c headers).  Built by ``make -C oracle/native``
+(``__graft_entry__.build()`` does it); used only by tests/, smoke() and the
+bench's CPU-baseline / reference arms.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "native")
+LIB = os.path.join(HERE, "liboracle.so")
+_lib = None
+pd = C.POINTER(C.c_double)
+pi = C.POINTER(C.c_int32)
+
+
+def build(force=False):
+    srcs = [os.path.join(HERE, f) for f in os.listdir(HERE) if f.endswith(".c")]
+    stale = not os.path.exists(LIB) or any(os.path.getmtime(s) > os.path.getmtime(LIB) for s in srcs)
+    if force or stale:
+        subprocess.run(["make", "-s", "-B", "-C", HERE], check=True)
+    return LIB
+
+
+def load():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(LIB)
+        _lib.orc_neighbours.restype = C.c_int
+        _lib.orc_neighbours.argtypes = [C.c_int, pd, C.c_double, pd, C.c_int, pi, pi]
+        _lib.orc_eam.restype = C.c_int
+        _lib.orc_eam.argtypes = [C.c_int, pd, C.c_double, C.c_int, C.c_double, pd, pd, C.c_int,
+                                 C.c_double, pd, pd, pd, pd, pd]
+        if hasattr(_lib, "orc_snap"):
+            _lib.orc_snap.restype = C.c_int
+            _lib.orc_snap.argtypes = [C.c_int, pd, C.c_int, C.c_double, C.c_double, C.c_double,
+                                      C.c_int, C.c_double, pd, C.c_int, pd, pd, pd, pd, pd]
+    return _lib
+
+
+def _d(a):
+    return np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(pd)
+
+
+def neighbours(q, box, rcut, maxn=256):
+    lib = load()
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    n = q.shape[0] // 3
+    nbr = np.zeros((n, maxn), dtype=np.int32)
+    cnt = np.zeros(n, dtype=np.int32)
+    box = np.ascontiguousarray(box, dtype=np.float64)
+    lib.orc_neighbours(n, _d(box), float(rcut), _d(q), maxn, nbr.ctypes.data_as(pi),
+                       cnt.ctypes.data_as(pi))
+    return [sorted(nbr[i, :cnt[i]].tolist()) for i in range(n)]
+
+
+def eam(q, box, tables):
+    """(energy, gradient, virial) of one system with EAM tables (tungsten.eam_tables)."""
+    lib = load()
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    n = q.shape[0] // 3
+    e = np.zeros(1)
+    g = np.zeros(3 * n)
+    v = np.zeros(6)
+    rho, phi, F = (np.ascontiguousarray(tables[k]) for k in ("rho", "phi", "F"))
+    box = np.ascontiguousarray(box, dtype=np.float64)
+    rc = lib.orc_eam(n, _d(box), float(tables["rcut"]), rho.shape[0], float(tables["dr"]), _d(rho),
+                     _d(phi), F.shape[0], float(tables["drho"]), _d(F), _d(q), _d(e), _d(g), _d(v))
+    if rc != 0:
+        raise RuntimeError("oracle EAM failed (neighbour overflow)")
+    return e[0], g, v

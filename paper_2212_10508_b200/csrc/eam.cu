@@ -1,0 +1,216 @@
+// Tabulated EAM / Finnis-Sinclair potential, batched over systems
+// (the coarse potential of the parareal pair).
+//
+//   E   = sum_i F(rho_i) + 1/2 sum_i sum_j phi(r_ij),   rho_i = sum_j rho(r_ij)
+//   dE/dr_i = -sum_j [ (F'(rho_i) + F'(rho_j)) rho'(r_ij) + phi'(r_ij) ] (r_j - r_i)/r_ij
+//
+// Two gather passes over a full neighbour list (density, then forces): no
+// atomics, every sum in neighbour-list order, so results are deterministic
+// and independent of launch shape.  The tables are cubic Hermite pieces; a
+// piece lookup costs one divide, one conversion and a Horner chain.
+#include <cmath>
+
+#include "neigh.cuh"
+#include "pl_common.cuh"
+
+namespace pl {
+
+constexpr int EAM_MAXN = 96;
+
+struct Table {
+  const double* c;  // [n][4]
+  int n;
+  double dx;
+};
+
+__device__ __forceinline__ void tab_eval(const Table& T, double x, double& f, double& df) {
+  double p = x / T.dx;
+  int k = (int)p;
+  k = k < 0 ? 0 : (k > T.n - 1 ? T.n - 1 : k);
+  double t = p - (double)k;
+  const double4 c = *reinterpret_cast<const double4*>(T.c + 4 * (int64_t)k);
+  f = c.x + t * (c.y + t * (c.z + t * c.w));
+  df = (c.y + t * (2.0 * c.z + t * (3.0 * c.w))) / T.dx;
+}
+
+__global__ void k_eam_density(int64_t B, int N, Box box, Table rho, Table F,
+                              const double* __restrict__ q, const int32_t* __restrict__ nbr,
+                              const int32_t* __restrict__ cnt, int maxn, double* __restrict__ Fp,
+                              double* __restrict__ Fe) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= B * N) return;
+  int64_t b = t / N;
+  int i = (int)(t - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const int32_t* nb = nbr + t * maxn;
+  int n = cnt[t];
+  double s = 0.0;
+  for (int k = 0; k < n; ++k) {
+    double dx, dy, dz;
+    pair_vec(qb, i, nb[k], box, dx, dy, dz);
+    double r = sqrt(dx * dx + dy * dy + dz * dz);
+    double f, df;
+    tab_eval(rho, r, f, df);
+    s += f;
+  }
+  double f, df;
+  tab_eval(F, s, f, df);
+  Fp[t] = df;
+  Fe[t] = f;
+}
+
+__global__ void k_eam_force(int64_t B, int N, Box box, Table rho, Table phi,
+                            const double* __restrict__ q, const int32_t* __restrict__ nbr,
+                            const int32_t* __restrict__ cnt, int maxn, const double* __restrict__ Fp,
+                            const double* __restrict__ Fe, double* __restrict__ grad,
+                            double* __restrict__ eatom, double* __restrict__ vatom) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= B * N) return;
+  int64_t b = t / N;
+  int i = (int)(t - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const double* Fpb = Fp + b * (int64_t)N;
+  const int32_t* nb = nbr + t * maxn;
+  int n = cnt[t];
+  double fpi = Fp[t];
+  double gx = 0, gy = 0, gz = 0, e = 0;
+  double vxx = 0, vyy = 0, vzz = 0, vxy = 0, vxz = 0, vyz = 0;
+  for (int k = 0; k < n; ++k) {
+    int j = nb[k];
+    double dx, dy, dz;
+    pair_vec(qb, i, j, box, dx, dy, dz);
+    double r = sqrt(dx * dx + dy * dy + dz * dz);
+    double rf, drf, pf, dpf;
+    tab_eval(rho, r, rf, drf);
+    tab_eval(phi, r, pf, dpf);
+    double coef = (fpi + Fpb[j]) * drf + dpf;
+    double s = coef / r;
+    gx -= s * dx;
+    gy -= s * dy;
+    gz -= s * dz;
+    e += 0.5 * pf;
+    double hs = 0.5 * s;  // pair virial shared by i and j
+    vxx -= hs * dx * dx;
+    vyy -= hs * dy * dy;
+    vzz -= hs * dz * dz;
+    vxy -= hs * dx * dy;
+    vxz -= hs * dx * dz;
+    vyz -= hs * dy * dz;
+  }
+  if (grad) {
+    grad[3 * t] = gx;
+    grad[3 * t + 1] = gy;
+    grad[3 * t + 2] = gz;
+  }
+  if (eatom) eatom[t] = Fe[t] + e;
+  if (vatom) {
+    double* v = vatom + 6 * t;
+    v[0] = vxx; v[1] = vyy; v[2] = vzz; v[3] = vxy; v[4] = vxz; v[5] = vyz;
+  }
+}
+
+// per-system fixed-order reductions of per-atom energy (and virial)
+__global__ void k_sys_reduce(int64_t B, int N, int width, const double* __restrict__ per_atom,
+                             double* __restrict__ out) {
+  __shared__ double sh[256];
+  int64_t b = blockIdx.x;
+  for (int c = 0; c < width; ++c) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s += per_atom[(b * N + i) * width + c];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[b * width + c] = sh[0];
+    __syncthreads();
+  }
+}
+
+int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out) {
+  int N = pot->n_atoms;
+  size_t lists = sizeof(int32_t) * (size_t)B * N * maxn;
+  size_t counts = sizeof(int32_t) * (size_t)B * N;
+  PL_TRY(pot->work[0].reserve(lists));
+  PL_TRY(pot->work[1].reserve(counts + 64));
+  out->nbr = (int32_t*)pot->work[0].ptr;
+  out->cnt = (int32_t*)pot->work[1].ptr;
+  out->overflow = (int*)((char*)pot->work[1].ptr + ((counts + 15) & ~(size_t)15));
+  out->maxn = maxn;
+  pot->nb_overflow = out->overflow;
+  if (B > 65535) return fail(PL_EARG, "at most 65535 systems per call");
+  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  double rc2 = rcut * rcut;
+  PL_CUDA(cudaMemsetAsync(out->overflow, 0, sizeof(int), pot->ctx->stream));
+  dim3 grid((N + NB_THREADS - 1) / NB_THREADS, (unsigned)B);
+  k_neigh_brute<<<grid, NB_THREADS, 0, pot->ctx->stream>>>(B, N, box, rc2, maxn, q, out->nbr, out->cnt,
+                                                           out->overflow);
+  PL_CHECK_LAUNCH();
+  return PL_OK;
+}
+
+int neigh_check(pl_pot* pot) {
+  switch (pot->kind) {
+    case POT_PERTURBED:
+      PL_TRY(neigh_check(pot->base));
+      return pot->lam != 0.0 ? neigh_check(pot->delta) : PL_OK;
+    case POT_EAM:
+    case POT_SNAP:
+      break;
+    default:
+      return PL_OK;
+  }
+  if (!pot->nb_overflow) return PL_OK;
+  int h = 0;
+  PL_CUDA(cudaMemcpyAsync(&h, pot->nb_overflow, sizeof(int), cudaMemcpyDeviceToHost, pot->ctx->stream));
+  PL_CUDA(cudaStreamSynchronize(pot->ctx->stream));
+  if (h) return fail(PL_EPOT, "neighbour capacity exceeded (atoms too close / dense)");
+  return PL_OK;
+}
+
+int eam_prepare(pl_pot* pot, const double* rho, const double* phi, const double* F) {
+  size_t nr = sizeof(double) * 4 * pot->n_r, nf = sizeof(double) * 4 * pot->n_rho;
+  PL_CUDA(cudaMalloc(&pot->d_rho, nr));
+  PL_CUDA(cudaMalloc(&pot->d_phi, nr));
+  PL_CUDA(cudaMalloc(&pot->d_F, nf));
+  PL_CUDA(cudaMemcpy(pot->d_rho, rho, nr, cudaMemcpyHostToDevice));
+  PL_CUDA(cudaMemcpy(pot->d_phi, phi, nr, cudaMemcpyHostToDevice));
+  PL_CUDA(cudaMemcpy(pot->d_F, F, nf, cudaMemcpyHostToDevice));
+  // algorithmic flops per system: ~ (2 table evals + 25) per pair x 2 passes
+  pot->flops = 0.0;
+  return PL_OK;
+}
+
+int compute_eam(pl_pot* pot, int64_t B, const double* q, double* energy, double* grad, double* virial) {
+  pl_ctx* ctx = pot->ctx;
+  int N = pot->n_atoms;
+  NeighList nl;
+  PL_TRY(build_neighbours(pot, B, q, pot->rcut, EAM_MAXN, &nl));
+  size_t na = (size_t)B * N;
+  PL_TRY(pot->work[2].reserve(sizeof(double) * na * (2 + 1 + 6)));
+  double* Fp = (double*)pot->work[2].ptr;
+  double* Fe = Fp + na;
+  double* ea = Fe + na;
+  double* va = ea + na;
+  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  Table trho{pot->d_rho, pot->n_r, pot->dr}, tphi{pot->d_phi, pot->n_r, pot->dr},
+      tF{pot->d_F, pot->n_rho, pot->drho};
+  unsigned g = (unsigned)((na + 127) / 128);
+  k_eam_density<<<g, 128, 0, ctx->stream>>>(B, N, box, trho, tF, q, nl.nbr, nl.cnt, nl.maxn, Fp, Fe);
+  PL_CHECK_LAUNCH();
+  k_eam_force<<<g, 128, 0, ctx->stream>>>(B, N, box, trho, tphi, q, nl.nbr, nl.cnt, nl.maxn, Fp, Fe,
+                                          grad, energy ? ea : nullptr, virial ? va : nullptr);
+  PL_CHECK_LAUNCH();
+  if (energy) {
+    k_sys_reduce<<<(unsigned)B, 256, 0, ctx->stream>>>(B, N, 1, ea, energy);
+    PL_CHECK_LAUNCH();
+  }
+  if (virial) {
+    k_sys_reduce<<<(unsigned)B, 256, 0, ctx->stream>>>(B, N, 6, va, virial);
+    PL_CHECK_LAUNCH();
+  }
+  return PL_OK;
+}
+
+}  // namespace pl

@@ -1,0 +1,94 @@
+// Periodic neighbour lists for batches of systems (B x N atoms, flat AoS q).
+//
+// Positions stay UNWRAPPED in the state (the reference's Euclidean error
+// metric, parareal.py:196-197, must see continuous coordinates); the minimum
+// image is applied here only.  The box must be >= 2*rcut, so every pair has at
+// most one image inside the cutoff.  Lists are ordered by ascending j: the
+// force sums are then in a fixed order, which keeps every kernel run-to-run
+// deterministic and lets the C oracle reproduce the same pair set bit for bit
+// (the cutoff test uses explicit round-to-nearest ops, no FMA).
+#pragma once
+
+#include "pl_common.cuh"
+
+namespace pl {
+
+struct Box {
+  double L[3];
+};
+
+__device__ __forceinline__ double min_image(double dx, double L) {
+  double k = rint(dvd(dx, L));
+  return sub(dx, mul(L, k));
+}
+
+__device__ __forceinline__ double r2_exact(double dx, double dy, double dz) {
+  return add(add(mul(dx, dx), mul(dy, dy)), mul(dz, dz));
+}
+
+constexpr int NB_THREADS = 128;
+
+// one thread per atom i of system b; j tiles staged in shared memory
+static __global__ void __launch_bounds__(NB_THREADS)
+k_neigh_brute(int64_t B, int N, Box box, double rc2, int maxn, const double* __restrict__ q,
+              int32_t* __restrict__ nbr, int32_t* __restrict__ cnt, int* __restrict__ overflow) {
+  __shared__ double sx[NB_THREADS * 3];
+  int64_t b = blockIdx.y;
+  int i = blockIdx.x * NB_THREADS + threadIdx.x;
+  const double* qb = q + b * (int64_t)N * 3;
+  double xi = 0, yi = 0, zi = 0;
+  if (i < N) {
+    xi = qb[3 * i];
+    yi = qb[3 * i + 1];
+    zi = qb[3 * i + 2];
+  }
+  int c = 0;
+  int32_t* my = nbr + (b * N + (i < N ? i : 0)) * (int64_t)maxn;
+  for (int j0 = 0; j0 < N; j0 += NB_THREADS) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < NB_THREADS * 3; t += NB_THREADS) {
+      int jj = j0 * 3 + t;
+      sx[t] = jj < N * 3 ? qb[jj] : 0.0;
+    }
+    __syncthreads();
+    if (i < N) {
+      int jmax = min(NB_THREADS, N - j0);
+      for (int jj = 0; jj < jmax; ++jj) {
+        int j = j0 + jj;
+        if (j == i) continue;
+        double dx = min_image(sub(sx[3 * jj], xi), box.L[0]);
+        double dy = min_image(sub(sx[3 * jj + 1], yi), box.L[1]);
+        double dz = min_image(sub(sx[3 * jj + 2], zi), box.L[2]);
+        double r2 = r2_exact(dx, dy, dz);
+        if (r2 < rc2) {
+          if (c < maxn) my[c] = j;
+          ++c;
+        }
+      }
+    }
+  }
+  if (i < N) {
+    cnt[b * N + i] = c < maxn ? c : maxn;
+    if (c > maxn) atomicExch(overflow, 1);
+  }
+}
+
+// displacement r_j - r_i under the minimum image (same ops as the builder)
+__device__ __forceinline__ void pair_vec(const double* qb, int i, int j, const Box& box, double& dx,
+                                         double& dy, double& dz) {
+  dx = min_image(sub(qb[3 * j], qb[3 * i]), box.L[0]);
+  dy = min_image(sub(qb[3 * j + 1], qb[3 * i + 1]), box.L[1]);
+  dz = min_image(sub(qb[3 * j + 2], qb[3 * i + 2]), box.L[2]);
+}
+
+struct NeighList {
+  int32_t* nbr = nullptr;
+  int32_t* cnt = nullptr;
+  int* overflow = nullptr;
+  int maxn = 0;
+};
+
+// builds into pot->work[0] (lists) / work[1] (counts + flag)
+int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out);
+
+}  // namespace pl

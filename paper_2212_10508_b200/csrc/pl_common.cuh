@@ -1,0 +1,130 @@
+// Shared internals of the paralangevin_b200 C ABI (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "paralangevin_b200.h"
+
+namespace pl {
+
+// ---- error reporting (thread-local, no global mutable state shared across threads)
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+#define PL_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t _e = (call);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return ::pl::fail(PL_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define PL_CHECK_LAUNCH() PL_CUDA(cudaGetLastError())
+
+#define PL_TRY(call)              \
+  do {                            \
+    int _rc = (call);             \
+    if (_rc != PL_OK) return _rc; \
+  } while (0)
+
+// ---- exact-order fp64 arithmetic: no FMA contraction on the parity path.
+// numpy evaluates left to right with one rounding per operation
+// (integrator.py:174-177, rng.py:130-135); these intrinsics pin that.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---- SplitMix64 (rng.py:31-45)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t GOLDEN = 0x9E3779B97F4A7C15ull;
+constexpr double BLOWUP_LIMIT = 1e12;
+
+// ---- device workspace: grow-only scratch owned by a context
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int reserve(size_t n);
+  ~Scratch();
+};
+
+}  // namespace pl
+
+// Potential kinds
+enum PotKind {
+  POT_FREE = 0,
+  POT_HARMONIC = 1,
+  POT_DOUBLE_WELL = 2,
+  POT_LJ = 3,
+  POT_PERTURBED = 4,
+  POT_EAM = 5,
+  POT_SNAP = 6,
+};
+
+struct SnapIndex;  // snap.cu
+
+struct pl_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  pl::Scratch work[8];  // named slots, see pl_ctx slot enum in each .cu
+  // pinned host staging for small scalars read back by sync calls
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+struct pl_pot {
+  pl_ctx* ctx = nullptr;
+  PotKind kind = POT_FREE;
+  int64_t dim = 0;  // fixed dimension, 0 = any
+  // elementwise coefficients (device): harmonic k / double-well a, b
+  double* d_c0 = nullptr;
+  double* d_c1 = nullptr;
+  double s0 = 0.0, s1 = 0.0;  // scalar coefficients when dim == 0
+  // LJ
+  double eps = 1.0, sigma = 1.0;
+  int n_atoms = 0, space_dim = 0;
+  // perturbed
+  pl_pot* base = nullptr;
+  pl_pot* delta = nullptr;
+  double lam = 0.0;
+  // periodic many-body potentials
+  double box[3] = {0, 0, 0};
+  double rcut = 0.0;
+  // EAM tables (device)
+  int n_r = 0, n_rho = 0;
+  double dr = 0.0, drho = 0.0;
+  double* d_rho = nullptr;
+  double* d_phi = nullptr;
+  double* d_F = nullptr;
+  // SNAP
+  int twojmax = 0;
+  double rfac0 = 0.0, rmin0 = 0.0, wself = 1.0;
+  int switchflag = 1;
+  int nbeta = 0;
+  SnapIndex* snap = nullptr;
+  double flops = 0.0;
+  int* nb_overflow = nullptr;  // device flag of the last neighbour build
+  // per-potential scratch (neighbour lists, per-atom buffers)
+  pl::Scratch work[8];
+};
+
+namespace pl {
+bool is_elementwise(const pl_pot* p);
+// Generic batched gradient (+energy) of B systems of dimension d on ctx->stream.
+int compute(pl_pot* pot, int64_t B, int64_t d, const double* q, double* energy, double* grad,
+            double* virial);
+int compute_eam(pl_pot* pot, int64_t B, const double* q, double* energy, double* grad,
+                double* virial);
+int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double* grad,
+                 double* virial);
+int snap_prepare(pl_pot* pot, const double* h_beta);
+int neigh_check(pl_pot* pot);
+void snap_release(pl_pot* pot);
+}  // namespace pl

@@ -1,0 +1,155 @@
+// Corrected coarse sweep of parareal (parareal.py:289-299, 195-198, 425-445).
+//
+// The sweep is the sequential critical path: window m's coarse propagation
+// needs cur[m], produced by window m-1.  States stay in HBM; per node only
+// the running error (two scalars) is read back, which is what the adaptive
+// engine's truncation decision needs (parareal.py:433-445).
+#include <cmath>
+
+#include "pl_common.cuh"
+
+namespace pl {
+
+int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, const double* q0,
+                      const double* p0, const double* noise, const double* h_amp,
+                      const double* mass, double dt, double h, double hg, double* q1, double* p1,
+                      int32_t* blow);
+
+namespace {
+
+constexpr int CT = 1024;
+
+// deterministic block sum of squares (fixed tree order)
+__device__ double block_sumsq(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int w = CT / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// acc = {num, den, delta, nonfinite}
+__global__ void __launch_bounds__(CT)
+k_combine(int64_t d, const double* __restrict__ base_q, const double* __restrict__ base_p,
+          const double* __restrict__ jump_q, const double* __restrict__ jump_p,
+          const double* __restrict__ prev_q, double* __restrict__ cur_q, double* __restrict__ cur_p,
+          double* __restrict__ acc, double* __restrict__ hist) {
+  __shared__ double sh[CT];
+  double s1 = 0.0, s2 = 0.0;
+  int bad = 0;
+  for (int64_t i = threadIdx.x; i < d; i += CT) {
+    // corrected value: coarse + jump, jump formed first (parareal.py:293)
+    double q = add(base_q[i], jump_q[i]);
+    double p = add(base_p[i], jump_p[i]);
+    cur_q[i] = q;
+    cur_p[i] = p;
+    if (!isfinite(q) || !isfinite(p)) bad = 1;
+    double e = sub(q, prev_q[i]);
+    s1 += e * e;
+    s2 += prev_q[i] * prev_q[i];
+  }
+  bad = __syncthreads_or(bad);
+  double n1 = sqrt(block_sumsq(s1, sh));
+  double n2 = sqrt(block_sumsq(s2, sh));
+  if (threadIdx.x == 0) {
+    double num = acc[0] + n1;  // parareal.py:196-197
+    double den = acc[1] + n2;
+    acc[0] = num;
+    acc[1] = den;
+    acc[2] = num / den;
+    acc[3] = bad ? 1.0 : 0.0;
+    *hist = num / den;
+  }
+}
+
+__global__ void __launch_bounds__(CT)
+k_accumulate_node(int64_t d, const double* __restrict__ q, double* __restrict__ acc) {
+  __shared__ double sh[CT];
+  double s2 = 0.0;
+  for (int64_t i = threadIdx.x; i < d; i += CT) s2 += q[i] * q[i];
+  double n2 = sqrt(block_sumsq(s2, sh));
+  if (threadIdx.x == 0) acc[1] += n2;  // num += ||q - q|| = 0
+}
+
+__global__ void k_sub(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                      double* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = sub(a[t], b[t]);
+}
+
+}  // namespace
+
+int sub_arrays(pl_ctx* ctx, int64_t n, const double* a, const double* b, double* out) {
+  if (n <= 0) return PL_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_sub<<<(unsigned)blocks, 256, 0, ctx->stream>>>(n, a, b, out);
+  PL_CHECK_LAUNCH();
+  return PL_OK;
+}
+
+int sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1, int include_m0,
+          double* traj_q, double* traj_p, const double* prev_q, double* base_q, double* base_p,
+          const double* jump_q, const double* jump_p, const double* noise_all, const double* h_amp,
+          const double* mass, double dt, double h, double hg, double expl, double* h_state,
+          double* d_hist, int64_t* h_out, int32_t* h_blowup) {
+  cudaStream_t st = ctx->stream;
+  h_out[0] = 0;
+  h_blowup[0] = 0;
+  if (m1 <= m0) return PL_OK;
+  PL_TRY(ctx->work[3].reserve(sizeof(double) * 8 + sizeof(int32_t) * 8));
+  double* acc = (double*)ctx->work[3].ptr;
+  int32_t* blow = (int32_t*)(acc + 4);
+  if (!ctx->pinned) {
+    PL_CUDA(cudaMallocHost(&ctx->pinned, 256));
+    ctx->pinned_bytes = 256;
+  }
+  double* hacc = (double*)ctx->pinned;
+  int32_t* hblow = (int32_t*)(hacc + 4);
+  double init[4] = {h_state[0], h_state[1], 0.0, 0.0};
+  PL_CUDA(cudaMemcpyAsync(acc, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  if (include_m0) {
+    k_accumulate_node<<<1, CT, 0, st>>>(d, traj_q + m0 * d, acc);
+    PL_CHECK_LAUNCH();
+  }
+  const int64_t nb = (int64_t)(L + 1) * d;
+  for (int64_t m = m0; m < m1; ++m) {
+    PL_TRY(propagate_windows(ctx, coarse, 1, d, L, traj_q + m * d, traj_p + m * d,
+                             noise_all + m * nb, h_amp, mass, dt, h, hg, base_q + m * d,
+                             base_p + m * d, blow));
+    k_combine<<<1, CT, 0, st>>>(d, base_q + m * d, base_p + m * d, jump_q + m * d, jump_p + m * d,
+                                prev_q + (m + 1) * d, traj_q + (m + 1) * d, traj_p + (m + 1) * d,
+                                acc, d_hist + (m - m0));
+    PL_CHECK_LAUNCH();
+    PL_CUDA(cudaMemcpyAsync(hacc, acc, sizeof(double) * 4 + sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    PL_CUDA(cudaStreamSynchronize(st));
+    h_state[0] = hacc[0];
+    h_state[1] = hacc[1];
+    if (hblow[0]) {
+      h_out[0] = m;
+      h_blowup[0] = hblow[0];
+      return fail(PL_EBLOWUP, "coarse window blew up");
+    }
+    if (hacc[3] != 0.0) {
+      h_out[0] = m;
+      h_blowup[0] = 0;
+      return fail(PL_EBLOWUP, "corrected state is not finite");
+    }
+    h_out[0] = m - m0 + 1;
+    if (hacc[1] == 0.0) return PL_OK;  // caller raises DegenerateNormalizationError
+    if (expl > 0.0 && hacc[2] > expl) return PL_OK;
+  }
+  return PL_OK;
+}
+
+}  // namespace pl
+
+extern "C" int pl_sub(pl_ctx* ctx, int64_t n, const double* a, const double* b, double* out) {
+  if (!ctx || (n > 0 && (!a || !b || !out))) return pl::fail(PL_EARG, "NULL argument");
+  return pl::sub_arrays(ctx, n, a, b, out);
+}

@@ -1,0 +1,612 @@
+"""Parareal engines with the fine stage batched on the GPU.
+
+Mirrors /root/reference/pkg/src/paralangevin/parareal.py:
+  PararealConfig / SlabAttempt / SlabRecord / PararealResult  parareal.py:65-192
+  relative_error                                              parareal.py:201-225
+  sequential_propagate                                        parareal.py:243-267
+  parareal_classic(_engine)                                   parareal.py:315-363, 490-509
+  parareal_adaptive(_engine)                                  parareal.py:366-475, 512-529
+
+Device engine (used whenever the propagators are device window propagators,
+i.e. always for ``parareal_classic`` / ``parareal_adaptive``):
+  * noise for every window is generated once and stays in HBM (it is
+    iteration-invariant);
+  * the jump stage F(prev[m]) - C(prev[m]) is ONE batched
+    ``pl_propagate_windows`` launch over all slab windows; C(prev[m]) is the
+    coarse output cached by the previous sweep/bootstrap (bitwise the same
+    value the reference recomputes, SURVEY.md finding 7);
+  * the corrected sweep runs in ``pl_sweep`` on the device; only the running
+    error crosses back to the host, once per node, to drive the slab logic.
+The control flow below is a line-by-line restatement of the reference
+engines, so slab records, iteration counts and error histories follow the
+same decisions.  Engines given arbitrary Python callables (scripted
+propagators) run the same control flow over those callables.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+from typing import Callable, NamedTuple
+
+import numpy as np
+
+from . import _lib
+from .integrator import BlowUpError, TemperatureSchedule, WindowKernel
+from .model import LangevinParams, NodeTrajectory, PhaseState
+from .potentials import PropagatorPair
+from .rng import NoisePlan
+
+WindowPropagator = Callable[[PhaseState, int], PhaseState]
+
+
+class DegenerateNormalizationError(ValueError):
+    """The relative-error denominator vanished."""
+
+
+class SlabCollapseError(RuntimeError):
+    def __init__(self, message: str, slab_index: int, n_init: int):
+        super().__init__(message)
+        self.slab_index = slab_index
+        self.n_init = n_init
+
+
+@dataclass(frozen=True)
+class PararealConfig:
+    n_windows: int
+    delta_conv: float
+    delta_expl: float | None = None
+    k_max: int | None = None
+
+    def __post_init__(self) -> None:
+        if not isinstance(self.n_windows, int) or self.n_windows < 1:
+            raise ValueError(f"n_windows must be a positive integer, got {self.n_windows}")
+        if not (np.isfinite(self.delta_conv) and self.delta_conv > 0.0):
+            raise ValueError(f"delta_conv must be positive and finite, got {self.delta_conv}")
+        if self.delta_expl is not None and not self.delta_expl > self.delta_conv:
+            raise ValueError(
+                f"delta_expl ({self.delta_expl}) must exceed delta_conv ({self.delta_conv})")
+        if self.k_max is not None and (not isinstance(self.k_max, int) or self.k_max < 1):
+            raise ValueError(f"k_max must be a positive integer, got {self.k_max}")
+
+    @property
+    def iteration_cap(self) -> int:
+        return self.k_max if self.k_max is not None else self.n_windows + 1
+
+
+class SlabAttempt(NamedTuple):
+    n_final: int
+    iterations: int
+
+
+@dataclass(frozen=True)
+class SlabRecord:
+    slab_index: int
+    n_init: int
+    attempts: tuple
+    n_final: int
+    k_conv: int
+
+    def __post_init__(self) -> None:
+        attempts = tuple(SlabAttempt(int(a[0]), int(a[1])) for a in self.attempts)
+        object.__setattr__(self, "attempts", attempts)
+        if self.slab_index < 1:
+            raise ValueError(f"slab_index must be >= 1, got {self.slab_index}")
+        if not attempts:
+            raise ValueError("a slab record needs at least one attempt")
+        if not 0 <= self.n_init < self.n_final:
+            raise ValueError(f"slab range [{self.n_init}, {self.n_final}] must be non-empty")
+        for a, b in zip(attempts, attempts[1:]):
+            if b.n_final > a.n_final:
+                raise ValueError("attempt endpoints must be non-increasing")
+        if attempts[-1].n_final != self.n_final:
+            raise ValueError(f"last attempt ends at {attempts[-1].n_final}, slab at {self.n_final}")
+        if any(a.iterations < 1 for a in attempts):
+            raise ValueError("every attempt must count at least one iteration")
+        if sum(a.iterations for a in attempts) != self.k_conv:
+            raise ValueError("k_conv must equal the sum of attempt iterations")
+
+    @property
+    def width(self) -> int:
+        return self.n_final - self.n_init
+
+
+@dataclass(frozen=True)
+class PararealResult:
+    trajectory: NodeTrajectory
+    slabs: tuple
+    error_history: tuple
+    converged: bool
+    iterates: tuple | None = None
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "slabs", tuple(self.slabs))
+        object.__setattr__(self, "error_history",
+                           tuple((int(s), int(k), float(e)) for s, k, e in self.error_history))
+        if self.iterates is not None:
+            object.__setattr__(self, "iterates", tuple(self.iterates))
+        if not self.slabs:
+            raise ValueError("a result needs at least one slab record")
+        if self.slabs[0].n_init != 0:
+            raise ValueError("the first slab must start at window 0")
+        for i, slab in enumerate(self.slabs):
+            if slab.slab_index != i + 1:
+                raise ValueError("slab indices must run 1..n_slab in order")
+        for a, b in zip(self.slabs, self.slabs[1:]):
+            if b.n_init != a.n_final:
+                raise ValueError(f"slabs must tile the window range: {a.n_final} != {b.n_init}")
+        if self.converged and self.slabs[-1].n_final != self.trajectory.n_windows:
+            raise ValueError("a converged result must cover every window")
+
+    @property
+    def n_slab(self) -> int:
+        return len(self.slabs)
+
+    @property
+    def total_iterations(self) -> int:
+        return sum(slab.k_conv for slab in self.slabs)
+
+
+def _close_attempt(attempts, n_init, n_final, iterations):
+    width = n_final - n_init
+    if iterations > width + 1:
+        warnings.warn(
+            f"slab [{n_init}, {n_final}] needed {iterations} iterations, beyond the width + 1 = "
+            f"{width + 1} exact-arithmetic bound; delta_conv may be below roundoff",
+            RuntimeWarning, stacklevel=3)
+    attempts.append(SlabAttempt(n_final=n_final, iterations=iterations))
+
+
+def relative_error(a, b, n_init: int, n_final: int) -> float:
+    """sum_n |b_n.q - a_n.q| / sum_n |a_n.q| over max(n_init,1)..n_final (host helper)."""
+    if n_init < 0:
+        raise ValueError(f"n_init must be >= 0, got {n_init}")
+    if n_final < max(n_init, 1):
+        raise ValueError(
+            f"n_final must be >= max(n_init, 1), got n_init={n_init}, n_final={n_final}")
+    if n_final >= len(a) or n_final >= len(b):
+        raise IndexError(
+            f"node {n_final} out of range for trajectories of {len(a)} and {len(b)} nodes")
+    num = den = 0.0
+    for n in range(max(n_init, 1), n_final + 1):
+        num += float(np.linalg.norm(b[n].q - a[n].q))
+        den += float(np.linalg.norm(a[n].q))
+    if den == 0.0:
+        raise DegenerateNormalizationError(
+            f"all reference positions on nodes {max(n_init, 1)}..{n_final} are zero")
+    return num / den
+
+
+# ======================================================================
+# device window propagator
+class DevicePropagator:
+    """``WindowPropagator`` backed by the GPU: (state, m) -> state, plus batch access."""
+
+    def __init__(self, pot, params: LangevinParams, schedule: TemperatureSchedule, plan: NoisePlan,
+                 dim: int):
+        self.pot, self.params, self.schedule, self.plan = pot, params, schedule, plan
+        self.kernel = WindowKernel(pot, params, schedule, dim)
+        self.d = dim
+        self._noise = None
+
+    def noise_all(self):
+        """(N, (L+1)*d) device noise of every planned window, generated once."""
+        if self._noise is None:
+            self._noise = self.kernel.noise(np.asarray(self.plan.window_seeds, dtype=np.uint64))
+        return self._noise
+
+    def share_noise(self, other: "DevicePropagator") -> None:
+        if other.plan == self.plan and other.kernel.L == self.kernel.L and other.d == self.d:
+            self._noise = other.noise_all()
+
+    def __call__(self, state: PhaseState, m: int) -> PhaseState:
+        import torch
+        dev = self.kernel.device
+        Q0 = torch.from_numpy(np.ascontiguousarray(state.q)[None]).to(dev)
+        P0 = torch.from_numpy(np.ascontiguousarray(state.p)[None]).to(dev)
+        Q1, P1, blow = self.kernel.run(Q0, P0, self.noise_all()[m:m + 1])
+        b = int(blow.cpu()[0])
+        if b:
+            raise BlowUpError(
+                f"state left the trusted range (|component| > 1e+12 or non-finite) at substep {b}",
+                substep=b)
+        return PhaseState(q=Q1[0].cpu().numpy(), p=P1[0].cpu().numpy())
+
+
+def _window_propagator(pot, params, schedule, plan, dim) -> DevicePropagator:
+    return DevicePropagator(pot, params, schedule, plan, dim)
+
+
+def _attach_context(err: BlowUpError, window: int, iteration: int) -> None:
+    if err.window is None:
+        err.window = window
+    if err.iteration is None:
+        err.iteration = iteration
+
+
+def _call(prop, state, m, iteration):
+    try:
+        return prop(state, m)
+    except BlowUpError as err:
+        _attach_context(err, window=m + 1, iteration=iteration)
+        raise
+
+
+class _DeviceRun:
+    """Device-resident trajectory + cached coarse outputs for one engine run."""
+
+    def __init__(self, initial: PhaseState, fine: DevicePropagator, coarse: DevicePropagator, n: int):
+        import torch
+        self.fine, self.coarse, self.n, self.d = fine, coarse, n, initial.dim
+        if fine.d != initial.dim or coarse.d != initial.dim:
+            raise ValueError("propagator dimension does not match the initial state")
+        if fine.plan.n_windows < n:
+            raise ValueError(f"noise plan covers {fine.plan.n_windows} windows, need {n}")
+        coarse.share_noise(fine)
+        dev = fine.kernel.device
+        d = self.d
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.Q = torch.zeros((n + 1, d), **f64)
+        self.P = torch.zeros((n + 1, d), **f64)
+        self.Q[0] = torch.from_numpy(np.ascontiguousarray(initial.q))
+        self.P[0] = torch.from_numpy(np.ascontiguousarray(initial.p))
+        self.prevQ = torch.zeros((n + 1, d), **f64)
+        self.baseQ = torch.zeros((n, d), **f64)
+        self.baseP = torch.zeros((n, d), **f64)
+        self.jumpQ = torch.zeros((n, d), **f64)
+        self.jumpP = torch.zeros((n, d), **f64)
+        self.hist = torch.zeros(n, **f64)
+        self.noise_f = fine.noise_all()
+        self.noise_c = coarse.noise_all()
+
+    def bootstrap(self, n_init: int) -> None:
+        """cur[m+1] = C(cur[m]) for m = n_init..N-1 (parareal.py:404-405); caches base."""
+        import torch
+        k = self.coarse.kernel
+        blows = torch.zeros(self.n, dtype=torch.int32, device=self.Q.device)
+        for m in range(n_init, self.n):
+            k.run(self.Q[m:m + 1], self.P[m:m + 1], self.noise_c[m:m + 1],
+                  self.baseQ[m:m + 1], self.baseP[m:m + 1], blows[m:m + 1])
+            self.Q[m + 1].copy_(self.baseQ[m])
+            self.P[m + 1].copy_(self.baseP[m])
+        b = blows.cpu().numpy()
+        bad = np.nonzero(b)[0]
+        if bad.size:
+            m = int(bad[0])
+            raise BlowUpError(f"state left the trusted range at substep {b[m]}", substep=int(b[m]),
+                              window=m + 1, iteration=0)
+
+    def jumps(self, n_init: int, n_final: int, iteration: int) -> None:
+        """jump[m] = F(prev[m]) - C(prev[m]) for all slab windows in one launch."""
+        W = n_final - n_init
+        FQ, FP, blow = self.fine.kernel.run(self.Q[n_init:n_final], self.P[n_init:n_final],
+                                            self.noise_f[n_init:n_final])
+        b = blow.cpu().numpy()
+        bad = np.nonzero(b)[0]
+        if bad.size:
+            i = int(bad[0])
+            raise BlowUpError(
+                f"state left the trusted range (|component| > 1e+12 or non-finite) at substep {b[i]}",
+                substep=int(b[i]), window=n_init + i + 1, iteration=iteration)
+        lib, ctx = _lib.load(), _lib.context()
+        n = W * self.d
+        _lib.check(lib.pl_sub(ctx.handle, n, _lib.ptr(FQ), _lib.ptr(self.baseQ[n_init:n_final]),
+                              _lib.ptr(self.jumpQ[n_init:n_final])))
+        _lib.check(lib.pl_sub(ctx.handle, n, _lib.ptr(FP), _lib.ptr(self.baseP[n_init:n_final]),
+                              _lib.ptr(self.jumpP[n_init:n_final])))
+
+    def snapshot_prev(self, n_init: int, n_final: int) -> None:
+        self.prevQ[n_init:n_final + 1].copy_(self.Q[n_init:n_final + 1])
+
+    def sweep(self, n_init: int, n_final: int, include_m0: bool, expl: float, iteration: int):
+        """Corrected sweep on the device; returns (deltas, den) for the nodes updated."""
+        import ctypes as C
+        k = self.coarse.kernel
+        lib, ctx = _lib.load(), _lib.context()
+        state = np.zeros(2)
+        out = np.zeros(1, dtype=np.int64)
+        blow = np.zeros(1, dtype=np.int32)
+        rc = lib.pl_sweep(
+            ctx.handle, self.coarse.pot.handle(ctx), self.d, k.L, n_init, n_final,
+            1 if include_m0 else 0, _lib.ptr(self.Q), _lib.ptr(self.P), _lib.ptr(self.prevQ),
+            _lib.ptr(self.baseQ), _lib.ptr(self.baseP), _lib.ptr(self.jumpQ), _lib.ptr(self.jumpP),
+            _lib.ptr(self.noise_c), _lib.dptr(k.amp), _lib.ptr(k.mass), k.dt, k.h, k.hg,
+            float(expl), _lib.dptr(state), _lib.ptr(self.hist),
+            out.ctypes.data_as(_lib.pi64), blow.ctypes.data_as(_lib.pi32))
+        if rc == _lib.PL_EBLOWUP:
+            m = int(out[0])
+            if blow[0]:
+                raise BlowUpError(f"coarse window blew up at substep {int(blow[0])}",
+                                  substep=int(blow[0]), window=m + 1, iteration=iteration)
+            raise BlowUpError(f"corrected state is not finite at window {m + 1} "
+                              f"(iteration {iteration})", window=m + 1, iteration=iteration)
+        _lib.check(rc)
+        n_done = int(out[0])
+        deltas = self.hist[:n_done].cpu().numpy()
+        return deltas, state[1]
+
+    def trajectory(self) -> NodeTrajectory:
+        return NodeTrajectory.from_arrays(self.Q.cpu().numpy(), self.P.cpu().numpy())
+
+
+def _is_device(fine, coarse) -> bool:
+    return isinstance(fine, DevicePropagator) and isinstance(coarse, DevicePropagator)
+
+
+# ======================================================================
+# engines
+def sequential_propagate(initial: PhaseState, n_windows: int, pot, params: LangevinParams,
+                         schedule: TemperatureSchedule, plan: NoisePlan) -> NodeTrajectory:
+    """Chain n_windows fine windows on the device; node n+1 uses seed n+1."""
+    if n_windows < 0:
+        raise ValueError(f"n_windows must be >= 0, got {n_windows}")
+    if plan.n_windows < n_windows:
+        raise ValueError(f"noise plan covers {plan.n_windows} windows, need {n_windows}")
+    if n_windows == 0:
+        return NodeTrajectory((initial,))
+    import torch
+    prop = _window_propagator(pot, params, schedule, plan, initial.dim)
+    k = prop.kernel
+    noise = k.noise(np.asarray(plan.window_seeds[:n_windows], dtype=np.uint64))
+    d = initial.dim
+    Q = torch.empty((n_windows + 1, d), dtype=torch.float64, device=k.device)
+    P = torch.empty_like(Q)
+    Q[0] = torch.from_numpy(np.ascontiguousarray(initial.q))
+    P[0] = torch.from_numpy(np.ascontiguousarray(initial.p))
+    blows = torch.zeros(n_windows, dtype=torch.int32, device=k.device)
+    for m in range(n_windows):
+        _, _, b = k.run(Q[m:m + 1], P[m:m + 1], noise[m:m + 1], Q[m + 1:m + 2], P[m + 1:m + 2])
+        blows[m:m + 1].copy_(b)
+    bl = blows.cpu().numpy()
+    bad = np.nonzero(bl)[0]
+    if bad.size:
+        m = int(bad[0])
+        raise BlowUpError(f"state left the trusted range at substep {bl[m]}", substep=int(bl[m]),
+                          window=m + 1, iteration=0)
+    return NodeTrajectory.from_arrays(Q.cpu().numpy(), P.cpu().numpy())
+
+
+def _classic_device(initial, fine, coarse, config, record_iterates):
+    n = config.n_windows
+    run = _DeviceRun(initial, fine, coarse, n)
+    run.bootstrap(0)
+    iterates = [run.trajectory()] if record_iterates else None
+    history = []
+    k = 0
+    delta = 2.0 * config.delta_conv
+    while delta >= config.delta_conv:
+        if k >= config.iteration_cap:
+            break
+        k += 1
+        run.jumps(0, n, k)
+        run.snapshot_prev(0, n)
+        deltas, den = run.sweep(0, n, False, 0.0, k)
+        if den == 0.0:
+            raise DegenerateNormalizationError(f"all reference positions on nodes 1..{n} are zero")
+        delta = float(deltas[-1])
+        history.append((1, k, delta))
+        if record_iterates:
+            iterates.append(run.trajectory())
+    attempts = []
+    _close_attempt(attempts, 0, n, k)
+    slab = SlabRecord(slab_index=1, n_init=0, attempts=tuple(attempts), n_final=n, k_conv=k)
+    return PararealResult(trajectory=run.trajectory(), slabs=(slab,), error_history=tuple(history),
+                          converged=delta < config.delta_conv,
+                          iterates=tuple(iterates) if record_iterates else None)
+
+
+def _adaptive_device(initial, fine, coarse, config):
+    n = config.n_windows
+    conv, expl = config.delta_conv, config.delta_expl
+    mid = 0.5 * (conv + expl)
+    run = _DeviceRun(initial, fine, coarse, n)
+    n_init = n_final = 0
+    delta = mid
+    n_slab = 0
+    slabs, history, attempts = [], [], []
+    k_in_slab = 0
+    converged = True
+    while n_final < n:
+        if delta < expl:
+            n_init, n_final = n_final, n
+            run.bootstrap(n_init)
+            n_slab += 1
+            attempts = []
+            k_in_slab = 0
+        delta = mid
+        k_attempt = 0
+        aborted = False
+        while conv <= delta <= expl:
+            if k_attempt >= config.iteration_cap:
+                aborted = True
+                break
+            run.jumps(n_init, n_final, k_in_slab + 1)
+            run.snapshot_prev(n_init, n_final)
+            k_attempt += 1
+            k_in_slab += 1
+            deltas, den = run.sweep(n_init, n_final, n_init >= 1, expl, k_in_slab)
+            for i, dl in enumerate(deltas):
+                m = n_init + i
+                history.append((n_slab, k_in_slab, float(dl)))
+                delta = float(dl)
+            if den == 0.0:
+                raise DegenerateNormalizationError(
+                    f"all reference positions on nodes {max(n_init, 1)}..{n_init + len(deltas)} "
+                    f"are zero")
+            if delta > expl:
+                m = n_init + len(deltas) - 1
+                if m == n_init:
+                    raise SlabCollapseError(
+                        f"slab {n_slab} exploded at its first window {n_init + 1}; "
+                        f"no shorter slab exists", slab_index=n_slab, n_init=n_init)
+                _close_attempt(attempts, n_init, n_final, k_attempt)
+                n_final = m
+        if aborted:
+            _close_attempt(attempts, n_init, n_final, k_attempt)
+            slabs.append(SlabRecord(n_slab, n_init, tuple(attempts), n_final,
+                                    sum(a.iterations for a in attempts)))
+            converged = False
+            break
+        if delta < conv:
+            _close_attempt(attempts, n_init, n_final, k_attempt)
+            slabs.append(SlabRecord(n_slab, n_init, tuple(attempts), n_final,
+                                    sum(a.iterations for a in attempts)))
+    return PararealResult(trajectory=run.trajectory(), slabs=tuple(slabs),
+                          error_history=tuple(history), converged=converged)
+
+
+# ---- generic control flow over arbitrary callables (scripted propagators)
+def _accumulate(num, den, prev_state, cur_state):
+    num += float(np.linalg.norm(cur_state.q - prev_state.q))
+    den += float(np.linalg.norm(prev_state.q))
+    return num, den
+
+
+def _compute_jumps(fine, coarse, states, window_indices, iteration):
+    out = []
+    for m in window_indices:
+        f = _call(fine, states[m], m, iteration)
+        c = _call(coarse, states[m], m, iteration)
+        out.append((f.q - c.q, f.p - c.p))
+    return out
+
+
+def _corrected(coarse, state, m, iteration, jump):
+    base = _call(coarse, state, m, iteration)
+    try:
+        return PhaseState(q=base.q + jump[0], p=base.p + jump[1])
+    except ValueError as err:
+        raise BlowUpError(f"corrected state is not finite at window {m + 1} (iteration {iteration})",
+                          window=m + 1, iteration=iteration) from err
+
+
+def parareal_classic_engine(initial: PhaseState, fine: WindowPropagator, coarse: WindowPropagator,
+                            config: PararealConfig, workers: int | None = None,
+                            record_iterates: bool = False) -> PararealResult:
+    """Classic parareal (Algorithm 1); device-resident when both propagators are device ones."""
+    if _is_device(fine, coarse):
+        return _classic_device(initial, fine, coarse, config, record_iterates)
+    n = config.n_windows
+    cur = [initial]
+    for m in range(n):
+        cur.append(_call(coarse, cur[m], m, 0))
+    iterates = [NodeTrajectory(tuple(cur))] if record_iterates else None
+    history = []
+    k = 0
+    delta = 2.0 * config.delta_conv
+    while delta >= config.delta_conv:
+        if k >= config.iteration_cap:
+            break
+        k += 1
+        prev = list(cur)
+        jumps = _compute_jumps(fine, coarse, prev, range(n), k)
+        num = den = 0.0
+        for m in range(n):
+            cur[m + 1] = _corrected(coarse, cur[m], m, k, jumps[m])
+            num, den = _accumulate(num, den, prev[m + 1], cur[m + 1])
+        if den == 0.0:
+            raise DegenerateNormalizationError(f"all reference positions on nodes 1..{n} are zero")
+        delta = num / den
+        history.append((1, k, delta))
+        if record_iterates:
+            iterates.append(NodeTrajectory(tuple(cur)))
+    attempts = []
+    _close_attempt(attempts, 0, n, k)
+    slab = SlabRecord(slab_index=1, n_init=0, attempts=tuple(attempts), n_final=n, k_conv=k)
+    return PararealResult(trajectory=NodeTrajectory(tuple(cur)), slabs=(slab,),
+                          error_history=tuple(history), converged=delta < config.delta_conv,
+                          iterates=tuple(iterates) if record_iterates else None)
+
+
+def parareal_adaptive_engine(initial: PhaseState, fine: WindowPropagator, coarse: WindowPropagator,
+                             config: PararealConfig, workers: int | None = None) -> PararealResult:
+    """Adaptive slab-shortening parareal (Algorithm 2)."""
+    if config.delta_expl is None:
+        raise ValueError("adaptive mode needs delta_expl in the configuration")
+    if _is_device(fine, coarse):
+        return _adaptive_device(initial, fine, coarse, config)
+    n = config.n_windows
+    conv, expl = config.delta_conv, config.delta_expl
+    mid = 0.5 * (conv + expl)
+    cur = [initial] + [None] * n
+    n_init = n_final = 0
+    delta = mid
+    n_slab = 0
+    slabs, history, attempts = [], [], []
+    k_in_slab = 0
+    converged = True
+    while n_final < n:
+        if delta < expl:
+            n_init, n_final = n_final, n
+            for m in range(n_init, n):
+                cur[m + 1] = _call(coarse, cur[m], m, 0)
+            n_slab += 1
+            attempts = []
+            k_in_slab = 0
+        delta = mid
+        k_attempt = 0
+        aborted = False
+        while conv <= delta <= expl:
+            if k_attempt >= config.iteration_cap:
+                aborted = True
+                break
+            prev = list(cur)
+            jumps = _compute_jumps(fine, coarse, prev, range(n_init, n_final), k_in_slab + 1)
+            k_attempt += 1
+            k_in_slab += 1
+            num = den = 0.0
+            if n_init >= 1:
+                num, den = _accumulate(num, den, prev[n_init], cur[n_init])
+            for m in range(n_init, n_final):
+                cur[m + 1] = _corrected(coarse, cur[m], m, k_in_slab, jumps[m - n_init])
+                num, den = _accumulate(num, den, prev[m + 1], cur[m + 1])
+                if den == 0.0:
+                    raise DegenerateNormalizationError(
+                        f"all reference positions on nodes {max(n_init, 1)}..{m + 1} are zero")
+                delta = num / den
+                history.append((n_slab, k_in_slab, delta))
+                if delta > expl:
+                    if m == n_init:
+                        raise SlabCollapseError(
+                            f"slab {n_slab} exploded at its first window {n_init + 1}; "
+                            f"no shorter slab exists", slab_index=n_slab, n_init=n_init)
+                    _close_attempt(attempts, n_init, n_final, k_attempt)
+                    n_final = m
+                    break
+        if aborted:
+            _close_attempt(attempts, n_init, n_final, k_attempt)
+            slabs.append(SlabRecord(n_slab, n_init, tuple(attempts), n_final,
+                                    sum(a.iterations for a in attempts)))
+            converged = False
+            break
+        if delta < conv:
+            _close_attempt(attempts, n_init, n_final, k_attempt)
+            slabs.append(SlabRecord(n_slab, n_init, tuple(attempts), n_final,
+                                    sum(a.iterations for a in attempts)))
+    return PararealResult(trajectory=NodeTrajectory(tuple(cur)), slabs=tuple(slabs),
+                          error_history=tuple(history), converged=converged)
+
+
+def _check_plan(plan: NoisePlan, n_windows: int) -> None:
+    if plan.n_windows < n_windows:
+        raise ValueError(f"noise plan covers {plan.n_windows} windows, need {n_windows}")
+
+
+def parareal_classic(initial: PhaseState, pair: PropagatorPair, params: LangevinParams,
+                     schedule: TemperatureSchedule, plan: NoisePlan, config: PararealConfig,
+                     workers: int | None = None, record_iterates: bool = False) -> PararealResult:
+    _check_plan(plan, config.n_windows)
+    return parareal_classic_engine(
+        initial, _window_propagator(pair.fine, params, schedule, plan, initial.dim),
+        _window_propagator(pair.coarse, params, schedule, plan, initial.dim), config,
+        workers=workers, record_iterates=record_iterates)
+
+
+def parareal_adaptive(initial: PhaseState, pair: PropagatorPair, params: LangevinParams,
+                      schedule: TemperatureSchedule, plan: NoisePlan, config: PararealConfig,
+                      workers: int | None = None) -> PararealResult:
+    _check_plan(plan, config.n_windows)
+    return parareal_adaptive_engine(
+        initial, _window_propagator(pair.fine, params, schedule, plan, initial.dim),
+        _window_propagator(pair.coarse, params, schedule, plan, initial.dim), config,
+        workers=workers)

@@ -1,0 +1,104 @@
+"""GPU parity of the periodic neighbour lists and EAM against the C oracle
+(oracle/native), on the BASELINE W + SIA systems.
+
+Bar: neighbour pair sets bit-exact; energies/forces/virials <= 1e-10 relative
+(fp64; the device uses FMA, the oracle does not); short trajectories <= 1e-8 A.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2212_10508_b200 as pl
+    return pl
+
+
+def _configs(n, count, sigma=0.1, seed=3):
+    from paper_2212_10508_b200 import tungsten as W
+    q0, box = W.bcc_sia(n)
+    rs = np.random.default_rng(seed)
+    Q = q0[None, :] + sigma * rs.normal(size=(count, q0.shape[0]))
+    # unwrapped coordinates: shift some atoms by whole box vectors
+    Q[:, :6] += box[0]
+    return Q, box
+
+
+def _device_neighbours(pl, pot, Q, maxn=128):
+    import torch
+    from paper_2212_10508_b200 import _lib
+    ctx = _lib.context()
+    B, d = Q.shape
+    n = d // 3
+    q = torch.from_numpy(Q).cuda()
+    nbr = torch.zeros((B, n, maxn), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros((B, n), dtype=torch.int32, device="cuda")
+    _lib.check(_lib.load().pl_neighbours(ctx.handle, pot.handle(ctx), B, _lib.ptr(q), maxn,
+                                         _lib.ptr(nbr), _lib.ptr(cnt)))
+    nbr, cnt = nbr.cpu().numpy(), cnt.cpu().numpy()
+    return [[sorted(nbr[b, i, :cnt[b, i]].tolist()) for i in range(n)] for b in range(B)]
+
+
+@pytest.mark.parametrize("ncell,rcut", [(4, 5.5), (4, 4.73), (8, 5.5)])
+def test_neighbour_lists_bit_exact(pl, ncell, rcut):
+    from oracle import native
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(ncell, 3)
+    n = Q.shape[1] // 3
+    pot = W.make_eam(n, box, ) if rcut == 5.5 else W.make_snap(n, box)
+    dev = _device_neighbours(pl, pot, Q)
+    for b in range(Q.shape[0]):
+        assert dev[b] == native.neighbours(Q[b], box, rcut)
+
+
+def test_eam_vs_oracle(pl):
+    from oracle import native
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(4, 16)
+    n = Q.shape[1] // 3
+    pot = W.make_eam(n, box)
+    t = W.eam_tables()
+    E, G, V = (x.cpu().numpy() for x in pot.evaluate(Q, True, True, True))
+    for b in range(Q.shape[0]):
+        e, g, v = native.eam(Q[b], box, t)
+        assert E[b] == pytest.approx(e, rel=1e-10)
+        np.testing.assert_allclose(G[b], g, rtol=1e-10, atol=1e-10 * np.abs(g).max())
+        np.testing.assert_allclose(V[b], v, rtol=1e-10, atol=1e-10 * np.abs(v).max())
+
+
+def test_eam_gradient_check_and_momentum(pl):
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(4, 1)
+    pot = W.make_eam(Q.shape[1] // 3, box)
+    assert pl.gradient_check(pot, Q[0], h=1e-5) < 1e-6
+    g = pot.gradient(Q[0]).reshape(-1, 3)
+    assert np.abs(g.sum(axis=0)).max() < 1e-10
+
+
+def test_eam_window_vs_oracle(pl):
+    """100 BBK substeps of EAM W+SIA at 1000 K: device vs oracle integrator + C EAM."""
+    from oracle import integrator as oint, native, rng as orng
+    from paper_2212_10508_b200 import tungsten as W
+    q0, box = W.bcc_sia(4)
+    n = q0.shape[0] // 3
+    t = W.eam_tables()
+    pot = W.make_eam(n, box)
+    mass = np.full(3 * n, W.MASS_W)
+    params = pl.LangevinParams(1.0, W.KB * 1000.0, 0.001, 100, mass=mass)
+    sched = pl.TemperatureSchedule.robust(100)
+    p0 = W.maxwell_boltzmann(n, 1000.0, 11)
+    seed = pl.derive_seed(11, 1)
+    noise = orng.gaussian_stream(seed, 101 * 3 * n)
+    out = pl.propagate_windows([pl.PhaseState(q=q0, p=p0)], pot, params, sched, [seed],
+                               noise=noise[None, :])[0]
+    grad = lambda q: native.eam(q, box, t)[1]
+    q1, p1 = oint.propagate_window(q0, p0, grad, 1.0, W.KB * 1000.0, 0.001, 100, sched.coefficients,
+                                   0, mass=mass, noise=noise)
+    assert np.abs(out.q - q1).max() < 1e-8
+    assert np.abs(out.p - p1).max() < 1e-8 * np.abs(p1).max()
