@@ -88,6 +88,12 @@ int pl_pot_snap(pl_ctx* ctx, int n_atoms, const double* h_box, int twojmax, doub
                 double rfac0, double rmin0, int switchflag, double wself, const double* h_beta,
                 int nbeta, pl_pot** out);
 int pl_pot_destroy(pl_pot* pot);
+/* SNAP per-atom bispectrum components B (B*n_atoms x n_B), canonical order
+ * (j1 ascending, j2 <= j1 ascending, J ascending).  Parity/debug path. */
+int pl_snap_bispectrum(pl_ctx* ctx, pl_pot* pot, int64_t B, const double* d_q, double* d_out);
+/* SNAP index sizes {nhalf, nfull, n_B, n_items, n_units} and the algorithmic
+ * fp64 FLOP counts {per pair (U), per atom (Z/Y), per pair (dU + contraction)}. */
+int pl_snap_info(pl_pot* pot, int32_t* h_counts, double* h_flops);
 /* Expected fp64 FLOPs of one evaluation of one system (algorithmic count). */
 double pl_pot_flops(pl_pot* pot);
 

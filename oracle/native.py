@@ -77,3 +77,33 @@ def eam(q, box, tables):
     if rc != 0:
         raise RuntimeError("oracle EAM failed (neighbour overflow)")
     return e[0], g, v
+
+
+def _snap_args(pot):
+    return (int(pot.twojmax), float(pot.rcut), float(pot.rfac0), float(pot.rmin0), int(pot.switchflag),
+            float(pot.wself))
+
+
+def snap(q, box, pot, want_bispectrum=False):
+    """(energy, gradient, virial[, B (n x nB)]) of one system for a SNAP parameter set."""
+    lib = load()
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    n = q.shape[0] // 3
+    beta = np.ascontiguousarray(pot.beta, dtype=np.float64)
+    e = np.zeros(1)
+    g = np.zeros(3 * n)
+    v = np.zeros(6)
+    nb = beta.shape[0] - 1
+    bs = np.zeros((n, nb))
+    tj, rc, rf, rm, sw, ws = _snap_args(pot)
+    box = np.ascontiguousarray(box, dtype=np.float64)
+    rcode = lib.orc_snap(n, _d(box), tj, rc, rf, rm, sw, ws, _d(beta), beta.shape[0], _d(q), _d(e),
+                         _d(g), _d(v), _d(bs) if want_bispectrum else None)
+    if rcode < 0:
+        raise RuntimeError(f"oracle SNAP failed ({rcode})")
+    return (e[0], g, v, bs) if want_bispectrum else (e[0], g, v)
+
+
+def snap_fn(pot):
+    """gradient closure for the oracle integrator."""
+    return lambda q: snap(q, pot.box, pot)[1]

@@ -48,6 +48,8 @@ SIGNATURES = {
     "pl_pot_snap": (C.c_int, [vp, C.c_int, pd, C.c_int, dbl, dbl, dbl, C.c_int, dbl, pd,
                               C.c_int, C.POINTER(vp)]),
     "pl_pot_destroy": (C.c_int, [vp]),
+    "pl_snap_bispectrum": (C.c_int, [vp, vp, i64, vp, vp]),
+    "pl_snap_info": (C.c_int, [vp, pi32, pd]),
     "pl_pot_flops": (C.c_double, [vp]),
     "pl_neighbours": (C.c_int, [vp, vp, i64, vp, C.c_int, vp, vp]),
     "pl_compute": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, vp]),

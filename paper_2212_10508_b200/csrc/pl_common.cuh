@@ -68,7 +68,7 @@ enum PotKind {
   POT_SNAP = 6,
 };
 
-struct SnapIndex;  // snap.cu
+namespace pl { struct SnapIndex; }  // snap.cu
 
 struct pl_ctx {
   int device = 0;
@@ -108,7 +108,7 @@ struct pl_pot {
   double rfac0 = 0.0, rmin0 = 0.0, wself = 1.0;
   int switchflag = 1;
   int nbeta = 0;
-  SnapIndex* snap = nullptr;
+  pl::SnapIndex* snap = nullptr;
   double flops = 0.0;
   int* nb_overflow = nullptr;  // device flag of the last neighbour build
   // per-potential scratch (neighbour lists, per-atom buffers)

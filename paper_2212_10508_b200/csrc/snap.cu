@@ -1,10 +1,867 @@
-// SNAP placeholder (replaced by the fp64 bispectrum kernels).
+// fp64 SNAP (single element) batched over systems x atoms, sm_100a.
+//
+// Formalism (2j-integer indices J = 0..twojmax; see oracle/native/snap_oracle.c
+// for the full-matrix statement this file is checked against):
+//   U^J of a neighbour from the Cayley-Klein pair (a, b) by the recursion
+//     U^J[ma][mb] = sqrt((J-ma)/(J-mb)) a* U^{J-1}[ma][mb] - sqrt(ma/(J-mb)) b* U^{J-1}[ma-1][mb]
+//   Utot = wself I + sum_k fc(r_k) U(r_k);  Z^{xy}_J = CG (x) CG contraction of Utot^x Utot^y
+//   E_i = beta_0 + sum_b beta_b B_b,  B_{j1j2J} = Re <Utot^J, Z^{j1j2}_J>
+//   dE_i/dr_ik = Re sum_J <d(fc U^J)/dr, Y^J>,  Y^J = sum coefY(x,y,J) Z^{xy}_J
+// Only the half rows mb <= J/2 of every layer are computed and stored: the
+// other half follows from U[J-ma][J-mb] = (-1)^(ma+mb) conj(U[ma][mb]), and
+// the full-matrix sums are recovered with weights w(ma,mb) in {0,1,2}.
+//
+// Kernels (one force evaluation of B systems of N atoms):
+//   k_snap_ui      CTA per atom, one warp per neighbour slot: U recursion with
+//                  lanes over the elements of a layer (layers ping-pong in
+//                  shared memory), per-warp partial Utot, fixed-order combine.
+//   k_snap_yi      CTA per atom: Utot expanded to full matrices in shared
+//                  memory, the Z/Y contraction split into cost-balanced work
+//                  units (host schedule), fixed-order segmented reduction to
+//                  Y (half rows) and the atom energy.
+//   k_snap_deidrj  CTA per atom, one warp per neighbour slot: U and dU/dr
+//                  recursion contracted on the fly with Y (shared memory).
+//   k_snap_gather  thread per atom: dE/dr_a = sum_k dE_k/dr_ka - dE_a/dr_ak
+//                  (reverse slot by binary search; no atomics), energies and
+//                  virials reduced per system in a fixed order.
+// Everything is deterministic (no floating-point atomics): reruns are bitwise
+// identical, as parareal's convergence test requires (SURVEY.md finding 4).
+#include <cmath>
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "neigh.cuh"
 #include "pl_common.cuh"
+
 namespace pl {
-int snap_prepare(pl_pot* pot, const double* h_beta) { (void)pot; (void)h_beta; return fail(PL_EARG, "SNAP not built yet"); }
-void snap_release(pl_pot* pot) { (void)pot; }
-int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double* grad, double* virial) {
-  (void)pot; (void)B; (void)q; (void)energy; (void)grad; (void)virial;
-  return fail(PL_EARG, "SNAP not built yet");
+
+constexpr int SNAP_MAXN = 64;
+constexpr int SNAP_JMAX = 14;
+constexpr int UI_WARPS = 4;
+constexpr int DE_WARPS = 4;
+constexpr int YI_THREADS = 256;
+
+struct SnapItem {      // one half-row element of one Z^{xy}_J
+  int16_t x, y, J, ma, mb;
+  int16_t ma1lo, na, mb1lo, nb;
+  int16_t bidx;        // canonical B index or -1
+  int32_t cga, cgb;    // offsets into the CG pool (na, nb values)
+  double coefY;        // weight of this Z element in Y^J (0 if none)
+  double coefE;        // beta_b * w(ma,mb) if canonical, else 0
+  double w;            // half-row weight
+};
+
+struct SnapUnit {      // a contiguous run of items of one target half index
+  int32_t target, i0, i1;
+};
+
+struct SnapIndex {
+  int tj = 0, nhalf = 0, nfull = 0, nB = 0, nitems = 0, nunits = 0;
+  int hoff[SNAP_JMAX + 2], foff[SNAP_JMAX + 2];
+  SnapItem* d_items = nullptr;
+  SnapUnit* d_units = nullptr;
+  int32_t* d_useg = nullptr;   // units of target h: [useg[h], useg[h+1])
+  double* d_cg = nullptr;
+  double beta0 = 0.0;
+  double flops_ui_pair = 0, flops_yi_atom = 0, flops_de_pair = 0;
+};
+
+struct SnapDev {  // POD view passed to kernels
+  int tj, nhalf, nfull, nB, nunits;
+  int hoff[SNAP_JMAX + 2], foff[SNAP_JMAX + 2];
+  const SnapItem* items;
+  const SnapUnit* units;
+  const int32_t* useg;
+  const double* cg;
+  double beta0, rcut, rfac0, rmin0, wself;
+  int switchflag;
+};
+
+__constant__ double c_rootpq[SNAP_JMAX + 2][SNAP_JMAX + 2];  // sqrt(p/q)
+
+// ------------------------------------------------------------------ host setup
+static double fact(int n) {
+  double f = 1.0;
+  for (int i = 2; i <= n; ++i) f *= (double)i;
+  return f;
 }
+
+// Condon-Shortley <j1 m1 j2 m2 | J M> (Racah formula), arguments are 2j / 2m
+static double clebsch(int j1, int m1, int j2, int m2, int J, int M) {
+  if (m1 + m2 != M || std::abs(m1) > j1 || std::abs(m2) > j2 || std::abs(M) > J) return 0.0;
+  if (J < std::abs(j1 - j2) || J > j1 + j2 || ((j1 + j2 + J) & 1)) return 0.0;
+  double pre = std::sqrt((J + 1) * fact((j1 + j2 - J) / 2) * fact((j1 - j2 + J) / 2) *
+                         fact((-j1 + j2 + J) / 2) / fact((j1 + j2 + J) / 2 + 1));
+  pre *= std::sqrt(fact((J + M) / 2) * fact((J - M) / 2) * fact((j1 - m1) / 2) *
+                   fact((j1 + m1) / 2) * fact((j2 - m2) / 2) * fact((j2 + m2) / 2));
+  double s = 0.0;
+  for (int k = 0;; ++k) {
+    int d1 = (j1 + j2 - J) / 2 - k, d2 = (j1 - m1) / 2 - k, d3 = (j2 + m2) / 2 - k;
+    int d4 = (J - j2 + m1) / 2 + k, d5 = (J - j1 - m2) / 2 + k;
+    if (d1 < 0 || d2 < 0 || d3 < 0) break;
+    if (d4 < 0 || d5 < 0) continue;
+    double t = 1.0 / (fact(k) * fact(d1) * fact(d2) * fact(d3) * fact(d4) * fact(d5));
+    s += (k & 1) ? -t : t;
+  }
+  return pre * s;
+}
+
+static double half_weight(int J, int ma, int mb) {
+  if (2 * mb < J) return 2.0;
+  if (2 * ma < J) return 2.0;
+  if (2 * ma == J) return 1.0;
+  return 0.0;
+}
+
+int snap_prepare(pl_pot* pot, const double* beta) {
+  const int tj = pot->twojmax;
+  SnapIndex* S = new SnapIndex();
+  S->tj = tj;
+  int h = 0, f = 0;
+  for (int J = 0; J <= tj + 1; ++J) {
+    S->hoff[J] = h;
+    S->foff[J] = f;
+    h += (J + 1) * (J / 2 + 1);
+    f += (J + 1) * (J + 1);
+  }
+  S->nhalf = S->hoff[tj + 1];
+  S->nfull = S->foff[tj + 1];
+  // canonical triples (j1 >= j2, J >= j1) -> B index
+  std::map<std::tuple<int, int, int>, int> bindex;
+  std::vector<std::tuple<int, int, int>> canon;
+  for (int j1 = 0; j1 <= tj; ++j1)
+    for (int j2 = 0; j2 <= j1; ++j2)
+      for (int J = j1 - j2; J <= std::min(tj, j1 + j2); J += 2)
+        if (J >= j1) {
+          bindex[{j1, j2, J}] = (int)canon.size();
+          canon.push_back({j1, j2, J});
+        }
+  S->nB = (int)canon.size();
+  if (pot->nbeta != S->nB + 1) {
+    delete S;
+    return fail(PL_EARG, "beta must have 1 + n_B(twojmax) = " + std::to_string(S->nB + 1) +
+                             " entries, got " + std::to_string(pot->nbeta));
+  }
+  S->beta0 = beta[0];
+  // Y coefficients per Z^{xy}_z (x >= y) from the three slots of every canonical triple
+  std::map<std::tuple<int, int, int>, double> coefY;
+  for (size_t b = 0; b < canon.size(); ++b) {
+    int j1, j2, J;
+    std::tie(j1, j2, J) = canon[b];
+    double bb = beta[b + 1];
+    coefY[{j1, j2, J}] += bb;                                        // slot J
+    coefY[{J, j2, j1}] += bb * (double)(J + 1) / (double)(j1 + 1);   // slot j1
+    coefY[{J, j1, j2}] += bb * (double)(J + 1) / (double)(j2 + 1);   // slot j2
+  }
+  // items grouped by target half index
+  std::vector<std::vector<SnapItem>> per_target(S->nhalf);
+  std::vector<double> pool;
+  for (int x = 0; x <= tj; ++x)
+    for (int y = 0; y <= x; ++y)
+      for (int J = x - y; J <= std::min(tj, x + y); J += 2) {
+        auto itc = coefY.find({x, y, J});
+        double cy = itc == coefY.end() ? 0.0 : itc->second;
+        auto itb = bindex.find({x, y, J});
+        int bidx = itb == bindex.end() ? -1 : itb->second;
+        for (int mb = 0; 2 * mb <= J; ++mb)
+          for (int ma = 0; ma <= J; ++ma) {
+            SnapItem it{};
+            it.x = x; it.y = y; it.J = J; it.ma = ma; it.mb = mb;
+            int M = 2 * ma - J, Mp = 2 * mb - J;
+            // ma1 range with ma2 = (M - m1 + y)/2 in [0, y]
+            std::vector<double> ca, cb;
+            int lo = -1;
+            for (int ma1 = 0; ma1 <= x; ++ma1) {
+              int m2 = M - (2 * ma1 - x);
+              if (std::abs(m2) > y) continue;
+              if (lo < 0) lo = ma1;
+              ca.push_back(clebsch(x, 2 * ma1 - x, y, m2, J, M));
+            }
+            it.ma1lo = (int16_t)lo;
+            it.na = (int16_t)ca.size();
+            lo = -1;
+            for (int mb1 = 0; mb1 <= x; ++mb1) {
+              int m2 = Mp - (2 * mb1 - x);
+              if (std::abs(m2) > y) continue;
+              if (lo < 0) lo = mb1;
+              cb.push_back(clebsch(x, 2 * mb1 - x, y, m2, J, Mp));
+            }
+            it.mb1lo = (int16_t)lo;
+            it.nb = (int16_t)cb.size();
+            it.cga = (int32_t)pool.size();
+            pool.insert(pool.end(), ca.begin(), ca.end());
+            it.cgb = (int32_t)pool.size();
+            pool.insert(pool.end(), cb.begin(), cb.end());
+            it.w = half_weight(J, ma, mb);
+            it.coefY = cy;
+            it.bidx = (int16_t)bidx;
+            it.coefE = bidx >= 0 ? beta[bidx + 1] * it.w : 0.0;
+            int target = S->hoff[J] + mb * (J + 1) + ma;
+            per_target[target].push_back(it);
+          }
+      }
+  // cost-balanced units: ~4 units per thread of a YI CTA
+  std::vector<SnapItem> items;
+  std::vector<SnapUnit> units;
+  std::vector<int32_t> useg(S->nhalf + 1, 0);
+  double total = 0.0;
+  for (auto& v : per_target)
+    for (auto& it : v) total += (double)it.na * it.nb + 2.0;
+  double unit_cost = total / (4.0 * YI_THREADS);
+  double yflops = 0.0;
+  for (int t = 0; t < S->nhalf; ++t) {
+    useg[t] = (int32_t)units.size();
+    auto& v = per_target[t];
+    int start = (int)items.size();
+    double acc = 0.0;
+    int u0 = start;
+    for (size_t k = 0; k < v.size(); ++k) {
+      items.push_back(v[k]);
+      double c = (double)v[k].na * v[k].nb + 2.0;
+      yflops += 10.0 * v[k].na * v[k].nb + 4.0 * v[k].nb + 10.0;
+      acc += c;
+      if (acc >= unit_cost) {
+        units.push_back({t, u0, (int32_t)items.size()});
+        u0 = (int)items.size();
+        acc = 0.0;
+      }
+    }
+    if ((int)items.size() > u0 || units.empty() || useg[t] == (int32_t)units.size())
+      units.push_back({t, u0, (int32_t)items.size()});
+  }
+  useg[S->nhalf] = (int32_t)units.size();
+  S->nitems = (int)items.size();
+  S->nunits = (int)units.size();
+  // algorithmic flop counts (used for the roofline numerator)
+  S->flops_yi_atom = yflops;
+  S->flops_ui_pair = 0.0;
+  S->flops_de_pair = 0.0;
+  for (int J = 1; J <= tj; ++J) {
+    int nel = (J + 1) * (J / 2 + 1);
+    S->flops_ui_pair += nel * 24.0;   // 2 x (complex product + scaled accumulate) + fc accumulate
+    S->flops_de_pair += nel * 160.0;  // U (20) + 3 dU (108) + 3 weighted contractions (~32)
+  }
+  S->flops_ui_pair += 40.0;
+  S->flops_de_pair += 80.0;
+  cudaError_t e1 = cudaMalloc(&S->d_items, sizeof(SnapItem) * items.size());
+  cudaError_t e2 = cudaMalloc(&S->d_units, sizeof(SnapUnit) * units.size());
+  cudaError_t e3 = cudaMalloc(&S->d_useg, sizeof(int32_t) * useg.size());
+  cudaError_t e4 = cudaMalloc(&S->d_cg, sizeof(double) * std::max<size_t>(pool.size(), 1));
+  if (e1 || e2 || e3 || e4) {
+    delete S;
+    return fail(PL_ECUDA, "cudaMalloc SNAP index");
+  }
+  cudaMemcpy(S->d_items, items.data(), sizeof(SnapItem) * items.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(S->d_units, units.data(), sizeof(SnapUnit) * units.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(S->d_useg, useg.data(), sizeof(int32_t) * useg.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(S->d_cg, pool.data(), sizeof(double) * pool.size(), cudaMemcpyHostToDevice);
+  double rp[SNAP_JMAX + 2][SNAP_JMAX + 2];
+  for (int p = 0; p < SNAP_JMAX + 2; ++p)
+    for (int q = 0; q < SNAP_JMAX + 2; ++q) rp[p][q] = q ? std::sqrt((double)p / (double)q) : 0.0;
+  PL_CUDA(cudaMemcpyToSymbol(c_rootpq, rp, sizeof(rp)));
+  pot->snap = S;
+  // one system: N atoms x ~26 pairs (perfect BCC at rcut 4.73) is only an
+  // estimate for reporting; the bench counts real pairs per launch.
+  pot->flops = 0.0;
+  return PL_OK;
+}
+
+void snap_release(pl_pot* pot) {
+  SnapIndex* S = pot->snap;
+  if (!S) return;
+  cudaFree(S->d_items);
+  cudaFree(S->d_units);
+  cudaFree(S->d_useg);
+  cudaFree(S->d_cg);
+  delete S;
+  pot->snap = nullptr;
+}
+
+static SnapDev snap_dev(const pl_pot* pot) {
+  const SnapIndex* S = pot->snap;
+  SnapDev D;
+  D.tj = S->tj; D.nhalf = S->nhalf; D.nfull = S->nfull; D.nB = S->nB; D.nunits = S->nunits;
+  for (int J = 0; J <= SNAP_JMAX + 1; ++J) {
+    D.hoff[J] = J <= S->tj + 1 ? S->hoff[J] : 0;
+    D.foff[J] = J <= S->tj + 1 ? S->foff[J] : 0;
+  }
+  D.items = S->d_items; D.units = S->d_units; D.useg = S->d_useg; D.cg = S->d_cg;
+  D.beta0 = S->beta0; D.rcut = pot->rcut; D.rfac0 = pot->rfac0; D.rmin0 = pot->rmin0;
+  D.wself = pot->wself; D.switchflag = pot->switchflag;
+  return D;
+}
+
+// ------------------------------------------------------------------ device helpers
+struct C2 {
+  double re, im;
+};
+__device__ __forceinline__ C2 cmulc(C2 a, C2 b) {  // conj(a) * b
+  return C2{a.re * b.re + a.im * b.im, a.re * b.im - a.im * b.re};
+}
+__device__ __forceinline__ C2 cmul(C2 a, C2 b) {
+  return C2{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+
+struct PairGeom {
+  double u[3], r, fc, dfc;
+  C2 a, b, da[3], db[3];
+};
+
+__device__ __forceinline__ void pair_geom(const SnapDev& D, double dx, double dy, double dz, PairGeom& g,
+                                          bool with_deriv) {
+  double r = sqrt(dx * dx + dy * dy + dz * dz);
+  double inv = 1.0 / r;
+  g.r = r;
+  g.u[0] = dx * inv; g.u[1] = dy * inv; g.u[2] = dz * inv;
+  double span = D.rcut - D.rmin0;
+  double kappa = D.rfac0 * M_PI / span;
+  double s, c;
+  sincos(kappa * (r - D.rmin0), &s, &c);
+  g.a = C2{c, -g.u[2] * s};
+  g.b = C2{g.u[1] * s, -g.u[0] * s};
+  if (D.switchflag) {
+    double sa, ca;
+    sincos(M_PI * (r - D.rmin0) / span, &sa, &ca);
+    g.fc = 0.5 * (ca + 1.0);
+    g.dfc = -0.5 * M_PI / span * sa;
+  } else {
+    g.fc = 1.0;
+    g.dfc = 0.0;
+  }
+  if (with_deriv) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double dxk = (k == 0) - g.u[0] * g.u[k], dyk = (k == 1) - g.u[1] * g.u[k];
+      double dzk = (k == 2) - g.u[2] * g.u[k];
+      g.da[k] = C2{-s * kappa * g.u[k], -(c * kappa * g.u[k] * g.u[2] + s * dzk * inv)};
+      g.db[k] = C2{c * kappa * g.u[k] * g.u[1] + s * dyk * inv, -(c * kappa * g.u[k] * g.u[0] + s * dxk * inv)};
+    }
+  }
+}
+
+// element (ma, mb) of layer Jp = J-1 from its half-row buffer (row length J);
+// rows beyond Jp/2 through the inversion symmetry.
+__device__ __forceinline__ C2 prev_elem(const C2* buf, int J, int ma, int mb) {
+  const int Jp = J - 1;
+  if (2 * mb <= Jp) return buf[mb * J + ma];
+  // mb = J/2 (J even): U[ma][mb] = (-1)^(ma+mb) conj(U[Jp-ma][Jp-mb])
+  C2 v = buf[(Jp - mb) * J + (Jp - ma)];
+  return ((ma + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+}
+
+// ------------------------------------------------------------------ kernel: Utot
+__global__ void __launch_bounds__(UI_WARPS * 32)
+k_snap_ui(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+          const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+          C2* __restrict__ utot) {
+  extern __shared__ double smem[];
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  C2* part = reinterpret_cast<C2*>(smem) + warp * nh;              // per-warp partial Utot
+  const int layer_max = (D.tj + 1) * (D.tj / 2 + 1);
+  C2* lay = reinterpret_cast<C2*>(smem) + UI_WARPS * nh + warp * 2 * layer_max;
+  int64_t atom = blockIdx.x;
+  int64_t b = atom / N;
+  int i = (int)(atom - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  for (int t = lane; t < nh; t += 32) part[t] = C2{0.0, 0.0};
+  int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  for (int s = warp; s < n; s += UI_WARPS) {
+    double dx, dy, dz;
+    pair_vec(qb, i, nb[s], box, dx, dy, dz);
+    PairGeom g;
+    pair_geom(D, dx, dy, dz, g, false);
+    C2* prev = lay;
+    C2* cur = lay + layer_max;
+    if (lane == 0) {
+      prev[0] = C2{1.0, 0.0};
+      part[0].re += g.fc;
+    }
+    __syncwarp();
+    for (int J = 1; J <= D.tj; ++J) {
+      int nel = (J + 1) * (J / 2 + 1);
+      for (int e = lane; e < nel; e += 32) {
+        int mb = e / (J + 1), ma = e - mb * (J + 1);
+        C2 v{0.0, 0.0};
+        if (ma < J) {
+          C2 p = prev_elem(prev, J, ma, mb);
+          C2 t = cmulc(g.a, p);
+          double A = c_rootpq[J - ma][J - mb];
+          v.re += A * t.re;
+          v.im += A * t.im;
+        }
+        if (ma > 0) {
+          C2 p = prev_elem(prev, J, ma - 1, mb);
+          C2 t = cmulc(g.b, p);
+          double Bc = c_rootpq[ma][J - mb];
+          v.re -= Bc * t.re;
+          v.im -= Bc * t.im;
+        }
+        cur[e] = v;
+        C2& acc = part[D.hoff[J] + e];
+        acc.re += g.fc * v.re;
+        acc.im += g.fc * v.im;
+      }
+      __syncwarp();
+      C2* tmp = prev;
+      prev = cur;
+      cur = tmp;
+    }
+  }
+  __syncthreads();
+  // fixed-order combine of the warp partials + self term on the diagonal
+  C2* out = utot + atom * nh;
+  for (int t = threadIdx.x; t < nh; t += blockDim.x) {
+    C2 s{0.0, 0.0};
+#pragma unroll
+    for (int w = 0; w < UI_WARPS; ++w) {
+      C2 v = reinterpret_cast<C2*>(smem)[w * nh + t];
+      s.re += v.re;
+      s.im += v.im;
+    }
+    // decode (J, ma, mb) of t to add wself on ma == mb
+    int J = 0;
+    while (J < D.tj && t >= D.hoff[J + 1]) ++J;
+    int e = t - D.hoff[J];
+    int mb = e / (J + 1), ma = e - mb * (J + 1);
+    if (ma == mb) s.re += D.wself;
+    out[t] = s;
+  }
+}
+
+// ------------------------------------------------------------------ kernel: Y, E_i
+__global__ void __launch_bounds__(YI_THREADS)
+k_snap_yi(SnapDev D, const C2* __restrict__ utot, C2* __restrict__ ylist, double* __restrict__ eatom,
+          double* __restrict__ bout) {
+  extern __shared__ double smem[];
+  C2* U = reinterpret_cast<C2*>(smem);                         // full matrices (nfull)
+  C2* partY = U + D.nfull;                                      // per unit
+  double* partE = reinterpret_cast<double*>(partY + D.nunits);  // per unit
+  double* partB = partE + D.nunits;                             // per unit (only if bout)
+  int64_t atom = blockIdx.x;
+  const C2* ut = utot + atom * D.nhalf;
+  // expand half rows to full matrices
+  for (int J = 0; J <= D.tj; ++J) {
+    int sz = (J + 1) * (J + 1);
+    for (int t = threadIdx.x; t < sz; t += blockDim.x) {
+      int mb = t / (J + 1), ma = t - mb * (J + 1);
+      C2 v;
+      if (2 * mb <= J) {
+        v = ut[D.hoff[J] + mb * (J + 1) + ma];
+      } else {
+        C2 w = ut[D.hoff[J] + (J - mb) * (J + 1) + (J - ma)];
+        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
+      }
+      U[D.foff[J] + t] = v;
+    }
+  }
+  __syncthreads();
+  for (int u = threadIdx.x; u < D.nunits; u += blockDim.x) {
+    SnapUnit un = D.units[u];
+    C2 ysum{0.0, 0.0};
+    double esum = 0.0, bsum = 0.0;
+    for (int k = un.i0; k < un.i1; ++k) {
+      const SnapItem it = D.items[k];
+      const double* ca = D.cg + it.cga;
+      const double* cb = D.cg + it.cgb;
+      const int x = it.x, y = it.y, J = it.J;
+      const C2* Ux = U + D.foff[x];
+      const C2* Uy = U + D.foff[y];
+      // ma2 = ma - ma1 + (x + y - J)/2 ; mb2 likewise
+      const int sh = (x + y - J) / 2;
+      C2 z{0.0, 0.0};
+      for (int jb = 0; jb < it.nb; ++jb) {
+        int mb1 = it.mb1lo + jb, mb2 = it.mb - mb1 + sh;
+        C2 s{0.0, 0.0};
+        for (int ja = 0; ja < it.na; ++ja) {
+          int ma1 = it.ma1lo + ja, ma2 = it.ma - ma1 + sh;
+          C2 t = cmul(Ux[mb1 * (x + 1) + ma1], Uy[mb2 * (y + 1) + ma2]);
+          double c = ca[ja];
+          s.re += c * t.re;
+          s.im += c * t.im;
+        }
+        double c = cb[jb];
+        z.re += c * s.re;
+        z.im += c * s.im;
+      }
+      ysum.re += it.coefY * z.re;
+      ysum.im += it.coefY * z.im;
+      if (it.bidx >= 0) {
+        C2 uJ = U[D.foff[J] + it.mb * (J + 1) + it.ma];
+        double re = uJ.re * z.re + uJ.im * z.im;  // Re(conj(U) z)
+        esum += it.coefE * re;
+        bsum += it.w * re;
+      }
+    }
+    partY[u] = ysum;
+    partE[u] = esum;
+    if (bout) partB[u] = bsum;
+  }
+  __syncthreads();
+  C2* yo = ylist + atom * D.nhalf;
+  for (int t = threadIdx.x; t < D.nhalf; t += blockDim.x) {
+    C2 s{0.0, 0.0};
+    for (int u = D.useg[t]; u < D.useg[t + 1]; ++u) {
+      s.re += partY[u].re;
+      s.im += partY[u].im;
+    }
+    yo[t] = s;
+  }
+  // atom energy: fixed-order tree over units
+  __shared__ double red[YI_THREADS];
+  double e = 0.0;
+  for (int u = threadIdx.x; u < D.nunits; u += blockDim.x) e += partE[u];
+  red[threadIdx.x] = e;
+  __syncthreads();
+  for (int w = YI_THREADS / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) eatom[atom] = D.beta0 + red[0];
+}
+
+// per-atom bispectrum (debug / parity path; per item, deterministic)
+__global__ void k_snap_bispectrum(SnapDev D, const C2* __restrict__ utot, double* __restrict__ bout,
+                                  int nitems) {
+  extern __shared__ double smem[];
+  C2* U = reinterpret_cast<C2*>(smem);
+  int64_t atom = blockIdx.x;
+  const C2* ut = utot + atom * D.nhalf;
+  for (int J = 0; J <= D.tj; ++J) {
+    int sz = (J + 1) * (J + 1);
+    for (int t = threadIdx.x; t < sz; t += blockDim.x) {
+      int mb = t / (J + 1), ma = t - mb * (J + 1);
+      C2 v;
+      if (2 * mb <= J) {
+        v = ut[D.hoff[J] + mb * (J + 1) + ma];
+      } else {
+        C2 w = ut[D.hoff[J] + (J - mb) * (J + 1) + (J - ma)];
+        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
+      }
+      U[D.foff[J] + t] = v;
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < D.nB; b += blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < nitems; ++k) {
+      const SnapItem it = D.items[k];
+      if (it.bidx != b) continue;
+      const double* ca = D.cg + it.cga;
+      const double* cb = D.cg + it.cgb;
+      const int x = it.x, y = it.y, J = it.J, sh = (x + y - J) / 2;
+      C2 z{0.0, 0.0};
+      for (int jb = 0; jb < it.nb; ++jb) {
+        int mb1 = it.mb1lo + jb, mb2 = it.mb - mb1 + sh;
+        C2 s{0.0, 0.0};
+        for (int ja = 0; ja < it.na; ++ja) {
+          int ma1 = it.ma1lo + ja, ma2 = it.ma - ma1 + sh;
+          C2 t = cmul(U[D.foff[x] + mb1 * (x + 1) + ma1], U[D.foff[y] + mb2 * (y + 1) + ma2]);
+          s.re += ca[ja] * t.re;
+          s.im += ca[ja] * t.im;
+        }
+        z.re += cb[jb] * s.re;
+        z.im += cb[jb] * s.im;
+      }
+      C2 uJ = U[D.foff[J] + it.mb * (J + 1) + it.ma];
+      acc += it.w * (uJ.re * z.re + uJ.im * z.im);
+    }
+    bout[atom * D.nB + b] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ kernel: dE_i/dr_ik
+__global__ void __launch_bounds__(DE_WARPS * 32)
+k_snap_deidrj(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+              const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+              const C2* __restrict__ ylist, double* __restrict__ dedr) {
+  extern __shared__ double smem[];
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  C2* Y = reinterpret_cast<C2*>(smem);
+  const int layer_max = (D.tj + 1) * (D.tj / 2 + 1);
+  // per warp: 2 layers x (U, dU0, dU1, dU2)
+  C2* lay = Y + nh + warp * 2 * 4 * layer_max;
+  int64_t atom = blockIdx.x;
+  int64_t b = atom / N;
+  int i = (int)(atom - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  for (int t = threadIdx.x; t < nh; t += blockDim.x) Y[t] = ylist[atom * nh + t];
+  __syncthreads();
+  int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  for (int s = warp; s < n; s += DE_WARPS) {
+    double dx, dy, dz;
+    pair_vec(qb, i, nb[s], box, dx, dy, dz);
+    PairGeom g;
+    pair_geom(D, dx, dy, dz, g, true);
+    C2* prev = lay;
+    C2* cur = lay + 4 * layer_max;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    if (lane == 0) {
+      prev[0] = C2{1.0, 0.0};
+      prev[layer_max] = prev[2 * layer_max] = prev[3 * layer_max] = C2{0.0, 0.0};
+      // J = 0: U = 1, dU = 0, weight 1
+      double y0 = Y[0].re;
+      acc0 = g.dfc * g.u[0] * y0;
+      acc1 = g.dfc * g.u[1] * y0;
+      acc2 = g.dfc * g.u[2] * y0;
+    }
+    __syncwarp();
+    for (int J = 1; J <= D.tj; ++J) {
+      int nel = (J + 1) * (J / 2 + 1);
+      for (int e = lane; e < nel; e += 32) {
+        int mb = e / (J + 1), ma = e - mb * (J + 1);
+        C2 v{0.0, 0.0}, dv0{0.0, 0.0}, dv1{0.0, 0.0}, dv2{0.0, 0.0};
+        if (ma < J) {
+          double A = c_rootpq[J - ma][J - mb];
+          C2 p = prev_elem(prev, J, ma, mb);
+          C2 p0 = prev_elem(prev + layer_max, J, ma, mb);
+          C2 p1 = prev_elem(prev + 2 * layer_max, J, ma, mb);
+          C2 p2 = prev_elem(prev + 3 * layer_max, J, ma, mb);
+          C2 t = cmulc(g.a, p);
+          v.re += A * t.re; v.im += A * t.im;
+          C2 t0 = cmulc(g.da[0], p), s0 = cmulc(g.a, p0);
+          C2 t1 = cmulc(g.da[1], p), s1 = cmulc(g.a, p1);
+          C2 t2 = cmulc(g.da[2], p), s2 = cmulc(g.a, p2);
+          dv0.re += A * (t0.re + s0.re); dv0.im += A * (t0.im + s0.im);
+          dv1.re += A * (t1.re + s1.re); dv1.im += A * (t1.im + s1.im);
+          dv2.re += A * (t2.re + s2.re); dv2.im += A * (t2.im + s2.im);
+        }
+        if (ma > 0) {
+          double Bc = c_rootpq[ma][J - mb];
+          C2 p = prev_elem(prev, J, ma - 1, mb);
+          C2 p0 = prev_elem(prev + layer_max, J, ma - 1, mb);
+          C2 p1 = prev_elem(prev + 2 * layer_max, J, ma - 1, mb);
+          C2 p2 = prev_elem(prev + 3 * layer_max, J, ma - 1, mb);
+          C2 t = cmulc(g.b, p);
+          v.re -= Bc * t.re; v.im -= Bc * t.im;
+          C2 t0 = cmulc(g.db[0], p), s0 = cmulc(g.b, p0);
+          C2 t1 = cmulc(g.db[1], p), s1 = cmulc(g.b, p1);
+          C2 t2 = cmulc(g.db[2], p), s2 = cmulc(g.b, p2);
+          dv0.re -= Bc * (t0.re + s0.re); dv0.im -= Bc * (t0.im + s0.im);
+          dv1.re -= Bc * (t1.re + s1.re); dv1.im -= Bc * (t1.im + s1.im);
+          dv2.re -= Bc * (t2.re + s2.re); dv2.im -= Bc * (t2.im + s2.im);
+        }
+        cur[e] = v;
+        cur[layer_max + e] = dv0;
+        cur[2 * layer_max + e] = dv1;
+        cur[3 * layer_max + e] = dv2;
+        // weight of a half-row element in the full-matrix sum
+        double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+        C2 y = Y[D.hoff[J] + e];
+        double yu = v.re * y.re + v.im * y.im;
+        acc0 += w * (g.fc * (dv0.re * y.re + dv0.im * y.im) + g.dfc * g.u[0] * yu);
+        acc1 += w * (g.fc * (dv1.re * y.re + dv1.im * y.im) + g.dfc * g.u[1] * yu);
+        acc2 += w * (g.fc * (dv2.re * y.re + dv2.im * y.im) + g.dfc * g.u[2] * yu);
+      }
+      __syncwarp();
+      C2* tmp = prev;
+      prev = cur;
+      cur = tmp;
+    }
+    // fixed-order warp reduction
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      acc0 += __shfl_down_sync(0xffffffffu, acc0, off);
+      acc1 += __shfl_down_sync(0xffffffffu, acc1, off);
+      acc2 += __shfl_down_sync(0xffffffffu, acc2, off);
+    }
+    if (lane == 0) {
+      double* o = dedr + (atom * maxn + s) * 3;
+      o[0] = acc0;
+      o[1] = acc1;
+      o[2] = acc2;
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ kernel: gather
+__global__ void k_snap_gather(int64_t natoms, int N, Box box, const double* __restrict__ q,
+                              const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
+                              int maxn, const double* __restrict__ dedr, double* __restrict__ grad,
+                              double* __restrict__ vatom) {
+  int64_t atom = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (atom >= natoms) return;
+  int64_t b = atom / N;
+  int a = (int)(atom - b * N);
+  int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+  double v[6] = {0, 0, 0, 0, 0, 0};
+  const double* qb = q + b * (int64_t)N * 3;
+  for (int s = 0; s < n; ++s) {
+    int k = nb[s];
+    int64_t katom = b * N + k;
+    const int32_t* kl = nbr + katom * maxn;
+    int lo = 0, hi = cnt[katom] - 1, sk = -1;
+    while (lo <= hi) {  // lists are sorted ascending
+      int mid = (lo + hi) >> 1;
+      int val = kl[mid];
+      if (val == a) { sk = mid; break; }
+      if (val < a) lo = mid + 1; else hi = mid - 1;
+    }
+    const double* ga = dedr + (atom * maxn + s) * 3;
+    gx -= ga[0];
+    gy -= ga[1];
+    gz -= ga[2];
+    if (sk >= 0) {
+      const double* gk = dedr + (katom * maxn + sk) * 3;
+      gx += gk[0];
+      gy += gk[1];
+      gz += gk[2];
+    }
+    if (vatom) {
+      double dx, dy, dz;
+      pair_vec(qb, a, k, box, dx, dy, dz);
+      v[0] -= ga[0] * dx;
+      v[1] -= ga[1] * dy;
+      v[2] -= ga[2] * dz;
+      v[3] -= 0.5 * (ga[0] * dy + ga[1] * dx);
+      v[4] -= 0.5 * (ga[0] * dz + ga[2] * dx);
+      v[5] -= 0.5 * (ga[1] * dz + ga[2] * dy);
+    }
+  }
+  if (grad) {
+    grad[3 * atom] = gx;
+    grad[3 * atom + 1] = gy;
+    grad[3 * atom + 2] = gz;
+  }
+  if (vatom)
+    for (int c = 0; c < 6; ++c) vatom[6 * atom + c] = v[c];
+}
+
+__global__ void k_sys_sum(int64_t B, int N, int width, const double* __restrict__ per_atom,
+                          double* __restrict__ out) {
+  __shared__ double sh[256];
+  int64_t b = blockIdx.x;
+  for (int c = 0; c < width; ++c) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s += per_atom[(b * N + i) * width + c];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[b * width + c] = sh[0];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ host driver
+struct SnapBuffers {
+  C2* utot;
+  C2* y;
+  double* eatom;
+  double* dedr;
+  double* vatom;
+};
+
+static size_t ui_smem(const SnapDev& D) {
+  int layer_max = (D.tj + 1) * (D.tj / 2 + 1);
+  return sizeof(C2) * (UI_WARPS * D.nhalf + UI_WARPS * 2 * layer_max);
+}
+static size_t yi_smem(const SnapDev& D, bool with_b) {
+  return sizeof(C2) * (D.nfull + D.nunits) + sizeof(double) * D.nunits * (with_b ? 2 : 1);
+}
+static size_t de_smem(const SnapDev& D) {
+  int layer_max = (D.tj + 1) * (D.tj / 2 + 1);
+  return sizeof(C2) * (D.nhalf + DE_WARPS * 2 * 4 * layer_max);
+}
+
+static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf, NeighList& nl) {
+  pl_ctx* ctx = pot->ctx;
+  SnapIndex* S = pot->snap;
+  SnapDev D = snap_dev(pot);
+  int N = pot->n_atoms;
+  int64_t na = B * N;
+  if (na > 0x7fffffff) return fail(PL_EARG, "too many atoms in one batch");
+  PL_TRY(build_neighbours(pot, B, q, pot->rcut, SNAP_MAXN, &nl));
+  size_t bytes = sizeof(C2) * 2 * na * S->nhalf + sizeof(double) * na * (1 + 3 * SNAP_MAXN + 6);
+  PL_TRY(pot->work[2].reserve(bytes));
+  buf.utot = (C2*)pot->work[2].ptr;
+  buf.y = buf.utot + na * S->nhalf;
+  buf.eatom = (double*)(buf.y + na * S->nhalf);
+  buf.dedr = buf.eatom + na;
+  buf.vatom = buf.dedr + na * 3 * SNAP_MAXN;
+  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  size_t s1 = ui_smem(D), s2 = yi_smem(D, false), s3 = de_smem(D);
+  static thread_local bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_snap_ui, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_yi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_bispectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_done = true;
+  }
+  k_snap_ui<<<(unsigned)na, UI_WARPS * 32, s1, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
+                                                               buf.utot);
+  PL_CHECK_LAUNCH();
+  k_snap_yi<<<(unsigned)na, YI_THREADS, s2, ctx->stream>>>(D, buf.utot, buf.y, buf.eatom, nullptr);
+  PL_CHECK_LAUNCH();
+  k_snap_deidrj<<<(unsigned)na, DE_WARPS * 32, s3, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
+                                                                   nl.maxn, buf.y, buf.dedr);
+  PL_CHECK_LAUNCH();
+  return PL_OK;
+}
+
+int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double* grad, double* virial) {
+  pl_ctx* ctx = pot->ctx;
+  int N = pot->n_atoms;
+  int64_t na = B * N;
+  SnapBuffers buf;
+  NeighList nl;
+  PL_TRY(snap_stages(pot, B, q, buf, nl));
+  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  k_snap_gather<<<(unsigned)((na + 127) / 128), 128, 0, ctx->stream>>>(
+      na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr);
+  PL_CHECK_LAUNCH();
+  if (energy) {
+    k_sys_sum<<<(unsigned)B, 256, 0, ctx->stream>>>(B, N, 1, buf.eatom, energy);
+    PL_CHECK_LAUNCH();
+  }
+  if (virial) {
+    k_sys_sum<<<(unsigned)B, 256, 0, ctx->stream>>>(B, N, 6, buf.vatom, virial);
+    PL_CHECK_LAUNCH();
+  }
+  return PL_OK;
+}
+
+int snap_bispectrum(pl_pot* pot, int64_t B, const double* q, double* out) {
+  SnapBuffers buf;
+  NeighList nl;
+  PL_TRY(snap_stages(pot, B, q, buf, nl));
+  SnapDev D = snap_dev(pot);
+  size_t smem = sizeof(C2) * D.nfull;
+  k_snap_bispectrum<<<(unsigned)(B * pot->n_atoms), 128, smem, pot->ctx->stream>>>(D, buf.utot, out,
+                                                                                  pot->snap->nitems);
+  PL_CHECK_LAUNCH();
+  return neigh_check(pot);
+}
+
+double snap_flops(const pl_pot* pot, double pairs, double atoms) {
+  const SnapIndex* S = pot->snap;
+  return pairs * (S->flops_ui_pair + S->flops_de_pair) + atoms * S->flops_yi_atom;
+}
+
+}  // namespace pl
+
+extern "C" int pl_snap_bispectrum(pl_ctx* ctx, pl_pot* pot, int64_t B, const double* d_q, double* d_out) {
+  if (!ctx || !pot || !d_q || !d_out) return pl::fail(PL_EARG, "NULL argument");
+  if (pot->kind != POT_SNAP) return pl::fail(PL_EARG, "not a SNAP potential");
+  return pl::snap_bispectrum(pot, B, d_q, d_out);
+}
+
+extern "C" int pl_snap_info(pl_pot* pot, int32_t* h_counts, double* h_flops) {
+  // h_counts: {nhalf, nfull, nB, nitems, nunits}; h_flops: {ui/pair, yi/atom, deidrj/pair}
+  if (!pot || pot->kind != POT_SNAP || !h_counts || !h_flops) return pl::fail(PL_EARG, "bad argument");
+  const pl::SnapIndex* S = pot->snap;
+  h_counts[0] = S->nhalf; h_counts[1] = S->nfull; h_counts[2] = S->nB; h_counts[3] = S->nitems;
+  h_counts[4] = S->nunits;
+  h_flops[0] = S->flops_ui_pair; h_flops[1] = S->flops_yi_atom; h_flops[2] = S->flops_de_pair;
+  return PL_OK;
 }

@@ -102,3 +102,95 @@ def test_eam_window_vs_oracle(pl):
                                    0, mass=mass, noise=noise)
     assert np.abs(out.q - q1).max() < 1e-8
     assert np.abs(out.p - p1).max() < 1e-8 * np.abs(p1).max()
+
+
+# ------------------------------------------------------------------ SNAP
+def _snap_bispectrum(pl, pot, Q):
+    import torch
+    from paper_2212_10508_b200 import _lib
+    ctx = _lib.context()
+    B, d = Q.shape
+    n = d // 3
+    nb = pot.beta.shape[0] - 1
+    q = torch.from_numpy(Q).cuda()
+    out = torch.zeros((B, n, nb), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.load().pl_snap_bispectrum(ctx.handle, pot.handle(ctx), B, _lib.ptr(q), _lib.ptr(out)))
+    return out.cpu().numpy()
+
+
+def test_snap_bispectrum_vs_oracle(pl):
+    from oracle import native
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(4, 3)
+    n = Q.shape[1] // 3
+    pot = W.make_snap(n, box)
+    Bd = _snap_bispectrum(pl, pot, Q)
+    for b in range(Q.shape[0]):
+        _, _, _, Bo = native.snap(Q[b], box, pot, want_bispectrum=True)
+        np.testing.assert_allclose(Bd[b], Bo, rtol=1e-10, atol=1e-10 * np.abs(Bo).max())
+
+
+@pytest.mark.parametrize("ncell,count", [(4, 6), (8, 1)])
+def test_snap_vs_oracle(pl, ncell, count):
+    from oracle import native
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(ncell, count)
+    n = Q.shape[1] // 3
+    pot = W.make_snap(n, box)
+    E, G, V = (x.cpu().numpy() for x in pot.evaluate(Q, True, True, True))
+    for b in range(Q.shape[0]):
+        e, g, v = native.snap(Q[b], box, pot)
+        assert E[b] == pytest.approx(e, rel=1e-10)
+        np.testing.assert_allclose(G[b], g, rtol=1e-10, atol=1e-10 * np.abs(g).max())
+        np.testing.assert_allclose(V[b], v, rtol=1e-10, atol=1e-10 * np.abs(v).max())
+
+
+def test_snap_invariances_on_device(pl):
+    """Sum F = 0, rotation invariance of E (cluster in a large box), FD gradient."""
+    from paper_2212_10508_b200.potentials import SNAP
+    from paper_2212_10508_b200 import tungsten as W
+    rs = np.random.default_rng(7)
+    X = rs.normal(size=(14, 3)) * 1.7
+    big = (60.0, 60.0, 60.0)
+    pot = SNAP(n_atoms=14, box=big, beta=W.snap_beta(11))
+    th, ax = 1.1, np.array([3.0, -1.0, 2.0]) / np.sqrt(14.0)
+    K = np.array([[0, -ax[2], ax[1]], [ax[2], 0, -ax[0]], [-ax[1], ax[0], 0]])
+    R = np.eye(3) + np.sin(th) * K + (1 - np.cos(th)) * K @ K
+    qa, qb = (X + 30).ravel(), (X @ R.T + 30).ravel()
+    E, G, _ = pot.evaluate(np.stack([qa, qb]), True, True)
+    E, G = E.cpu().numpy(), G.cpu().numpy()
+    assert E[0] == pytest.approx(E[1], rel=1e-12)
+    np.testing.assert_allclose(G[1].reshape(-1, 3), G[0].reshape(-1, 3) @ R.T, atol=1e-10)
+    assert np.abs(G[0].reshape(-1, 3).sum(axis=0)).max() < 1e-10
+    assert pl.gradient_check(pot, qa, h=1e-5) < 1e-6
+
+
+def test_snap_deterministic_rerun(pl):
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(4, 8)
+    pot = W.make_snap(Q.shape[1] // 3, box)
+    a = pot.evaluate(Q)[1].cpu().numpy()
+    b = pot.evaluate(Q)[1].cpu().numpy()
+    assert a.tobytes() == b.tobytes()
+
+
+def test_snap_window_vs_oracle(pl):
+    """20 BBK substeps of SNAP W+SIA at 1000 K: device vs oracle integrator + C SNAP."""
+    from oracle import integrator as oint, native, rng as orng
+    from paper_2212_10508_b200 import tungsten as W
+    q0, box = W.bcc_sia(4)
+    n = q0.shape[0] // 3
+    pot = W.make_snap(n, box)
+    L = 20
+    mass = np.full(3 * n, W.MASS_W)
+    params = pl.LangevinParams(1.0, W.KB * 1000.0, 0.001, L, mass=mass)
+    sched = pl.TemperatureSchedule.robust(L)
+    p0 = W.maxwell_boltzmann(n, 1000.0, 11)
+    seed = pl.derive_seed(11, 2)
+    noise = orng.gaussian_stream(seed, (L + 1) * 3 * n)
+    out = pl.propagate_windows([pl.PhaseState(q=q0, p=p0)], pot, params, sched, [seed],
+                               noise=noise[None, :])[0]
+    q1, p1 = oint.propagate_window(q0, p0, native.snap_fn(pot), 1.0, W.KB * 1000.0, 0.001, L,
+                                   sched.coefficients, 0, mass=mass, noise=noise)
+    assert np.abs(out.q - q1).max() < 1e-8
+    assert np.abs(out.p - p1).max() < 1e-8 * np.abs(p1).max()
