@@ -148,6 +148,16 @@ int pl_sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t 
 /* d_out[i] = d_a[i] - d_b[i]  (jump = f.q - c.q, parareal.py:280). */
 int pl_sub(pl_ctx* ctx, int64_t n, const double* d_a, const double* d_b, double* d_out);
 
+/* ---- measurement --------------------------------------------------------- */
+/* Record CUDA events around every kernel stage launched by this host thread
+ * until pl_prof_end, which synchronises and returns per-stage summed kernel
+ * milliseconds and launch counts (stages: 0 neighbour lists, 1 SNAP U,
+ * 2 SNAP Z/Y, 3 SNAP dE/dr, 4 SNAP gather, 5 EAM, 6 integrator). */
+int pl_prof_begin(pl_ctx* ctx);
+int pl_prof_end(pl_ctx* ctx, int n_stages, double* h_ms, int64_t* h_n);
+/* Dense FP64 FMA throughput of the device, measured (TFLOP/s). */
+int pl_fp64_peak(pl_ctx* ctx, double* h_tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -144,9 +144,11 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
   double rc2 = rcut * rcut;
   PL_CUDA(cudaMemsetAsync(out->overflow, 0, sizeof(int), pot->ctx->stream));
   dim3 grid((N + NB_THREADS - 1) / NB_THREADS, (unsigned)B);
+  prof_mark(pot->ctx->stream, ST_NEIGH, true);
   k_neigh_brute<<<grid, NB_THREADS, 0, pot->ctx->stream>>>(B, N, box, rc2, maxn, q, out->nbr, out->cnt,
                                                            out->overflow);
   PL_CHECK_LAUNCH();
+  prof_mark(pot->ctx->stream, ST_NEIGH, false);
   return PL_OK;
 }
 
@@ -197,11 +199,13 @@ int compute_eam(pl_pot* pot, int64_t B, const double* q, double* energy, double*
   Table trho{pot->d_rho, pot->n_r, pot->dr}, tphi{pot->d_phi, pot->n_r, pot->dr},
       tF{pot->d_F, pot->n_rho, pot->drho};
   unsigned g = (unsigned)((na + 127) / 128);
+  prof_mark(ctx->stream, ST_EAM, true);
   k_eam_density<<<g, 128, 0, ctx->stream>>>(B, N, box, trho, tF, q, nl.nbr, nl.cnt, nl.maxn, Fp, Fe);
   PL_CHECK_LAUNCH();
   k_eam_force<<<g, 128, 0, ctx->stream>>>(B, N, box, trho, tphi, q, nl.nbr, nl.cnt, nl.maxn, Fp, Fe,
                                           grad, energy ? ea : nullptr, virial ? va : nullptr);
   PL_CHECK_LAUNCH();
+  prof_mark(ctx->stream, ST_EAM, false);
   if (energy) {
     k_sys_reduce<<<(unsigned)B, 256, 0, ctx->stream>>>(B, N, 1, ea, energy);
     PL_CHECK_LAUNCH();

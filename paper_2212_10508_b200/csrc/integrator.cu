@@ -264,11 +264,15 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
   PL_TRY(compute(pot, W, d, q1, nullptr, grad, nullptr));
   unsigned g = grid_for((int64_t)nd);
   for (int s = 1; s <= L; ++s) {
+    prof_mark(st, ST_INT, true);
     k_open<<<g, 256, 0, st>>>(W, d, s, s == 1, K, amp, noise, mass, grad, p1, ph, q1);
     PL_CHECK_LAUNCH();
+    prof_mark(st, ST_INT, false);
     PL_TRY(compute(pot, W, d, q1, nullptr, grad, nullptr));
+    prof_mark(st, ST_INT, true);
     k_close<<<g, 256, 0, st>>>(W, d, s, K, amp, noise, mass, grad, ph, q1, p1, blow);
     PL_CHECK_LAUNCH();
+    prof_mark(st, ST_INT, false);
   }
   if (pot->kind == POT_LJ) return lj_check(pot);
   return neigh_check(pot);

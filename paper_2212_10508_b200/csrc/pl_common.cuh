@@ -126,5 +126,9 @@ int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double
                  double* virial);
 int snap_prepare(pl_pot* pot, const double* h_beta);
 int neigh_check(pl_pot* pot);
+// live stage timing (prof.cu): stages 0 neigh, 1 snap_ui, 2 snap_yi, 3 snap_deidrj,
+// 4 snap_gather, 5 eam, 6 integrator
+enum ProfStage { ST_NEIGH = 0, ST_UI = 1, ST_YI = 2, ST_DE = 3, ST_GATHER = 4, ST_EAM = 5, ST_INT = 6 };
+void prof_mark(cudaStream_t st, int stage, bool begin);
 void snap_release(pl_pot* pot);
 }  // namespace pl

@@ -798,14 +798,20 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_bispectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
+  prof_mark(ctx->stream, ST_UI, true);
   k_snap_ui<<<(unsigned)na, UI_WARPS * 32, s1, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
                                                                buf.utot);
   PL_CHECK_LAUNCH();
+  prof_mark(ctx->stream, ST_UI, false);
+  prof_mark(ctx->stream, ST_YI, true);
   k_snap_yi<<<(unsigned)na, YI_THREADS, s2, ctx->stream>>>(D, buf.utot, buf.y, buf.eatom, nullptr);
   PL_CHECK_LAUNCH();
+  prof_mark(ctx->stream, ST_YI, false);
+  prof_mark(ctx->stream, ST_DE, true);
   k_snap_deidrj<<<(unsigned)na, DE_WARPS * 32, s3, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
                                                                    nl.maxn, buf.y, buf.dedr);
   PL_CHECK_LAUNCH();
+  prof_mark(ctx->stream, ST_DE, false);
   return PL_OK;
 }
 
@@ -817,6 +823,7 @@ int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double
   NeighList nl;
   PL_TRY(snap_stages(pot, B, q, buf, nl));
   Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  prof_mark(ctx->stream, ST_GATHER, true);
   k_snap_gather<<<(unsigned)((na + 127) / 128), 128, 0, ctx->stream>>>(
       na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr);
   PL_CHECK_LAUNCH();
@@ -828,6 +835,7 @@ int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double
     k_sys_sum<<<(unsigned)B, 256, 0, ctx->stream>>>(B, N, 6, buf.vatom, virial);
     PL_CHECK_LAUNCH();
   }
+  prof_mark(ctx->stream, ST_GATHER, false);
   return PL_OK;
 }
 
