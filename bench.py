@@ -109,7 +109,7 @@ def build_inputs(cfg_name, rank, world):
     rs = np.random.default_rng(1000 + rank)
     # slice start states: thermalised-looking lattice (0.05 A jitter) + MB momenta
     Q = q0[None, :] + 0.05 * rs.normal(size=(slices, q0.shape[0]))
-    P = np.stack([W.maxwell_boltzmann(n, T, 97 + rank * slices + s) for s in range(slices)])
+    P = math.sqrt(W.MASS_W * W.KB * T) * rs.normal(size=(slices, q0.shape[0]))  # Maxwell-Boltzmann
     seeds = [int(x) for x in __import__("paper_2212_10508_b200").derive_seeds(11 + rank, slices)]
     return dict(q0=q0, box=box, n=n, Q=Q, P=P, seeds=seeds, L=L, T=T, slices=slices, cells=cells)
 
