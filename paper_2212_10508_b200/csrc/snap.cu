@@ -26,6 +26,7 @@
 //                  virials reduced per system in a fixed order.
 // Everything is deterministic (no floating-point atomics): reruns are bitwise
 // identical, as parareal's convergence test requires (SURVEY.md finding 4).
+#include <algorithm>
 #include <cmath>
 #include <map>
 #include <tuple>
@@ -41,6 +42,8 @@ constexpr int SNAP_JMAX = 14;
 constexpr int UI_WARPS = 4;
 constexpr int DE_WARPS = 4;
 constexpr int YI_THREADS = 256;
+constexpr int YI_ATOMS = 32;                 // lanes = atoms in k_snap_yi
+constexpr int YI_WARPS = YI_THREADS / 32;
 
 struct SnapItem {      // one half-row element of one Z^{xy}_J
   int16_t x, y, J, ma, mb;
@@ -62,6 +65,9 @@ struct SnapIndex {
   SnapItem* d_items = nullptr;
   SnapUnit* d_units = nullptr;
   int32_t* d_useg = nullptr;   // units of target h: [useg[h], useg[h+1])
+  int32_t* d_tseg = nullptr;   // items of target h: [tseg[h], tseg[h+1])
+  int32_t* d_wtarget = nullptr;  // targets owned by warp w of k_snap_yi: [wseg[w], wseg[w+1])
+  int32_t* d_wseg = nullptr;
   double* d_cg = nullptr;
   double beta0 = 0.0;
   double flops_ui_pair = 0, flops_yi_atom = 0, flops_de_pair = 0;
@@ -73,12 +79,18 @@ struct SnapDev {  // POD view passed to kernels
   const SnapItem* items;
   const SnapUnit* units;
   const int32_t* useg;
+  const int32_t* tseg;
+  const int32_t* wtarget;
+  const int32_t* wseg;
   const double* cg;
   double beta0, rcut, rfac0, rmin0, wself;
   int switchflag;
 };
 
 __constant__ double c_rootpq[SNAP_JMAX + 2][SNAP_JMAX + 2];  // sqrt(p/q)
+// layer offsets depend on J only (not on twojmax): half rows and full matrices
+__constant__ int c_hoff[SNAP_JMAX + 2];
+__constant__ int c_foff[SNAP_JMAX + 2];
 
 // ------------------------------------------------------------------ host setup
 static double fact(int n) {
@@ -231,6 +243,38 @@ int snap_prepare(pl_pot* pot, const double* beta) {
       units.push_back({t, u0, (int32_t)items.size()});
   }
   useg[S->nhalf] = (int32_t)units.size();
+  // items of each target are contiguous in `items`
+  std::vector<int32_t> tseg(S->nhalf + 1, 0);
+  {
+    int pos = 0;
+    for (int t = 0; t < S->nhalf; ++t) {
+      tseg[t] = pos;
+      pos += (int)per_target[t].size();
+    }
+    tseg[S->nhalf] = pos;
+  }
+  // targets -> warps of k_snap_yi by longest-processing-time greedy on cost
+  std::vector<std::pair<double, int>> tc;
+  for (int t = 0; t < S->nhalf; ++t) {
+    double c = 0.0;
+    for (auto& it : per_target[t]) c += (double)it.na * it.nb + 2.0 * it.nb + 4.0;
+    tc.push_back({c, t});
+  }
+  std::sort(tc.begin(), tc.end(), [](auto& a, auto& b) { return a.first > b.first; });
+  std::vector<std::vector<int32_t>> wt(YI_WARPS);
+  std::vector<double> wl(YI_WARPS, 0.0);
+  for (auto& c : tc) {
+    int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
+    wt[w].push_back(c.second);
+    wl[w] += c.first;
+  }
+  std::vector<int32_t> wtarget, wseg(YI_WARPS + 1, 0);
+  for (int w = 0; w < YI_WARPS; ++w) {
+    std::sort(wt[w].begin(), wt[w].end());
+    wseg[w] = (int32_t)wtarget.size();
+    wtarget.insert(wtarget.end(), wt[w].begin(), wt[w].end());
+  }
+  wseg[YI_WARPS] = (int32_t)wtarget.size();
   S->nitems = (int)items.size();
   S->nunits = (int)units.size();
   // algorithmic flop counts (used for the roofline numerator)
@@ -248,7 +292,10 @@ int snap_prepare(pl_pot* pot, const double* beta) {
   cudaError_t e2 = cudaMalloc(&S->d_units, sizeof(SnapUnit) * units.size());
   cudaError_t e3 = cudaMalloc(&S->d_useg, sizeof(int32_t) * useg.size());
   cudaError_t e4 = cudaMalloc(&S->d_cg, sizeof(double) * std::max<size_t>(pool.size(), 1));
-  if (e1 || e2 || e3 || e4) {
+  cudaError_t e5 = cudaMalloc(&S->d_tseg, sizeof(int32_t) * tseg.size());
+  cudaError_t e6 = cudaMalloc(&S->d_wtarget, sizeof(int32_t) * wtarget.size());
+  cudaError_t e7 = cudaMalloc(&S->d_wseg, sizeof(int32_t) * wseg.size());
+  if (e1 || e2 || e3 || e4 || e5 || e6 || e7) {
     delete S;
     return fail(PL_ECUDA, "cudaMalloc SNAP index");
   }
@@ -256,10 +303,22 @@ int snap_prepare(pl_pot* pot, const double* beta) {
   cudaMemcpy(S->d_units, units.data(), sizeof(SnapUnit) * units.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(S->d_useg, useg.data(), sizeof(int32_t) * useg.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(S->d_cg, pool.data(), sizeof(double) * pool.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(S->d_tseg, tseg.data(), sizeof(int32_t) * tseg.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(S->d_wtarget, wtarget.data(), sizeof(int32_t) * wtarget.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(S->d_wseg, wseg.data(), sizeof(int32_t) * wseg.size(), cudaMemcpyHostToDevice);
   double rp[SNAP_JMAX + 2][SNAP_JMAX + 2];
   for (int p = 0; p < SNAP_JMAX + 2; ++p)
     for (int q = 0; q < SNAP_JMAX + 2; ++q) rp[p][q] = q ? std::sqrt((double)p / (double)q) : 0.0;
   PL_CUDA(cudaMemcpyToSymbol(c_rootpq, rp, sizeof(rp)));
+  int ho[SNAP_JMAX + 2], fo[SNAP_JMAX + 2];
+  for (int J = 0, hh = 0, ff = 0; J < SNAP_JMAX + 2; ++J) {
+    ho[J] = hh;
+    fo[J] = ff;
+    hh += (J + 1) * (J / 2 + 1);
+    ff += (J + 1) * (J + 1);
+  }
+  PL_CUDA(cudaMemcpyToSymbol(c_hoff, ho, sizeof(ho)));
+  PL_CUDA(cudaMemcpyToSymbol(c_foff, fo, sizeof(fo)));
   pot->snap = S;
   // one system: N atoms x ~26 pairs (perfect BCC at rcut 4.73) is only an
   // estimate for reporting; the bench counts real pairs per launch.
@@ -274,6 +333,9 @@ void snap_release(pl_pot* pot) {
   cudaFree(S->d_units);
   cudaFree(S->d_useg);
   cudaFree(S->d_cg);
+  cudaFree(S->d_tseg);
+  cudaFree(S->d_wtarget);
+  cudaFree(S->d_wseg);
   delete S;
   pot->snap = nullptr;
 }
@@ -287,6 +349,7 @@ static SnapDev snap_dev(const pl_pot* pot) {
     D.foff[J] = J <= S->tj + 1 ? S->foff[J] : 0;
   }
   D.items = S->d_items; D.units = S->d_units; D.useg = S->d_useg; D.cg = S->d_cg;
+  D.tseg = S->d_tseg; D.wtarget = S->d_wtarget; D.wseg = S->d_wseg;
   D.beta0 = S->beta0; D.rcut = pot->rcut; D.rfac0 = pot->rfac0; D.rmin0 = pot->rmin0;
   D.wself = pot->wself; D.switchflag = pot->switchflag;
   return D;
@@ -400,7 +463,7 @@ k_snap_ui(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ 
           v.im -= Bc * t.im;
         }
         cur[e] = v;
-        C2& acc = part[D.hoff[J] + e];
+        C2& acc = part[c_hoff[J] + e];
         acc.re += g.fc * v.re;
         acc.im += g.fc * v.im;
       }
@@ -423,8 +486,8 @@ k_snap_ui(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ 
     }
     // decode (J, ma, mb) of t to add wself on ma == mb
     int J = 0;
-    while (J < D.tj && t >= D.hoff[J + 1]) ++J;
-    int e = t - D.hoff[J];
+    while (J < D.tj && t >= c_hoff[J + 1]) ++J;
+    int e = t - c_hoff[J];
     int mb = e / (J + 1), ma = e - mb * (J + 1);
     if (ma == mb) s.re += D.wself;
     out[t] = s;
@@ -432,94 +495,74 @@ k_snap_ui(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ 
 }
 
 // ------------------------------------------------------------------ kernel: Y, E_i
+// lanes = atoms: the 32 lanes of a warp walk the same Z items for 32 atoms,
+// so control flow and CG loads are warp-uniform and the [element][atom]
+// shared-memory layout is bank-conflict free.  Warps own disjoint sets of Y
+// targets (host LPT schedule), so every Y element is summed by one lane in a
+// fixed item order (deterministic, no atomics).
+__device__ __forceinline__ C2 half_get(const C2* Us, int x, int ma, int mb, int lane) {
+  // Utot^x[ma][mb] from half-row storage [nhalf][YI_ATOMS]
+  if (2 * mb <= x) return Us[(c_hoff[x] + mb * (x + 1) + ma) * YI_ATOMS + lane];
+  C2 v = Us[(c_hoff[x] + (x - mb) * (x + 1) + (x - ma)) * YI_ATOMS + lane];
+  return ((ma + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+}
+
 __global__ void __launch_bounds__(YI_THREADS)
-k_snap_yi(SnapDev D, const C2* __restrict__ utot, C2* __restrict__ ylist, double* __restrict__ eatom,
-          double* __restrict__ bout) {
+k_snap_yi(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
+          double* __restrict__ eatom) {
   extern __shared__ double smem[];
-  C2* U = reinterpret_cast<C2*>(smem);                         // full matrices (nfull)
-  C2* partY = U + D.nfull;                                      // per unit
-  double* partE = reinterpret_cast<double*>(partY + D.nunits);  // per unit
-  double* partB = partE + D.nunits;                             // per unit (only if bout)
-  int64_t atom = blockIdx.x;
-  const C2* ut = utot + atom * D.nhalf;
-  // expand half rows to full matrices
-  for (int J = 0; J <= D.tj; ++J) {
-    int sz = (J + 1) * (J + 1);
-    for (int t = threadIdx.x; t < sz; t += blockDim.x) {
-      int mb = t / (J + 1), ma = t - mb * (J + 1);
-      C2 v;
-      if (2 * mb <= J) {
-        v = ut[D.hoff[J] + mb * (J + 1) + ma];
-      } else {
-        C2 w = ut[D.hoff[J] + (J - mb) * (J + 1) + (J - ma)];
-        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
-      }
-      U[D.foff[J] + t] = v;
-    }
+  C2* Us = reinterpret_cast<C2*>(smem);                                // [nhalf][32]
+  double* epart = reinterpret_cast<double*>(Us + D.nhalf * YI_ATOMS);  // [warps][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
+  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
+  // stage Utot of 32 atoms, transposed to [element][atom]
+  for (int t = threadIdx.x; t < D.nhalf * YI_ATOMS; t += blockDim.x) {
+    int at = t / D.nhalf, e = t - at * D.nhalf;
+    Us[e * YI_ATOMS + at] = at < na_blk ? utot[(a0 + at) * D.nhalf + e] : C2{0.0, 0.0};
   }
   __syncthreads();
-  for (int u = threadIdx.x; u < D.nunits; u += blockDim.x) {
-    SnapUnit un = D.units[u];
+  double esum = 0.0;
+  const int64_t atom = a0 + lane;
+  for (int wt = D.wseg[warp]; wt < D.wseg[warp + 1]; ++wt) {
+    const int target = D.wtarget[wt];
     C2 ysum{0.0, 0.0};
-    double esum = 0.0, bsum = 0.0;
-    for (int k = un.i0; k < un.i1; ++k) {
+    for (int k = D.tseg[target]; k < D.tseg[target + 1]; ++k) {
       const SnapItem it = D.items[k];
       const double* ca = D.cg + it.cga;
       const double* cb = D.cg + it.cgb;
-      const int x = it.x, y = it.y, J = it.J;
-      const C2* Ux = U + D.foff[x];
-      const C2* Uy = U + D.foff[y];
-      // ma2 = ma - ma1 + (x + y - J)/2 ; mb2 likewise
-      const int sh = (x + y - J) / 2;
+      const int x = it.x, y = it.y, J = it.J, sh = (x + y - J) / 2;
       C2 z{0.0, 0.0};
       for (int jb = 0; jb < it.nb; ++jb) {
-        int mb1 = it.mb1lo + jb, mb2 = it.mb - mb1 + sh;
-        C2 s{0.0, 0.0};
+        const int mb1 = it.mb1lo + jb, mb2 = it.mb - mb1 + sh;
+        C2 sacc{0.0, 0.0};
         for (int ja = 0; ja < it.na; ++ja) {
-          int ma1 = it.ma1lo + ja, ma2 = it.ma - ma1 + sh;
-          C2 t = cmul(Ux[mb1 * (x + 1) + ma1], Uy[mb2 * (y + 1) + ma2]);
-          double c = ca[ja];
-          s.re += c * t.re;
-          s.im += c * t.im;
+          const int ma1 = it.ma1lo + ja, ma2 = it.ma - ma1 + sh;
+          C2 t = cmul(half_get(Us, x, ma1, mb1, lane), half_get(Us, y, ma2, mb2, lane));
+          const double c = ca[ja];
+          sacc.re += c * t.re;
+          sacc.im += c * t.im;
         }
-        double c = cb[jb];
-        z.re += c * s.re;
-        z.im += c * s.im;
+        const double c = cb[jb];
+        z.re += c * sacc.re;
+        z.im += c * sacc.im;
       }
       ysum.re += it.coefY * z.re;
       ysum.im += it.coefY * z.im;
       if (it.bidx >= 0) {
-        C2 uJ = U[D.foff[J] + it.mb * (J + 1) + it.ma];
-        double re = uJ.re * z.re + uJ.im * z.im;  // Re(conj(U) z)
-        esum += it.coefE * re;
-        bsum += it.w * re;
+        C2 uJ = Us[(c_hoff[J] + it.mb * (J + 1) + it.ma) * YI_ATOMS + lane];
+        esum += it.coefE * (uJ.re * z.re + uJ.im * z.im);  // Re(conj(U) z)
       }
     }
-    partY[u] = ysum;
-    partE[u] = esum;
-    if (bout) partB[u] = bsum;
+    if (lane < na_blk) ylist[atom * D.nhalf + target] = ysum;
   }
+  epart[warp * YI_ATOMS + lane] = esum;
   __syncthreads();
-  C2* yo = ylist + atom * D.nhalf;
-  for (int t = threadIdx.x; t < D.nhalf; t += blockDim.x) {
-    C2 s{0.0, 0.0};
-    for (int u = D.useg[t]; u < D.useg[t + 1]; ++u) {
-      s.re += partY[u].re;
-      s.im += partY[u].im;
-    }
-    yo[t] = s;
+  if (warp == 0 && lane < na_blk) {
+    double e = D.beta0;
+    for (int w = 0; w < YI_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
+    eatom[atom] = e;
   }
-  // atom energy: fixed-order tree over units
-  __shared__ double red[YI_THREADS];
-  double e = 0.0;
-  for (int u = threadIdx.x; u < D.nunits; u += blockDim.x) e += partE[u];
-  red[threadIdx.x] = e;
-  __syncthreads();
-  for (int w = YI_THREADS / 2; w > 0; w >>= 1) {
-    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) eatom[atom] = D.beta0 + red[0];
 }
 
 // per-atom bispectrum (debug / parity path; per item, deterministic)
@@ -535,12 +578,12 @@ __global__ void k_snap_bispectrum(SnapDev D, const C2* __restrict__ utot, double
       int mb = t / (J + 1), ma = t - mb * (J + 1);
       C2 v;
       if (2 * mb <= J) {
-        v = ut[D.hoff[J] + mb * (J + 1) + ma];
+        v = ut[c_hoff[J] + mb * (J + 1) + ma];
       } else {
-        C2 w = ut[D.hoff[J] + (J - mb) * (J + 1) + (J - ma)];
+        C2 w = ut[c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
         v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
       }
-      U[D.foff[J] + t] = v;
+      U[c_foff[J] + t] = v;
     }
   }
   __syncthreads();
@@ -558,14 +601,14 @@ __global__ void k_snap_bispectrum(SnapDev D, const C2* __restrict__ utot, double
         C2 s{0.0, 0.0};
         for (int ja = 0; ja < it.na; ++ja) {
           int ma1 = it.ma1lo + ja, ma2 = it.ma - ma1 + sh;
-          C2 t = cmul(U[D.foff[x] + mb1 * (x + 1) + ma1], U[D.foff[y] + mb2 * (y + 1) + ma2]);
+          C2 t = cmul(U[c_foff[x] + mb1 * (x + 1) + ma1], U[c_foff[y] + mb2 * (y + 1) + ma2]);
           s.re += ca[ja] * t.re;
           s.im += ca[ja] * t.im;
         }
         z.re += cb[jb] * s.re;
         z.im += cb[jb] * s.im;
       }
-      C2 uJ = U[D.foff[J] + it.mb * (J + 1) + it.ma];
+      C2 uJ = U[c_foff[J] + it.mb * (J + 1) + it.ma];
       acc += it.w * (uJ.re * z.re + uJ.im * z.im);
     }
     bout[atom * D.nB + b] = acc;
@@ -651,7 +694,7 @@ k_snap_deidrj(SnapDev D, int64_t natoms, int N, Box box, const double* __restric
         cur[3 * layer_max + e] = dv2;
         // weight of a half-row element in the full-matrix sum
         double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
-        C2 y = Y[D.hoff[J] + e];
+        C2 y = Y[c_hoff[J] + e];
         double yu = v.re * y.re + v.im * y.im;
         acc0 += w * (g.fc * (dv0.re * y.re + dv0.im * y.im) + g.dfc * g.u[0] * yu);
         acc1 += w * (g.fc * (dv1.re * y.re + dv1.im * y.im) + g.dfc * g.u[1] * yu);
@@ -765,8 +808,8 @@ static size_t ui_smem(const SnapDev& D) {
   int layer_max = (D.tj + 1) * (D.tj / 2 + 1);
   return sizeof(C2) * (UI_WARPS * D.nhalf + UI_WARPS * 2 * layer_max);
 }
-static size_t yi_smem(const SnapDev& D, bool with_b) {
-  return sizeof(C2) * (D.nfull + D.nunits) + sizeof(double) * D.nunits * (with_b ? 2 : 1);
+static size_t yi_smem(const SnapDev& D) {
+  return sizeof(C2) * D.nhalf * YI_ATOMS + sizeof(double) * YI_WARPS * YI_ATOMS;
 }
 static size_t de_smem(const SnapDev& D) {
   int layer_max = (D.tj + 1) * (D.tj / 2 + 1);
@@ -789,7 +832,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   buf.dedr = buf.eatom + na;
   buf.vatom = buf.dedr + na * 3 * SNAP_MAXN;
   Box box{{pot->box[0], pot->box[1], pot->box[2]}};
-  size_t s1 = ui_smem(D), s2 = yi_smem(D, false), s3 = de_smem(D);
+  size_t s1 = ui_smem(D), s2 = yi_smem(D), s3 = de_smem(D);
   static thread_local bool attr_done = false;
   if (!attr_done) {
     cudaFuncSetAttribute(k_snap_ui, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -804,7 +847,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_UI, false);
   prof_mark(ctx->stream, ST_YI, true);
-  k_snap_yi<<<(unsigned)na, YI_THREADS, s2, ctx->stream>>>(D, buf.utot, buf.y, buf.eatom, nullptr);
+  k_snap_yi<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI_THREADS, s2, ctx->stream>>>(D, na, buf.utot,
+                                                                                        buf.y, buf.eatom);
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_YI, false);
   prof_mark(ctx->stream, ST_DE, true);
