@@ -28,6 +28,7 @@
 // identical, as parareal's convergence test requires (SURVEY.md finding 4).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <tuple>
 #include <vector>
@@ -722,6 +723,261 @@ k_snap_deidrj(SnapDev D, int64_t natoms, int N, Box box, const double* __restric
   }
 }
 
+// ------------------------------------------------------------------ register-resident recursion
+// One lane owns one half row mb of U^J (and of dU^J/dr_k) for one neighbour
+// pair; R = TJ/2 + 1 lanes per pair, P = 32/R pairs per warp.  Layer J is
+// built from layer J-1 IN PLACE, descending ma, fully unrolled (J, ma are
+// compile-time), so U lives in registers.  At even J the new middle row
+// mb = J/2 is born from row J/2 - 1 of layer J-1 (held by the next lane down)
+// through U[x][J/2] = (-1)^(x+J/2) conj(U[J-1-x][J/2-1]), one shuffle per element.
+template <int TJ>
+struct RowGeom {
+  C2 a, b;     // Cayley-Klein parameters
+  C2 da, db;   // d/dr_k of a, b (current Cartesian component)
+};
+
+__device__ __forceinline__ C2 shfl_up_c2(C2 v, int delta) {
+  return C2{__shfl_up_sync(0xffffffffu, v.re, delta), __shfl_up_sync(0xffffffffu, v.im, delta)};
+}
+
+// advance row mb of (u, du) from layer J-1 to layer J (WITH_D: also du)
+template <int TJ, int J, bool WITH_D>
+__device__ __forceinline__ void row_step(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                         const double (*rp)[SNAP_JMAX + 2]) {
+  if (J % 2 == 0) {
+    // lane mb = J/2 receives row J/2-1 of layer J-1 from lane-1 (all lanes shuffle)
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      C2 v = shfl_up_c2(u[i], 1);
+      C2 dv = WITH_D ? shfl_up_c2(du[i], 1) : C2{0.0, 0.0};
+      if (2 * mb == J) {
+        const int x = J - 1 - i;  // destination index in row J/2 of layer J-1
+        const bool neg = ((x + J / 2) & 1) != 0;
+        u[x] = neg ? C2{-v.re, v.im} : C2{v.re, -v.im};
+        if (WITH_D) du[x] = neg ? C2{-dv.re, dv.im} : C2{dv.re, -dv.im};
+      }
+    }
+  }
+  if (2 * mb > J) return;
+#pragma unroll
+  for (int ma = J; ma >= 0; --ma) {
+    C2 nu{0.0, 0.0}, nd{0.0, 0.0};
+    if (ma < J) {
+      const double A = rp[J - ma][J - mb];
+      C2 t = cmulc(g.a, u[ma]);
+      nu.re += A * t.re;
+      nu.im += A * t.im;
+      if (WITH_D) {
+        C2 t1 = cmulc(g.da, u[ma]), t2 = cmulc(g.a, du[ma]);
+        nd.re += A * (t1.re + t2.re);
+        nd.im += A * (t1.im + t2.im);
+      }
+    }
+    if (ma > 0) {
+      const double Bc = rp[ma][J - mb];
+      C2 t = cmulc(g.b, u[ma - 1]);
+      nu.re -= Bc * t.re;
+      nu.im -= Bc * t.im;
+      if (WITH_D) {
+        C2 t1 = cmulc(g.db, u[ma - 1]), t2 = cmulc(g.b, du[ma - 1]);
+        nd.re -= Bc * (t1.re + t2.re);
+        nd.im -= Bc * (t1.im + t2.im);
+      }
+    }
+    u[ma] = nu;
+    if (WITH_D) du[ma] = nd;
+  }
+}
+
+// contraction of layer J's row with Y (full-matrix weights) for one component
+template <int TJ, int J>
+__device__ __forceinline__ double row_contract(const C2 (&u)[TJ + 1], const C2 (&du)[TJ + 1], const C2* Y,
+                                               int mb, double fc, double dfc_uk) {
+  if (2 * mb > J) return 0.0;
+  double acc = 0.0;
+  const C2* yr = Y + c_hoff[J] + mb * (J + 1);
+#pragma unroll
+  for (int ma = 0; ma <= J; ++ma) {
+    const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+    const C2 y = yr[ma];
+    acc += w * (fc * (du[ma].re * y.re + du[ma].im * y.im) + dfc_uk * (u[ma].re * y.re + u[ma].im * y.im));
+  }
+  return acc;
+}
+
+template <int TJ, int J>
+struct Layers {
+  __device__ __forceinline__ static void de(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                            const double (*rp)[SNAP_JMAX + 2], const C2* Y, double fc,
+                                            double dfc_uk, double& acc) {
+    Layers<TJ, J - 1>::de(u, du, g, mb, rp, Y, fc, dfc_uk, acc);
+    row_step<TJ, J, true>(u, du, g, mb, rp);
+    acc += row_contract<TJ, J>(u, du, Y, mb, fc, dfc_uk);
+  }
+  __device__ __forceinline__ static void ui(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                            const double (*rp)[SNAP_JMAX + 2], C2* part, double fc) {
+    Layers<TJ, J - 1>::ui(u, du, g, mb, rp, part, fc);
+    row_step<TJ, J, false>(u, du, g, mb, rp);
+    if (part && 2 * mb <= J) {
+      C2* pr = part + c_hoff[J] + mb * (J + 1);
+#pragma unroll
+      for (int ma = 0; ma <= J; ++ma) {
+        pr[ma].re += fc * u[ma].re;
+        pr[ma].im += fc * u[ma].im;
+      }
+    }
+  }
+};
+template <int TJ>
+struct Layers<TJ, 0> {
+  __device__ __forceinline__ static void de(C2 (&)[TJ + 1], C2 (&)[TJ + 1], const RowGeom<TJ>&, int,
+                                            const double (*)[SNAP_JMAX + 2], const C2*, double, double, double&) {}
+  __device__ __forceinline__ static void ui(C2 (&)[TJ + 1], C2 (&)[TJ + 1], const RowGeom<TJ>&, int,
+                                            const double (*)[SNAP_JMAX + 2], C2*, double) {}
+};
+
+constexpr int RR_WARPS = 4;  // warps per CTA of the register-resident kernels (one atom per warp)
+
+__device__ __forceinline__ void stage_rootpq(double (*rp)[SNAP_JMAX + 2]) {
+  for (int t = threadIdx.x; t < (SNAP_JMAX + 2) * (SNAP_JMAX + 2); t += blockDim.x)
+    rp[t / (SNAP_JMAX + 2)][t % (SNAP_JMAX + 2)] = c_rootpq[t / (SNAP_JMAX + 2)][t % (SNAP_JMAX + 2)];
+}
+
+template <int TJ>
+__global__ void __launch_bounds__(RR_WARPS * 32)
+k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+             C2* __restrict__ utot) {
+  constexpr int R = TJ / 2 + 1, P = 32 / R;
+  extern __shared__ double smem[];
+  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  C2* part = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * P * nh;
+  stage_rootpq(rp);
+  const int64_t atom = (int64_t)blockIdx.x * RR_WARPS + warp;
+  for (int t = lane; t < P * nh; t += 32) part[t] = C2{0.0, 0.0};
+  __syncthreads();
+  if (atom >= natoms) return;
+  const int64_t b = atom / N;
+  const int i = (int)(atom - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const int p = lane / R, mb = lane - p * R;
+  const bool lane_ok = lane < P * R;
+  const int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  for (int s0 = 0; s0 < n; s0 += P) {
+    const int s = s0 + p;
+    const bool valid = lane_ok && s < n;
+    RowGeom<TJ> g;
+    double fc = 0.0;
+    if (valid) {
+      double dx, dy, dz;
+      pair_vec(qb, i, nb[s], box, dx, dy, dz);
+      PairGeom pg;
+      pair_geom(D, dx, dy, dz, pg, false);
+      g.a = pg.a;
+      g.b = pg.b;
+      fc = pg.fc;
+    } else {
+      g.a = C2{1.0, 0.0};
+      g.b = C2{0.0, 0.0};
+    }
+    C2 u[TJ + 1], du[TJ + 1];
+#pragma unroll
+    for (int k = 0; k <= TJ; ++k) u[k] = du[k] = C2{0.0, 0.0};
+    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
+    C2* mypart = part + p * nh;
+    if (valid && mb == 0) mypart[0].re += fc;  // J = 0
+    // every lane runs the recursion (shuffles need the full warp); only valid
+    // lanes accumulate, each into its own pair slot
+    Layers<TJ, TJ>::ui(u, du, g, mb, rp, valid ? mypart : nullptr, fc);
+  }
+  __syncwarp();
+  // fixed-order sum over the P pair slots + self term
+  C2* out = utot + atom * nh;
+  for (int t = lane; t < nh; t += 32) {
+    C2 acc{0.0, 0.0};
+#pragma unroll
+    for (int pp = 0; pp < P; ++pp) {
+      acc.re += part[pp * nh + t].re;
+      acc.im += part[pp * nh + t].im;
+    }
+    int J = 0;
+    while (J < TJ && t >= c_hoff[J + 1]) ++J;
+    const int e = t - c_hoff[J];
+    const int mbb = e / (J + 1), maa = e - mbb * (J + 1);
+    if (maa == mbb) acc.re += D.wself;
+    out[t] = acc;
+  }
+}
+
+template <int TJ>
+__global__ void __launch_bounds__(RR_WARPS * 32)
+k_snap_deidrj_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+                 const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+                 const C2* __restrict__ ylist, double* __restrict__ dedr) {
+  constexpr int R = TJ / 2 + 1, P = 32 / R;
+  extern __shared__ double smem[];
+  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  C2* Y = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * nh;
+  stage_rootpq(rp);
+  const int64_t atom = (int64_t)blockIdx.x * RR_WARPS + warp;
+  if (atom < natoms)
+    for (int t = lane; t < nh; t += 32) Y[t] = ylist[atom * nh + t];
+  __syncthreads();
+  if (atom >= natoms) return;
+  const int64_t b = atom / N;
+  const int i = (int)(atom - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const int p = lane / R, mb = lane - p * R;
+  const bool lane_ok = lane < P * R;
+  const int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  const double y0 = Y[0].re;
+  for (int s0 = 0; s0 < n; s0 += P) {
+    const int s = s0 + p;
+    const bool valid = lane_ok && s < n;
+    PairGeom pg;
+    if (valid) {
+      double dx, dy, dz;
+      pair_vec(qb, i, nb[s], box, dx, dy, dz);
+      pair_geom(D, dx, dy, dz, pg, true);
+    } else {
+      pair_geom(D, 1.0, 0.0, 0.0, pg, true);
+      pg.fc = 0.0;
+      pg.dfc = 0.0;
+    }
+    double res0 = 0.0, res1 = 0.0, res2 = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) {
+      RowGeom<TJ> g{pg.a, pg.b, pg.da[k], pg.db[k]};
+      C2 u[TJ + 1], du[TJ + 1];
+#pragma unroll
+      for (int e = 0; e <= TJ; ++e) u[e] = du[e] = C2{0.0, 0.0};
+      u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
+      const double dfc_uk = pg.dfc * pg.u[k];
+      double acc = (mb == 0) ? dfc_uk * y0 : 0.0;  // J = 0: U = 1, dU = 0, weight 1
+      Layers<TJ, TJ>::de(u, du, g, mb, rp, Y, pg.fc, dfc_uk, acc);
+      // fixed-order sum over the R row lanes of this pair
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        double v = __shfl_down_sync(0xffffffffu, acc, r);
+        if (mb == 0) acc += v;  // acc(mb=0) + acc(1) + ... in row order
+      }
+      if (k == 0) res0 = acc; else if (k == 1) res1 = acc; else res2 = acc;
+    }
+    if (valid && mb == 0) {
+      double* o = dedr + (atom * maxn + s) * 3;
+      o[0] = res0;
+      o[1] = res1;
+      o[2] = res2;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel: gather
 __global__ void k_snap_gather(int64_t natoms, int N, Box box, const double* __restrict__ q,
                               const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
@@ -839,11 +1095,28 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_yi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_bispectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_ui_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
+  // register-resident kernels are instantiated for twojmax = 8 (PL_SNAP_RR=0 selects the
+  // shared-memory layer kernels, kept as the general-twojmax path and for A/B checks)
+  static const bool rr_env = [] {
+    const char* e = getenv("PL_SNAP_RR");
+    return !(e && e[0] == '0');
+  }();
+  const bool rr = rr_env && (D.tj == 8);
+  const size_t rp_bytes = sizeof(double) * (SNAP_JMAX + 2) * (SNAP_JMAX + 2);
+  const unsigned rr_grid = (unsigned)((na + RR_WARPS - 1) / RR_WARPS);
   prof_mark(ctx->stream, ST_UI, true);
-  k_snap_ui<<<(unsigned)na, UI_WARPS * 32, s1, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
-                                                               buf.utot);
+  if (rr) {
+    size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * (32 / 5) * D.nhalf;
+    k_snap_ui_rr<8><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
+                                                                 buf.utot);
+  } else {
+    k_snap_ui<<<(unsigned)na, UI_WARPS * 32, s1, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
+                                                                 buf.utot);
+  }
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_UI, false);
   prof_mark(ctx->stream, ST_YI, true);
@@ -852,8 +1125,14 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_YI, false);
   prof_mark(ctx->stream, ST_DE, true);
-  k_snap_deidrj<<<(unsigned)na, DE_WARPS * 32, s3, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
-                                                                   nl.maxn, buf.y, buf.dedr);
+  if (rr) {
+    size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * D.nhalf;
+    k_snap_deidrj_rr<8><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
+                                                                      nl.maxn, buf.y, buf.dedr);
+  } else {
+    k_snap_deidrj<<<(unsigned)na, DE_WARPS * 32, s3, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
+                                                                     nl.maxn, buf.y, buf.dedr);
+  }
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_DE, false);
   return PL_OK;
