@@ -45,12 +45,14 @@ constexpr int DE_WARPS = 4;
 constexpr int YI_THREADS = 256;
 constexpr int YI_ATOMS = 32;                 // lanes = atoms in k_snap_yi
 constexpr int YI_WARPS = YI_THREADS / 32;
+constexpr int YI3_WARPS = 16;                // k_snap_yi_full: 512 threads, one CTA per SM
 
 struct SnapItem {      // one half-row element of one Z^{xy}_J
   int16_t x, y, J, ma, mb;
   int16_t ma1lo, na, mb1lo, nb;
   int16_t bidx;        // canonical B index or -1
   int32_t cga, cgb;    // offsets into the CG pool (na, nb values)
+  int32_t cgblk;       // offset of the (x,y,J) block [(J+1) x (x+1)] in c_cgt (dense table)
   double coefY;        // weight of this Z element in Y^J (0 if none)
   double coefE;        // beta_b * w(ma,mb) if canonical, else 0
   double w;            // half-row weight
@@ -72,6 +74,7 @@ struct SnapIndex {
   double* d_cg = nullptr;
   double beta0 = 0.0;
   double flops_ui_pair = 0, flops_yi_atom = 0, flops_de_pair = 0;
+  bool cgt_fits = false;
 };
 
 struct SnapDev {  // POD view passed to kernels
@@ -92,6 +95,10 @@ __constant__ double c_rootpq[SNAP_JMAX + 2][SNAP_JMAX + 2];  // sqrt(p/q)
 // layer offsets depend on J only (not on twojmax): half rows and full matrices
 __constant__ int c_hoff[SNAP_JMAX + 2];
 __constant__ int c_foff[SNAP_JMAX + 2];
+// dense Clebsch-Gordan blocks C(x m1, y m2 | J M) as [M-row][m1] per (x, y, J),
+// x >= y, read with warp-uniform addresses by k_snap_yi (36.7 KB at twojmax 8)
+constexpr int CGT_MAX = 7800;  // doubles (61 KB)
+__constant__ double c_cgt[CGT_MAX];
 
 // ------------------------------------------------------------------ host setup
 static double fact(int n) {
@@ -167,6 +174,27 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     coefY[{J, j2, j1}] += bb * (double)(J + 1) / (double)(j1 + 1);   // slot j1
     coefY[{J, j1, j2}] += bb * (double)(J + 1) / (double)(j2 + 1);   // slot j2
   }
+  // dense CG blocks per (x, y, J)
+  std::map<std::tuple<int, int, int>, int> cgblk;
+  std::vector<double> cgt;
+  for (int x = 0; x <= tj; ++x)
+    for (int y = 0; y <= x; ++y)
+      for (int J = x - y; J <= std::min(tj, x + y); J += 2) {
+        cgblk[{x, y, J}] = (int)cgt.size();
+        for (int ma = 0; ma <= J; ++ma)
+          for (int m1 = 0; m1 <= x; ++m1) {
+            int M = 2 * ma - J, mm1 = 2 * m1 - x, m2 = M - mm1;
+            cgt.push_back(std::abs(m2) <= y ? clebsch(x, mm1, y, m2, J, M) : 0.0);
+          }
+      }
+  // the constant table's layout depends on twojmax: the first SNAP potential of
+  // the process owns it; potentials with another twojmax use the global CG pool
+  static int g_cgt_tj = -1;
+  S->cgt_fits = cgt.size() <= (size_t)CGT_MAX && (g_cgt_tj < 0 || g_cgt_tj == tj);
+  if (S->cgt_fits && g_cgt_tj < 0) {
+    PL_CUDA(cudaMemcpyToSymbol(c_cgt, cgt.data(), sizeof(double) * cgt.size()));
+    g_cgt_tj = tj;
+  }
   // items grouped by target half index
   std::vector<std::vector<SnapItem>> per_target(S->nhalf);
   std::vector<double> pool;
@@ -207,6 +235,7 @@ int snap_prepare(pl_pot* pot, const double* beta) {
             it.cgb = (int32_t)pool.size();
             pool.insert(pool.end(), cb.begin(), cb.end());
             it.w = half_weight(J, ma, mb);
+            it.cgblk = cgblk[{x, y, J}];
             it.coefY = cy;
             it.bidx = (int16_t)bidx;
             it.coefE = bidx >= 0 ? beta[bidx + 1] * it.w : 0.0;
@@ -255,6 +284,13 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     tseg[S->nhalf] = pos;
   }
   // targets -> warps of k_snap_yi by longest-processing-time greedy on cost
+  // (the CG table must be known to fit constant memory to pick the kernel)
+  size_t cg_doubles = 0;
+  for (int x = 0; x <= tj; ++x)
+    for (int y = 0; y <= x; ++y)
+      for (int J = x - y; J <= std::min(tj, x + y); J += 2) cg_doubles += (size_t)(J + 1) * (x + 1);
+  const int nwarps = S->cgt_fits ? YI3_WARPS : YI_WARPS;
+  (void)cg_doubles;
   std::vector<std::pair<double, int>> tc;
   for (int t = 0; t < S->nhalf; ++t) {
     double c = 0.0;
@@ -262,20 +298,20 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     tc.push_back({c, t});
   }
   std::sort(tc.begin(), tc.end(), [](auto& a, auto& b) { return a.first > b.first; });
-  std::vector<std::vector<int32_t>> wt(YI_WARPS);
-  std::vector<double> wl(YI_WARPS, 0.0);
+  std::vector<std::vector<int32_t>> wt(nwarps);
+  std::vector<double> wl(nwarps, 0.0);
   for (auto& c : tc) {
     int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
     wt[w].push_back(c.second);
     wl[w] += c.first;
   }
-  std::vector<int32_t> wtarget, wseg(YI_WARPS + 1, 0);
-  for (int w = 0; w < YI_WARPS; ++w) {
+  std::vector<int32_t> wtarget, wseg(nwarps + 1, 0);
+  for (int w = 0; w < nwarps; ++w) {
     std::sort(wt[w].begin(), wt[w].end());
     wseg[w] = (int32_t)wtarget.size();
     wtarget.insert(wtarget.end(), wt[w].begin(), wt[w].end());
   }
-  wseg[YI_WARPS] = (int32_t)wtarget.size();
+  wseg[nwarps] = (int32_t)wtarget.size();
   S->nitems = (int)items.size();
   S->nunits = (int)units.size();
   // algorithmic flop counts (used for the roofline numerator)
@@ -562,6 +598,83 @@ k_snap_yi(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict
   if (warp == 0 && lane < na_blk) {
     double e = D.beta0;
     for (int w = 0; w < YI_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
+    eatom[atom] = e;
+  }
+}
+
+// v3: full matrices in shared memory ([285][32 atoms], no symmetry branch in
+// the inner loop), CG from constant memory, strided inner walk.
+__global__ void __launch_bounds__(YI3_WARPS * 32)
+k_snap_yi_full(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
+               double* __restrict__ eatom) {
+  extern __shared__ double smem[];
+  C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
+  double* epart = reinterpret_cast<double*>(Uf + D.nfull * YI_ATOMS);  // [warps][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
+  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
+  // stage: half rows -> full matrices, transposed to [element][atom]
+  for (int t = threadIdx.x; t < D.nfull * YI_ATOMS; t += blockDim.x) {
+    const int at = t & (YI_ATOMS - 1), f = t >> 5;
+    int J = 0;
+    while (J < D.tj && f >= c_foff[J + 1]) ++J;
+    const int e = f - c_foff[J], mb = e / (J + 1), ma = e - mb * (J + 1);
+    C2 v{0.0, 0.0};
+    if (at < na_blk) {
+      if (2 * mb <= J) {
+        v = utot[(a0 + at) * D.nhalf + c_hoff[J] + mb * (J + 1) + ma];
+      } else {
+        C2 w = utot[(a0 + at) * D.nhalf + c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
+        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
+      }
+    }
+    Uf[f * YI_ATOMS + at] = v;
+  }
+  __syncthreads();
+  double esum = 0.0;
+  const int64_t atom = a0 + lane;
+  for (int wt = D.wseg[warp]; wt < D.wseg[warp + 1]; ++wt) {
+    const int target = D.wtarget[wt];
+    C2 ysum{0.0, 0.0};
+    for (int k = D.tseg[target]; k < D.tseg[target + 1]; ++k) {
+      const SnapItem it = D.items[k];
+      const int x = it.x, y = it.y, J = it.J, sh = (x + y - J) / 2;
+      const double* cga = c_cgt + it.cgblk + it.ma * (x + 1) + it.ma1lo;
+      const double* cgb = c_cgt + it.cgblk + it.mb * (x + 1) + it.mb1lo;
+      C2 z{0.0, 0.0};
+      for (int jb = 0; jb < it.nb; ++jb) {
+        const int mb1 = it.mb1lo + jb, mb2 = it.mb - mb1 + sh;
+        // U^x[ma1][mb1] walks +1 in ma1, U^y[ma2][mb2] walks -1 (ma2 = ma - ma1 + sh)
+        const C2* px = Uf + (c_foff[x] + mb1 * (x + 1) + it.ma1lo) * YI_ATOMS + lane;
+        const C2* py = Uf + (c_foff[y] + mb2 * (y + 1) + (it.ma - it.ma1lo + sh)) * YI_ATOMS + lane;
+        C2 sacc{0.0, 0.0};
+        for (int ja = 0; ja < it.na; ++ja) {
+          const C2 ux = px[ja * YI_ATOMS];
+          const C2 uy = py[-ja * YI_ATOMS];
+          const double c = cga[ja];
+          const double tre = ux.re * uy.re - ux.im * uy.im;
+          const double tim = ux.re * uy.im + ux.im * uy.re;
+          sacc.re += c * tre;
+          sacc.im += c * tim;
+        }
+        const double c = cgb[jb];
+        z.re += c * sacc.re;
+        z.im += c * sacc.im;
+      }
+      ysum.re += it.coefY * z.re;
+      ysum.im += it.coefY * z.im;
+      if (it.bidx >= 0) {
+        const C2 uJ = Uf[(c_foff[J] + it.mb * (J + 1) + it.ma) * YI_ATOMS + lane];
+        esum += it.coefE * (uJ.re * z.re + uJ.im * z.im);  // Re(conj(U) z)
+      }
+    }
+    if (lane < na_blk) ylist[atom * D.nhalf + target] = ysum;
+  }
+  epart[warp * YI_ATOMS + lane] = esum;
+  __syncthreads();
+  if (warp == 0 && lane < na_blk) {
+    double e = D.beta0;
+    for (int w = 0; w < YI3_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
     eatom[atom] = e;
   }
 }
@@ -1096,6 +1209,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_deidrj, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_bispectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_ui_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_yi_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
@@ -1120,8 +1234,14 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_UI, false);
   prof_mark(ctx->stream, ST_YI, true);
-  k_snap_yi<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI_THREADS, s2, ctx->stream>>>(D, na, buf.utot,
-                                                                                        buf.y, buf.eatom);
+  if (S->cgt_fits) {
+    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(double) * YI3_WARPS * YI_ATOMS;
+    k_snap_yi_full<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI3_WARPS * 32, sm, ctx->stream>>>(
+        D, na, buf.utot, buf.y, buf.eatom);
+  } else {
+    k_snap_yi<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI_THREADS, s2, ctx->stream>>>(D, na, buf.utot,
+                                                                                          buf.y, buf.eatom);
+  }
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_YI, false);
   prof_mark(ctx->stream, ST_DE, true);
