@@ -647,16 +647,25 @@ k_snap_yi_full(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __res
         // U^x[ma1][mb1] walks +1 in ma1, U^y[ma2][mb2] walks -1 (ma2 = ma - ma1 + sh)
         const C2* px = Uf + (c_foff[x] + mb1 * (x + 1) + it.ma1lo) * YI_ATOMS + lane;
         const C2* py = Uf + (c_foff[y] + mb2 * (y + 1) + (it.ma - it.ma1lo + sh)) * YI_ATOMS + lane;
-        C2 sacc{0.0, 0.0};
-        for (int ja = 0; ja < it.na; ++ja) {
-          const C2 ux = px[ja * YI_ATOMS];
-          const C2 uy = py[-ja * YI_ATOMS];
-          const double c = cga[ja];
-          const double tre = ux.re * uy.re - ux.im * uy.im;
-          const double tim = ux.re * uy.im + ux.im * uy.re;
-          sacc.re += c * tre;
-          sacc.im += c * tim;
+        // two independent accumulator chains (ILP); fixed pairing => deterministic
+        double s0r = 0.0, s0i = 0.0, s1r = 0.0, s1i = 0.0;
+        int ja = 0;
+        for (; ja + 1 < it.na; ja += 2) {
+          const C2 ux0 = px[ja * YI_ATOMS], ux1 = px[(ja + 1) * YI_ATOMS];
+          const C2 uy0 = py[-ja * YI_ATOMS], uy1 = py[-(ja + 1) * YI_ATOMS];
+          const double c0 = cga[ja], c1 = cga[ja + 1];
+          s0r += c0 * (ux0.re * uy0.re - ux0.im * uy0.im);
+          s0i += c0 * (ux0.re * uy0.im + ux0.im * uy0.re);
+          s1r += c1 * (ux1.re * uy1.re - ux1.im * uy1.im);
+          s1i += c1 * (ux1.re * uy1.im + ux1.im * uy1.re);
         }
+        if (ja < it.na) {
+          const C2 ux0 = px[ja * YI_ATOMS], uy0 = py[-ja * YI_ATOMS];
+          const double c0 = cga[ja];
+          s0r += c0 * (ux0.re * uy0.re - ux0.im * uy0.im);
+          s0i += c0 * (ux0.re * uy0.im + ux0.im * uy0.re);
+        }
+        const C2 sacc{s0r + s1r, s0i + s1i};
         const double c = cgb[jb];
         z.re += c * sacc.re;
         z.im += c * sacc.im;
