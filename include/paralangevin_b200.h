@@ -136,7 +136,9 @@ int pl_propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L,
  * expl (parareal.py:435-445).  h_state in/out {num, den}; h_out[0] = nodes
  * updated.  On a coarse blow-up returns PL_EBLOWUP with h_out[0] = window m,
  * h_blowup[0] = substep; a non-finite corrected state returns PL_EBLOWUP with
- * h_blowup[0] = 0.  d_noise_all: N x (L+1) x d.  Synchronises per node. */
+ * h_blowup[0] = 0.  d_noise_all: N x (L+1) x d.  EAM and elementwise coarse
+ * potentials run the whole sweep in one persistent CTA (sweep_cta.cu); others
+ * loop over windows on the host.  Synchronises. */
 int pl_sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1,
              int include_m0, double* d_traj_q, double* d_traj_p, const double* d_prev_q,
              double* d_base_q, double* d_base_p, const double* d_jump_q,
@@ -144,6 +146,15 @@ int pl_sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t 
              const double* d_mass, double dt, double half_dt, double half_dt_gamma,
              double expl, double* h_state, double* d_hist, int64_t* h_out,
              int32_t* h_blowup);
+
+/* Coarse bootstrap of a new slab (parareal.py:404-405): for m = m0..m1-1,
+ * base[m] = coarse(cur[m]) and cur[m+1] = base[m] exactly.  On a blow-up
+ * returns PL_EBLOWUP with h_out[0] = window m and h_blowup[0] = substep;
+ * otherwise h_out[0] = windows done.  Synchronises. */
+int pl_bootstrap(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1,
+                 double* d_traj_q, double* d_traj_p, double* d_base_q, double* d_base_p,
+                 const double* d_noise_all, const double* h_amp, const double* d_mass, double dt,
+                 double half_dt, double half_dt_gamma, int64_t* h_out, int32_t* h_blowup);
 
 /* d_out[i] = d_a[i] - d_b[i]  (jump = f.q - c.q, parareal.py:280). */
 int pl_sub(pl_ctx* ctx, int64_t n, const double* d_a, const double* d_b, double* d_out);

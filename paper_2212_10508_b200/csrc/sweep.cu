@@ -5,6 +5,8 @@
 // the running error (two scalars) is read back, which is what the adaptive
 // engine's truncation decision needs (parareal.py:433-445).
 #include <cmath>
+#include <cstdlib>
+#include <vector>
 
 #include "pl_common.cuh"
 
@@ -93,6 +95,68 @@ int sub_arrays(pl_ctx* ctx, int64_t n, const double* a, const double* b, double*
   return PL_OK;
 }
 
+int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1, int include_m0,
+              int mode, double* Q, double* P, const double* prevQ, double* baseQ, double* baseP,
+              const double* jumpQ, const double* jumpP, const double* noise, const double* h_amp,
+              const double* mass, double dt, double h, double hg, double expl, double* h_state,
+              int64_t* h_out4, double* d_hist);
+
+static int cta_status(const int64_t* o4, int64_t* h_out, int32_t* h_blowup) {
+  if (o4[3] == 1) {
+    h_out[0] = o4[1];
+    h_blowup[0] = (int32_t)o4[2];
+    return fail(PL_EBLOWUP, "coarse window blew up");
+  }
+  if (o4[3] == 2) {
+    h_out[0] = o4[1];
+    h_blowup[0] = 0;
+    return fail(PL_EBLOWUP, "corrected state is not finite");
+  }
+  h_out[0] = o4[0];
+  return PL_OK;
+}
+
+int bootstrap(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1, double* Q, double* P,
+              double* baseQ, double* baseP, const double* noise_all, const double* h_amp, const double* mass,
+              double dt, double h, double hg, int64_t* h_out, int32_t* h_blowup) {
+  h_out[0] = 0;
+  h_blowup[0] = 0;
+  if (m1 <= m0) return PL_OK;
+  if (coarse->dim && coarse->dim != d) return fail(PL_EARG, "potential dimension mismatch");
+  int64_t o4[4];
+  double state[2] = {0.0, 0.0};
+  PL_TRY(ctx->work[5].reserve(sizeof(double) * (m1 - m0 + 1)));
+  int rc = sweep_cta(ctx, coarse, d, L, m0, m1, 0, 1, Q, P, Q, baseQ, baseP, baseQ, baseP, noise_all, h_amp,
+                     mass, dt, h, hg, 0.0, state, o4, (double*)ctx->work[5].ptr);
+  if (rc != -1) {
+    PL_TRY(rc);
+    return cta_status(o4, h_out, h_blowup);
+  }
+  // generic: one batched-propagator call per window, first blow-up reported
+  cudaStream_t st = ctx->stream;
+  PL_TRY(ctx->work[6].reserve(sizeof(int32_t) * (m1 - m0 + 1)));
+  int32_t* blows = (int32_t*)ctx->work[6].ptr;
+  PL_CUDA(cudaMemsetAsync(blows, 0, sizeof(int32_t) * (m1 - m0), st));
+  const int64_t nb = (int64_t)(L + 1) * d;
+  for (int64_t m = m0; m < m1; ++m) {
+    PL_TRY(propagate_windows(ctx, coarse, 1, d, L, Q + m * d, P + m * d, noise_all + m * nb, h_amp, mass, dt,
+                             h, hg, baseQ + m * d, baseP + m * d, blows + (m - m0)));
+    PL_CUDA(cudaMemcpyAsync(Q + (m + 1) * d, baseQ + m * d, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+    PL_CUDA(cudaMemcpyAsync(P + (m + 1) * d, baseP + m * d, sizeof(double) * d, cudaMemcpyDeviceToDevice, st));
+  }
+  std::vector<int32_t> hb(m1 - m0);
+  PL_CUDA(cudaMemcpyAsync(hb.data(), blows, sizeof(int32_t) * (m1 - m0), cudaMemcpyDeviceToHost, st));
+  PL_CUDA(cudaStreamSynchronize(st));
+  for (int64_t k = 0; k < m1 - m0; ++k)
+    if (hb[k]) {
+      h_out[0] = m0 + k;
+      h_blowup[0] = hb[k];
+      return fail(PL_EBLOWUP, "coarse bootstrap blew up");
+    }
+  h_out[0] = m1 - m0;
+  return PL_OK;
+}
+
 int sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1, int include_m0,
           double* traj_q, double* traj_p, const double* prev_q, double* base_q, double* base_p,
           const double* jump_q, const double* jump_p, const double* noise_all, const double* h_amp,
@@ -102,6 +166,16 @@ int sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1,
   h_out[0] = 0;
   h_blowup[0] = 0;
   if (m1 <= m0) return PL_OK;
+  if (coarse->dim && coarse->dim != d) return fail(PL_EARG, "potential dimension mismatch");
+  if (!getenv("PL_SWEEP_GENERIC")) {
+    int64_t o4[4];
+    int rc = sweep_cta(ctx, coarse, d, L, m0, m1, include_m0, 0, traj_q, traj_p, prev_q, base_q, base_p,
+                       jump_q, jump_p, noise_all, h_amp, mass, dt, h, hg, expl, h_state, o4, d_hist);
+    if (rc != -1) {
+      PL_TRY(rc);
+      return cta_status(o4, h_out, h_blowup);
+    }
+  }
   PL_TRY(ctx->work[3].reserve(sizeof(double) * 8 + sizeof(int32_t) * 8));
   double* acc = (double*)ctx->work[3].ptr;
   int32_t* blow = (int32_t*)(acc + 4);
@@ -148,6 +222,18 @@ int sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1,
 }
 
 }  // namespace pl
+
+extern "C" int pl_bootstrap(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1,
+                            double* d_traj_q, double* d_traj_p, double* d_base_q, double* d_base_p,
+                            const double* d_noise_all, const double* h_amp, const double* d_mass, double dt,
+                            double half_dt, double half_dt_gamma, int64_t* h_out, int32_t* h_blowup) {
+  if (!ctx || !coarse || !d_traj_q || !d_traj_p || !d_base_q || !d_base_p || !d_noise_all || !h_amp ||
+      !h_out || !h_blowup)
+    return pl::fail(PL_EARG, "NULL argument");
+  if (d < 1 || L < 1 || m0 < 0) return pl::fail(PL_EARG, "need d >= 1, L >= 1, m0 >= 0");
+  return pl::bootstrap(ctx, coarse, d, L, m0, m1, d_traj_q, d_traj_p, d_base_q, d_base_p, d_noise_all, h_amp,
+                       d_mass, dt, half_dt, half_dt_gamma, h_out, h_blowup);
+}
 
 extern "C" int pl_sub(pl_ctx* ctx, int64_t n, const double* a, const double* b, double* out) {
   if (!ctx || (n > 0 && (!a || !b || !out))) return pl::fail(PL_EARG, "NULL argument");

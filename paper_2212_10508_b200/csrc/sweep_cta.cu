@@ -1,0 +1,409 @@
+// Persistent single-CTA coarse sweep (parareal.py:289-299, 195-198, 404-405, 425-445).
+//
+// The corrected sweep is the sequential critical path of parareal: window m
+// needs cur[m], produced by window m-1.  For the small systems of the
+// BASELINE configs (129 / 1025 atoms) one CTA holds the whole state in shared
+// memory and runs every window of the sweep -- L BBK substeps each, EAM (or
+// elementwise) forces, the corrected update, the running relative error and
+// the adaptive truncation test -- in ONE launch.  Per substep there is no
+// kernel boundary, only __syncthreads.
+//
+// Modes: 0 = corrected sweep (cur[m+1] = C(cur[m]) + jump[m]); 1 = coarse
+// bootstrap (cur[m+1] = C(cur[m]) exactly).  Both cache base[m] = C(cur[m]).
+// Integrator arithmetic = integrator.cu (explicit round-to-nearest, numpy
+// order); EAM sums in neighbour order; every reduction in a fixed tree:
+// the sweep is bitwise deterministic.
+#include "eam.cuh"
+#include "neigh.cuh"
+#include "pl_common.cuh"
+#include "toy.cuh"
+
+namespace pl {
+
+constexpr int SW_THREADS = 1024;
+constexpr int SW_MAXN = 128;      // Verlet candidates per atom (rc + skin)
+constexpr double SW_SKIN = 0.4;   // Angstrom
+
+struct SweepArgs {
+  int64_t d;
+  int n_atoms, L, mode, include_m0, tpa, use_ew;
+  int64_t m0, m1;
+  double* Q;
+  double* P;
+  const double* prevQ;
+  double* baseQ;
+  double* baseP;
+  const double* jumpQ;
+  const double* jumpP;
+  const double* noise;
+  const double* amp;
+  const double* mass;
+  double dt, h, hg, expl;
+  double* acc;    // {num, den}
+  double* hist;   // running error after each node
+  int64_t* out;   // {nodes done, fail window, fail substep, fail kind (1 blow-up, 2 non-finite)}
+  // EAM
+  Box box;
+  double rc2, rl2;  // cutoff^2, (cutoff + skin)^2
+  Table rho, phi, F;
+  int32_t* cand;    // [n_atoms][SW_MAXN]
+  int32_t* ncand;   // [n_atoms]
+  int* overflow;
+  // elementwise
+  EwProg ew;
+};
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  // fixed-order: warp xor-tree, then warp 0 over the 32 warp sums
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+    if (lane == 0) red[32] = r;
+  }
+  __syncthreads();
+  r = red[32];
+  __syncthreads();
+  return r;
+}
+
+// Verlet candidate lists (ascending j) of the current positions
+__device__ void sw_build(const SweepArgs& A, const double* q, double* qref) {
+  const int n = A.n_atoms;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double xi = q[3 * i], yi = q[3 * i + 1], zi = q[3 * i + 2];
+    int c = 0;
+    int32_t* my = A.cand + (int64_t)i * SW_MAXN;
+    for (int j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const double dx = min_image(sub(q[3 * j], xi), A.box.L[0]);
+      const double dy = min_image(sub(q[3 * j + 1], yi), A.box.L[1]);
+      const double dz = min_image(sub(q[3 * j + 2], zi), A.box.L[2]);
+      if (r2_exact(dx, dy, dz) < A.rl2) {
+        if (c < SW_MAXN) my[c] = j;
+        ++c;
+      }
+    }
+    A.ncand[i] = c < SW_MAXN ? c : SW_MAXN;
+    if (c > SW_MAXN) *A.overflow = 1;
+  }
+  for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) qref[t] = q[t];
+}
+
+// EAM gradient of the CTA's system into g (tpa threads per atom, fixed-order group reduction)
+__device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* fp, double* qref, int* s_flag,
+                       bool force_rebuild) {
+  const int n = A.n_atoms;
+  // rebuild when forced or when any atom moved more than skin/2 since the last build
+  int moved = 0;
+  if (!force_rebuild) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double dx = q[3 * i] - qref[3 * i], dy = q[3 * i + 1] - qref[3 * i + 1];
+      const double dz = q[3 * i + 2] - qref[3 * i + 2];
+      if (!(dx * dx + dy * dy + dz * dz <= 0.25 * SW_SKIN * SW_SKIN)) moved = 1;
+    }
+  }
+  if (__syncthreads_or(moved) || force_rebuild) {
+    sw_build(A, q, qref);
+    __syncthreads();
+  }
+  const int tpa = A.tpa;
+  const int groups = blockDim.x / tpa;
+  const int gi0 = threadIdx.x / tpa, sub = threadIdx.x % tpa;
+  const unsigned gmask = 0xffffffffu;
+  // density pass
+  for (int base = 0; base < n; base += groups) {
+    const int i = base + gi0;
+    double s = 0.0;
+    if (i < n) {
+      const int nc = A.ncand[i];
+      const int32_t* cl = A.cand + (int64_t)i * SW_MAXN;
+      for (int k = sub; k < nc; k += tpa) {
+        double dx, dy, dz;
+        pair_vec(q, i, cl[k], A.box, dx, dy, dz);
+        if (!(r2_exact(dx, dy, dz) < A.rc2)) continue;
+        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+        double f, df;
+        tab_eval(A.rho, r, f, df);
+        s += f;
+      }
+    }
+    for (int off = tpa >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(gmask, s, off);
+    if (i < n && sub == 0) {
+      double f, df;
+      tab_eval(A.F, s, f, df);
+      fp[i] = df;
+    }
+  }
+  __syncthreads();
+  // force pass
+  for (int base = 0; base < n; base += groups) {
+    const int i = base + gi0;
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    if (i < n) {
+      const int nc = A.ncand[i];
+      const int32_t* cl = A.cand + (int64_t)i * SW_MAXN;
+      const double fpi = fp[i];
+      for (int k = sub; k < nc; k += tpa) {
+        const int j = cl[k];
+        double dx, dy, dz;
+        pair_vec(q, i, j, A.box, dx, dy, dz);
+        if (!(r2_exact(dx, dy, dz) < A.rc2)) continue;
+        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+        double rf, drf, pf, dpf;
+        tab_eval(A.rho, r, rf, drf);
+        tab_eval(A.phi, r, pf, dpf);
+        const double sc = ((fpi + fp[j]) * drf + dpf) / r;
+        gx -= sc * dx;
+        gy -= sc * dy;
+        gz -= sc * dz;
+      }
+    }
+    for (int off = tpa >> 1; off > 0; off >>= 1) {
+      gx += __shfl_xor_sync(gmask, gx, off);
+      gy += __shfl_xor_sync(gmask, gy, off);
+      gz += __shfl_xor_sync(gmask, gz, off);
+    }
+    if (i < n && sub == 0) {
+      g[3 * i] = gx;
+      g[3 * i + 1] = gy;
+      g[3 * i + 2] = gz;
+    }
+  }
+  (void)s_flag;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void sw_force(const SweepArgs& A, const double* q, double* g, double* fp,
+                                         double* qref, int* s_flag, bool force_rebuild) {
+  if (A.use_ew) {
+    for (int64_t t = threadIdx.x; t < A.d; t += blockDim.x) g[t] = ew_grad(A.ew, q[t], t);
+    __syncthreads();
+  } else {
+    sw_eam(A, q, g, fp, qref, s_flag, force_rebuild);
+  }
+}
+
+__global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
+  extern __shared__ double sm[];
+  const int64_t d = A.d;
+  double* q = sm;
+  double* p = q + d;
+  double* ph = p + d;
+  double* g = ph + d;
+  double* fp = g + d;                    // n doubles (EAM)
+  double* qref = fp + (A.use_ew ? 0 : A.n_atoms);
+  __shared__ double red[33];
+  __shared__ int s_fail, s_flag;
+  __shared__ double s_num, s_den;
+  if (threadIdx.x == 0) {
+    s_num = A.acc[0];
+    s_den = A.acc[1];
+    A.out[0] = 0;
+    A.out[1] = -1;
+    A.out[2] = 0;
+    A.out[3] = 0;
+  }
+  const int64_t m0 = A.m0;
+  for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
+    q[t] = A.Q[m0 * d + t];
+    p[t] = A.P[m0 * d + t];
+  }
+  __syncthreads();
+  if (A.include_m0) {
+    double s2 = 0.0;
+    for (int64_t t = threadIdx.x; t < d; t += blockDim.x) s2 += q[t] * q[t];
+    const double tot = block_sum(s2, red);
+    if (threadIdx.x == 0) s_den += sqrt(tot);  // num += ||q - q|| = 0
+  }
+  int64_t done = 0;
+  for (int64_t m = m0; m < A.m1; ++m) {
+    const double* G = A.noise + m * (int64_t)(A.L + 1) * d;
+    if (threadIdx.x == 0) s_fail = 0;
+    sw_force(A, q, g, fp, qref, &s_flag, true);
+    for (int s = 1; s <= A.L; ++s) {
+      // open substep s (integrator.py:174-175, 182-183)
+      for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
+        const double mm = A.mass ? A.mass[t] : 1.0;
+        const double smm = A.mass ? __dsqrt_rn(mm) : 1.0;
+        const double al = mul(A.amp[s - 1], smm);
+        const double pref = (s == 1) ? p[t] : ph[t];
+        const double hv = add(sub(sub(p[t], mul(A.h, g[t])), mul(A.hg, pref)), mul(al, G[(int64_t)(s - 1) * d + t]));
+        ph[t] = hv;
+        q[t] = add(q[t], mul(A.dt, dvd(hv, mm)));
+      }
+      __syncthreads();
+      sw_force(A, q, g, fp, qref, &s_flag, false);
+      // close substep s (integrator.py:177, 185) + blow-up check (163-170)
+      int bad = 0;
+      for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
+        const double smm = A.mass ? __dsqrt_rn(A.mass[t]) : 1.0;
+        const double al = mul(A.amp[s], smm);
+        const double hv = ph[t];
+        const double pn = add(sub(sub(hv, mul(A.h, g[t])), mul(A.hg, hv)), mul(al, G[(int64_t)s * d + t]));
+        p[t] = pn;
+        if (!(fabs(q[t]) <= BLOWUP_LIMIT && fabs(pn) <= BLOWUP_LIMIT)) bad = 1;
+      }
+      if (__syncthreads_or(bad) && threadIdx.x == 0 && s_fail == 0) s_fail = s;
+    }
+    __syncthreads();
+    // base[m] = C(cur[m])
+    for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
+      A.baseQ[m * d + t] = q[t];
+      A.baseP[m * d + t] = p[t];
+    }
+    if (s_fail) {
+      if (threadIdx.x == 0) {
+        A.out[1] = m;
+        A.out[2] = s_fail;
+        A.out[3] = 1;
+      }
+      break;
+    }
+    if (A.mode == 1) {
+      for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
+        A.Q[(m + 1) * d + t] = q[t];
+        A.P[(m + 1) * d + t] = p[t];
+      }
+      ++done;
+      continue;
+    }
+    // corrected value base + jump (jump formed first, parareal.py:293) and the
+    // running relative error (parareal.py:196-197)
+    double e1 = 0.0, e2 = 0.0;
+    int nonfinite = 0;
+    for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
+      const double cq = add(q[t], A.jumpQ[m * d + t]);
+      const double cp = add(p[t], A.jumpP[m * d + t]);
+      A.Q[(m + 1) * d + t] = cq;
+      A.P[(m + 1) * d + t] = cp;
+      q[t] = cq;
+      p[t] = cp;
+      if (!isfinite(cq) || !isfinite(cp)) nonfinite = 1;
+      const double pv = A.prevQ[(m + 1) * d + t];
+      const double e = sub(cq, pv);
+      e1 += e * e;
+      e2 += pv * pv;
+    }
+    nonfinite = __syncthreads_or(nonfinite);
+    const double n1 = sqrt(block_sum(e1, red));
+    const double n2 = sqrt(block_sum(e2, red));
+    ++done;
+    bool stop = false;
+    if (threadIdx.x == 0) {
+      s_num = s_num + n1;
+      s_den = s_den + n2;
+      A.hist[m - m0] = s_num / s_den;
+    }
+    __syncthreads();
+    if (nonfinite) {
+      if (threadIdx.x == 0) {
+        A.out[1] = m;
+        A.out[3] = 2;
+      }
+      break;
+    }
+    if (s_den == 0.0) stop = true;
+    else if (A.expl > 0.0 && s_num / s_den > A.expl) stop = true;
+    if (stop) break;
+  }
+  if (threadIdx.x == 0) {
+    A.acc[0] = s_num;
+    A.acc[1] = s_den;
+    A.out[0] = done;
+  }
+}
+
+int ew_program(const pl_pot* p, EwProg* out);
+
+// returns PL_OK if handled, -1 if this coarse potential needs the generic path
+int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1, int include_m0,
+              int mode, double* Q, double* P, const double* prevQ, double* baseQ, double* baseP,
+              const double* jumpQ, const double* jumpP, const double* noise, const double* h_amp,
+              const double* mass, double dt, double h, double hg, double expl, double* h_state,
+              int64_t* h_out4, double* d_hist) {
+  SweepArgs A{};
+  const bool ew = is_elementwise(coarse);
+  if (!ew && coarse->kind != POT_EAM) return -1;
+  const int n = ew ? 0 : coarse->n_atoms;
+  const size_t smem = sizeof(double) * (4 * (size_t)d + (ew ? 0 : (size_t)n + 3 * (size_t)n));
+  if (smem > 200 * 1024) return -1;
+  A.d = d;
+  A.n_atoms = n;
+  A.L = L;
+  A.mode = mode;
+  A.include_m0 = include_m0;
+  A.use_ew = ew ? 1 : 0;
+  A.m0 = m0;
+  A.m1 = m1;
+  A.Q = Q; A.P = P; A.prevQ = prevQ; A.baseQ = baseQ; A.baseP = baseP; A.jumpQ = jumpQ; A.jumpP = jumpP;
+  A.noise = noise;
+  A.mass = mass;
+  A.dt = dt; A.h = h; A.hg = hg; A.expl = expl;
+  cudaStream_t st = ctx->stream;
+  // device scratch: amp, acc, out, (EAM lists)
+  size_t lists = ew ? 0 : sizeof(int32_t) * (size_t)n * (SW_MAXN + 1) + 64;
+  PL_TRY(ctx->work[4].reserve(sizeof(double) * (L + 1 + 2) + sizeof(int64_t) * 4 + 64 + lists));
+  char* w = (char*)ctx->work[4].ptr;
+  double* amp = (double*)w;
+  double* acc = amp + (L + 1);
+  int64_t* out = (int64_t*)(acc + 2);
+  char* lw = (char*)(out + 4);
+  A.amp = amp;
+  A.acc = acc;
+  A.out = out;
+  A.hist = d_hist;
+  if (ew) {
+    PL_TRY(ew_program(coarse, &A.ew));
+  } else {
+    A.box = Box{{coarse->box[0], coarse->box[1], coarse->box[2]}};
+    A.rc2 = coarse->rcut * coarse->rcut;
+    A.rl2 = (coarse->rcut + SW_SKIN) * (coarse->rcut + SW_SKIN);
+    A.rho = Table{coarse->d_rho, coarse->n_r, coarse->dr};
+    A.phi = Table{coarse->d_phi, coarse->n_r, coarse->dr};
+    A.F = Table{coarse->d_F, coarse->n_rho, coarse->drho};
+    A.ncand = (int32_t*)lw;
+    A.overflow = (int*)(A.ncand + n);
+    A.cand = (int32_t*)(((uintptr_t)(A.overflow + 4) + 15) & ~(uintptr_t)15);
+    // threads per atom: minimise rounds/tpa (all atoms of the system in as few passes as possible)
+    int best = 1;
+    double bestc = 1e30;
+    for (int t = 1; t <= 32; t *= 2) {
+      const int groups = SW_THREADS / t;
+      const double c = (double)((n + groups - 1) / groups) / t + 0.02 * t;
+      if (c < bestc) {
+        bestc = c;
+        best = t;
+      }
+    }
+    A.tpa = best;
+    PL_CUDA(cudaMemsetAsync(A.overflow, 0, sizeof(int), st));
+  }
+  double init[2] = {h_state[0], h_state[1]};
+  PL_CUDA(cudaMemcpyAsync(amp, h_amp, sizeof(double) * (L + 1), cudaMemcpyHostToDevice, st));
+  PL_CUDA(cudaMemcpyAsync(acc, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  static thread_local bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_sweep_cta<<<1, SW_THREADS, smem, st>>>(A);
+  PL_CHECK_LAUNCH();
+  double hacc[2];
+  int ovf = 0;
+  PL_CUDA(cudaMemcpyAsync(hacc, acc, sizeof(hacc), cudaMemcpyDeviceToHost, st));
+  PL_CUDA(cudaMemcpyAsync(h_out4, out, sizeof(int64_t) * 4, cudaMemcpyDeviceToHost, st));
+  if (!ew) PL_CUDA(cudaMemcpyAsync(&ovf, A.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PL_CUDA(cudaStreamSynchronize(st));
+  if (ovf) return fail(PL_EPOT, "neighbour capacity exceeded in the coarse sweep");
+  h_state[0] = hacc[0];
+  h_state[1] = hacc[1];
+  return PL_OK;
+}
+
+}  // namespace pl

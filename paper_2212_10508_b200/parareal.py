@@ -261,20 +261,20 @@ class _DeviceRun:
 
     def bootstrap(self, n_init: int) -> None:
         """cur[m+1] = C(cur[m]) for m = n_init..N-1 (parareal.py:404-405); caches base."""
-        import torch
         k = self.coarse.kernel
-        blows = torch.zeros(self.n, dtype=torch.int32, device=self.Q.device)
-        for m in range(n_init, self.n):
-            k.run(self.Q[m:m + 1], self.P[m:m + 1], self.noise_c[m:m + 1],
-                  self.baseQ[m:m + 1], self.baseP[m:m + 1], blows[m:m + 1])
-            self.Q[m + 1].copy_(self.baseQ[m])
-            self.P[m + 1].copy_(self.baseP[m])
-        b = blows.cpu().numpy()
-        bad = np.nonzero(b)[0]
-        if bad.size:
-            m = int(bad[0])
-            raise BlowUpError(f"state left the trusted range at substep {b[m]}", substep=int(b[m]),
-                              window=m + 1, iteration=0)
+        lib, ctx = _lib.load(), _lib.context()
+        out = np.zeros(1, dtype=np.int64)
+        blow = np.zeros(1, dtype=np.int32)
+        rc = lib.pl_bootstrap(
+            ctx.handle, self.coarse.pot.handle(ctx), self.d, k.L, n_init, self.n, _lib.ptr(self.Q),
+            _lib.ptr(self.P), _lib.ptr(self.baseQ), _lib.ptr(self.baseP), _lib.ptr(self.noise_c),
+            _lib.dptr(k.amp), _lib.ptr(k.mass), k.dt, k.h, k.hg, out.ctypes.data_as(_lib.pi64),
+            blow.ctypes.data_as(_lib.pi32))
+        if rc == _lib.PL_EBLOWUP:
+            m = int(out[0])
+            raise BlowUpError(f"state left the trusted range at substep {int(blow[0])}",
+                              substep=int(blow[0]), window=m + 1, iteration=0)
+        _lib.check(rc)
 
     def jumps(self, n_init: int, n_final: int, iteration: int) -> None:
         """jump[m] = F(prev[m]) - C(prev[m]) for all slab windows in one launch."""

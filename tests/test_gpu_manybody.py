@@ -194,3 +194,82 @@ def test_snap_window_vs_oracle(pl):
                                    sched.coefficients, 0, mass=mass, noise=noise)
     assert np.abs(out.q - q1).max() < 1e-8
     assert np.abs(out.p - p1).max() < 1e-8 * np.abs(p1).max()
+
+
+# ------------------------------------------------------------------ W + SIA parareal
+def _w_pr1_setup(pl, L=5, N=4, T=1000.0):
+    from paper_2212_10508_b200 import tungsten as W
+    q0, box = W.bcc_sia(4)
+    n = q0.shape[0] // 3
+    mass = np.full(3 * n, W.MASS_W)
+    params = pl.LangevinParams(1.0, W.KB * T, 0.001, L, mass=mass)
+    sched = pl.TemperatureSchedule.robust(L)
+    p0 = np.sqrt(W.MASS_W * W.KB * T) * np.random.default_rng(5).normal(size=3 * n)
+    return q0, box, n, mass, params, sched, p0
+
+
+def test_w_sia_adaptive_parareal_vs_oracle(pl):
+    """SNAP fine / EAM coarse adaptive parareal (persistent EAM sweep) vs the oracle engine."""
+    import torch
+    from oracle import integrator as oint, native, parareal as opar, rng as orng
+    from paper_2212_10508_b200 import tungsten as W
+    from paper_2212_10508_b200.parareal import DevicePropagator
+    L, N = 5, 4
+    q0, box, n, mass, params, sched, p0 = _w_pr1_setup(pl, L, N)
+    snap, eam = W.make_snap(n, box), W.make_eam(n, box)
+    plan = pl.NoisePlan.for_windows(11, N)
+    noise = orng.gaussian_streams(orng.derive_seeds(11, N), (L + 1) * 3 * n)
+    f = DevicePropagator(snap, params, sched, plan, 3 * n)
+    c = DevicePropagator(eam, params, sched, plan, 3 * n)
+    for prop in (f, c):
+        prop._noise = torch.from_numpy(noise).cuda()
+    cfg = pl.PararealConfig(N, 1e-10, 0.35)
+    res = pl.parareal_adaptive_engine(pl.PhaseState(q=q0, p=p0), f, c, cfg)
+    t = W.eam_tables()
+    sg, eg = native.snap_fn(snap), (lambda q: native.eam(q, box, t)[1])
+
+    def mk(g):
+        return lambda s, m: oint.propagate_window(s[0], s[1], g, 1.0, params.inv_beta, 0.001, L,
+                                                  sched.coefficients, 0, mass=mass, noise=noise[m])
+    ref = opar.adaptive((q0, p0), mk(sg), mk(eg), N, 1e-10, 0.35)
+    Qr = np.array([s[0] for s in ref["trajectory"]])
+    assert np.abs(res.trajectory.positions() - Qr).max() < 1e-8
+    assert [(s.slab_index, s.n_init, s.n_final, s.k_conv) for s in res.slabs] == \
+        [(s[0], s[1], s[3], s[4]) for s in ref["slabs"]]
+    h = np.array(res.error_history)[:, 2]
+    hr = np.array(ref["history"])[:, 2]
+    assert h.shape == hr.shape
+    big = hr > 1e-6
+    np.testing.assert_allclose(h[big], hr[big], rtol=1e-6)
+
+
+def test_persistent_sweep_matches_generic(pl, monkeypatch):
+    """Persistent single-CTA sweep == per-window generic sweep (EAM coarse)."""
+    import torch
+    from paper_2212_10508_b200 import tungsten as W
+    L, N = 10, 6
+    q0, box, n, mass, params, sched, p0 = _w_pr1_setup(pl, L, N)
+    pair = pl.PropagatorPair(W.make_eam(n, box), W.make_eam(n, box), 1.0, 1.0)
+    fine_pert = pl.Perturbed(W.make_eam(n, box), W.make_snap(n, box), 0.1)
+    pair = pl.PropagatorPair(fine_pert, W.make_eam(n, box), 10.0, 1.0)
+    plan = pl.NoisePlan.for_windows(3, N)
+    cfg = pl.PararealConfig(N, 1e-9, 0.35)
+    init = pl.PhaseState(q=q0, p=p0)
+    a = pl.parareal_adaptive(init, pair, params, sched, plan, cfg)
+    monkeypatch.setenv("PL_SWEEP_GENERIC", "1")
+    b = pl.parareal_adaptive(init, pair, params, sched, plan, cfg)
+    assert a.slabs == b.slabs
+    np.testing.assert_allclose(a.trajectory.positions(), b.trajectory.positions(), rtol=0, atol=1e-9)
+
+
+def test_degenerate_pair_converges_in_one_iteration(pl):
+    """coarse == fine: jumps are exactly zero, k_conv = 1 (acceptance criterion 5)."""
+    from paper_2212_10508_b200 import tungsten as W
+    L, N = 5, 5
+    q0, box, n, mass, params, sched, p0 = _w_pr1_setup(pl, L, N)
+    eam = W.make_eam(n, box)
+    pair = pl.PropagatorPair(eam, eam, 1.0, 1.0)
+    plan = pl.NoisePlan.for_windows(7, N)
+    res = pl.parareal_adaptive(pl.PhaseState(q=q0, p=p0), pair, params, sched, plan,
+                               pl.PararealConfig(N, 1e-10, 0.35))
+    assert res.converged and res.n_slab == 1 and res.total_iterations == 1
