@@ -18,79 +18,59 @@ namespace pl {
 
 constexpr int EAM_MAXN = 96;
 
-__global__ void k_eam_density(int64_t B, int N, Box box, Table rho, Table F,
+// tpa threads per atom (eam_tpa rule), one atom per group, groups strided over
+// the batch; group-reduced in the same xor-tree as the persistent sweep
+__global__ void k_eam_density(int64_t B, int N, int tpa, Box box, double rc2, Table rho, Table F,
                               const double* __restrict__ q, const int32_t* __restrict__ nbr,
                               const int32_t* __restrict__ cnt, int maxn, double* __restrict__ Fp,
                               double* __restrict__ Fe) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= B * N) return;
-  int64_t b = t / N;
-  int i = (int)(t - b * N);
-  const double* qb = q + b * (int64_t)N * 3;
-  const int32_t* nb = nbr + t * maxn;
-  int n = cnt[t];
-  double s = 0.0;
-  for (int k = 0; k < n; ++k) {
-    double dx, dy, dz;
-    pair_vec(qb, i, nb[k], box, dx, dy, dz);
-    double r = sqrt(dx * dx + dy * dy + dz * dz);
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / tpa;
+  const int sub = threadIdx.x % tpa;
+  const int64_t t = gid < B * N ? gid : B * N - 1;  // keep whole groups alive for the shuffles
+  const int64_t b = t / N;
+  const int i = (int)(t - b * N);
+  const double s = group_sum(eam_rho_part(q + b * (int64_t)N * 3, i, nbr + t * maxn, cnt[t], sub, tpa, box,
+                                          rc2, rho), tpa);
+  if (gid < B * N && sub == 0) {
     double f, df;
-    tab_eval(rho, r, f, df);
-    s += f;
+    tab_eval(F, s, f, df);
+    Fp[t] = df;
+    Fe[t] = f;
   }
-  double f, df;
-  tab_eval(F, s, f, df);
-  Fp[t] = df;
-  Fe[t] = f;
 }
 
-__global__ void k_eam_force(int64_t B, int N, Box box, Table rho, Table phi,
+__global__ void k_eam_force(int64_t B, int N, int tpa, Box box, double rc2, Table rho, Table phi,
                             const double* __restrict__ q, const int32_t* __restrict__ nbr,
                             const int32_t* __restrict__ cnt, int maxn, const double* __restrict__ Fp,
                             const double* __restrict__ Fe, double* __restrict__ grad,
                             double* __restrict__ eatom, double* __restrict__ vatom) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= B * N) return;
-  int64_t b = t / N;
-  int i = (int)(t - b * N);
-  const double* qb = q + b * (int64_t)N * 3;
-  const double* Fpb = Fp + b * (int64_t)N;
-  const int32_t* nb = nbr + t * maxn;
-  int n = cnt[t];
-  double fpi = Fp[t];
-  double gx = 0, gy = 0, gz = 0, e = 0;
-  double vxx = 0, vyy = 0, vzz = 0, vxy = 0, vxz = 0, vyz = 0;
-  for (int k = 0; k < n; ++k) {
-    int j = nb[k];
-    double dx, dy, dz;
-    pair_vec(qb, i, j, box, dx, dy, dz);
-    double r = sqrt(dx * dx + dy * dy + dz * dz);
-    double rf, drf, pf, dpf;
-    tab_eval(rho, r, rf, drf);
-    tab_eval(phi, r, pf, dpf);
-    double coef = (fpi + Fpb[j]) * drf + dpf;
-    double s = coef / r;
-    gx -= s * dx;
-    gy -= s * dy;
-    gz -= s * dz;
-    e += 0.5 * pf;
-    double hs = 0.5 * s;  // pair virial shared by i and j
-    vxx -= hs * dx * dx;
-    vyy -= hs * dy * dy;
-    vzz -= hs * dz * dz;
-    vxy -= hs * dx * dy;
-    vxz -= hs * dx * dz;
-    vyz -= hs * dy * dz;
-  }
-  if (grad) {
-    grad[3 * t] = gx;
-    grad[3 * t + 1] = gy;
-    grad[3 * t + 2] = gz;
-  }
-  if (eatom) eatom[t] = Fe[t] + e;
-  if (vatom) {
-    double* v = vatom + 6 * t;
-    v[0] = vxx; v[1] = vyy; v[2] = vzz; v[3] = vxy; v[4] = vxz; v[5] = vyz;
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / tpa;
+  const int sub = threadIdx.x % tpa;
+  const int64_t t = gid < B * N ? gid : B * N - 1;
+  const int64_t b = t / N;
+  const int i = (int)(t - b * N);
+  double g[3] = {0.0, 0.0, 0.0}, e = 0.0, v[6] = {0, 0, 0, 0, 0, 0};
+  if (eatom || vatom)
+    eam_force_part<true>(q + b * (int64_t)N * 3, Fp + b * (int64_t)N, i, nbr + t * maxn, cnt[t], sub, tpa, box,
+                         rc2, rho, phi, g, &e, v);
+  else
+    eam_force_part<false>(q + b * (int64_t)N * 3, Fp + b * (int64_t)N, i, nbr + t * maxn, cnt[t], sub, tpa,
+                          box, rc2, rho, phi, g, &e, v);
+  g[0] = group_sum(g[0], tpa);
+  g[1] = group_sum(g[1], tpa);
+  g[2] = group_sum(g[2], tpa);
+  if (eatom) e = group_sum(e, tpa);
+  if (vatom)
+    for (int c = 0; c < 6; ++c) v[c] = group_sum(v[c], tpa);
+  if (gid < B * N && sub == 0) {
+    if (grad) {
+      grad[3 * t] = g[0];
+      grad[3 * t + 1] = g[1];
+      grad[3 * t + 2] = g[2];
+    }
+    if (eatom) eatom[t] = Fe[t] + e;
+    if (vatom)
+      for (int c = 0; c < 6; ++c) vatom[6 * t + c] = v[c];
   }
 }
 
@@ -183,11 +163,13 @@ int compute_eam(pl_pot* pot, int64_t B, const double* q, double* energy, double*
   Box box{{pot->box[0], pot->box[1], pot->box[2]}};
   Table trho{pot->d_rho, pot->n_r, pot->dr}, tphi{pot->d_phi, pot->n_r, pot->dr},
       tF{pot->d_F, pot->n_rho, pot->drho};
-  unsigned g = (unsigned)((na + 127) / 128);
+  const int tpa = eam_tpa(N, 1024);  // the persistent sweep's rule (same reduction tree)
+  const double rc2 = pot->rcut * pot->rcut;
+  unsigned g = (unsigned)((na * tpa + 127) / 128);
   prof_mark(ctx->stream, ST_EAM, true);
-  k_eam_density<<<g, 128, 0, ctx->stream>>>(B, N, box, trho, tF, q, nl.nbr, nl.cnt, nl.maxn, Fp, Fe);
+  k_eam_density<<<g, 128, 0, ctx->stream>>>(B, N, tpa, box, rc2, trho, tF, q, nl.nbr, nl.cnt, nl.maxn, Fp, Fe);
   PL_CHECK_LAUNCH();
-  k_eam_force<<<g, 128, 0, ctx->stream>>>(B, N, box, trho, tphi, q, nl.nbr, nl.cnt, nl.maxn, Fp, Fe,
+  k_eam_force<<<g, 128, 0, ctx->stream>>>(B, N, tpa, box, rc2, trho, tphi, q, nl.nbr, nl.cnt, nl.maxn, Fp, Fe,
                                           grad, energy ? ea : nullptr, virial ? va : nullptr);
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_EAM, false);

@@ -115,25 +115,12 @@ __device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* f
   const int tpa = A.tpa;
   const int groups = blockDim.x / tpa;
   const int gi0 = threadIdx.x / tpa, sub = threadIdx.x % tpa;
-  const unsigned gmask = 0xffffffffu;
-  // density pass
+  // density pass (same device functions / reduction tree as k_eam_density)
   for (int base = 0; base < n; base += groups) {
     const int i = base + gi0;
-    double s = 0.0;
-    if (i < n) {
-      const int nc = A.ncand[i];
-      const int32_t* cl = A.cand + (int64_t)i * SW_MAXN;
-      for (int k = sub; k < nc; k += tpa) {
-        double dx, dy, dz;
-        pair_vec(q, i, cl[k], A.box, dx, dy, dz);
-        if (!(r2_exact(dx, dy, dz) < A.rc2)) continue;
-        const double r = sqrt(dx * dx + dy * dy + dz * dz);
-        double f, df;
-        tab_eval(A.rho, r, f, df);
-        s += f;
-      }
-    }
-    for (int off = tpa >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(gmask, s, off);
+    const int ii = i < n ? i : n - 1;
+    const double s = group_sum(eam_rho_part(q, ii, A.cand + (int64_t)ii * SW_MAXN, A.ncand[ii], sub, tpa, A.box,
+                                            A.rc2, A.rho), tpa);
     if (i < n && sub == 0) {
       double f, df;
       tab_eval(A.F, s, f, df);
@@ -144,35 +131,17 @@ __device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* f
   // force pass
   for (int base = 0; base < n; base += groups) {
     const int i = base + gi0;
-    double gx = 0.0, gy = 0.0, gz = 0.0;
-    if (i < n) {
-      const int nc = A.ncand[i];
-      const int32_t* cl = A.cand + (int64_t)i * SW_MAXN;
-      const double fpi = fp[i];
-      for (int k = sub; k < nc; k += tpa) {
-        const int j = cl[k];
-        double dx, dy, dz;
-        pair_vec(q, i, j, A.box, dx, dy, dz);
-        if (!(r2_exact(dx, dy, dz) < A.rc2)) continue;
-        const double r = sqrt(dx * dx + dy * dy + dz * dz);
-        double rf, drf, pf, dpf;
-        tab_eval(A.rho, r, rf, drf);
-        tab_eval(A.phi, r, pf, dpf);
-        const double sc = ((fpi + fp[j]) * drf + dpf) / r;
-        gx -= sc * dx;
-        gy -= sc * dy;
-        gz -= sc * dz;
-      }
-    }
-    for (int off = tpa >> 1; off > 0; off >>= 1) {
-      gx += __shfl_xor_sync(gmask, gx, off);
-      gy += __shfl_xor_sync(gmask, gy, off);
-      gz += __shfl_xor_sync(gmask, gz, off);
-    }
+    const int ii = i < n ? i : n - 1;
+    double gg[3] = {0.0, 0.0, 0.0}, e = 0.0, v[6];
+    eam_force_part<false>(q, fp, ii, A.cand + (int64_t)ii * SW_MAXN, A.ncand[ii], sub, tpa, A.box, A.rc2, A.rho,
+                          A.phi, gg, &e, v);
+    gg[0] = group_sum(gg[0], tpa);
+    gg[1] = group_sum(gg[1], tpa);
+    gg[2] = group_sum(gg[2], tpa);
     if (i < n && sub == 0) {
-      g[3 * i] = gx;
-      g[3 * i + 1] = gy;
-      g[3 * i + 2] = gz;
+      g[3 * i] = gg[0];
+      g[3 * i + 1] = gg[1];
+      g[3 * i + 2] = gg[2];
     }
   }
   (void)s_flag;
@@ -370,18 +339,7 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
     A.ncand = (int32_t*)lw;
     A.overflow = (int*)(A.ncand + n);
     A.cand = (int32_t*)(((uintptr_t)(A.overflow + 4) + 15) & ~(uintptr_t)15);
-    // threads per atom: minimise rounds/tpa (all atoms of the system in as few passes as possible)
-    int best = 1;
-    double bestc = 1e30;
-    for (int t = 1; t <= 32; t *= 2) {
-      const int groups = SW_THREADS / t;
-      const double c = (double)((n + groups - 1) / groups) / t + 0.02 * t;
-      if (c < bestc) {
-        bestc = c;
-        best = t;
-      }
-    }
-    A.tpa = best;
+    A.tpa = eam_tpa(n, SW_THREADS);
     PL_CUDA(cudaMemsetAsync(A.overflow, 0, sizeof(int), st));
   }
   double init[2] = {h_state[0], h_state[1]};

@@ -273,3 +273,6 @@ def test_degenerate_pair_converges_in_one_iteration(pl):
     res = pl.parareal_adaptive(pl.PhaseState(q=q0, p=p0), pair, params, sched, plan,
                                pl.PararealConfig(N, 1e-10, 0.35))
     assert res.converged and res.n_slab == 1 and res.total_iterations == 1
+    # batched EAM (fine) and the persistent sweep (coarse) are bitwise identical:
+    # every jump is exactly zero, so the error history is exactly zero
+    assert all(e == 0.0 for _, _, e in res.error_history)
