@@ -20,7 +20,8 @@ roofline  dominant kernel (k_snap_yi / k_snap_deidrj / ...) algorithmic FP64
 cpu_baseline  the C oracle (oracle/native, "port") on the host cores, bounded
           sample, rank 0 only
 parareal  wall-clock of one adaptive parareal run of BASELINE configs[0] (PR1:
-          129 atoms, 16 slices x 100, SNAP fine / EAM coarse) on this GPU
+          129 atoms, 16 slices x 100, SNAP fine / EAM coarse), fine stage
+          sharded over all ranks (max over ranks)
 --impl reference  the CPU reference arm: the oracle port of the reference
           path (oracle/: BBK integrator + C SNAP) on all host cores.
 """
@@ -251,8 +252,15 @@ def run_ours(args, rank, world, local_rank):
     parareal = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args, inp, pot, budget_s=args.cpu_seconds)
-    if rank == 0 and world == 1 and not args.no_parareal:
+    if not args.no_parareal:
+        # every rank runs the engine: the fine stage is sharded over ranks with one
+        # NCCL all-gather per iteration (distributed.sharded_fine)
         parareal = parareal_run()
+        if world > 1 and isinstance(parareal, dict) and "wall_s" in parareal:
+            t = torch.tensor([parareal["wall_s"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            parareal["wall_s"] = float(t.item())
+            parareal["ranks"] = world
 
     if rank == 0:
         launches_per_step = (5 + 7 * L)  # SNAP eval = neigh + ui + yi + deidrj + gather; + open/close

@@ -32,6 +32,7 @@ from typing import Callable, NamedTuple
 import numpy as np
 
 from . import _lib
+from .distributed import sharded_fine
 from .integrator import BlowUpError, TemperatureSchedule, WindowKernel
 from .model import LangevinParams, NodeTrajectory, PhaseState
 from .potentials import PropagatorPair
@@ -277,10 +278,19 @@ class _DeviceRun:
         _lib.check(rc)
 
     def jumps(self, n_init: int, n_final: int, iteration: int) -> None:
-        """jump[m] = F(prev[m]) - C(prev[m]) for all slab windows in one launch."""
+        """jump[m] = F(prev[m]) - C(prev[m]) for all slab windows.
+
+        One batched launch per rank: with several ranks (torch.distributed
+        initialised) each propagates a contiguous block of windows and one
+        all-gather of the endpoints gives every rank the full set
+        (distributed.sharded_fine).
+        """
         W = n_final - n_init
-        FQ, FP, blow = self.fine.kernel.run(self.Q[n_init:n_final], self.P[n_init:n_final],
-                                            self.noise_f[n_init:n_final])
+
+        def run_block(lo, hi):
+            return self.fine.kernel.run(self.Q[lo:hi], self.P[lo:hi], self.noise_f[lo:hi])
+
+        FQ, FP, blow = sharded_fine(run_block, n_init, n_final)
         b = blow.cpu().numpy()
         bad = np.nonzero(b)[0]
         if bad.size:
