@@ -93,49 +93,6 @@ __global__ void k_sys_reduce(int64_t B, int N, int width, const double* __restri
   }
 }
 
-int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out) {
-  int N = pot->n_atoms;
-  size_t lists = sizeof(int32_t) * (size_t)B * N * maxn;
-  size_t counts = sizeof(int32_t) * (size_t)B * N;
-  PL_TRY(pot->work[0].reserve(lists));
-  PL_TRY(pot->work[1].reserve(counts + 64));
-  out->nbr = (int32_t*)pot->work[0].ptr;
-  out->cnt = (int32_t*)pot->work[1].ptr;
-  out->overflow = (int*)((char*)pot->work[1].ptr + ((counts + 15) & ~(size_t)15));
-  out->maxn = maxn;
-  pot->nb_overflow = out->overflow;
-  if (B > 65535) return fail(PL_EARG, "at most 65535 systems per call");
-  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
-  double rc2 = rcut * rcut;
-  PL_CUDA(cudaMemsetAsync(out->overflow, 0, sizeof(int), pot->ctx->stream));
-  dim3 grid((N + NB_THREADS - 1) / NB_THREADS, (unsigned)B);
-  prof_mark(pot->ctx->stream, ST_NEIGH, true);
-  k_neigh_brute<<<grid, NB_THREADS, 0, pot->ctx->stream>>>(B, N, box, rc2, maxn, q, out->nbr, out->cnt,
-                                                           out->overflow);
-  PL_CHECK_LAUNCH();
-  prof_mark(pot->ctx->stream, ST_NEIGH, false);
-  return PL_OK;
-}
-
-int neigh_check(pl_pot* pot) {
-  switch (pot->kind) {
-    case POT_PERTURBED:
-      PL_TRY(neigh_check(pot->base));
-      return pot->lam != 0.0 ? neigh_check(pot->delta) : PL_OK;
-    case POT_EAM:
-    case POT_SNAP:
-      break;
-    default:
-      return PL_OK;
-  }
-  if (!pot->nb_overflow) return PL_OK;
-  int h = 0;
-  PL_CUDA(cudaMemcpyAsync(&h, pot->nb_overflow, sizeof(int), cudaMemcpyDeviceToHost, pot->ctx->stream));
-  PL_CUDA(cudaStreamSynchronize(pot->ctx->stream));
-  if (h) return fail(PL_EPOT, "neighbour capacity exceeded (atoms too close / dense)");
-  return PL_OK;
-}
-
 int eam_prepare(pl_pot* pot, const double* rho, const double* phi, const double* F) {
   size_t nr = sizeof(double) * 4 * pot->n_r, nf = sizeof(double) * 4 * pot->n_rho;
   PL_CUDA(cudaMalloc(&pot->d_rho, nr));

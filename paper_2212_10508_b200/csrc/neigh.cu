@@ -1,0 +1,196 @@
+// Periodic neighbour lists: brute force for small systems, cell lists above
+// CELL_MIN_ATOMS.  Both produce the same lists bit for bit: ascending j, pair
+// test r^2 < rc^2 on the exactly rounded minimum-image displacement
+// (neigh.cuh), so every force sum downstream sees the same pairs in the same
+// order regardless of the builder.
+#include <cub/block/block_scan.cuh>
+
+#include "neigh.cuh"
+#include "pl_common.cuh"
+
+namespace pl {
+
+constexpr int CELL_MIN_ATOMS = 4096;
+constexpr int CELL_MAXN = 128;  // per-thread collection buffer (local memory)
+
+struct CellGrid {
+  int n[3];
+  double inv[3];  // cells per Angstrom
+};
+
+// cell of a (possibly unwrapped) position component
+__device__ __forceinline__ int cell_of(double x, double L, double inv, int n) {
+  double w = x - L * floor(x / L);  // wrap into [0, L)
+  int c = (int)(w * inv);
+  return c < 0 ? 0 : (c >= n ? n - 1 : c);
+}
+
+__global__ void k_cell_count(int64_t B, int N, Box box, CellGrid g, const double* __restrict__ q,
+                             int32_t* __restrict__ cell_of_atom, int32_t* __restrict__ ccount) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= B * N) return;
+  int64_t b = t / N;
+  const double* x = q + 3 * t;
+  int cx = cell_of(x[0], box.L[0], g.inv[0], g.n[0]);
+  int cy = cell_of(x[1], box.L[1], g.inv[1], g.n[1]);
+  int cz = cell_of(x[2], box.L[2], g.inv[2], g.n[2]);
+  int c = (cz * g.n[1] + cy) * g.n[0] + cx;
+  int64_t gc = b * (int64_t)g.n[0] * g.n[1] * g.n[2] + c;
+  cell_of_atom[t] = (int32_t)gc;
+  atomicAdd(&ccount[gc], 1);  // integer: the counts are order independent
+}
+
+// exclusive scan of cell counts (single CTA, chunked)
+__global__ void __launch_bounds__(1024) k_cell_scan(int64_t ncell, const int32_t* __restrict__ ccount,
+                                                   int32_t* __restrict__ cstart, int32_t* __restrict__ cfill) {
+  typedef cub::BlockScan<int32_t, 1024> S;
+  __shared__ typename S::TempStorage tmp;
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < ncell; base += 1024) {
+    int64_t i = base + threadIdx.x;
+    int32_t v = i < ncell ? ccount[i] : 0, ex, tot;
+    S(tmp).ExclusiveSum(v, ex, tot);
+    if (i < ncell) {
+      cstart[i] = carry + ex;
+      cfill[i] = carry + ex;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cstart[ncell] = carry;
+}
+
+__global__ void k_cell_fill(int64_t natoms, int N, const int32_t* __restrict__ cell_of_atom,
+                            int32_t* __restrict__ cfill, int32_t* __restrict__ catoms) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= natoms) return;
+  int slot = atomicAdd(&cfill[cell_of_atom[t]], 1);
+  catoms[slot] = (int32_t)(t % N);  // order inside a cell is arbitrary: lists are sorted below
+}
+
+__global__ void __launch_bounds__(128)
+k_neigh_cell(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, const double* __restrict__ q,
+             const int32_t* __restrict__ cell_of_atom, const int32_t* __restrict__ cstart,
+             const int32_t* __restrict__ catoms, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
+             int* __restrict__ overflow) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= B * N) return;
+  int64_t b = t / N;
+  int i = (int)(t - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const int64_t cells = (int64_t)g.n[0] * g.n[1] * g.n[2];
+  const int c = (int)(cell_of_atom[t] - b * cells);
+  const int cx = c % g.n[0], cy = (c / g.n[0]) % g.n[1], cz = c / (g.n[0] * g.n[1]);
+  const double xi = qb[3 * i], yi = qb[3 * i + 1], zi = qb[3 * i + 2];
+  int32_t found[CELL_MAXN];
+  int nf = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        int ex = (cx + dx + g.n[0]) % g.n[0], ey = (cy + dy + g.n[1]) % g.n[1], ez = (cz + dz + g.n[2]) % g.n[2];
+        int64_t cc = b * cells + (ez * g.n[1] + ey) * g.n[0] + ex;
+        for (int s = cstart[cc]; s < cstart[cc + 1]; ++s) {
+          int j = catoms[s];
+          if (j == i) continue;
+          double ddx = min_image(sub(qb[3 * j], xi), box.L[0]);
+          double ddy = min_image(sub(qb[3 * j + 1], yi), box.L[1]);
+          double ddz = min_image(sub(qb[3 * j + 2], zi), box.L[2]);
+          if (r2_exact(ddx, ddy, ddz) < rc2) {
+            if (nf < CELL_MAXN) found[nf] = j;
+            ++nf;
+          }
+        }
+      }
+  int keep = nf < CELL_MAXN ? nf : CELL_MAXN;
+  // ascending j (insertion sort of a few dozen entries)
+  for (int a = 1; a < keep; ++a) {
+    int v = found[a], k = a - 1;
+    while (k >= 0 && found[k] > v) {
+      found[k + 1] = found[k];
+      --k;
+    }
+    found[k + 1] = v;
+  }
+  int outn = keep < maxn ? keep : maxn;
+  int32_t* my = nbr + t * maxn;
+  for (int a = 0; a < outn; ++a) my[a] = found[a];
+  cnt[t] = outn;
+  if (nf > maxn) atomicExch(overflow, 1);
+}
+
+int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out) {
+  int N = pot->n_atoms;
+  size_t lists = sizeof(int32_t) * (size_t)B * N * maxn;
+  size_t counts = sizeof(int32_t) * (size_t)B * N;
+  PL_TRY(pot->work[0].reserve(lists));
+  PL_TRY(pot->work[1].reserve(counts + 64));
+  out->nbr = (int32_t*)pot->work[0].ptr;
+  out->cnt = (int32_t*)pot->work[1].ptr;
+  out->overflow = (int*)((char*)pot->work[1].ptr + ((counts + 15) & ~(size_t)15));
+  out->maxn = maxn;
+  pot->nb_overflow = out->overflow;
+  if (B > 65535) return fail(PL_EARG, "at most 65535 systems per call");
+  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  double rc2 = rcut * rcut;
+  cudaStream_t st = pot->ctx->stream;
+  PL_CUDA(cudaMemsetAsync(out->overflow, 0, sizeof(int), st));
+  CellGrid g;
+  bool cells_ok = N >= CELL_MIN_ATOMS && !getenv("PL_NEIGH_BRUTE");
+  for (int c = 0; c < 3; ++c) {
+    g.n[c] = (int)(pot->box[c] / rcut);
+    if (g.n[c] < 3) cells_ok = false;
+    g.inv[c] = g.n[c] / pot->box[c];
+  }
+  prof_mark(st, ST_NEIGH, true);
+  if (!cells_ok) {
+    dim3 grid((N + NB_THREADS - 1) / NB_THREADS, (unsigned)B);
+    k_neigh_brute<<<grid, NB_THREADS, 0, st>>>(B, N, box, rc2, maxn, q, out->nbr, out->cnt, out->overflow);
+    PL_CHECK_LAUNCH();
+  } else {
+    int64_t cells = (int64_t)g.n[0] * g.n[1] * g.n[2];
+    int64_t nc = B * cells;
+    int64_t na = B * N;
+    size_t bytes = sizeof(int32_t) * (na + 3 * (nc + 1) + na) + 256;
+    PL_TRY(pot->work[3].reserve(bytes));
+    int32_t* cell_of_atom = (int32_t*)pot->work[3].ptr;
+    int32_t* ccount = cell_of_atom + na;
+    int32_t* cstart = ccount + (nc + 1);
+    int32_t* cfill = cstart + (nc + 1);
+    int32_t* catoms = cfill + (nc + 1);
+    PL_CUDA(cudaMemsetAsync(ccount, 0, sizeof(int32_t) * nc, st));
+    unsigned ga = (unsigned)((na + 255) / 256);
+    k_cell_count<<<ga, 256, 0, st>>>(B, N, box, g, q, cell_of_atom, ccount);
+    k_cell_scan<<<1, 1024, 0, st>>>(nc, ccount, cstart, cfill);
+    k_cell_fill<<<ga, 256, 0, st>>>(na, N, cell_of_atom, cfill, catoms);
+    k_neigh_cell<<<(unsigned)((na + 127) / 128), 128, 0, st>>>(B, N, box, g, rc2, maxn, q, cell_of_atom,
+                                                              cstart, catoms, out->nbr, out->cnt, out->overflow);
+    PL_CHECK_LAUNCH();
+  }
+  prof_mark(st, ST_NEIGH, false);
+  return PL_OK;
+}
+
+int neigh_check(pl_pot* pot) {
+  switch (pot->kind) {
+    case POT_PERTURBED:
+      PL_TRY(neigh_check(pot->base));
+      return pot->lam != 0.0 ? neigh_check(pot->delta) : PL_OK;
+    case POT_EAM:
+    case POT_SNAP:
+      break;
+    default:
+      return PL_OK;
+  }
+  if (!pot->nb_overflow) return PL_OK;
+  int h = 0;
+  PL_CUDA(cudaMemcpyAsync(&h, pot->nb_overflow, sizeof(int), cudaMemcpyDeviceToHost, pot->ctx->stream));
+  PL_CUDA(cudaStreamSynchronize(pot->ctx->stream));
+  if (h) return fail(PL_EPOT, "neighbour capacity exceeded (atoms too close / dense)");
+  return PL_OK;
+}
+
+
+}  // namespace pl

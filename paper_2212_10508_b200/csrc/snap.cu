@@ -688,6 +688,123 @@ k_snap_yi_full(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __res
   }
 }
 
+// v4: half rows in shared memory ([155][32 atoms] = 79 KB -> 2 CTAs per SM).
+// A column mb1 > x/2 of U^x is read through U[ma][mb] = (-1)^(ma+mb)
+// conj(U[x-ma][x-mb]): per jb the two columns are direct or mirrored (warp-
+// uniform), the conjugations select one of four compiled inner loops, and the
+// alternating signs fold into the even/odd accumulator chains.
+template <bool CX, bool CY>
+__device__ __forceinline__ void yi_inner(const C2* px, int sx, const C2* py, int sy, const double* cga, int na,
+                                         double& e_re, double& e_im, double& o_re, double& o_im) {
+  // px/py: first element, sx/sy: element stride (+-YI_ATOMS); conj applied when CX/CY
+  int ja = 0;
+  for (; ja + 1 < na; ja += 2) {
+    const C2 ux0 = px[ja * sx], ux1 = px[(ja + 1) * sx];
+    const C2 uy0 = py[ja * sy], uy1 = py[(ja + 1) * sy];
+    const double c0 = cga[ja], c1 = cga[ja + 1];
+    const double x0i = CX ? -ux0.im : ux0.im, x1i = CX ? -ux1.im : ux1.im;
+    const double y0i = CY ? -uy0.im : uy0.im, y1i = CY ? -uy1.im : uy1.im;
+    e_re += c0 * (ux0.re * uy0.re - x0i * y0i);
+    e_im += c0 * (ux0.re * y0i + x0i * uy0.re);
+    o_re += c1 * (ux1.re * uy1.re - x1i * y1i);
+    o_im += c1 * (ux1.re * y1i + x1i * uy1.re);
+  }
+  if (ja < na) {
+    const C2 ux0 = px[ja * sx], uy0 = py[ja * sy];
+    const double c0 = cga[ja];
+    const double x0i = CX ? -ux0.im : ux0.im, y0i = CY ? -uy0.im : uy0.im;
+    e_re += c0 * (ux0.re * uy0.re - x0i * y0i);
+    e_im += c0 * (ux0.re * y0i + x0i * uy0.re);
+  }
+}
+
+__global__ void __launch_bounds__(YI3_WARPS * 32, 2)
+k_snap_yi_half(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
+               double* __restrict__ eatom) {
+  extern __shared__ double smem[];
+  C2* Us = reinterpret_cast<C2*>(smem);                                // [nhalf][32]
+  double* epart = reinterpret_cast<double*>(Us + D.nhalf * YI_ATOMS);  // [warps][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
+  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
+  for (int t = threadIdx.x; t < D.nhalf * YI_ATOMS; t += blockDim.x) {
+    const int at = t / D.nhalf, e = t - at * D.nhalf;
+    Us[e * YI_ATOMS + at] = at < na_blk ? utot[(a0 + at) * D.nhalf + e] : C2{0.0, 0.0};
+  }
+  __syncthreads();
+  double esum = 0.0;
+  const int64_t atom = a0 + lane;
+  const C2* Ul = Us + lane;
+  for (int wt = D.wseg[warp]; wt < D.wseg[warp + 1]; ++wt) {
+    const int target = D.wtarget[wt];
+    C2 ysum{0.0, 0.0};
+    for (int k = D.tseg[target]; k < D.tseg[target + 1]; ++k) {
+      const SnapItem it = D.items[k];
+      const int x = it.x, y = it.y, J = it.J, sh = (x + y - J) / 2;
+      const double* cga = c_cgt + it.cgblk + it.ma * (x + 1) + it.ma1lo;
+      const double* cgb = c_cgt + it.cgblk + it.mb * (x + 1) + it.mb1lo;
+      const int ma2s = it.ma - it.ma1lo + sh;  // ma2 of ja = 0 (then -1 per ja)
+      C2 z{0.0, 0.0};
+      for (int jb = 0; jb < it.nb; ++jb) {
+        const int mb1 = it.mb1lo + jb, mb2 = it.mb - mb1 + sh;
+        const bool mx = 2 * mb1 > x, my = 2 * mb2 > y;
+        // first element addresses and strides ([element][atom] layout)
+        const C2* px;
+        int sx;
+        int sgx = 1;
+        if (!mx) {
+          px = Ul + (c_hoff[x] + mb1 * (x + 1) + it.ma1lo) * YI_ATOMS;
+          sx = YI_ATOMS;
+        } else {
+          px = Ul + (c_hoff[x] + (x - mb1) * (x + 1) + (x - it.ma1lo)) * YI_ATOMS;
+          sx = -YI_ATOMS;
+          sgx = ((it.ma1lo + mb1) & 1) ? -1 : 1;
+        }
+        const C2* py;
+        int sy;
+        int sgy = 1;
+        if (!my) {
+          py = Ul + (c_hoff[y] + mb2 * (y + 1) + ma2s) * YI_ATOMS;
+          sy = -YI_ATOMS;
+        } else {
+          py = Ul + (c_hoff[y] + (y - mb2) * (y + 1) + (y - ma2s)) * YI_ATOMS;
+          sy = YI_ATOMS;
+          sgy = ((ma2s + mb2) & 1) ? -1 : 1;
+        }
+        double e_re = 0.0, e_im = 0.0, o_re = 0.0, o_im = 0.0;
+        switch ((mx ? 2 : 0) | (my ? 1 : 0)) {
+          case 0: yi_inner<false, false>(px, sx, py, sy, cga, it.na, e_re, e_im, o_re, o_im); break;
+          case 1: yi_inner<false, true>(px, sx, py, sy, cga, it.na, e_re, e_im, o_re, o_im); break;
+          case 2: yi_inner<true, false>(px, sx, py, sy, cga, it.na, e_re, e_im, o_re, o_im); break;
+          default: yi_inner<true, true>(px, sx, py, sy, cga, it.na, e_re, e_im, o_re, o_im); break;
+        }
+        // signs: mirrored columns alternate with ja (x: +1 per step, y: -1 per step)
+        const int s0 = sgx * sgy;
+        const int s1 = s0 * (mx ? -1 : 1) * (my ? -1 : 1);
+        const double sr = s0 > 0 ? e_re : -e_re, si = s0 > 0 ? e_im : -e_im;
+        const double tr = s1 > 0 ? o_re : -o_re, ti = s1 > 0 ? o_im : -o_im;
+        const double c = cgb[jb];
+        z.re += c * (sr + tr);
+        z.im += c * (si + ti);
+      }
+      ysum.re += it.coefY * z.re;
+      ysum.im += it.coefY * z.im;
+      if (it.bidx >= 0) {
+        const C2 uJ = Ul[(c_hoff[J] + it.mb * (J + 1) + it.ma) * YI_ATOMS];
+        esum += it.coefE * (uJ.re * z.re + uJ.im * z.im);  // Re(conj(U) z)
+      }
+    }
+    if (lane < na_blk) ylist[atom * D.nhalf + target] = ysum;
+  }
+  epart[warp * YI_ATOMS + lane] = esum;
+  __syncthreads();
+  if (warp == 0 && lane < na_blk) {
+    double e = D.beta0;
+    for (int w = 0; w < YI3_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
+    eatom[atom] = e;
+  }
+}
+
 // per-atom bispectrum (debug / parity path; per item, deterministic)
 __global__ void k_snap_bispectrum(SnapDev D, const C2* __restrict__ utot, double* __restrict__ bout,
                                   int nitems) {
@@ -1219,6 +1336,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_bispectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_ui_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_yi_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_snap_yi_half, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
@@ -1243,7 +1361,15 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_UI, false);
   prof_mark(ctx->stream, ST_YI, true);
-  if (S->cgt_fits) {
+  static const int yi_var = [] {
+    const char* e = getenv("PL_SNAP_YI");
+    return e ? atoi(e) : 4;
+  }();
+  if (S->cgt_fits && yi_var == 4) {
+    size_t sm = sizeof(C2) * D.nhalf * YI_ATOMS + sizeof(double) * YI3_WARPS * YI_ATOMS;
+    k_snap_yi_half<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI3_WARPS * 32, sm, ctx->stream>>>(
+        D, na, buf.utot, buf.y, buf.eatom);
+  } else if (S->cgt_fits) {
     size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(double) * YI3_WARPS * YI_ATOMS;
     k_snap_yi_full<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI3_WARPS * 32, sm, ctx->stream>>>(
         D, na, buf.utot, buf.y, buf.eatom);

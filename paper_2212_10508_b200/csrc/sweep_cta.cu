@@ -46,8 +46,10 @@ struct SweepArgs {
   Box box;
   double rc2, rl2;  // cutoff^2, (cutoff + skin)^2
   Table rho, phi, F;
-  int32_t* cand;    // [n_atoms][SW_MAXN]
+  int32_t* cand;    // [n_atoms][SW_MAXN] Verlet candidates (rc + skin)
   int32_t* ncand;   // [n_atoms]
+  int32_t* nbr;     // [n_atoms][SW_MAXN] exact list (r < rc) of the current positions
+  int32_t* nnbr;    // [n_atoms]
   int* overflow;
   // elementwise
   EwProg ew;
@@ -112,6 +114,21 @@ __device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* f
     sw_build(A, q, qref);
     __syncthreads();
   }
+  // exact list of this step (candidates filtered in order): the lane partition of
+  // the list below is then identical to k_eam_density / k_eam_force's
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int nc = A.ncand[i];
+    const int32_t* cl = A.cand + (int64_t)i * SW_MAXN;
+    int32_t* el = A.nbr + (int64_t)i * SW_MAXN;
+    int c = 0;
+    for (int k = 0; k < nc; ++k) {
+      double dx, dy, dz;
+      pair_vec(q, i, cl[k], A.box, dx, dy, dz);
+      if (r2_exact(dx, dy, dz) < A.rc2) el[c++] = cl[k];
+    }
+    A.nnbr[i] = c;
+  }
+  __syncthreads();
   const int tpa = A.tpa;
   const int groups = blockDim.x / tpa;
   const int gi0 = threadIdx.x / tpa, sub = threadIdx.x % tpa;
@@ -119,7 +136,7 @@ __device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* f
   for (int base = 0; base < n; base += groups) {
     const int i = base + gi0;
     const int ii = i < n ? i : n - 1;
-    const double s = group_sum(eam_rho_part(q, ii, A.cand + (int64_t)ii * SW_MAXN, A.ncand[ii], sub, tpa, A.box,
+    const double s = group_sum(eam_rho_part(q, ii, A.nbr + (int64_t)ii * SW_MAXN, A.nnbr[ii], sub, tpa, A.box,
                                             A.rc2, A.rho), tpa);
     if (i < n && sub == 0) {
       double f, df;
@@ -133,7 +150,7 @@ __device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* f
     const int i = base + gi0;
     const int ii = i < n ? i : n - 1;
     double gg[3] = {0.0, 0.0, 0.0}, e = 0.0, v[6];
-    eam_force_part<false>(q, fp, ii, A.cand + (int64_t)ii * SW_MAXN, A.ncand[ii], sub, tpa, A.box, A.rc2, A.rho,
+    eam_force_part<false>(q, fp, ii, A.nbr + (int64_t)ii * SW_MAXN, A.nnbr[ii], sub, tpa, A.box, A.rc2, A.rho,
                           A.phi, gg, &e, v);
     gg[0] = group_sum(gg[0], tpa);
     gg[1] = group_sum(gg[1], tpa);
@@ -316,7 +333,7 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
   A.dt = dt; A.h = h; A.hg = hg; A.expl = expl;
   cudaStream_t st = ctx->stream;
   // device scratch: amp, acc, out, (EAM lists)
-  size_t lists = ew ? 0 : sizeof(int32_t) * (size_t)n * (SW_MAXN + 1) + 64;
+  size_t lists = ew ? 0 : 2 * sizeof(int32_t) * (size_t)n * (SW_MAXN + 1) + 128;
   PL_TRY(ctx->work[4].reserve(sizeof(double) * (L + 1 + 2) + sizeof(int64_t) * 4 + 64 + lists));
   char* w = (char*)ctx->work[4].ptr;
   double* amp = (double*)w;
@@ -339,6 +356,8 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
     A.ncand = (int32_t*)lw;
     A.overflow = (int*)(A.ncand + n);
     A.cand = (int32_t*)(((uintptr_t)(A.overflow + 4) + 15) & ~(uintptr_t)15);
+    A.nnbr = A.cand + (size_t)n * SW_MAXN;
+    A.nbr = A.nnbr + n + 4;
     A.tpa = eam_tpa(n, SW_THREADS);
     PL_CUDA(cudaMemsetAsync(A.overflow, 0, sizeof(int), st));
   }

@@ -276,3 +276,17 @@ def test_degenerate_pair_converges_in_one_iteration(pl):
     # batched EAM (fine) and the persistent sweep (coarse) are bitwise identical:
     # every jump is exactly zero, so the error history is exactly zero
     assert all(e == 0.0 for _, _, e in res.error_history)
+
+
+@pytest.mark.parametrize("rcut_kind", ["snap", "eam"])
+def test_cell_list_matches_brute_force(pl, rcut_kind):
+    """4395 atoms (>= CELL_MIN_ATOMS): cell-list lists == oracle brute force, bit for bit."""
+    from oracle import native
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(13, 2, sigma=0.08)
+    n = Q.shape[1] // 3
+    pot = W.make_snap(n, box) if rcut_kind == "snap" else W.make_eam(n, box)
+    rc = 4.73 if rcut_kind == "snap" else 5.5
+    dev = _device_neighbours(pl, pot, Q)
+    for b in range(Q.shape[0]):
+        assert dev[b] == native.neighbours(Q[b], box, rc)
