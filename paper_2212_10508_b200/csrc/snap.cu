@@ -1217,6 +1217,205 @@ k_snap_deidrj_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
   }
 }
 
+// ------------------------------------------------------------------ reverse-mode dE/dr
+// dE_i/dr_ik = dfc u_k F + fc Re(da_k S_a + db_k S_b), with F = sum w Re<U, Y> and
+// the complex sensitivities S_a = dF/da, S_b = dF/db from ONE backward sweep of
+// the adjoint through the U recursion
+//   G^{J-1}[x] = w Y^{J-1}[x] + A(J,x) a G^J[x] - B(J,x+1) b G^J[x+1]
+//   S_a += A(J,ma) conj(U^{J-1}[ma]) G^J[ma],  S_b -= B(J,ma) conj(U^{J-1}[ma-1]) G^J[ma]
+// The forward rows are kept in shared memory ([slot][lane]); the middle row
+// born at even J from row J/2-1 by symmetry passes its adjoint back the same
+// way (G_{mb-1}[J-1-x] += (-1)^(x+mb) conj(G_mb[x])).  ~3x fewer FP64
+// operations than propagating the three dU/dr_k.
+constexpr int ADJ_WARPS = 2;
+
+template <int TJ>
+struct AdjLayers {
+  // forward: layer J from J-1 (in place), store the row, accumulate F
+  template <int J>
+  __device__ __forceinline__ static void fwd(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                             const double (*rp)[SNAP_JMAX + 2], const C2* Y, C2* hist,
+                                             int lane, double& F) {
+    if constexpr (J > 0) {
+      fwd<J - 1>(u, g, mb, rp, Y, hist, lane, F);
+      C2 du[TJ + 1];
+      row_step<TJ, J, false>(u, du, g, mb, rp);
+    }
+    if (2 * mb <= J) {
+      const C2* yr = Y + c_hoff[J] + mb * (J + 1);
+#pragma unroll
+      for (int ma = 0; ma <= J; ++ma) {
+        hist[(J * (J + 1) / 2 + ma) * 32 + lane] = u[ma];
+        const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+        F += w * (u[ma].re * yr[ma].re + u[ma].im * yr[ma].im);
+      }
+    }
+  }
+
+  // backward from layer J to J-1 (G holds the adjoint of layer J on entry)
+  template <int J>
+  __device__ __forceinline__ static void bwd(C2 (&G)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                             const double (*rp)[SNAP_JMAX + 2], const C2* Y, const C2* hist,
+                                             int lane, C2& Sa, C2& Sb) {
+    if constexpr (J > 0) {
+      const bool active = 2 * mb <= J;
+      const bool born = (J % 2 == 0) && (2 * mb == J);  // row mb of layer J-1 is virtual
+      if (active) {
+        // U^{J-1} row mb (stored, or the symmetric image of row mb-1 of the lane below)
+        C2 up[TJ + 1];
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          if (!born) {
+            up[x] = hist[((J - 1) * J / 2 + x) * 32 + lane];
+          } else {
+            const C2 v = hist[((J - 1) * J / 2 + (J - 1 - x)) * 32 + lane - 1];
+            up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+          }
+        }
+#pragma unroll
+        for (int ma = 0; ma <= J; ++ma) {
+          if (ma < J) {
+            const double A = rp[J - ma][J - mb];
+            const C2 t = cmulc(up[ma], G[ma]);  // conj(U') G
+            Sa.re += A * t.re;
+            Sa.im += A * t.im;
+          }
+          if (ma > 0) {
+            const double Bc = rp[ma][J - mb];
+            const C2 t = cmulc(up[ma - 1], G[ma]);
+            Sb.re -= Bc * t.re;
+            Sb.im -= Bc * t.im;
+          }
+        }
+        // G^{J-1}[x] = A(J,x) a G[x] - B(J,x+1) b G[x+1]  (ascending x, in place)
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          const double A = rp[J - x][J - mb];
+          const double Bc = rp[x + 1][J - mb];
+          const C2 t1 = cmul(g.a, G[x]);
+          const C2 t2 = cmul(g.b, G[x + 1]);
+          G[x] = C2{A * t1.re - Bc * t2.re, A * t1.im - Bc * t2.im};
+        }
+        G[J] = C2{0.0, 0.0};
+      }
+      // adjoint of the virtual row flows to the lane below (row mb-1), all lanes shuffle
+      if (J % 2 == 0) {
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          const C2 v = C2{__shfl_down_sync(0xffffffffu, G[x].re, 1), __shfl_down_sync(0xffffffffu, G[x].im, 1)};
+          if (2 * (mb + 1) == J) {  // this lane is row J/2-1; the lane above was born at J
+            const int xs = J - 1 - x;
+            const bool neg = ((x + mb + 1) & 1) != 0;
+            G[xs].re += neg ? -v.re : v.re;
+            G[xs].im += neg ? v.im : -v.im;
+          }
+        }
+        if (born) {
+#pragma unroll
+          for (int x = 0; x <= J; ++x) G[x] = C2{0.0, 0.0};
+        }
+      }
+      // direct term of layer J-1 on stored rows
+      if (2 * mb <= J - 1) {
+        const C2* yr = Y + c_hoff[J - 1] + mb * J;
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          const double w = (2 * mb < J - 1 || 2 * x < J - 1) ? 2.0 : (2 * x == J - 1 ? 1.0 : 0.0);
+          G[x].re += w * yr[x].re;
+          G[x].im += w * yr[x].im;
+        }
+      }
+      bwd<J - 1>(G, g, mb, rp, Y, hist, lane, Sa, Sb);
+    }
+  }
+};
+
+template <int TJ>
+__global__ void __launch_bounds__(ADJ_WARPS * 32)
+k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+                  const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+                  const C2* __restrict__ ylist, double* __restrict__ dedr) {
+  constexpr int R = TJ / 2 + 1, P = 32 / R;
+  constexpr int NSLOT = (TJ + 1) * (TJ + 2) / 2;
+  extern __shared__ double smem[];
+  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  C2* Y = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * nh;
+  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + ADJ_WARPS * nh +
+             warp * NSLOT * 32;
+  stage_rootpq(rp);
+  const int64_t atom = (int64_t)blockIdx.x * ADJ_WARPS + warp;
+  if (atom < natoms)
+    for (int t = lane; t < nh; t += 32) Y[t] = ylist[atom * nh + t];
+  __syncthreads();
+  if (atom >= natoms) return;
+  const int64_t b = atom / N;
+  const int i = (int)(atom - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const int p = lane / R, mb = lane - p * R;
+  const bool lane_ok = lane < P * R;
+  const int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  for (int s0 = 0; s0 < n; s0 += P) {
+    const int s = s0 + p;
+    const bool valid = lane_ok && s < n;
+    PairGeom pg;
+    if (valid) {
+      double dx, dy, dz;
+      pair_vec(qb, i, nb[s], box, dx, dy, dz);
+      pair_geom(D, dx, dy, dz, pg, true);
+    } else {
+      pair_geom(D, 1.0, 0.0, 0.0, pg, true);
+      pg.fc = 0.0;
+      pg.dfc = 0.0;
+    }
+    RowGeom<TJ> g{pg.a, pg.b, C2{0.0, 0.0}, C2{0.0, 0.0}};
+    C2 u[TJ + 1];
+#pragma unroll
+    for (int e = 0; e <= TJ; ++e) u[e] = C2{0.0, 0.0};
+    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
+    double F = 0.0;
+    AdjLayers<TJ>::template fwd<TJ>(u, g, mb, rp, Y, hist, lane, F);
+    __syncwarp();
+    // adjoint of the top layer: its direct term
+    C2 G[TJ + 1];
+#pragma unroll
+    for (int e = 0; e <= TJ; ++e) G[e] = C2{0.0, 0.0};
+    if (2 * mb <= TJ) {
+      const C2* yr = Y + c_hoff[TJ] + mb * (TJ + 1);
+#pragma unroll
+      for (int x = 0; x <= TJ; ++x) {
+        const double w = (2 * mb < TJ || 2 * x < TJ) ? 2.0 : (2 * x == TJ ? 1.0 : 0.0);
+        G[x] = C2{w * yr[x].re, w * yr[x].im};
+      }
+    }
+    C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
+    AdjLayers<TJ>::template bwd<TJ>(G, g, mb, rp, Y, hist, lane, Sa, Sb);
+    __syncwarp();
+    // fixed-order sums over the R row lanes of the pair
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double f = __shfl_down_sync(0xffffffffu, F, r);
+      const double ar = __shfl_down_sync(0xffffffffu, Sa.re, r), ai = __shfl_down_sync(0xffffffffu, Sa.im, r);
+      const double br = __shfl_down_sync(0xffffffffu, Sb.re, r), bi = __shfl_down_sync(0xffffffffu, Sb.im, r);
+      if (mb == 0) {
+        F += f;
+        Sa.re += ar; Sa.im += ai;
+        Sb.re += br; Sb.im += bi;
+      }
+    }
+    if (valid && mb == 0) {
+      double* o = dedr + (atom * maxn + s) * 3;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double re = pg.da[k].re * Sa.re - pg.da[k].im * Sa.im + pg.db[k].re * Sb.re - pg.db[k].im * Sb.im;
+        o[k] = pg.dfc * pg.u[k] * F + pg.fc * re;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel: gather
 __global__ void k_snap_gather(int64_t natoms, int N, Box box, const double* __restrict__ q,
                               const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
@@ -1338,6 +1537,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_yi_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_yi_half, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_adj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
   // register-resident kernels are instantiated for twojmax = 8 (PL_SNAP_RR=0 selects the
@@ -1363,7 +1563,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   prof_mark(ctx->stream, ST_YI, true);
   static const int yi_var = [] {
     const char* e = getenv("PL_SNAP_YI");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 3;
   }();
   if (S->cgt_fits && yi_var == 4) {
     size_t sm = sizeof(C2) * D.nhalf * YI_ATOMS + sizeof(double) * YI3_WARPS * YI_ATOMS;
@@ -1380,7 +1580,15 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_YI, false);
   prof_mark(ctx->stream, ST_DE, true);
-  if (rr) {
+  static const bool adj_env = [] {
+    const char* e = getenv("PL_SNAP_ADJ");
+    return !(e && e[0] == '0');
+  }();
+  if (rr && adj_env) {
+    size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + 45 * 32);
+    k_snap_deidrj_adj<8><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
+        D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
+  } else if (rr) {
     size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * D.nhalf;
     k_snap_deidrj_rr<8><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
                                                                       nl.maxn, buf.y, buf.dedr);
