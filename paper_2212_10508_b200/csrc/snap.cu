@@ -75,6 +75,8 @@ struct SnapIndex {
   double beta0 = 0.0;
   double flops_ui_pair = 0, flops_yi_atom = 0, flops_de_pair = 0;
   bool cgt_fits = false;
+  bool yi_reg = false;  // k_snap_yi_reg usable (twojmax = 8, CG table in constant memory)
+  double* d_yi5 = nullptr;  // [2][NT]: coefY(X,Y,J), beta_b of canonical triples (else 0)
 };
 
 struct SnapDev {  // POD view passed to kernels
@@ -86,6 +88,7 @@ struct SnapDev {  // POD view passed to kernels
   const int32_t* tseg;
   const int32_t* wtarget;
   const int32_t* wseg;
+  const double* yi5;  // [2][NT]
   const double* cg;
   double beta0, rcut, rfac0, rmin0, wself;
   int switchflag;
@@ -97,8 +100,43 @@ __constant__ int c_hoff[SNAP_JMAX + 2];
 __constant__ int c_foff[SNAP_JMAX + 2];
 // dense Clebsch-Gordan blocks C(x m1, y m2 | J M) as [M-row][m1] per (x, y, J),
 // x >= y, read with warp-uniform addresses by k_snap_yi (36.7 KB at twojmax 8)
-constexpr int CGT_MAX = 7800;  // doubles (61 KB)
+constexpr int CGT_MAX = 5000;  // doubles (40 KB; twojmax = 8 needs 4698)
 __constant__ double c_cgt[CGT_MAX];
+
+namespace yi5 {
+constexpr int TJ = 8;
+constexpr int foff(int J) { return J * (J + 1) * (2 * J + 1) / 6; }
+constexpr int hoff(int J) {
+  int h = 0;
+  for (int j = 0; j < J; ++j) h += (j + 1) * (j / 2 + 1);
+  return h;
+}
+constexpr int cgoff(int X, int Y, int J) {  // offset of block (X, Y, J) in c_cgt
+  int o = 0;
+  for (int x = 0; x <= TJ; ++x)
+    for (int y = 0; y <= x; ++y)
+      for (int j = x - y; j <= (TJ < x + y ? TJ : x + y); j += 2) {
+        if (x == X && y == Y && j == J) return o;
+        o += (j + 1) * (x + 1);
+      }
+  return -1;
+}
+constexpr int ntriples() {
+  int n = 0;
+  for (int x = 0; x <= TJ; ++x)
+    for (int y = 0; y <= x; ++y)
+      for (int j = x - y; j <= (TJ < x + y ? TJ : x + y); j += 2) ++n;
+  return n;
+}
+constexpr int NT = ntriples();
+}  // namespace yi5
+
+constexpr int YI5_WARPS = 8;
+__constant__ int c_yi5_code[130];     // triple id -> X*100 + Y*10 + J
+__constant__ int c_yi5_jstart[yi5::TJ + 2];  // triples of row-layer J: [jstart[J], jstart[J+1]) in tlist
+__constant__ int c_yi5_tlist[130];    // triple ids sorted by J
+__constant__ int c_yi5_gseg[YI5_WARPS + 1];  // groups of warp w
+__constant__ int c_yi5_groups[32];    // (J << 8) | mb
 
 // ------------------------------------------------------------------ host setup
 static double fact(int n) {
@@ -194,6 +232,70 @@ int snap_prepare(pl_pot* pot, const double* beta) {
   if (S->cgt_fits && g_cgt_tj < 0) {
     PL_CUDA(cudaMemcpyToSymbol(c_cgt, cgt.data(), sizeof(double) * cgt.size()));
     g_cgt_tj = tj;
+  }
+  // register-tiled Y (k_snap_yi_reg, twojmax = 8): per-triple coefficients, rows by J,
+  // LPT schedule of the (J, mb) rows over the CTA's warps
+  S->yi_reg = false;
+  if (tj == 8 && S->cgt_fits) {
+    std::vector<double> cy, be;
+    std::vector<int> code;
+    std::vector<std::vector<int>> byJ(tj + 1);
+    std::vector<double> rowcost(64, 0.0);
+    for (int x = 0; x <= tj; ++x)
+      for (int y = 0; y <= x; ++y)
+        for (int J = x - y; J <= std::min(tj, x + y); J += 2) {
+          int tid = (int)code.size();
+          auto itc = coefY.find({x, y, J});
+          cy.push_back(itc == coefY.end() ? 0.0 : itc->second);
+          auto itb = bindex.find({x, y, J});
+          be.push_back(itb == bindex.end() ? 0.0 : beta[itb->second + 1]);
+          code.push_back(x * 100 + y * 10 + J);
+          byJ[J].push_back(tid);
+        }
+    std::vector<int> tlist, jstart(tj + 2, 0);
+    for (int J = 0; J <= tj; ++J) {
+      jstart[J] = (int)tlist.size();
+      tlist.insert(tlist.end(), byJ[J].begin(), byJ[J].end());
+    }
+    jstart[tj + 1] = (int)tlist.size();
+    // row costs: sum over the row's triples of nb * (J+1) * (X+1)
+    std::vector<std::pair<double, int>> rows;
+    for (int J = 0; J <= tj; ++J)
+      for (int mb = 0; 2 * mb <= J; ++mb) {
+        double c = 0.0;
+        for (int tid : byJ[J]) {
+          int x = code[tid] / 100, y = (code[tid] / 10) % 10, sh = (x + y - J) / 2;
+          int nb = 0;
+          for (int mb1 = 0; mb1 <= x; ++mb1) nb += (mb + sh - mb1 >= 0 && mb + sh - mb1 <= y);
+          c += (double)nb * (J + 1) * (x + 1) + 20.0;
+        }
+        rows.push_back({c, (J << 8) | mb});
+      }
+    std::sort(rows.begin(), rows.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    const int NW = 8;
+    std::vector<std::vector<int>> wr(NW);
+    std::vector<double> wl(NW, 0.0);
+    for (auto& r : rows) {
+      int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
+      wr[w].push_back(r.second);
+      wl[w] += r.first;
+    }
+    std::vector<int> groups, gseg(NW + 1, 0);
+    for (int w = 0; w < NW; ++w) {
+      gseg[w] = (int)groups.size();
+      groups.insert(groups.end(), wr[w].begin(), wr[w].end());
+    }
+    gseg[NW] = (int)groups.size();
+    std::vector<double> cb2(cy);
+    cb2.insert(cb2.end(), be.begin(), be.end());
+    PL_CUDA(cudaMalloc(&S->d_yi5, sizeof(double) * cb2.size()));
+    PL_CUDA(cudaMemcpy(S->d_yi5, cb2.data(), sizeof(double) * cb2.size(), cudaMemcpyHostToDevice));
+    PL_CUDA(cudaMemcpyToSymbol(c_yi5_code, code.data(), sizeof(int) * code.size()));
+    PL_CUDA(cudaMemcpyToSymbol(c_yi5_tlist, tlist.data(), sizeof(int) * tlist.size()));
+    PL_CUDA(cudaMemcpyToSymbol(c_yi5_jstart, jstart.data(), sizeof(int) * jstart.size()));
+    PL_CUDA(cudaMemcpyToSymbol(c_yi5_gseg, gseg.data(), sizeof(int) * gseg.size()));
+    PL_CUDA(cudaMemcpyToSymbol(c_yi5_groups, groups.data(), sizeof(int) * groups.size()));
+    S->yi_reg = true;
   }
   // items grouped by target half index
   std::vector<std::vector<SnapItem>> per_target(S->nhalf);
@@ -373,6 +475,7 @@ void snap_release(pl_pot* pot) {
   cudaFree(S->d_tseg);
   cudaFree(S->d_wtarget);
   cudaFree(S->d_wseg);
+  cudaFree(S->d_yi5);
   delete S;
   pot->snap = nullptr;
 }
@@ -387,6 +490,7 @@ static SnapDev snap_dev(const pl_pot* pot) {
   }
   D.items = S->d_items; D.units = S->d_units; D.useg = S->d_useg; D.cg = S->d_cg;
   D.tseg = S->d_tseg; D.wtarget = S->d_wtarget; D.wseg = S->d_wseg;
+  D.yi5 = S->d_yi5;
   D.beta0 = S->beta0; D.rcut = pot->rcut; D.rfac0 = pot->rfac0; D.rmin0 = pot->rmin0;
   D.wself = pot->wself; D.switchflag = pot->switchflag;
   return D;
@@ -801,6 +905,149 @@ k_snap_yi_half(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __res
   if (warp == 0 && lane < na_blk) {
     double e = D.beta0;
     for (int w = 0; w < YI3_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
+    eatom[atom] = e;
+  }
+}
+
+// v5: register-tiled Z/Y for twojmax = 8.  Work = whole Y rows (J, mb) per warp
+// (LPT schedule).  For every contributing (X, Y) pair one instantiation of
+// yi_xyj<X,Y,J> loads the U^X column mb1 and the U^Y column mb2 into registers
+// once per mb1 and produces all J+1 outputs of the row; all ma / ma1 indices
+// are compile-time, CG coefficients are constant-bank operands at compile-time
+// offsets (c_cgt layout = host enumeration, reproduced by constexpr below).
+
+
+
+template <int X, int Y, int J>
+__device__ __forceinline__ void yi_xyj(const C2* __restrict__ Ul, int mb, double cy, double be,
+                                       C2 (&yacc)[yi5::TJ + 1], double& esum) {
+  constexpr int SH = (X + Y - J) / 2;
+  constexpr int OFF = yi5::cgoff(X, Y, J);
+  constexpr int FX = yi5::foff(X), FY = yi5::foff(Y);
+  C2 z[J + 1];
+#pragma unroll
+  for (int m = 0; m <= J; ++m) z[m] = C2{0.0, 0.0};
+  const bool mid = (2 * mb == J);
+  const int lo = max(0, mb + SH - Y), hi = min(X, mb + SH);
+  for (int mb1 = lo; mb1 <= hi; ++mb1) {
+    const int mb2 = mb + SH - mb1;
+    C2 ux[X + 1], uy[Y + 1];
+    const C2* px = Ul + (FX + mb1 * (X + 1)) * YI_ATOMS;
+    const C2* py = Ul + (FY + mb2 * (Y + 1)) * YI_ATOMS;
+#pragma unroll
+    for (int a = 0; a <= X; ++a) ux[a] = px[a * YI_ATOMS];
+#pragma unroll
+    for (int a = 0; a <= Y; ++a) uy[a] = py[a * YI_ATOMS];
+    const double cb = c_cgt[OFF + mb * (X + 1) + mb1];
+#pragma unroll
+    for (int ma = 0; ma <= J; ++ma) {
+      if (mid && 2 * ma > J) continue;  // zero weight on the middle row's upper half
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int ma1 = 0; ma1 <= X; ++ma1) {
+        const int ma2 = ma + SH - ma1;
+        if (ma2 < 0 || ma2 > Y) continue;  // folded after unrolling
+        const double c = c_cgt[OFF + ma * (X + 1) + ma1];
+        sr += c * (ux[ma1].re * uy[ma2].re - ux[ma1].im * uy[ma2].im);
+        si += c * (ux[ma1].re * uy[ma2].im + ux[ma1].im * uy[ma2].re);
+      }
+      z[ma].re += cb * sr;
+      z[ma].im += cb * si;
+    }
+  }
+  const C2* pj = Ul + (yi5::foff(J) + mb * (J + 1)) * YI_ATOMS;
+#pragma unroll
+  for (int ma = 0; ma <= J; ++ma) {
+    yacc[ma].re += cy * z[ma].re;
+    yacc[ma].im += cy * z[ma].im;
+    if (be != 0.0) {
+      const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+      const C2 u = pj[ma * YI_ATOMS];
+      esum += be * w * (u.re * z[ma].re + u.im * z[ma].im);
+    }
+  }
+}
+
+// flat switch (faster than the recursive compare chain): generated per triple id
+#define YI5_CASES(F) \
+  F(0,0,0) F(1,0,1) F(1,1,0) F(1,1,2) F(2,0,2) F(2,1,1) F(2,1,3) F(2,2,0) F(2,2,2) F(2,2,4) \
+  F(3,0,3) F(3,1,2) F(3,1,4) F(3,2,1) F(3,2,3) F(3,2,5) F(3,3,0) F(3,3,2) F(3,3,4) F(3,3,6) \
+  F(4,0,4) F(4,1,3) F(4,1,5) F(4,2,2) F(4,2,4) F(4,2,6) F(4,3,1) F(4,3,3) F(4,3,5) F(4,3,7) \
+  F(4,4,0) F(4,4,2) F(4,4,4) F(4,4,6) F(4,4,8) F(5,0,5) F(5,1,4) F(5,1,6) F(5,2,3) F(5,2,5) \
+  F(5,2,7) F(5,3,2) F(5,3,4) F(5,3,6) F(5,3,8) F(5,4,1) F(5,4,3) F(5,4,5) F(5,4,7) F(5,5,0) \
+  F(5,5,2) F(5,5,4) F(5,5,6) F(5,5,8) F(6,0,6) F(6,1,5) F(6,1,7) F(6,2,4) F(6,2,6) F(6,2,8) \
+  F(6,3,3) F(6,3,5) F(6,3,7) F(6,4,2) F(6,4,4) F(6,4,6) F(6,4,8) F(6,5,1) F(6,5,3) F(6,5,5) \
+  F(6,5,7) F(6,6,0) F(6,6,2) F(6,6,4) F(6,6,6) F(6,6,8) F(7,0,7) F(7,1,6) F(7,1,8) F(7,2,5) \
+  F(7,2,7) F(7,3,4) F(7,3,6) F(7,3,8) F(7,4,3) F(7,4,5) F(7,4,7) F(7,5,2) F(7,5,4) F(7,5,6) \
+  F(7,5,8) F(7,6,1) F(7,6,3) F(7,6,5) F(7,6,7) F(7,7,0) F(7,7,2) F(7,7,4) F(7,7,6) F(7,7,8) \
+  F(8,0,8) F(8,1,7) F(8,2,6) F(8,2,8) F(8,3,5) F(8,3,7) F(8,4,4) F(8,4,6) F(8,4,8) F(8,5,3) \
+  F(8,5,5) F(8,5,7) F(8,6,2) F(8,6,4) F(8,6,6) F(8,6,8) F(8,7,1) F(8,7,3) F(8,7,5) F(8,7,7) \
+  F(8,8,0) F(8,8,2) F(8,8,4) F(8,8,6) F(8,8,8)
+
+__device__ __forceinline__ void yi5_call(int code, double cy, double be, const C2* Ul, int mb,
+                                         C2 (&yacc)[yi5::TJ + 1], double& esum) {
+  // code = X*100 + Y*10 + J
+  switch (code) {
+#define YI5_CASE(X, Y, J) \
+  case X * 100 + Y * 10 + J: yi_xyj<X, Y, J>(Ul, mb, cy, be, yacc, esum); break;
+    YI5_CASES(YI5_CASE)
+#undef YI5_CASE
+    default: break;
+  }
+}
+
+
+
+__global__ void __launch_bounds__(YI5_WARPS * 32, 1)
+k_snap_yi_reg(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
+              double* __restrict__ eatom) {
+  extern __shared__ double smem[];
+  C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
+  double* epart = reinterpret_cast<double*>(Uf + D.nfull * YI_ATOMS);  // [warps][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
+  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
+  for (int t = threadIdx.x; t < D.nfull * YI_ATOMS; t += blockDim.x) {
+    const int at = t & (YI_ATOMS - 1), f = t >> 5;
+    int J = 0;
+    while (J < D.tj && f >= c_foff[J + 1]) ++J;
+    const int e = f - c_foff[J], mb = e / (J + 1), ma = e - mb * (J + 1);
+    C2 v{0.0, 0.0};
+    if (at < na_blk) {
+      if (2 * mb <= J) {
+        v = utot[(a0 + at) * D.nhalf + c_hoff[J] + mb * (J + 1) + ma];
+      } else {
+        C2 w = utot[(a0 + at) * D.nhalf + c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
+        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
+      }
+    }
+    Uf[f * YI_ATOMS + at] = v;
+  }
+  __syncthreads();
+  const C2* Ul = Uf + lane;
+  const int64_t atom = a0 + lane;
+  double esum = 0.0;
+  for (int gi = c_yi5_gseg[warp]; gi < c_yi5_gseg[warp + 1]; ++gi) {
+    const int J = c_yi5_groups[gi] >> 8, mb = c_yi5_groups[gi] & 0xff;
+    C2 yacc[yi5::TJ + 1];
+#pragma unroll
+    for (int m = 0; m <= yi5::TJ; ++m) yacc[m] = C2{0.0, 0.0};
+    for (int k = c_yi5_jstart[J]; k < c_yi5_jstart[J + 1]; ++k) {
+      const int tid = c_yi5_tlist[k];
+      yi5_call(c_yi5_code[tid], D.yi5[tid], D.yi5[yi5::NT + tid], Ul, mb, yacc, esum);
+    }
+    if (lane < na_blk) {
+      C2* yo = ylist + atom * D.nhalf + c_hoff[J] + mb * (J + 1);
+#pragma unroll
+      for (int m = 0; m <= yi5::TJ; ++m)
+        if (m <= J) yo[m] = yacc[m];
+    }
+  }
+  epart[warp * YI_ATOMS + lane] = esum;
+  __syncthreads();
+  if (warp == 0 && lane < na_blk) {
+    double e = D.beta0;
+    for (int w = 0; w < YI5_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
     eatom[atom] = e;
   }
 }
@@ -1536,6 +1783,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_ui_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_yi_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_yi_half, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaFuncSetAttribute(k_snap_yi_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
@@ -1563,9 +1811,13 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   prof_mark(ctx->stream, ST_YI, true);
   static const int yi_var = [] {
     const char* e = getenv("PL_SNAP_YI");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 5;
   }();
-  if (S->cgt_fits && yi_var == 4) {
+  if (S->yi_reg && yi_var >= 5) {
+    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(double) * YI5_WARPS * YI_ATOMS;
+    k_snap_yi_reg<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI5_WARPS * 32, sm, ctx->stream>>>(
+        D, na, buf.utot, buf.y, buf.eatom);
+  } else if (S->cgt_fits && yi_var == 4) {
     size_t sm = sizeof(C2) * D.nhalf * YI_ATOMS + sizeof(double) * YI3_WARPS * YI_ATOMS;
     k_snap_yi_half<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI3_WARPS * 32, sm, ctx->stream>>>(
         D, na, buf.utot, buf.y, buf.eatom);
