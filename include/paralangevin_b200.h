@@ -156,6 +156,21 @@ int pl_bootstrap(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int6
                  const double* d_noise_all, const double* h_amp, const double* d_mass, double dt,
                  double half_dt, double half_dt_gamma, int64_t* h_out, int32_t* h_blowup);
 
+/* Replica batch of corrected sweeps (mode 0) or bootstraps (mode 1), one
+ * persistent CTA per replica slot, for EAM / elementwise coarse potentials.
+ * Arrays carry a leading replica dimension: d_Q and d_P (R, N+1, d), the
+ * base and jump arrays (R, N, d), d_noise (R, N, L+1, d), d_hist (R, N).  Slot s works on
+ * replica h_ridx[s], windows h_m0[s]..h_m1[s]-1; h_state (2 per slot, {num,
+ * den} in/out) and h_out4 (4 per slot: nodes done, failing window, failing
+ * substep, kind 1 blow-up / 2 non-finite).  Synchronises. */
+int pl_sweep_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, int R_act,
+                   const int32_t* h_ridx, const int64_t* h_m0, const int64_t* h_m1,
+                   const int32_t* h_include_m0, int mode, double* d_Q, double* d_P,
+                   double* d_baseQ, double* d_baseP, const double* d_jumpQ, const double* d_jumpP,
+                   const double* d_noise, const double* h_amp, const double* d_mass, double dt,
+                   double half_dt, double half_dt_gamma, double expl, double* h_state,
+                   int64_t* h_out4, double* d_hist);
+
 /* d_out[i] = d_a[i] - d_b[i]  (jump = f.q - c.q, parareal.py:280). */
 int pl_sub(pl_ctx* ctx, int64_t n, const double* d_a, const double* d_b, double* d_out);
 

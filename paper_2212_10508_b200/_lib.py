@@ -58,6 +58,8 @@ SIGNATURES = {
     "pl_sweep": (C.c_int, [vp, vp, i64, C.c_int, i64, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp,
                            vp, pd, vp, dbl, dbl, dbl, dbl, pd, vp, pi64, pi32]),
     "pl_sub": (C.c_int, [vp, i64, vp, vp, vp]),
+    "pl_sweep_batch": (C.c_int, [vp, vp, i64, C.c_int, i64, C.c_int, pi32, pi64, pi64, pi32, C.c_int, vp, vp,
+                                 vp, vp, vp, vp, vp, pd, vp, dbl, dbl, dbl, dbl, pd, pi64, vp]),
     "pl_bootstrap": (C.c_int, [vp, vp, i64, C.c_int, i64, i64, vp, vp, vp, vp, vp, pd, vp, dbl, dbl, dbl,
                                pi64, pi32]),
     "pl_prof_begin": (C.c_int, [vp]),

@@ -53,6 +53,12 @@ struct SweepArgs {
   int* overflow;
   // elementwise
   EwProg ew;
+  // replica batch (grid = slots): per-slot replica index and slab, NULL for a single run
+  const int32_t* b_ridx;
+  const int64_t* b_m0;
+  const int64_t* b_m1;
+  const int32_t* b_inc;
+  int64_t s_traj, s_win, s_noise, s_hist;  // per-replica strides (elements)
 };
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -177,6 +183,31 @@ __device__ __forceinline__ void sw_force(const SweepArgs& A, const double* q, do
 
 __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
   extern __shared__ double sm[];
+  if (A.b_ridx) {
+    // replica slot: offset every per-replica array, take this slot's slab
+    const int slot = blockIdx.x;
+    const int64_t r = A.b_ridx[slot];
+    A.Q += r * A.s_traj;
+    A.P += r * A.s_traj;
+    A.prevQ += r * A.s_traj;
+    A.baseQ += r * A.s_win;
+    A.baseP += r * A.s_win;
+    A.jumpQ += r * A.s_win;
+    A.jumpP += r * A.s_win;
+    A.noise += r * A.s_noise;
+    A.hist += r * A.s_hist;
+    A.acc += 2 * slot;
+    A.out += 4 * slot;
+    A.m0 = A.b_m0[slot];
+    A.m1 = A.b_m1[slot];
+    A.include_m0 = A.b_inc[slot];
+    if (!A.use_ew) {
+      A.cand += (int64_t)slot * 2 * ((int64_t)A.n_atoms * (SW_MAXN + 1) + 8);
+      A.ncand = A.cand + (int64_t)A.n_atoms * SW_MAXN;
+      A.nbr = A.ncand + A.n_atoms + 4;
+      A.nnbr = A.nbr + (int64_t)A.n_atoms * SW_MAXN;
+    }
+  }
   const int64_t d = A.d;
   double* q = sm;
   double* p = q + d;
@@ -264,6 +295,8 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
     double e1 = 0.0, e2 = 0.0;
     int nonfinite = 0;
     for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
+      // prev[m+1] is read before cur[m+1] overwrites it (prevQ may alias Q)
+      const double pv = A.prevQ[(m + 1) * d + t];
       const double cq = add(q[t], A.jumpQ[m * d + t]);
       const double cp = add(p[t], A.jumpP[m * d + t]);
       A.Q[(m + 1) * d + t] = cq;
@@ -271,7 +304,6 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
       q[t] = cq;
       p[t] = cp;
       if (!isfinite(cq) || !isfinite(cp)) nonfinite = 1;
-      const double pv = A.prevQ[(m + 1) * d + t];
       const double e = sub(cq, pv);
       e1 += e * e;
       e2 += pv * pv;
@@ -383,4 +415,95 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
   return PL_OK;
 }
 
+// R_act replica slots in one launch (grid = R_act CTAs); arrays carry a leading
+// replica dimension: Q/P (R, N+1, d), base/jump (R, N, d), noise (R, N, L+1, d),
+// d_hist (R, N).  h_state (2 R_act) and h_out4 (4 R_act) per slot.
+int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, int R_act, const int32_t* h_ridx,
+                    const int64_t* h_m0, const int64_t* h_m1, const int32_t* h_inc, int mode, double* Q, double* P,
+                    double* baseQ, double* baseP, const double* jumpQ, const double* jumpP, const double* noise,
+                    const double* h_amp, const double* mass, double dt, double h, double hg, double expl,
+                    double* h_state, int64_t* h_out4, double* d_hist) {
+  if (R_act <= 0) return PL_OK;
+  SweepArgs A{};
+  const bool ew = is_elementwise(coarse);
+  if (!ew && coarse->kind != POT_EAM) return fail(PL_EARG, "batched sweep needs an EAM or elementwise coarse potential");
+  const int n = ew ? 0 : coarse->n_atoms;
+  const size_t smem = sizeof(double) * (4 * (size_t)d + (ew ? 0 : (size_t)n + 3 * (size_t)n));
+  if (smem > 200 * 1024) return fail(PL_EARG, "system too large for the persistent sweep");
+  A.d = d; A.n_atoms = n; A.L = L; A.mode = mode; A.use_ew = ew ? 1 : 0;
+  A.Q = Q; A.P = P; A.prevQ = Q; A.baseQ = baseQ; A.baseP = baseP; A.jumpQ = jumpQ; A.jumpP = jumpP;
+  A.noise = noise; A.mass = mass; A.dt = dt; A.h = h; A.hg = hg; A.expl = expl;
+  A.s_traj = (N + 1) * d;
+  A.s_win = N * d;
+  A.s_noise = N * (int64_t)(L + 1) * d;
+  A.s_hist = N;
+  cudaStream_t st = ctx->stream;
+  const size_t per_slot_lists = ew ? 0 : sizeof(int32_t) * 2 * ((size_t)n * (SW_MAXN + 1) + 8);
+  const size_t hdr = sizeof(double) * (L + 1) + sizeof(double) * 2 * R_act + sizeof(int64_t) * 4 * R_act +
+                     sizeof(int64_t) * 2 * R_act + sizeof(int32_t) * 2 * R_act + 256;
+  PL_TRY(ctx->work[4].reserve(hdr + per_slot_lists * R_act + 256));
+  char* w = (char*)ctx->work[4].ptr;
+  double* amp = (double*)w;
+  double* acc = amp + (L + 1);
+  int64_t* out = (int64_t*)(acc + 2 * R_act);
+  int64_t* m0 = out + 4 * R_act;
+  int64_t* m1 = m0 + R_act;
+  int32_t* ridx = (int32_t*)(m1 + R_act);
+  int32_t* inc = ridx + R_act;
+  int* ovf = (int*)(inc + R_act);
+  char* lists = (char*)(((uintptr_t)(ovf + 4) + 255) & ~(uintptr_t)255);
+  A.amp = amp; A.acc = acc; A.out = out; A.hist = d_hist;
+  A.b_ridx = ridx; A.b_m0 = m0; A.b_m1 = m1; A.b_inc = inc;
+  if (ew) {
+    PL_TRY(ew_program(coarse, &A.ew));
+  } else {
+    A.box = Box{{coarse->box[0], coarse->box[1], coarse->box[2]}};
+    A.rc2 = coarse->rcut * coarse->rcut;
+    A.rl2 = (coarse->rcut + SW_SKIN) * (coarse->rcut + SW_SKIN);
+    A.rho = Table{coarse->d_rho, coarse->n_r, coarse->dr};
+    A.phi = Table{coarse->d_phi, coarse->n_r, coarse->dr};
+    A.F = Table{coarse->d_F, coarse->n_rho, coarse->drho};
+    A.cand = (int32_t*)lists;
+    A.overflow = ovf;
+    A.tpa = eam_tpa(n, SW_THREADS);
+    PL_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
+  }
+  PL_CUDA(cudaMemcpyAsync(amp, h_amp, sizeof(double) * (L + 1), cudaMemcpyHostToDevice, st));
+  PL_CUDA(cudaMemcpyAsync(acc, h_state, sizeof(double) * 2 * R_act, cudaMemcpyHostToDevice, st));
+  PL_CUDA(cudaMemcpyAsync(m0, h_m0, sizeof(int64_t) * R_act, cudaMemcpyHostToDevice, st));
+  PL_CUDA(cudaMemcpyAsync(m1, h_m1, sizeof(int64_t) * R_act, cudaMemcpyHostToDevice, st));
+  PL_CUDA(cudaMemcpyAsync(ridx, h_ridx, sizeof(int32_t) * R_act, cudaMemcpyHostToDevice, st));
+  PL_CUDA(cudaMemcpyAsync(inc, h_inc, sizeof(int32_t) * R_act, cudaMemcpyHostToDevice, st));
+  static thread_local bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sweep_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_sweep_cta<<<R_act, SW_THREADS, smem, st>>>(A);
+  PL_CHECK_LAUNCH();
+  int hovf = 0;
+  PL_CUDA(cudaMemcpyAsync(h_state, acc, sizeof(double) * 2 * R_act, cudaMemcpyDeviceToHost, st));
+  PL_CUDA(cudaMemcpyAsync(h_out4, out, sizeof(int64_t) * 4 * R_act, cudaMemcpyDeviceToHost, st));
+  if (!ew) PL_CUDA(cudaMemcpyAsync(&hovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PL_CUDA(cudaStreamSynchronize(st));
+  if (hovf) return fail(PL_EPOT, "neighbour capacity exceeded in the coarse sweep");
+  return PL_OK;
+}
+
 }  // namespace pl
+
+extern "C" int pl_sweep_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, int R_act,
+                              const int32_t* h_ridx, const int64_t* h_m0, const int64_t* h_m1,
+                              const int32_t* h_include_m0, int mode, double* d_Q, double* d_P, double* d_baseQ,
+                              double* d_baseP, const double* d_jumpQ, const double* d_jumpP,
+                              const double* d_noise, const double* h_amp, const double* d_mass, double dt,
+                              double half_dt, double half_dt_gamma, double expl, double* h_state,
+                              int64_t* h_out4, double* d_hist) {
+  if (!ctx || !coarse || !h_ridx || !h_m0 || !h_m1 || !h_include_m0 || !d_Q || !d_P || !d_baseQ || !d_baseP ||
+      !d_noise || !h_amp || !h_state || !h_out4 || !d_hist)
+    return pl::fail(PL_EARG, "NULL argument");
+  if (mode == 0 && (!d_jumpQ || !d_jumpP)) return pl::fail(PL_EARG, "NULL jumps");
+  return pl::sweep_cta_batch(ctx, coarse, d, L, N, R_act, h_ridx, h_m0, h_m1, h_include_m0, mode, d_Q, d_P,
+                             d_baseQ, d_baseP, mode == 0 ? d_jumpQ : d_baseQ, mode == 0 ? d_jumpP : d_baseP,
+                             d_noise, h_amp, d_mass, dt, half_dt, half_dt_gamma, expl, h_state, h_out4, d_hist);
+}

@@ -405,11 +405,15 @@ def _classic_device(initial, fine, coarse, config, record_iterates):
                           iterates=tuple(iterates) if record_iterates else None)
 
 
-def _adaptive_device(initial, fine, coarse, config):
-    n = config.n_windows
-    conv, expl = config.delta_conv, config.delta_expl
+def _adaptive_machine(n, conv, expl, cap):
+    """Algorithm 2 (parareal.py:366-475) as a generator of device actions.
+
+    Yields ('bootstrap', n_init) and ('iterate', n_init, n_final, include_m0,
+    iteration); an 'iterate' is answered with (deltas, den) of the sweep.
+    Returns (slabs, history, converged).  The single-run and the replica-batch
+    engines drive this same machine, so both take the reference's decisions.
+    """
     mid = 0.5 * (conv + expl)
-    run = _DeviceRun(initial, fine, coarse, n)
     n_init = n_final = 0
     delta = mid
     n_slab = 0
@@ -419,7 +423,7 @@ def _adaptive_device(initial, fine, coarse, config):
     while n_final < n:
         if delta < expl:
             n_init, n_final = n_final, n
-            run.bootstrap(n_init)
+            yield ("bootstrap", n_init)
             n_slab += 1
             attempts = []
             k_in_slab = 0
@@ -427,28 +431,24 @@ def _adaptive_device(initial, fine, coarse, config):
         k_attempt = 0
         aborted = False
         while conv <= delta <= expl:
-            if k_attempt >= config.iteration_cap:
+            if k_attempt >= cap:
                 aborted = True
                 break
-            run.jumps(n_init, n_final, k_in_slab + 1)
-            run.snapshot_prev(n_init, n_final)
+            deltas, den = yield ("iterate", n_init, n_final, n_init >= 1, k_in_slab + 1)
             k_attempt += 1
             k_in_slab += 1
-            deltas, den = run.sweep(n_init, n_final, n_init >= 1, expl, k_in_slab)
-            for i, dl in enumerate(deltas):
-                m = n_init + i
+            for dl in deltas:
                 history.append((n_slab, k_in_slab, float(dl)))
                 delta = float(dl)
             if den == 0.0:
                 raise DegenerateNormalizationError(
-                    f"all reference positions on nodes {max(n_init, 1)}..{n_init + len(deltas)} "
-                    f"are zero")
+                    f"all reference positions on nodes {max(n_init, 1)}..{n_init + len(deltas)} are zero")
             if delta > expl:
                 m = n_init + len(deltas) - 1
                 if m == n_init:
                     raise SlabCollapseError(
-                        f"slab {n_slab} exploded at its first window {n_init + 1}; "
-                        f"no shorter slab exists", slab_index=n_slab, n_init=n_init)
+                        f"slab {n_slab} exploded at its first window {n_init + 1}; no shorter slab exists",
+                        slab_index=n_slab, n_init=n_init)
                 _close_attempt(attempts, n_init, n_final, k_attempt)
                 n_final = m
         if aborted:
@@ -461,8 +461,179 @@ def _adaptive_device(initial, fine, coarse, config):
             _close_attempt(attempts, n_init, n_final, k_attempt)
             slabs.append(SlabRecord(n_slab, n_init, tuple(attempts), n_final,
                                     sum(a.iterations for a in attempts)))
+    return slabs, history, converged
+
+
+def _adaptive_device(initial, fine, coarse, config):
+    n = config.n_windows
+    run = _DeviceRun(initial, fine, coarse, n)
+    machine = _adaptive_machine(n, config.delta_conv, config.delta_expl, config.iteration_cap)
+    reply = None
+    try:
+        while True:
+            act = machine.send(reply)
+            if act[0] == "bootstrap":
+                run.bootstrap(act[1])
+                reply = None
+            else:
+                _, n_init, n_final, inc, it = act
+                run.jumps(n_init, n_final, it)
+                run.snapshot_prev(n_init, n_final)
+                reply = run.sweep(n_init, n_final, inc, config.delta_expl, it)
+    except StopIteration as stop:
+        slabs, history, converged = stop.value
     return PararealResult(trajectory=run.trajectory(), slabs=tuple(slabs),
                           error_history=tuple(history), converged=converged)
+
+
+class _BatchRun:
+    """R independent replicas (own initial state and noise plan) on one device."""
+
+    def __init__(self, initials, fine_pot, coarse_pot, params, schedule, plans, n):
+        import torch
+        self.R, self.n = len(initials), n
+        d = initials[0].dim
+        self.d = d
+        self.fk = WindowKernel(fine_pot, params, schedule, d)
+        self.ck = WindowKernel(coarse_pot, params, schedule, d)
+        self.coarse_pot = coarse_pot
+        dev = self.fk.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        R, L = self.R, self.fk.L
+        self.Q = torch.zeros((R, n + 1, d), **f64)
+        self.P = torch.zeros((R, n + 1, d), **f64)
+        for r, st in enumerate(initials):
+            self.Q[r, 0] = torch.from_numpy(np.ascontiguousarray(st.q))
+            self.P[r, 0] = torch.from_numpy(np.ascontiguousarray(st.p))
+        self.baseQ = torch.zeros((R, n, d), **f64)
+        self.baseP = torch.zeros((R, n, d), **f64)
+        self.jumpQ = torch.zeros((R, n, d), **f64)
+        self.jumpP = torch.zeros((R, n, d), **f64)
+        self.hist = torch.zeros((R, n), **f64)
+        seeds = np.concatenate([np.asarray(p.window_seeds[:n], dtype=np.uint64) for p in plans])
+        self.noise = self.fk.noise(seeds).reshape(R, n, (L + 1) * d)
+
+    def _batch_call(self, slots, mode, expl):
+        import numpy as np_
+        lib, ctx = _lib.load(), _lib.context()
+        k = self.ck
+        Ra = len(slots)
+        ridx = np_.array([r for r, _, _, _ in slots], dtype=np_.int32)
+        m0 = np_.array([a for _, a, _, _ in slots], dtype=np_.int64)
+        m1 = np_.array([b for _, _, b, _ in slots], dtype=np_.int64)
+        inc = np_.array([1 if c else 0 for _, _, _, c in slots], dtype=np_.int32)
+        state = np_.zeros(2 * Ra)
+        out4 = np_.zeros(4 * Ra, dtype=np_.int64)
+        rc = lib.pl_sweep_batch(
+            ctx.handle, self.coarse_pot.handle(ctx), self.d, k.L, self.n, Ra, ridx.ctypes.data_as(_lib.pi32),
+            m0.ctypes.data_as(_lib.pi64), m1.ctypes.data_as(_lib.pi64), inc.ctypes.data_as(_lib.pi32), mode,
+            _lib.ptr(self.Q), _lib.ptr(self.P), _lib.ptr(self.baseQ), _lib.ptr(self.baseP),
+            _lib.ptr(self.jumpQ), _lib.ptr(self.jumpP), _lib.ptr(self.noise), _lib.dptr(k.amp),
+            _lib.ptr(k.mass), k.dt, k.h, k.hg, float(expl), _lib.dptr(state),
+            out4.ctypes.data_as(_lib.pi64), _lib.ptr(self.hist))
+        _lib.check(rc)
+        return state.reshape(Ra, 2), out4.reshape(Ra, 4)
+
+    def bootstrap(self, items):
+        """items: [(replica, n_init)]"""
+        slots = [(r, a, self.n, False) for r, a in items]
+        _, out4 = self._batch_call(slots, 1, 0.0)
+        for (r, a), o in zip(items, out4):
+            if o[3] == 1:
+                raise BlowUpError(f"replica {r}: coarse bootstrap blew up at substep {int(o[2])}",
+                                  substep=int(o[2]), window=int(o[1]) + 1, iteration=0)
+
+    def iterate(self, items, expl):
+        """items: [(replica, n_init, n_final, include_m0, iteration)] -> [(deltas, den)]"""
+        import torch
+        d, n = self.d, self.n
+        rows_q = torch.tensor([r * (n + 1) + m for r, a, b, _, _ in items for m in range(a, b)],
+                              dtype=torch.long, device=self.Q.device)
+        rows_w = torch.tensor([r * n + m for r, a, b, _, _ in items for m in range(a, b)],
+                              dtype=torch.long, device=self.Q.device)
+        Qs = self.Q.view(-1, d).index_select(0, rows_q)
+        Ps = self.P.view(-1, d).index_select(0, rows_q)
+        Ns = self.noise.view(-1, self.noise.shape[-1]).index_select(0, rows_w)
+
+        def run_block(lo, hi):
+            return self.fk.run(Qs[lo:hi].contiguous(), Ps[lo:hi].contiguous(), Ns[lo:hi].contiguous())
+
+        FQ, FP, blow = sharded_fine(run_block, 0, rows_w.numel())
+        b = blow.cpu().numpy()
+        if b.any():
+            i = int(np.nonzero(b)[0][0])
+            raise BlowUpError(f"fine window blew up at substep {int(b[i])} (batch row {i})",
+                              substep=int(b[i]))
+        lib, ctx = _lib.load(), _lib.context()
+        bq = self.baseQ.view(-1, d).index_select(0, rows_w)
+        bp = self.baseP.view(-1, d).index_select(0, rows_w)
+        jq = torch.empty_like(bq)
+        jp = torch.empty_like(bp)
+        _lib.check(lib.pl_sub(ctx.handle, jq.numel(), _lib.ptr(FQ), _lib.ptr(bq), _lib.ptr(jq)))
+        _lib.check(lib.pl_sub(ctx.handle, jp.numel(), _lib.ptr(FP), _lib.ptr(bp), _lib.ptr(jp)))
+        self.jumpQ.view(-1, d).index_copy_(0, rows_w, jq)
+        self.jumpP.view(-1, d).index_copy_(0, rows_w, jp)
+        slots = [(r, a, b, inc) for r, a, b, inc, _ in items]
+        state, out4 = self._batch_call(slots, 0, expl)
+        hist = self.hist.cpu().numpy()
+        res = []
+        for (r, a, b_, inc, it), st, o in zip(items, state, out4):
+            if o[3] == 1:
+                raise BlowUpError(f"replica {r}: coarse window blew up at substep {int(o[2])}",
+                                  substep=int(o[2]), window=int(o[1]) + 1, iteration=it)
+            if o[3] == 2:
+                raise BlowUpError(f"replica {r}: corrected state is not finite at window {int(o[1]) + 1}",
+                                  window=int(o[1]) + 1, iteration=it)
+            res.append((hist[r, a:a + int(o[0])].copy(), float(st[1])))
+        return res
+
+    def trajectory(self, r):
+        return NodeTrajectory.from_arrays(self.Q[r].cpu().numpy(), self.P[r].cpu().numpy())
+
+
+def parareal_adaptive_batch(initials, pair: PropagatorPair, params: LangevinParams,
+                            schedule: TemperatureSchedule, plans, config: PararealConfig):
+    """Adaptive parareal for many independent replicas at once (ensemble protocol).
+
+    Replica r starts from ``initials[r]`` with noise plan ``plans[r]`` and runs
+    exactly the reference algorithm (the same ``_adaptive_machine``); the
+    device work of all replicas is batched: one bootstrap launch, one
+    fine-stage launch (slices x replicas, sharded over ranks) and one sweep
+    launch (one persistent CTA per replica) per round.  Returns one
+    ``PararealResult`` per replica.
+    """
+    if config.delta_expl is None:
+        raise ValueError("adaptive mode needs delta_expl in the configuration")
+    n = config.n_windows
+    for p in plans:
+        _check_plan(p, n)
+    run = _BatchRun(initials, pair.fine, pair.coarse, params, schedule, plans, n)
+    machines = [_adaptive_machine(n, config.delta_conv, config.delta_expl, config.iteration_cap)
+                for _ in initials]
+    results = [None] * len(initials)
+    pending = {}
+    for r, mch in enumerate(machines):
+        pending[r] = next(mch)
+    while pending:
+        boots = [(r, act[1]) for r, act in pending.items() if act[0] == "bootstrap"]
+        replies = {}
+        if boots:
+            run.bootstrap(boots)
+            for r, _ in boots:
+                replies[r] = None
+        else:
+            its = [(r,) + act[1:] for r, act in pending.items()]
+            for (r, *_), rep in zip(its, run.iterate(its, config.delta_expl)):
+                replies[r] = rep
+        for r, rep in replies.items():
+            try:
+                pending[r] = machines[r].send(rep)
+            except StopIteration as stop:
+                slabs, history, converged = stop.value
+                results[r] = PararealResult(trajectory=run.trajectory(r), slabs=tuple(slabs),
+                                            error_history=tuple(history), converged=converged)
+                del pending[r]
+    return results
 
 
 # ---- generic control flow over arbitrary callables (scripted propagators)

@@ -227,3 +227,20 @@ def test_lj13_adaptive_vs_reference(pl, golden):
     np.testing.assert_allclose(res.trajectory.positions(), z["lj13_Q"], rtol=0, atol=1e-10)
     h = np.array(res.error_history, float)
     np.testing.assert_allclose(h[:, 2], z["lj13_hist"][:, 2], rtol=1e-6, atol=1e-13)
+
+
+def test_batched_replicas_equal_single_runs_dw(pl):
+    """parareal_adaptive_batch == per-replica parareal_adaptive, bit for bit (adaptive.json params)."""
+    params = pl.LangevinParams(0.5, 0.4, 0.05, 2)
+    sched = pl.TemperatureSchedule.robust(2)
+    n = 200
+    pair = pl.PropagatorPair(pl.DoubleWell(1.0, 1.0), pl.DoubleWell(0.8, 1.0), 175.0, 1.0)
+    cfg = pl.PararealConfig(n, 1e-10, 0.35)
+    plans = [pl.NoisePlan.for_windows(pl.derive_seed(77, 10**9 + i), n) for i in range(5)]
+    inits = [pl.PhaseState(q=[-1.0 + 0.1 * i], p=[0.0]) for i in range(5)]
+    batch = pl.parareal_adaptive_batch(inits, pair, params, sched, plans, cfg)
+    for i in range(5):
+        one = pl.parareal_adaptive(inits[i], pair, params, sched, plans[i], cfg)
+        assert one.slabs == batch[i].slabs
+        assert one.error_history == batch[i].error_history
+        assert one.trajectory.positions().tobytes() == batch[i].trajectory.positions().tobytes()

@@ -290,3 +290,21 @@ def test_cell_list_matches_brute_force(pl, rcut_kind):
     dev = _device_neighbours(pl, pot, Q)
     for b in range(Q.shape[0]):
         assert dev[b] == native.neighbours(Q[b], box, rc)
+
+
+def test_batched_replicas_equal_single_runs_snap_eam(pl):
+    """Replica batch (SNAP fine / EAM coarse) == single runs, bit for bit."""
+    from paper_2212_10508_b200 import tungsten as W
+    L, N = 5, 4
+    q0, box, n, mass, params, sched, p0 = _w_pr1_setup(pl, L, N)
+    pair = pl.PropagatorPair(W.make_snap(n, box), W.make_eam(n, box), 100.0, 1.0)
+    cfg = pl.PararealConfig(N, 1e-10, 0.35)
+    rs = np.random.default_rng(3)
+    inits = [pl.PhaseState(q=q0 + 0.02 * rs.normal(size=q0.shape), p=p0) for _ in range(3)]
+    plans = [pl.NoisePlan.for_windows(pl.derive_seed(5, 10**9 + i), N) for i in range(3)]
+    batch = pl.parareal_adaptive_batch(inits, pair, params, sched, plans, cfg)
+    for i in range(3):
+        one = pl.parareal_adaptive(inits[i], pair, params, sched, plans[i], cfg)
+        assert one.slabs == batch[i].slabs
+        assert one.error_history == batch[i].error_history
+        assert one.trajectory.positions().tobytes() == batch[i].trajectory.positions().tobytes()
