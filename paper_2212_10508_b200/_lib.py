@@ -129,6 +129,10 @@ class Context:
         return self.handle
 
     def __del__(self):
+        # at interpreter shutdown the CUDA runtime may already be gone: leave it to the driver
+        import sys
+        if sys.is_finalizing():
+            return
         try:
             if _lib is not None and self.handle:
                 _lib.pl_ctx_destroy(self.handle)

@@ -252,8 +252,9 @@ int pl_pot_snap(pl_ctx* ctx, int n_atoms, const double* h_box, int twojmax, doub
 }
 
 int pl_pot_destroy(pl_pot* p) {
+  // does not touch p->ctx: contexts and potentials may be released in any order
+  // (e.g. at interpreter shutdown); cudaFree synchronises with the device itself
   if (!p) return PL_OK;
-  if (p->ctx) cudaStreamSynchronize(p->ctx->stream);
   cudaFree(p->d_c0);
   cudaFree(p->d_c1);
   cudaFree(p->d_rho);

@@ -74,6 +74,7 @@ struct SnapIndex {
   double* d_cg = nullptr;
   double beta0 = 0.0;
   double flops_ui_pair = 0, flops_yi_atom = 0, flops_de_pair = 0;
+  double flops_de_pair_adj = 0, flops_yi_atom_reg = 0;
   bool cgt_fits = false;
   bool yi_reg = false;  // k_snap_yi_reg usable (twojmax = 8, CG table in constant memory)
   double* d_yi5 = nullptr;  // [2][NT]: coefY(X,Y,J), beta_b of canonical triples (else 0)
@@ -137,6 +138,7 @@ __constant__ int c_yi5_jstart[yi5::TJ + 2];  // triples of row-layer J: [jstart[
 __constant__ int c_yi5_tlist[130];    // triple ids sorted by J
 __constant__ int c_yi5_gseg[YI5_WARPS + 1];  // groups of warp w
 __constant__ int c_yi5_groups[32];    // (J << 8) | mb
+__constant__ int c_yi5_cgoff[130];    // triple id -> offset of its block in c_cgt
 
 // ------------------------------------------------------------------ host setup
 static double fact(int n) {
@@ -291,6 +293,11 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     PL_CUDA(cudaMalloc(&S->d_yi5, sizeof(double) * cb2.size()));
     PL_CUDA(cudaMemcpy(S->d_yi5, cb2.data(), sizeof(double) * cb2.size(), cudaMemcpyHostToDevice));
     PL_CUDA(cudaMemcpyToSymbol(c_yi5_code, code.data(), sizeof(int) * code.size()));
+    {
+      std::vector<int> offs;
+      for (int c : code) offs.push_back(cgblk[{c / 100, (c / 10) % 10, c % 10}]);
+      PL_CUDA(cudaMemcpyToSymbol(c_yi5_cgoff, offs.data(), sizeof(int) * offs.size()));
+    }
     PL_CUDA(cudaMemcpyToSymbol(c_yi5_tlist, tlist.data(), sizeof(int) * tlist.size()));
     PL_CUDA(cudaMemcpyToSymbol(c_yi5_jstart, jstart.data(), sizeof(int) * jstart.size()));
     PL_CUDA(cudaMemcpyToSymbol(c_yi5_gseg, gseg.data(), sizeof(int) * gseg.size()));
@@ -427,6 +434,27 @@ int snap_prepare(pl_pot* pot, const double* beta) {
   }
   S->flops_ui_pair += 40.0;
   S->flops_de_pair += 80.0;
+  // reverse-mode pair kernel: forward U + F contraction (25/element), adjoint
+  // (S_a, S_b, G update, direct Y term: 42/element), geometry + final (150)
+  S->flops_de_pair_adj = 150.0;
+  for (int J = 1; J <= tj; ++J) S->flops_de_pair_adj += (J + 1) * (J / 2 + 1) * 67.0;
+  // register-tiled Z/Y: the middle row's upper half (zero weight) is skipped
+  S->flops_yi_atom_reg = 0.0;
+  for (int x = 0; x <= tj; ++x)
+    for (int y = 0; y <= x; ++y)
+      for (int J = x - y; J <= std::min(tj, x + y); J += 2) {
+        const int sh = (x + y - J) / 2;
+        for (int mb = 0; 2 * mb <= J; ++mb) {
+          int nb = 0;
+          for (int mb1 = 0; mb1 <= x; ++mb1) nb += (mb + sh - mb1 >= 0 && mb + sh - mb1 <= y);
+          for (int ma = 0; ma <= J; ++ma) {
+            if (2 * mb == J && 2 * ma > J) continue;
+            int na = 0;
+            for (int ma1 = 0; ma1 <= x; ++ma1) na += (ma + sh - ma1 >= 0 && ma + sh - ma1 <= y);
+            S->flops_yi_atom_reg += 10.0 * na * nb + 4.0 * nb + 8.0;
+          }
+        }
+      }
   cudaError_t e1 = cudaMalloc(&S->d_items, sizeof(SnapItem) * items.size());
   cudaError_t e2 = cudaMalloc(&S->d_units, sizeof(SnapUnit) * units.size());
   cudaError_t e3 = cudaMalloc(&S->d_useg, sizeof(int32_t) * useg.size());
@@ -1035,6 +1063,132 @@ k_snap_yi_reg(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __rest
     for (int k = c_yi5_jstart[J]; k < c_yi5_jstart[J + 1]; ++k) {
       const int tid = c_yi5_tlist[k];
       yi5_call(c_yi5_code[tid], D.yi5[tid], D.yi5[yi5::NT + tid], Ul, mb, yacc, esum);
+    }
+    if (lane < na_blk) {
+      C2* yo = ylist + atom * D.nhalf + c_hoff[J] + mb * (J + 1);
+#pragma unroll
+      for (int m = 0; m <= yi5::TJ; ++m)
+        if (m <= J) yo[m] = yacc[m];
+    }
+  }
+  epart[warp * YI_ATOMS + lane] = esum;
+  __syncthreads();
+  if (warp == 0 && lane < na_blk) {
+    double e = D.beta0;
+    for (int w = 0; w < YI5_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
+    eatom[atom] = e;
+  }
+}
+
+// v6: small code.  Row work (J, mb) per warp as in v5, but one instantiation per X
+// only: the U^X column sits in registers (compile-time ma1), U^Y is read from
+// shared memory (one load per product), the z row accumulates in a per-lane
+// shared strip, CG rows come from constant memory with warp-uniform offsets.
+template <int X>
+__device__ __forceinline__ void yi6_xyj(const C2* __restrict__ Ul, int Y, int J, int mb, int off, double cy,
+                                        double be, C2* __restrict__ zs, C2 (&yacc)[yi5::TJ + 1], double& esum) {
+  const int SH = (X + Y - J) / 2;
+  const bool mid = (2 * mb == J);
+  const int jtop = mid ? J / 2 : J;  // middle row: upper half has zero weight
+  for (int ma = 0; ma <= jtop; ++ma) zs[ma * 32] = C2{0.0, 0.0};
+  const int lo = max(0, mb + SH - Y), hi = min(X, mb + SH);
+  const int FX = c_foff[X], FY = c_foff[Y];
+  for (int mb1 = lo; mb1 <= hi; ++mb1) {
+    const int mb2 = mb + SH - mb1;
+    C2 ux[X + 1];
+    const C2* px = Ul + (FX + mb1 * (X + 1)) * YI_ATOMS;
+#pragma unroll
+    for (int a = 0; a <= X; ++a) ux[a] = px[a * YI_ATOMS];
+    const C2* py = Ul + (FY + mb2 * (Y + 1)) * YI_ATOMS;
+    const double cb = c_cgt[off + mb * (X + 1) + mb1];
+    for (int ma = 0; ma <= jtop; ++ma) {
+      const double* cga = c_cgt + off + ma * (X + 1);
+      const int base2 = ma + SH;  // ma2 = base2 - ma1
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int ma1 = 0; ma1 <= X; ++ma1) {
+        const int ma2 = base2 - ma1;
+        if (ma2 >= 0 && ma2 <= Y) {
+          const C2 uy = py[ma2 * YI_ATOMS];
+          const double c = cga[ma1];
+          sr += c * (ux[ma1].re * uy.re - ux[ma1].im * uy.im);
+          si += c * (ux[ma1].re * uy.im + ux[ma1].im * uy.re);
+        }
+      }
+      C2 zz = zs[ma * 32];
+      zz.re += cb * sr;
+      zz.im += cb * si;
+      zs[ma * 32] = zz;
+    }
+  }
+  const C2* pj = Ul + (c_foff[J] + mb * (J + 1)) * YI_ATOMS;
+#pragma unroll
+  for (int ma = 0; ma <= yi5::TJ; ++ma) {
+    if (ma > jtop) break;
+    const C2 z = zs[ma * 32];
+    yacc[ma].re += cy * z.re;
+    yacc[ma].im += cy * z.im;
+    if (be != 0.0) {
+      const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+      const C2 u = pj[ma * YI_ATOMS];
+      esum += be * w * (u.re * z.re + u.im * z.im);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(YI5_WARPS * 32)
+k_snap_yi_six(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
+              double* __restrict__ eatom) {
+  extern __shared__ double smem[];
+  C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
+  C2* zsm = Uf + D.nfull * YI_ATOMS;                                   // [warps][9][32]
+  double* epart = reinterpret_cast<double*>(zsm + YI5_WARPS * (yi5::TJ + 1) * YI_ATOMS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
+  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
+  for (int t = threadIdx.x; t < D.nfull * YI_ATOMS; t += blockDim.x) {
+    const int at = t & (YI_ATOMS - 1), f = t >> 5;
+    int J = 0;
+    while (J < D.tj && f >= c_foff[J + 1]) ++J;
+    const int e = f - c_foff[J], mb = e / (J + 1), ma = e - mb * (J + 1);
+    C2 v{0.0, 0.0};
+    if (at < na_blk) {
+      if (2 * mb <= J) {
+        v = utot[(a0 + at) * D.nhalf + c_hoff[J] + mb * (J + 1) + ma];
+      } else {
+        C2 w = utot[(a0 + at) * D.nhalf + c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
+        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
+      }
+    }
+    Uf[f * YI_ATOMS + at] = v;
+  }
+  __syncthreads();
+  const C2* Ul = Uf + lane;
+  C2* zs = zsm + warp * (yi5::TJ + 1) * YI_ATOMS + lane;
+  const int64_t atom = a0 + lane;
+  double esum = 0.0;
+  for (int gi = c_yi5_gseg[warp]; gi < c_yi5_gseg[warp + 1]; ++gi) {
+    const int J = c_yi5_groups[gi] >> 8, mb = c_yi5_groups[gi] & 0xff;
+    C2 yacc[yi5::TJ + 1];
+#pragma unroll
+    for (int m = 0; m <= yi5::TJ; ++m) yacc[m] = C2{0.0, 0.0};
+    for (int k = c_yi5_jstart[J]; k < c_yi5_jstart[J + 1]; ++k) {
+      const int tid = c_yi5_tlist[k];
+      const int code = c_yi5_code[tid];
+      const int X = code / 100, Y = (code / 10) % 10;
+      const int off = c_yi5_cgoff[tid];
+      const double cy = D.yi5[tid], be = D.yi5[yi5::NT + tid];
+      switch (X) {
+        case 0: yi6_xyj<0>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 1: yi6_xyj<1>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 2: yi6_xyj<2>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 3: yi6_xyj<3>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 4: yi6_xyj<4>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 5: yi6_xyj<5>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 6: yi6_xyj<6>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 7: yi6_xyj<7>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+        default: yi6_xyj<8>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+      }
     }
     if (lane < na_blk) {
       C2* yo = ylist + atom * D.nhalf + c_hoff[J] + mb * (J + 1);
@@ -1784,6 +1938,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_yi_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_yi_half, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cudaFuncSetAttribute(k_snap_yi_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_snap_yi_six, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
@@ -1813,7 +1968,12 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     const char* e = getenv("PL_SNAP_YI");
     return e ? atoi(e) : 5;
   }();
-  if (S->yi_reg && yi_var >= 5) {
+  if (S->yi_reg && yi_var == 6) {
+    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI5_WARPS * 9 * YI_ATOMS +
+                sizeof(double) * YI5_WARPS * YI_ATOMS;
+    k_snap_yi_six<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI5_WARPS * 32, sm, ctx->stream>>>(
+        D, na, buf.utot, buf.y, buf.eatom);
+  } else if (S->yi_reg && yi_var >= 5) {
     size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(double) * YI5_WARPS * YI_ATOMS;
     k_snap_yi_reg<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI5_WARPS * 32, sm, ctx->stream>>>(
         D, na, buf.utot, buf.y, buf.eatom);
@@ -1908,6 +2068,15 @@ extern "C" int pl_snap_info(pl_pot* pot, int32_t* h_counts, double* h_flops) {
   const pl::SnapIndex* S = pot->snap;
   h_counts[0] = S->nhalf; h_counts[1] = S->nfull; h_counts[2] = S->nB; h_counts[3] = S->nitems;
   h_counts[4] = S->nunits;
-  h_flops[0] = S->flops_ui_pair; h_flops[1] = S->flops_yi_atom; h_flops[2] = S->flops_de_pair;
+  // FLOPs of the kernel variants that compute_snap actually launches
+  const char* ey = getenv("PL_SNAP_YI");
+  const int yv = ey ? atoi(ey) : 5;
+  const char* ea = getenv("PL_SNAP_ADJ");
+  const char* er = getenv("PL_SNAP_RR");
+  const bool rr = !(er && er[0] == '0') && S->tj == 8;
+  const bool adj = rr && !(ea && ea[0] == '0');
+  h_flops[0] = S->flops_ui_pair;
+  h_flops[1] = (S->yi_reg && yv >= 5) ? S->flops_yi_atom_reg : S->flops_yi_atom;
+  h_flops[2] = adj ? S->flops_de_pair_adj : S->flops_de_pair;
   return PL_OK;
 }

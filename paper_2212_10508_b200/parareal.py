@@ -584,7 +584,7 @@ class _BatchRun:
             if o[3] == 2:
                 raise BlowUpError(f"replica {r}: corrected state is not finite at window {int(o[1]) + 1}",
                                   window=int(o[1]) + 1, iteration=it)
-            res.append((hist[r, a:a + int(o[0])].copy(), float(st[1])))
+            res.append((hist[r, :int(o[0])].copy(), float(st[1])))  # hist[r, m - m0]
         return res
 
     def trajectory(self, r):

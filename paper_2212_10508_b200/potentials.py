@@ -73,6 +73,9 @@ class Potential:
         return h
 
     def __del__(self):
+        import sys
+        if sys.is_finalizing():
+            return
         try:
             for h in self.__dict__.get("_handles", {}).values():
                 if _lib._lib is not None and h:
