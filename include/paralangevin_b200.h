@@ -174,6 +174,12 @@ int pl_sweep_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, int
 /* d_out[i] = d_a[i] - d_b[i]  (jump = f.q - c.q, parareal.py:280). */
 int pl_sub(pl_ctx* ctx, int64_t n, const double* d_a, const double* d_b, double* d_out);
 
+/* ---- SIA hop detection (next row after the hot path) ---- */
+/* d_label[b] = smallest doubly occupied BCC site (Wigner-Seitz occupancy) of
+ * configuration b (B x 3*n_atoms, unwrapped positions, cubic box n_cells*a). */
+int pl_sia_sites(pl_ctx* ctx, int64_t B, int n_atoms, int n_cells, double a, const double* d_q,
+                 int32_t* d_label);
+
 /* ---- measurement --------------------------------------------------------- */
 /* Record CUDA events around every kernel stage launched by this host thread
  * until pl_prof_end, which synchronises and returns per-stage summed kernel

@@ -8,6 +8,7 @@ CUDA device is missing, every entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import sys as _sys
 import os
 import threading
 
@@ -62,6 +63,7 @@ SIGNATURES = {
                                  vp, vp, vp, vp, vp, pd, vp, dbl, dbl, dbl, dbl, pd, pi64, vp]),
     "pl_bootstrap": (C.c_int, [vp, vp, i64, C.c_int, i64, i64, vp, vp, vp, vp, vp, pd, vp, dbl, dbl, dbl,
                                pi64, pi32]),
+    "pl_sia_sites": (C.c_int, [vp, i64, C.c_int, C.c_int, dbl, vp, vp]),
     "pl_prof_begin": (C.c_int, [vp]),
     "pl_prof_end": (C.c_int, [vp, C.c_int, pd, pi64]),
     "pl_fp64_peak": (C.c_int, [vp, pd]),
@@ -130,10 +132,9 @@ class Context:
 
     def __del__(self):
         # at interpreter shutdown the CUDA runtime may already be gone: leave it to the driver
-        import sys
-        if sys.is_finalizing():
-            return
         try:
+            if _sys.is_finalizing():
+                return
             if _lib is not None and self.handle:
                 _lib.pl_ctx_destroy(self.handle)
         except Exception:

@@ -17,6 +17,7 @@ accept device tensors, which is how the engines call them.
 from __future__ import annotations
 
 import ctypes as C
+import sys as _sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -73,10 +74,9 @@ class Potential:
         return h
 
     def __del__(self):
-        import sys
-        if sys.is_finalizing():
-            return
         try:
+            if _sys.is_finalizing():
+                return
             for h in self.__dict__.get("_handles", {}).values():
                 if _lib._lib is not None and h:
                     _lib._lib.pl_pot_destroy(h)

@@ -180,10 +180,24 @@ def make_parareal():
                         versions=json.dumps(_versions()), **out)
 
 
+def make_residence():
+    from paralangevin import analysis as an
+    rs = np.random.default_rng(42)
+    labels = np.repeat(rs.integers(0, 4, size=60), rs.integers(1, 7, size=60))
+    out = {"labels": labels}
+    for mr in (1, 3):
+        ev = an.residence_times(labels, min_run=mr)
+        out[f"events_{mr}"] = np.array([[e.basin, e.duration, int(e.censored)] for e in ev], dtype=np.int64)
+        done = [e.duration for e in ev if not e.censored]
+        out[f"ci_{mr}"] = np.array(an.mean_ci(done))
+    np.savez_compressed(os.path.join(OUT, "residence_golden.npz"), versions=json.dumps(_versions()), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     make_rng()
     make_window()
     make_parareal()
+    make_residence()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -308,3 +308,32 @@ def test_batched_replicas_equal_single_runs_snap_eam(pl):
         assert one.slabs == batch[i].slabs
         assert one.error_history == batch[i].error_history
         assert one.trajectory.positions().tobytes() == batch[i].trajectory.positions().tobytes()
+
+
+def test_sia_site_labels(pl):
+    """Wigner-Seitz SIA site: dumbbell site found, moves with a lattice translation, PBC-invariant."""
+    from paper_2212_10508_b200 import sia, tungsten as W
+    n = 4
+    q0, box = W.bcc_sia(n)
+    a = W.A0
+    # the removed host site of bcc_sia is the site nearest (n/2, n/2, n/2) a
+    lab = sia.sia_site_labels(q0[None, :], n, a)[0]
+    c = n // 2
+    host = n ** 3 + ((c % n) * n + (c % n)) * n + (c % n) if False else None
+    X = q0.reshape(-1, 3)
+    mid = X[-2:].mean(axis=0)  # dumbbell centre = host site
+    u = mid / a
+    if np.allclose(u, np.round(u)):
+        i, j, k = (np.round(u).astype(int) % n)
+        host = (i * n + j) * n + k
+    else:
+        i, j, k = (np.floor(u).astype(int) % n)
+        host = n ** 3 + (i * n + j) * n + k
+    assert lab == host
+    # unwrapped copy (+ box) and a whole-lattice translation by one cubic cell
+    shifted = (X + np.array(box)).ravel()
+    moved = (X + np.array([a, 0.0, 0.0])).ravel()
+    labs = sia.sia_site_labels(np.stack([q0, shifted, moved]), n, a)
+    i2 = ((lab // n ** 2 % n) + 1) % n if lab < n ** 3 else None
+    assert labs[0] == labs[1] == lab
+    assert labs[2] != lab

@@ -107,3 +107,14 @@ def test_oracle_neighbour_counts():
     q, box = W.bcc_sia(4, sia=False)
     assert {len(x) for x in native.neighbours(q, box, 4.73)} == {26}
     assert {len(x) for x in native.neighbours(q, box, 5.5)} == {58}
+
+
+def test_residence_times_match_reference(golden):
+    from paper_2212_10508_b200 import sia
+    z = golden("residence_golden.npz")
+    for mr in (1, 3):
+        ev = sia.residence_times(z["labels"], min_run=mr)
+        got = np.array([[e.basin, e.duration, int(e.censored)] for e in ev], dtype=np.int64)
+        assert np.array_equal(got, z[f"events_{mr}"])
+        ci = sia.mean_ci([e.duration for e in ev if not e.censored])
+        assert np.array(ci).tobytes() == z[f"ci_{mr}"].tobytes()
