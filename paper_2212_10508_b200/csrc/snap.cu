@@ -139,6 +139,9 @@ __constant__ int c_yi5_tlist[130];    // triple ids sorted by J
 __constant__ int c_yi5_gseg[YI5_WARPS + 1];  // groups of warp w
 __constant__ int c_yi5_groups[32];    // (J << 8) | mb
 __constant__ int c_yi5_cgoff[130];    // triple id -> offset of its block in c_cgt
+constexpr int YI6_WARPS = 16;
+__constant__ int c_yi6_gseg[YI6_WARPS + 1];
+__constant__ int c_yi6_groups[32];
 
 // ------------------------------------------------------------------ host setup
 static double fact(int n) {
@@ -274,20 +277,27 @@ int snap_prepare(pl_pot* pot, const double* beta) {
         rows.push_back({c, (J << 8) | mb});
       }
     std::sort(rows.begin(), rows.end(), [](auto& a, auto& b) { return a.first > b.first; });
-    const int NW = 8;
-    std::vector<std::vector<int>> wr(NW);
-    std::vector<double> wl(NW, 0.0);
-    for (auto& r : rows) {
-      int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
-      wr[w].push_back(r.second);
-      wl[w] += r.first;
-    }
-    std::vector<int> groups, gseg(NW + 1, 0);
-    for (int w = 0; w < NW; ++w) {
-      gseg[w] = (int)groups.size();
-      groups.insert(groups.end(), wr[w].begin(), wr[w].end());
-    }
-    gseg[NW] = (int)groups.size();
+    auto lpt = [&](int NW, std::vector<int>& groups, std::vector<int>& gseg) {
+      std::vector<std::vector<int>> wr(NW);
+      std::vector<double> wl(NW, 0.0);
+      for (auto& r : rows) {
+        int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
+        wr[w].push_back(r.second);
+        wl[w] += r.first;
+      }
+      gseg.assign(NW + 1, 0);
+      groups.clear();
+      for (int w = 0; w < NW; ++w) {
+        gseg[w] = (int)groups.size();
+        groups.insert(groups.end(), wr[w].begin(), wr[w].end());
+      }
+      gseg[NW] = (int)groups.size();
+    };
+    std::vector<int> groups, gseg, groups16, gseg16;
+    lpt(8, groups, gseg);
+    lpt(YI6_WARPS, groups16, gseg16);
+    PL_CUDA(cudaMemcpyToSymbol(c_yi6_gseg, gseg16.data(), sizeof(int) * gseg16.size()));
+    PL_CUDA(cudaMemcpyToSymbol(c_yi6_groups, groups16.data(), sizeof(int) * groups16.size()));
     std::vector<double> cb2(cy);
     cb2.insert(cb2.end(), be.begin(), be.end());
     PL_CUDA(cudaMalloc(&S->d_yi5, sizeof(double) * cb2.size()));
@@ -1136,13 +1146,13 @@ __device__ __forceinline__ void yi6_xyj(const C2* __restrict__ Ul, int Y, int J,
   }
 }
 
-__global__ void __launch_bounds__(YI5_WARPS * 32)
+__global__ void __launch_bounds__(YI6_WARPS * 32)
 k_snap_yi_six(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
               double* __restrict__ eatom) {
   extern __shared__ double smem[];
   C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
   C2* zsm = Uf + D.nfull * YI_ATOMS;                                   // [warps][9][32]
-  double* epart = reinterpret_cast<double*>(zsm + YI5_WARPS * (yi5::TJ + 1) * YI_ATOMS);
+  double* epart = reinterpret_cast<double*>(zsm + YI6_WARPS * (yi5::TJ + 1) * YI_ATOMS);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
   const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
@@ -1167,8 +1177,8 @@ k_snap_yi_six(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __rest
   C2* zs = zsm + warp * (yi5::TJ + 1) * YI_ATOMS + lane;
   const int64_t atom = a0 + lane;
   double esum = 0.0;
-  for (int gi = c_yi5_gseg[warp]; gi < c_yi5_gseg[warp + 1]; ++gi) {
-    const int J = c_yi5_groups[gi] >> 8, mb = c_yi5_groups[gi] & 0xff;
+  for (int gi = c_yi6_gseg[warp]; gi < c_yi6_gseg[warp + 1]; ++gi) {
+    const int J = c_yi6_groups[gi] >> 8, mb = c_yi6_groups[gi] & 0xff;
     C2 yacc[yi5::TJ + 1];
 #pragma unroll
     for (int m = 0; m <= yi5::TJ; ++m) yacc[m] = C2{0.0, 0.0};
@@ -1201,7 +1211,7 @@ k_snap_yi_six(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __rest
   __syncthreads();
   if (warp == 0 && lane < na_blk) {
     double e = D.beta0;
-    for (int w = 0; w < YI5_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
+    for (int w = 0; w < YI6_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
     eatom[atom] = e;
   }
 }
@@ -1938,7 +1948,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_yi_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_yi_half, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cudaFuncSetAttribute(k_snap_yi_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_snap_yi_six, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_snap_yi_six, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
@@ -1969,9 +1979,9 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     return e ? atoi(e) : 5;
   }();
   if (S->yi_reg && yi_var == 6) {
-    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI5_WARPS * 9 * YI_ATOMS +
-                sizeof(double) * YI5_WARPS * YI_ATOMS;
-    k_snap_yi_six<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI5_WARPS * 32, sm, ctx->stream>>>(
+    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI6_WARPS * 9 * YI_ATOMS +
+                sizeof(double) * YI6_WARPS * YI_ATOMS;
+    k_snap_yi_six<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI6_WARPS * 32, sm, ctx->stream>>>(
         D, na, buf.utot, buf.y, buf.eatom);
   } else if (S->yi_reg && yi_var >= 5) {
     size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(double) * YI5_WARPS * YI_ATOMS;
