@@ -1114,20 +1114,28 @@ __device__ __forceinline__ void yi6_xyj(const C2* __restrict__ Ul, int Y, int J,
     for (int ma = 0; ma <= jtop; ++ma) {
       const double* cga = c_cgt + off + ma * (X + 1);
       const int base2 = ma + SH;  // ma2 = base2 - ma1
-      double sr = 0.0, si = 0.0;
+      // two accumulator pairs (even / odd ma1): shorter dependent FMA chains
+      double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
 #pragma unroll
       for (int ma1 = 0; ma1 <= X; ++ma1) {
         const int ma2 = base2 - ma1;
         if (ma2 >= 0 && ma2 <= Y) {
           const C2 uy = py[ma2 * YI_ATOMS];
           const double c = cga[ma1];
-          sr += c * (ux[ma1].re * uy.re - ux[ma1].im * uy.im);
-          si += c * (ux[ma1].re * uy.im + ux[ma1].im * uy.re);
+          const double tr = ux[ma1].re * uy.re - ux[ma1].im * uy.im;
+          const double ti = ux[ma1].re * uy.im + ux[ma1].im * uy.re;
+          if (ma1 & 1) {
+            sr1 += c * tr;
+            si1 += c * ti;
+          } else {
+            sr0 += c * tr;
+            si0 += c * ti;
+          }
         }
       }
       C2 zz = zs[ma * 32];
-      zz.re += cb * sr;
-      zz.im += cb * si;
+      zz.re += cb * (sr0 + sr1);
+      zz.im += cb * (si0 + si1);
       zs[ma * 32] = zz;
     }
   }
@@ -1976,7 +1984,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   prof_mark(ctx->stream, ST_YI, true);
   static const int yi_var = [] {
     const char* e = getenv("PL_SNAP_YI");
-    return e ? atoi(e) : 5;
+    return e ? atoi(e) : 6;
   }();
   if (S->yi_reg && yi_var == 6) {
     size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI6_WARPS * 9 * YI_ATOMS +
@@ -2080,7 +2088,7 @@ extern "C" int pl_snap_info(pl_pot* pot, int32_t* h_counts, double* h_flops) {
   h_counts[4] = S->nunits;
   // FLOPs of the kernel variants that compute_snap actually launches
   const char* ey = getenv("PL_SNAP_YI");
-  const int yv = ey ? atoi(ey) : 5;
+  const int yv = ey ? atoi(ey) : 6;
   const char* ea = getenv("PL_SNAP_ADJ");
   const char* er = getenv("PL_SNAP_RR");
   const bool rr = !(er && er[0] == '0') && S->tj == 8;
