@@ -1154,6 +1154,65 @@ __device__ __forceinline__ void yi6_xyj(const C2* __restrict__ Ul, int Y, int J,
   }
 }
 
+template <int Y>
+__device__ __forceinline__ void yi7_xyj(const C2* __restrict__ Ul, int X, int J, int mb, int off, double cy,
+                                        double be, C2* __restrict__ zs, C2 (&yacc)[yi5::TJ + 1], double& esum) {
+  const int SH = (X + Y - J) / 2;
+  const bool mid = (2 * mb == J);
+  const int jtop = mid ? J / 2 : J;  // middle row: upper half has zero weight
+  for (int ma = 0; ma <= jtop; ++ma) zs[ma * 32] = C2{0.0, 0.0};
+  const int lo = max(0, mb + SH - Y), hi = min(X, mb + SH);
+  const int FX = c_foff[X], FY = c_foff[Y];
+  for (int mb1 = lo; mb1 <= hi; ++mb1) {
+    const int mb2 = mb + SH - mb1;
+    C2 uy[Y + 1];
+    const C2* py = Ul + (FY + mb2 * (Y + 1)) * YI_ATOMS;
+#pragma unroll
+    for (int a = 0; a <= Y; ++a) uy[a] = py[a * YI_ATOMS];
+    const C2* px = Ul + (FX + mb1 * (X + 1)) * YI_ATOMS;
+    const double cb = c_cgt[off + mb * (X + 1) + mb1];
+    for (int ma = 0; ma <= jtop; ++ma) {
+      const double* cga = c_cgt + off + ma * (X + 1);
+      const int base1 = ma + SH;  // ma1 = base1 - ma2
+      double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
+#pragma unroll
+      for (int ma2 = 0; ma2 <= Y; ++ma2) {
+        const int ma1 = base1 - ma2;
+        if (ma1 >= 0 && ma1 <= X) {
+          const C2 ux = px[ma1 * YI_ATOMS];
+          const double c = cga[ma1];
+          const double tr = ux.re * uy[ma2].re - ux.im * uy[ma2].im;
+          const double ti = ux.re * uy[ma2].im + ux.im * uy[ma2].re;
+          if (ma2 & 1) {
+            sr1 += c * tr;
+            si1 += c * ti;
+          } else {
+            sr0 += c * tr;
+            si0 += c * ti;
+          }
+        }
+      }
+      C2 zz = zs[ma * 32];
+      zz.re += cb * (sr0 + sr1);
+      zz.im += cb * (si0 + si1);
+      zs[ma * 32] = zz;
+    }
+  }
+  const C2* pj = Ul + (c_foff[J] + mb * (J + 1)) * YI_ATOMS;
+#pragma unroll
+  for (int ma = 0; ma <= yi5::TJ; ++ma) {
+    if (ma > jtop) break;
+    const C2 z = zs[ma * 32];
+    yacc[ma].re += cy * z.re;
+    yacc[ma].im += cy * z.im;
+    if (be != 0.0) {
+      const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+      const C2 u = pj[ma * YI_ATOMS];
+      esum += be * w * (u.re * z.re + u.im * z.im);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(YI6_WARPS * 32)
 k_snap_yi_six(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
               double* __restrict__ eatom) {
@@ -1206,6 +1265,76 @@ k_snap_yi_six(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __rest
         case 6: yi6_xyj<6>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
         case 7: yi6_xyj<7>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
         default: yi6_xyj<8>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
+      }
+    }
+    if (lane < na_blk) {
+      C2* yo = ylist + atom * D.nhalf + c_hoff[J] + mb * (J + 1);
+#pragma unroll
+      for (int m = 0; m <= yi5::TJ; ++m)
+        if (m <= J) yo[m] = yacc[m];
+    }
+  }
+  epart[warp * YI_ATOMS + lane] = esum;
+  __syncthreads();
+  if (warp == 0 && lane < na_blk) {
+    double e = D.beta0;
+    for (int w = 0; w < YI6_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
+    eatom[atom] = e;
+  }
+}
+
+__global__ void __launch_bounds__(YI6_WARPS * 32)
+k_snap_yi_seven(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
+              double* __restrict__ eatom) {
+  extern __shared__ double smem[];
+  C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
+  C2* zsm = Uf + D.nfull * YI_ATOMS;                                   // [warps][9][32]
+  double* epart = reinterpret_cast<double*>(zsm + YI6_WARPS * (yi5::TJ + 1) * YI_ATOMS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
+  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
+  for (int t = threadIdx.x; t < D.nfull * YI_ATOMS; t += blockDim.x) {
+    const int at = t & (YI_ATOMS - 1), f = t >> 5;
+    int J = 0;
+    while (J < D.tj && f >= c_foff[J + 1]) ++J;
+    const int e = f - c_foff[J], mb = e / (J + 1), ma = e - mb * (J + 1);
+    C2 v{0.0, 0.0};
+    if (at < na_blk) {
+      if (2 * mb <= J) {
+        v = utot[(a0 + at) * D.nhalf + c_hoff[J] + mb * (J + 1) + ma];
+      } else {
+        C2 w = utot[(a0 + at) * D.nhalf + c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
+        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
+      }
+    }
+    Uf[f * YI_ATOMS + at] = v;
+  }
+  __syncthreads();
+  const C2* Ul = Uf + lane;
+  C2* zs = zsm + warp * (yi5::TJ + 1) * YI_ATOMS + lane;
+  const int64_t atom = a0 + lane;
+  double esum = 0.0;
+  for (int gi = c_yi6_gseg[warp]; gi < c_yi6_gseg[warp + 1]; ++gi) {
+    const int J = c_yi6_groups[gi] >> 8, mb = c_yi6_groups[gi] & 0xff;
+    C2 yacc[yi5::TJ + 1];
+#pragma unroll
+    for (int m = 0; m <= yi5::TJ; ++m) yacc[m] = C2{0.0, 0.0};
+    for (int k = c_yi5_jstart[J]; k < c_yi5_jstart[J + 1]; ++k) {
+      const int tid = c_yi5_tlist[k];
+      const int code = c_yi5_code[tid];
+      const int X = code / 100, Y = (code / 10) % 10;
+      const int off = c_yi5_cgoff[tid];
+      const double cy = D.yi5[tid], be = D.yi5[yi5::NT + tid];
+      switch (Y) {
+        case 0: yi7_xyj<0>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 1: yi7_xyj<1>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 2: yi7_xyj<2>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 3: yi7_xyj<3>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 4: yi7_xyj<4>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 5: yi7_xyj<5>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 6: yi7_xyj<6>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
+        case 7: yi7_xyj<7>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
+        default: yi7_xyj<8>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
       }
     }
     if (lane < na_blk) {
@@ -1477,11 +1606,13 @@ struct Layers {
     Layers<TJ, J - 1>::ui(u, du, g, mb, rp, part, fc);
     row_step<TJ, J, false>(u, du, g, mb, rp);
     if (part && 2 * mb <= J) {
-      C2* pr = part + c_hoff[J] + mb * (J + 1);
+      // partials interleaved [element][pair slot] (stride P): conflict-light smem
+      constexpr int P = 32 / (TJ / 2 + 1);
+      C2* pr = part + (c_hoff[J] + mb * (J + 1)) * P;
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
-        pr[ma].re += fc * u[ma].re;
-        pr[ma].im += fc * u[ma].im;
+        pr[ma * P].re += fc * u[ma].re;
+        pr[ma * P].im += fc * u[ma].im;
       }
     }
   }
@@ -1545,7 +1676,7 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
 #pragma unroll
     for (int k = 0; k <= TJ; ++k) u[k] = du[k] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
-    C2* mypart = part + p * nh;
+    C2* mypart = part + p;  // element e of pair slot p at part[e * P + p]
     if (valid && mb == 0) mypart[0].re += fc;  // J = 0
     // every lane runs the recursion (shuffles need the full warp); only valid
     // lanes accumulate, each into its own pair slot
@@ -1558,8 +1689,8 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
     C2 acc{0.0, 0.0};
 #pragma unroll
     for (int pp = 0; pp < P; ++pp) {
-      acc.re += part[pp * nh + t].re;
-      acc.im += part[pp * nh + t].im;
+      acc.re += part[t * P + pp].re;
+      acc.im += part[t * P + pp].im;
     }
     int J = 0;
     while (J < TJ && t >= c_hoff[J + 1]) ++J;
@@ -1957,6 +2088,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_yi_half, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cudaFuncSetAttribute(k_snap_yi_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_yi_six, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+    cudaFuncSetAttribute(k_snap_yi_seven, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
@@ -1986,7 +2118,12 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     const char* e = getenv("PL_SNAP_YI");
     return e ? atoi(e) : 6;
   }();
-  if (S->yi_reg && yi_var == 6) {
+  if (S->yi_reg && yi_var == 7) {
+    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI6_WARPS * 9 * YI_ATOMS +
+                sizeof(double) * YI6_WARPS * YI_ATOMS;
+    k_snap_yi_seven<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI6_WARPS * 32, sm, ctx->stream>>>(
+        D, na, buf.utot, buf.y, buf.eatom);
+  } else if (S->yi_reg && yi_var == 6) {
     size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI6_WARPS * 9 * YI_ATOMS +
                 sizeof(double) * YI6_WARPS * YI_ATOMS;
     k_snap_yi_six<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI6_WARPS * 32, sm, ctx->stream>>>(
