@@ -1606,13 +1606,11 @@ struct Layers {
     Layers<TJ, J - 1>::ui(u, du, g, mb, rp, part, fc);
     row_step<TJ, J, false>(u, du, g, mb, rp);
     if (part && 2 * mb <= J) {
-      // partials interleaved [element][pair slot] (stride P): conflict-light smem
-      constexpr int P = 32 / (TJ / 2 + 1);
-      C2* pr = part + (c_hoff[J] + mb * (J + 1)) * P;
+      C2* pr = part + c_hoff[J] + mb * (J + 1);
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
-        pr[ma * P].re += fc * u[ma].re;
-        pr[ma * P].im += fc * u[ma].im;
+        pr[ma].re += fc * u[ma].re;
+        pr[ma].im += fc * u[ma].im;
       }
     }
   }
@@ -1676,7 +1674,7 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
 #pragma unroll
     for (int k = 0; k <= TJ; ++k) u[k] = du[k] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
-    C2* mypart = part + p;  // element e of pair slot p at part[e * P + p]
+    C2* mypart = part + p * nh;
     if (valid && mb == 0) mypart[0].re += fc;  // J = 0
     // every lane runs the recursion (shuffles need the full warp); only valid
     // lanes accumulate, each into its own pair slot
@@ -1689,8 +1687,8 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
     C2 acc{0.0, 0.0};
 #pragma unroll
     for (int pp = 0; pp < P; ++pp) {
-      acc.re += part[t * P + pp].re;
-      acc.im += part[t * P + pp].im;
+      acc.re += part[pp * nh + t].re;
+      acc.im += part[pp * nh + t].im;
     }
     int J = 0;
     while (J < TJ && t >= c_hoff[J + 1]) ++J;
