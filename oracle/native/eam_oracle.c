@@ -14,7 +14,9 @@
 #include <string.h>
 
 static double min_image(double dx, double L) {
-  double k = rint(dx / L);
+  /* rint(dx * (1/L)): the device evaluates the same expression (neigh.cuh) */
+  double inv = 1.0 / L;
+  double k = rint(dx * inv);
   return dx - L * k;
 }
 

@@ -117,9 +117,9 @@ int compute_eam(pl_pot* pot, int64_t B, const double* q, double* energy, double*
   double* Fe = Fp + na;
   double* ea = Fe + na;
   double* va = ea + na;
-  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
-  Table trho{pot->d_rho, pot->n_r, pot->dr}, tphi{pot->d_phi, pot->n_r, pot->dr},
-      tF{pot->d_F, pot->n_rho, pot->drho};
+  Box box = make_box(pot->box);
+  Table trho{pot->d_rho, pot->n_r, pot->dr, 1.0 / pot->dr}, tphi{pot->d_phi, pot->n_r, pot->dr, 1.0 / pot->dr},
+      tF{pot->d_F, pot->n_rho, pot->drho, 1.0 / pot->drho};
   const int tpa = eam_tpa(N, 1024);  // the persistent sweep's rule (same reduction tree)
   const double rc2 = pot->rcut * pot->rcut;
   unsigned g = (unsigned)((na * tpa + 127) / 128);

@@ -10,7 +10,7 @@
 
 namespace pl {
 
-constexpr int CELL_MIN_ATOMS = 4096;
+constexpr int CELL_MIN_ATOMS = 512;
 constexpr int CELL_MAXN = 128;  // per-thread collection buffer (local memory)
 
 struct CellGrid {
@@ -95,9 +95,9 @@ k_neigh_cell(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, const 
         for (int s = cstart[cc]; s < cstart[cc + 1]; ++s) {
           int j = catoms[s];
           if (j == i) continue;
-          double ddx = min_image(sub(qb[3 * j], xi), box.L[0]);
-          double ddy = min_image(sub(qb[3 * j + 1], yi), box.L[1]);
-          double ddz = min_image(sub(qb[3 * j + 2], zi), box.L[2]);
+          double ddx = min_image(sub(qb[3 * j], xi), box.L[0], box.inv[0]);
+          double ddy = min_image(sub(qb[3 * j + 1], yi), box.L[1], box.inv[1]);
+          double ddz = min_image(sub(qb[3 * j + 2], zi), box.L[2], box.inv[2]);
           if (r2_exact(ddx, ddy, ddz) < rc2) {
             if (nf < CELL_MAXN) found[nf] = j;
             ++nf;
@@ -133,7 +133,7 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
   out->maxn = maxn;
   pot->nb_overflow = out->overflow;
   if (B > 65535) return fail(PL_EARG, "at most 65535 systems per call");
-  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  Box box = make_box(pot->box);
   double rc2 = rcut * rcut;
   cudaStream_t st = pot->ctx->stream;
   PL_CUDA(cudaMemsetAsync(out->overflow, 0, sizeof(int), st));

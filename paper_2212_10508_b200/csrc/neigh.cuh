@@ -15,10 +15,22 @@ namespace pl {
 
 struct Box {
   double L[3];
+  double inv[3];  // 1/L, formed on the host (the C oracle forms the same quotient)
 };
 
-__device__ __forceinline__ double min_image(double dx, double L) {
-  double k = rint(dvd(dx, L));
+inline Box make_box(const double* L) {
+  Box b;
+  for (int c = 0; c < 3; ++c) {
+    b.L[c] = L[c];
+    b.inv[c] = 1.0 / L[c];
+  }
+  return b;
+}
+
+// image index rint(dx / L) evaluated as rint(dx * (1/L)): no divide on the hot
+// path; the oracle uses the identical expression, so pair sets stay bit-exact
+__device__ __forceinline__ double min_image(double dx, double L, double inv) {
+  double k = rint(mul(dx, inv));
   return sub(dx, mul(L, k));
 }
 
@@ -56,9 +68,9 @@ k_neigh_brute(int64_t B, int N, Box box, double rc2, int maxn, const double* __r
       for (int jj = 0; jj < jmax; ++jj) {
         int j = j0 + jj;
         if (j == i) continue;
-        double dx = min_image(sub(sx[3 * jj], xi), box.L[0]);
-        double dy = min_image(sub(sx[3 * jj + 1], yi), box.L[1]);
-        double dz = min_image(sub(sx[3 * jj + 2], zi), box.L[2]);
+        double dx = min_image(sub(sx[3 * jj], xi), box.L[0], box.inv[0]);
+        double dy = min_image(sub(sx[3 * jj + 1], yi), box.L[1], box.inv[1]);
+        double dz = min_image(sub(sx[3 * jj + 2], zi), box.L[2], box.inv[2]);
         double r2 = r2_exact(dx, dy, dz);
         if (r2 < rc2) {
           if (c < maxn) my[c] = j;
@@ -76,9 +88,9 @@ k_neigh_brute(int64_t B, int N, Box box, double rc2, int maxn, const double* __r
 // displacement r_j - r_i under the minimum image (same ops as the builder)
 __device__ __forceinline__ void pair_vec(const double* qb, int i, int j, const Box& box, double& dx,
                                          double& dy, double& dz) {
-  dx = min_image(sub(qb[3 * j], qb[3 * i]), box.L[0]);
-  dy = min_image(sub(qb[3 * j + 1], qb[3 * i + 1]), box.L[1]);
-  dz = min_image(sub(qb[3 * j + 2], qb[3 * i + 2]), box.L[2]);
+  dx = min_image(sub(qb[3 * j], qb[3 * i]), box.L[0], box.inv[0]);
+  dy = min_image(sub(qb[3 * j + 1], qb[3 * i + 1]), box.L[1], box.inv[1]);
+  dz = min_image(sub(qb[3 * j + 2], qb[3 * i + 2]), box.L[2], box.inv[2]);
 }
 
 struct NeighList {

@@ -92,6 +92,7 @@ struct SnapDev {  // POD view passed to kernels
   const double* yi5;  // [2][NT]
   const double* cg;
   double beta0, rcut, rfac0, rmin0, wself;
+  double kappa, pi_span, half_pi_span;  // rfac0*pi/(rcut-rmin0), pi/(rcut-rmin0), 0.5*pi/(rcut-rmin0)
   int switchflag;
 };
 
@@ -531,6 +532,9 @@ static SnapDev snap_dev(const pl_pot* pot) {
   D.yi5 = S->d_yi5;
   D.beta0 = S->beta0; D.rcut = pot->rcut; D.rfac0 = pot->rfac0; D.rmin0 = pot->rmin0;
   D.wself = pot->wself; D.switchflag = pot->switchflag;
+  D.kappa = pot->rfac0 * M_PI / (pot->rcut - pot->rmin0);
+  D.pi_span = M_PI / (pot->rcut - pot->rmin0);
+  D.half_pi_span = 0.5 * M_PI / (pot->rcut - pot->rmin0);
   return D;
 }
 
@@ -556,17 +560,16 @@ __device__ __forceinline__ void pair_geom(const SnapDev& D, double dx, double dy
   double inv = 1.0 / r;
   g.r = r;
   g.u[0] = dx * inv; g.u[1] = dy * inv; g.u[2] = dz * inv;
-  double span = D.rcut - D.rmin0;
-  double kappa = D.rfac0 * M_PI / span;
+  const double kappa = D.kappa;
   double s, c;
   sincos(kappa * (r - D.rmin0), &s, &c);
   g.a = C2{c, -g.u[2] * s};
   g.b = C2{g.u[1] * s, -g.u[0] * s};
   if (D.switchflag) {
     double sa, ca;
-    sincos(M_PI * (r - D.rmin0) / span, &sa, &ca);
+    sincos(D.pi_span * (r - D.rmin0), &sa, &ca);
     g.fc = 0.5 * (ca + 1.0);
-    g.dfc = -0.5 * M_PI / span * sa;
+    g.dfc = -D.half_pi_span * sa;
   } else {
     g.fc = 1.0;
     g.dfc = 0.0;
@@ -2073,7 +2076,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   buf.eatom = (double*)(buf.y + na * S->nhalf);
   buf.dedr = buf.eatom + na;
   buf.vatom = buf.dedr + na * 3 * SNAP_MAXN;
-  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  Box box = make_box(pot->box);
   size_t s1 = ui_smem(D), s2 = yi_smem(D), s3 = de_smem(D);
   static thread_local bool attr_done = false;
   if (!attr_done) {
@@ -2173,7 +2176,7 @@ int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double
   SnapBuffers buf;
   NeighList nl;
   PL_TRY(snap_stages(pot, B, q, buf, nl));
-  Box box{{pot->box[0], pot->box[1], pot->box[2]}};
+  Box box = make_box(pot->box);
   prof_mark(ctx->stream, ST_GATHER, true);
   k_snap_gather<<<(unsigned)((na + 127) / 128), 128, 0, ctx->stream>>>(
       na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr);

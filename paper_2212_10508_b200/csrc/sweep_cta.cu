@@ -89,9 +89,9 @@ __device__ void sw_build(const SweepArgs& A, const double* q, double* qref) {
     int32_t* my = A.cand + (int64_t)i * SW_MAXN;
     for (int j = 0; j < n; ++j) {
       if (j == i) continue;
-      const double dx = min_image(sub(q[3 * j], xi), A.box.L[0]);
-      const double dy = min_image(sub(q[3 * j + 1], yi), A.box.L[1]);
-      const double dz = min_image(sub(q[3 * j + 2], zi), A.box.L[2]);
+      const double dx = min_image(sub(q[3 * j], xi), A.box.L[0], A.box.inv[0]);
+      const double dy = min_image(sub(q[3 * j + 1], yi), A.box.L[1], A.box.inv[1]);
+      const double dz = min_image(sub(q[3 * j + 2], zi), A.box.L[2], A.box.inv[2]);
       if (r2_exact(dx, dy, dz) < A.rl2) {
         if (c < SW_MAXN) my[c] = j;
         ++c;
@@ -379,12 +379,12 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
   if (ew) {
     PL_TRY(ew_program(coarse, &A.ew));
   } else {
-    A.box = Box{{coarse->box[0], coarse->box[1], coarse->box[2]}};
+    A.box = make_box(coarse->box);
     A.rc2 = coarse->rcut * coarse->rcut;
     A.rl2 = (coarse->rcut + SW_SKIN) * (coarse->rcut + SW_SKIN);
-    A.rho = Table{coarse->d_rho, coarse->n_r, coarse->dr};
-    A.phi = Table{coarse->d_phi, coarse->n_r, coarse->dr};
-    A.F = Table{coarse->d_F, coarse->n_rho, coarse->drho};
+    A.rho = Table{coarse->d_rho, coarse->n_r, coarse->dr, 1.0 / coarse->dr};
+    A.phi = Table{coarse->d_phi, coarse->n_r, coarse->dr, 1.0 / coarse->dr};
+    A.F = Table{coarse->d_F, coarse->n_rho, coarse->drho, 1.0 / coarse->drho};
     A.ncand = (int32_t*)lw;
     A.overflow = (int*)(A.ncand + n);
     A.cand = (int32_t*)(((uintptr_t)(A.overflow + 4) + 15) & ~(uintptr_t)15);
@@ -457,12 +457,12 @@ int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, in
   if (ew) {
     PL_TRY(ew_program(coarse, &A.ew));
   } else {
-    A.box = Box{{coarse->box[0], coarse->box[1], coarse->box[2]}};
+    A.box = make_box(coarse->box);
     A.rc2 = coarse->rcut * coarse->rcut;
     A.rl2 = (coarse->rcut + SW_SKIN) * (coarse->rcut + SW_SKIN);
-    A.rho = Table{coarse->d_rho, coarse->n_r, coarse->dr};
-    A.phi = Table{coarse->d_phi, coarse->n_r, coarse->dr};
-    A.F = Table{coarse->d_F, coarse->n_rho, coarse->drho};
+    A.rho = Table{coarse->d_rho, coarse->n_r, coarse->dr, 1.0 / coarse->dr};
+    A.phi = Table{coarse->d_phi, coarse->n_r, coarse->dr, 1.0 / coarse->dr};
+    A.F = Table{coarse->d_F, coarse->n_rho, coarse->drho, 1.0 / coarse->drho};
     A.cand = (int32_t*)lists;
     A.overflow = ovf;
     A.tpa = eam_tpa(n, SW_THREADS);
