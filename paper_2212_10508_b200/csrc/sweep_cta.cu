@@ -48,8 +48,6 @@ struct SweepArgs {
   Table rho, phi, F;
   int32_t* cand;    // [n_atoms][SW_MAXN] Verlet candidates (rc + skin)
   int32_t* ncand;   // [n_atoms]
-  int32_t* nbr;     // [n_atoms][SW_MAXN] exact list (r < rc) of the current positions
-  int32_t* nnbr;    // [n_atoms]
   int* overflow;
   // elementwise
   EwProg ew;
@@ -80,13 +78,31 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return r;
 }
 
-// Verlet candidate lists (ascending j) of the current positions
-__device__ void sw_build(const SweepArgs& A, const double* q, double* qref) {
+struct Slot {  // per-CTA (replica slot) view of the arrays, kept in registers
+  double* Q;
+  double* P;
+  const double* prevQ;
+  double* baseQ;
+  double* baseP;
+  const double* jumpQ;
+  const double* jumpP;
+  const double* noise;
+  double* hist;
+  double* acc;
+  int64_t* out;
+  int64_t m0, m1;
+  int include_m0;
+  int32_t* cand;
+  int32_t* ncand;
+};
+
+// Verlet candidate lists (ascending j, rc + skin) of the current positions
+__device__ void sw_build(const SweepArgs& A, const Slot& S, const double* q, double* qref) {
   const int n = A.n_atoms;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double xi = q[3 * i], yi = q[3 * i + 1], zi = q[3 * i + 2];
     int c = 0;
-    int32_t* my = A.cand + (int64_t)i * SW_MAXN;
+    int32_t* my = S.cand + (int64_t)i * SW_MAXN;
     for (int j = 0; j < n; ++j) {
       if (j == i) continue;
       const double dx = min_image(sub(q[3 * j], xi), A.box.L[0], A.box.inv[0]);
@@ -97,17 +113,19 @@ __device__ void sw_build(const SweepArgs& A, const double* q, double* qref) {
         ++c;
       }
     }
-    A.ncand[i] = c < SW_MAXN ? c : SW_MAXN;
+    S.ncand[i] = c < SW_MAXN ? c : SW_MAXN;
     if (c > SW_MAXN) *A.overflow = 1;
   }
   for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) qref[t] = q[t];
 }
 
-// EAM gradient of the CTA's system into g (tpa threads per atom, fixed-order group reduction)
-__device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* fp, double* qref, int* s_flag,
+// EAM gradient of the CTA's system into g: tpa lanes per atom over the Verlet
+// candidates (r < rc filter inside); the j % tpa lane partition and the
+// xor-tree equal k_eam_density / k_eam_force on exact lists, so the gradient
+// is bitwise the batched one
+__device__ void sw_eam(const SweepArgs& A, const Slot& S, const double* q, double* g, double* fp, double* qref,
                        bool force_rebuild) {
   const int n = A.n_atoms;
-  // rebuild when forced or when any atom moved more than skin/2 since the last build
   int moved = 0;
   if (!force_rebuild) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -117,32 +135,16 @@ __device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* f
     }
   }
   if (__syncthreads_or(moved) || force_rebuild) {
-    sw_build(A, q, qref);
+    sw_build(A, S, q, qref);
     __syncthreads();
   }
-  // exact list of this step (candidates filtered in order): the lane partition of
-  // the list below is then identical to k_eam_density / k_eam_force's
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int nc = A.ncand[i];
-    const int32_t* cl = A.cand + (int64_t)i * SW_MAXN;
-    int32_t* el = A.nbr + (int64_t)i * SW_MAXN;
-    int c = 0;
-    for (int k = 0; k < nc; ++k) {
-      double dx, dy, dz;
-      pair_vec(q, i, cl[k], A.box, dx, dy, dz);
-      if (r2_exact(dx, dy, dz) < A.rc2) el[c++] = cl[k];
-    }
-    A.nnbr[i] = c;
-  }
-  __syncthreads();
   const int tpa = A.tpa;
   const int groups = blockDim.x / tpa;
   const int gi0 = threadIdx.x / tpa, sub = threadIdx.x % tpa;
-  // density pass (same device functions / reduction tree as k_eam_density)
   for (int base = 0; base < n; base += groups) {
     const int i = base + gi0;
     const int ii = i < n ? i : n - 1;
-    const double s = group_sum(eam_rho_part(q, ii, A.nbr + (int64_t)ii * SW_MAXN, A.nnbr[ii], sub, tpa, A.box,
+    const double s = group_sum(eam_rho_part(q, ii, S.cand + (int64_t)ii * SW_MAXN, S.ncand[ii], sub, tpa, A.box,
                                             A.rc2, A.rho), tpa);
     if (i < n && sub == 0) {
       double f, df;
@@ -151,12 +153,11 @@ __device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* f
     }
   }
   __syncthreads();
-  // force pass
   for (int base = 0; base < n; base += groups) {
     const int i = base + gi0;
     const int ii = i < n ? i : n - 1;
     double gg[3] = {0.0, 0.0, 0.0}, e = 0.0, v[6];
-    eam_force_part<false>(q, fp, ii, A.nbr + (int64_t)ii * SW_MAXN, A.nnbr[ii], sub, tpa, A.box, A.rc2, A.rho,
+    eam_force_part<false>(q, fp, ii, S.cand + (int64_t)ii * SW_MAXN, S.ncand[ii], sub, tpa, A.box, A.rc2, A.rho,
                           A.phi, gg, &e, v);
     gg[0] = group_sum(gg[0], tpa);
     gg[1] = group_sum(gg[1], tpa);
@@ -167,45 +168,44 @@ __device__ void sw_eam(const SweepArgs& A, const double* q, double* g, double* f
       g[3 * i + 2] = gg[2];
     }
   }
-  (void)s_flag;
   __syncthreads();
 }
 
-__device__ __forceinline__ void sw_force(const SweepArgs& A, const double* q, double* g, double* fp,
-                                         double* qref, int* s_flag, bool force_rebuild) {
+__device__ __forceinline__ void sw_force(const SweepArgs& A, const Slot& S, const double* q, double* g,
+                                         double* fp, double* qref, bool force_rebuild) {
   if (A.use_ew) {
     for (int64_t t = threadIdx.x; t < A.d; t += blockDim.x) g[t] = ew_grad(A.ew, q[t], t);
     __syncthreads();
   } else {
-    sw_eam(A, q, g, fp, qref, s_flag, force_rebuild);
+    sw_eam(A, S, q, g, fp, qref, force_rebuild);
   }
 }
 
-__global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
+__global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(const SweepArgs A) {
   extern __shared__ double sm[];
+  Slot S{A.Q, A.P, A.prevQ, A.baseQ, A.baseP, A.jumpQ, A.jumpP, A.noise, A.hist, A.acc, A.out,
+         A.m0, A.m1, A.include_m0, A.cand, A.ncand};
   if (A.b_ridx) {
     // replica slot: offset every per-replica array, take this slot's slab
     const int slot = blockIdx.x;
     const int64_t r = A.b_ridx[slot];
-    A.Q += r * A.s_traj;
-    A.P += r * A.s_traj;
-    A.prevQ += r * A.s_traj;
-    A.baseQ += r * A.s_win;
-    A.baseP += r * A.s_win;
-    A.jumpQ += r * A.s_win;
-    A.jumpP += r * A.s_win;
-    A.noise += r * A.s_noise;
-    A.hist += r * A.s_hist;
-    A.acc += 2 * slot;
-    A.out += 4 * slot;
-    A.m0 = A.b_m0[slot];
-    A.m1 = A.b_m1[slot];
-    A.include_m0 = A.b_inc[slot];
+    S.Q += r * A.s_traj;
+    S.P += r * A.s_traj;
+    S.prevQ += r * A.s_traj;
+    S.baseQ += r * A.s_win;
+    S.baseP += r * A.s_win;
+    S.jumpQ += r * A.s_win;
+    S.jumpP += r * A.s_win;
+    S.noise += r * A.s_noise;
+    S.hist += r * A.s_hist;
+    S.acc += 2 * slot;
+    S.out += 4 * slot;
+    S.m0 = A.b_m0[slot];
+    S.m1 = A.b_m1[slot];
+    S.include_m0 = A.b_inc[slot];
     if (!A.use_ew) {
-      A.cand += (int64_t)slot * 2 * ((int64_t)A.n_atoms * (SW_MAXN + 1) + 8);
-      A.ncand = A.cand + (int64_t)A.n_atoms * SW_MAXN;
-      A.nbr = A.ncand + A.n_atoms + 4;
-      A.nnbr = A.nbr + (int64_t)A.n_atoms * SW_MAXN;
+      S.cand += (int64_t)slot * ((int64_t)A.n_atoms * (SW_MAXN + 1) + 8);
+      S.ncand = S.cand + (int64_t)A.n_atoms * SW_MAXN;
     }
   }
   const int64_t d = A.d;
@@ -213,56 +213,59 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
   double* p = q + d;
   double* ph = p + d;
   double* g = ph + d;
-  double* fp = g + d;                    // n doubles (EAM)
+  double* fp = g + d;  // n doubles (EAM)
   double* qref = fp + (A.use_ew ? 0 : A.n_atoms);
   __shared__ double red[33];
-  __shared__ int s_fail, s_flag;
+  __shared__ int s_fail;
   __shared__ double s_num, s_den;
   if (threadIdx.x == 0) {
-    s_num = A.acc[0];
-    s_den = A.acc[1];
-    A.out[0] = 0;
-    A.out[1] = -1;
-    A.out[2] = 0;
-    A.out[3] = 0;
+    s_num = S.acc[0];
+    s_den = S.acc[1];
+    S.out[0] = 0;
+    S.out[1] = -1;
+    S.out[2] = 0;
+    S.out[3] = 0;
   }
-  const int64_t m0 = A.m0;
+  const int64_t m0 = S.m0;
   for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
-    q[t] = A.Q[m0 * d + t];
-    p[t] = A.P[m0 * d + t];
+    q[t] = S.Q[m0 * d + t];
+    p[t] = S.P[m0 * d + t];
   }
   __syncthreads();
-  if (A.include_m0) {
+  if (S.include_m0) {
     double s2 = 0.0;
     for (int64_t t = threadIdx.x; t < d; t += blockDim.x) s2 += q[t] * q[t];
     const double tot = block_sum(s2, red);
     if (threadIdx.x == 0) s_den += sqrt(tot);  // num += ||q - q|| = 0
   }
+  const double h = A.h, hg = A.hg, dt = A.dt;
+  const double* mass = A.mass;
+  const int L = A.L;
   int64_t done = 0;
-  for (int64_t m = m0; m < A.m1; ++m) {
-    const double* G = A.noise + m * (int64_t)(A.L + 1) * d;
+  for (int64_t m = m0; m < S.m1; ++m) {
+    const double* G = S.noise + m * (int64_t)(L + 1) * d;
     if (threadIdx.x == 0) s_fail = 0;
-    sw_force(A, q, g, fp, qref, &s_flag, true);
-    for (int s = 1; s <= A.L; ++s) {
+    sw_force(A, S, q, g, fp, qref, true);
+    for (int s = 1; s <= L; ++s) {
       // open substep s (integrator.py:174-175, 182-183)
       for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
-        const double mm = A.mass ? A.mass[t] : 1.0;
-        const double smm = A.mass ? __dsqrt_rn(mm) : 1.0;
+        const double mm = mass ? mass[t] : 1.0;
+        const double smm = mass ? __dsqrt_rn(mm) : 1.0;
         const double al = mul(A.amp[s - 1], smm);
         const double pref = (s == 1) ? p[t] : ph[t];
-        const double hv = add(sub(sub(p[t], mul(A.h, g[t])), mul(A.hg, pref)), mul(al, G[(int64_t)(s - 1) * d + t]));
+        const double hv = add(sub(sub(p[t], mul(h, g[t])), mul(hg, pref)), mul(al, G[(int64_t)(s - 1) * d + t]));
         ph[t] = hv;
-        q[t] = add(q[t], mul(A.dt, dvd(hv, mm)));
+        q[t] = add(q[t], mul(dt, dvd(hv, mm)));
       }
       __syncthreads();
-      sw_force(A, q, g, fp, qref, &s_flag, false);
+      sw_force(A, S, q, g, fp, qref, false);
       // close substep s (integrator.py:177, 185) + blow-up check (163-170)
       int bad = 0;
       for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
-        const double smm = A.mass ? __dsqrt_rn(A.mass[t]) : 1.0;
+        const double smm = mass ? __dsqrt_rn(mass[t]) : 1.0;
         const double al = mul(A.amp[s], smm);
         const double hv = ph[t];
-        const double pn = add(sub(sub(hv, mul(A.h, g[t])), mul(A.hg, hv)), mul(al, G[(int64_t)s * d + t]));
+        const double pn = add(sub(sub(hv, mul(h, g[t])), mul(hg, hv)), mul(al, G[(int64_t)s * d + t]));
         p[t] = pn;
         if (!(fabs(q[t]) <= BLOWUP_LIMIT && fabs(pn) <= BLOWUP_LIMIT)) bad = 1;
       }
@@ -271,21 +274,21 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
     __syncthreads();
     // base[m] = C(cur[m])
     for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
-      A.baseQ[m * d + t] = q[t];
-      A.baseP[m * d + t] = p[t];
+      S.baseQ[m * d + t] = q[t];
+      S.baseP[m * d + t] = p[t];
     }
     if (s_fail) {
       if (threadIdx.x == 0) {
-        A.out[1] = m;
-        A.out[2] = s_fail;
-        A.out[3] = 1;
+        S.out[1] = m;
+        S.out[2] = s_fail;
+        S.out[3] = 1;
       }
       break;
     }
     if (A.mode == 1) {
       for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
-        A.Q[(m + 1) * d + t] = q[t];
-        A.P[(m + 1) * d + t] = p[t];
+        S.Q[(m + 1) * d + t] = q[t];
+        S.P[(m + 1) * d + t] = p[t];
       }
       ++done;
       continue;
@@ -296,11 +299,11 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
     int nonfinite = 0;
     for (int64_t t = threadIdx.x; t < d; t += blockDim.x) {
       // prev[m+1] is read before cur[m+1] overwrites it (prevQ may alias Q)
-      const double pv = A.prevQ[(m + 1) * d + t];
-      const double cq = add(q[t], A.jumpQ[m * d + t]);
-      const double cp = add(p[t], A.jumpP[m * d + t]);
-      A.Q[(m + 1) * d + t] = cq;
-      A.P[(m + 1) * d + t] = cp;
+      const double pv = S.prevQ[(m + 1) * d + t];
+      const double cq = add(q[t], S.jumpQ[m * d + t]);
+      const double cp = add(p[t], S.jumpP[m * d + t]);
+      S.Q[(m + 1) * d + t] = cq;
+      S.P[(m + 1) * d + t] = cp;
       q[t] = cq;
       p[t] = cp;
       if (!isfinite(cq) || !isfinite(cp)) nonfinite = 1;
@@ -316,13 +319,13 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
     if (threadIdx.x == 0) {
       s_num = s_num + n1;
       s_den = s_den + n2;
-      A.hist[m - m0] = s_num / s_den;
+      S.hist[m - m0] = s_num / s_den;
     }
     __syncthreads();
     if (nonfinite) {
       if (threadIdx.x == 0) {
-        A.out[1] = m;
-        A.out[3] = 2;
+        S.out[1] = m;
+        S.out[3] = 2;
       }
       break;
     }
@@ -331,9 +334,9 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(SweepArgs A) {
     if (stop) break;
   }
   if (threadIdx.x == 0) {
-    A.acc[0] = s_num;
-    A.acc[1] = s_den;
-    A.out[0] = done;
+    S.acc[0] = s_num;
+    S.acc[1] = s_den;
+    S.out[0] = done;
   }
 }
 
@@ -365,7 +368,7 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
   A.dt = dt; A.h = h; A.hg = hg; A.expl = expl;
   cudaStream_t st = ctx->stream;
   // device scratch: amp, acc, out, (EAM lists)
-  size_t lists = ew ? 0 : 2 * sizeof(int32_t) * (size_t)n * (SW_MAXN + 1) + 128;
+  size_t lists = ew ? 0 : sizeof(int32_t) * ((size_t)n * (SW_MAXN + 1) + 8) + 128;
   PL_TRY(ctx->work[4].reserve(sizeof(double) * (L + 1 + 2) + sizeof(int64_t) * 4 + 64 + lists));
   char* w = (char*)ctx->work[4].ptr;
   double* amp = (double*)w;
@@ -385,11 +388,10 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
     A.rho = Table{coarse->d_rho, coarse->n_r, coarse->dr, 1.0 / coarse->dr};
     A.phi = Table{coarse->d_phi, coarse->n_r, coarse->dr, 1.0 / coarse->dr};
     A.F = Table{coarse->d_F, coarse->n_rho, coarse->drho, 1.0 / coarse->drho};
-    A.ncand = (int32_t*)lw;
-    A.overflow = (int*)(A.ncand + n);
+    // scratch: [overflow flag][pad][candidates n x SW_MAXN][counts n]
+    A.overflow = (int*)lw;
     A.cand = (int32_t*)(((uintptr_t)(A.overflow + 4) + 15) & ~(uintptr_t)15);
-    A.nnbr = A.cand + (size_t)n * SW_MAXN;
-    A.nbr = A.nnbr + n + 4;
+    A.ncand = A.cand + (size_t)n * SW_MAXN;
     A.tpa = eam_tpa(n, SW_THREADS);
     PL_CUDA(cudaMemsetAsync(A.overflow, 0, sizeof(int), st));
   }
@@ -438,7 +440,7 @@ int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, in
   A.s_noise = N * (int64_t)(L + 1) * d;
   A.s_hist = N;
   cudaStream_t st = ctx->stream;
-  const size_t per_slot_lists = ew ? 0 : sizeof(int32_t) * 2 * ((size_t)n * (SW_MAXN + 1) + 8);
+  const size_t per_slot_lists = ew ? 0 : sizeof(int32_t) * ((size_t)n * (SW_MAXN + 1) + 8);
   const size_t hdr = sizeof(double) * (L + 1) + sizeof(double) * 2 * R_act + sizeof(int64_t) * 4 * R_act +
                      sizeof(int64_t) * 2 * R_act + sizeof(int32_t) * 2 * R_act + 256;
   PL_TRY(ctx->work[4].reserve(hdr + per_slot_lists * R_act + 256));
@@ -464,6 +466,7 @@ int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, in
     A.phi = Table{coarse->d_phi, coarse->n_r, coarse->dr, 1.0 / coarse->dr};
     A.F = Table{coarse->d_F, coarse->n_rho, coarse->drho, 1.0 / coarse->drho};
     A.cand = (int32_t*)lists;
+    A.ncand = A.cand + (size_t)n * SW_MAXN;  // slot 0; the kernel offsets per slot
     A.overflow = ovf;
     A.tpa = eam_tpa(n, SW_THREADS);
     PL_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
