@@ -43,16 +43,14 @@ __host__ __device__ inline int eam_tpa(int n, int threads) {
   return best;
 }
 
-// partial density of atom i over the list entries j with j % tpa == sub (r < rc
-// filter).  Partitioning by j, not by list position, gives every lane the same
-// pair sequence for an exact list and for a Verlet candidate list (the
-// persistent sweep), so both paths sum identically.
+// partial density of atom i over EXACT-list entries sub, sub+tpa, ... (the
+// persistent sweep compacts its Verlet candidates to the exact list each step,
+// so both paths see the same entries in the same lanes)
 __device__ __forceinline__ double eam_rho_part(const double* qb, int i, const int32_t* list, int nl, int sub,
                                                int tpa, const Box& box, double rc2, const Table& rho) {
   double s = 0.0;
-  for (int k = 0; k < nl; ++k) {
+  for (int k = sub; k < nl; k += tpa) {
     const int j = list[k];
-    if ((j & (tpa - 1)) != sub) continue;
     double dx, dy, dz;
     pair_vec(qb, i, j, box, dx, dy, dz);
     const double r2 = r2_exact(dx, dy, dz);
@@ -77,9 +75,8 @@ __device__ __forceinline__ void eam_force_part(const double* qb, const double* f
                                                const Table& rho, const Table& phi, double* g, double* e,
                                                double* v) {
   const double fpi = fpb[i];
-  for (int k = 0; k < nl; ++k) {
+  for (int k = sub; k < nl; k += tpa) {
     const int j = list[k];
-    if ((j & (tpa - 1)) != sub) continue;
     double dx, dy, dz;
     pair_vec(qb, i, j, box, dx, dy, dz);
     const double r2 = r2_exact(dx, dy, dz);

@@ -94,6 +94,8 @@ struct Slot {  // per-CTA (replica slot) view of the arrays, kept in registers
   int include_m0;
   int32_t* cand;
   int32_t* ncand;
+  int32_t* nbr;   // exact list of the current step (compacted candidates)
+  int32_t* nnbr;
 };
 
 // Verlet candidate lists (ascending j, rc + skin) of the current positions
@@ -138,13 +140,28 @@ __device__ void sw_eam(const SweepArgs& A, const Slot& S, const double* q, doubl
     sw_build(A, S, q, qref);
     __syncthreads();
   }
+  // exact list of this step: candidates filtered in order (same entries, same
+  // lane partition as k_eam_density / k_eam_force)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int nc = S.ncand[i];
+    const int32_t* cl = S.cand + (int64_t)i * SW_MAXN;
+    int32_t* el = S.nbr + (int64_t)i * SW_MAXN;
+    int c = 0;
+    for (int k = 0; k < nc; ++k) {
+      double dx, dy, dz;
+      pair_vec(q, i, cl[k], A.box, dx, dy, dz);
+      if (r2_exact(dx, dy, dz) < A.rc2) el[c++] = cl[k];
+    }
+    S.nnbr[i] = c;
+  }
+  __syncthreads();
   const int tpa = A.tpa;
   const int groups = blockDim.x / tpa;
   const int gi0 = threadIdx.x / tpa, sub = threadIdx.x % tpa;
   for (int base = 0; base < n; base += groups) {
     const int i = base + gi0;
     const int ii = i < n ? i : n - 1;
-    const double s = group_sum(eam_rho_part(q, ii, S.cand + (int64_t)ii * SW_MAXN, S.ncand[ii], sub, tpa, A.box,
+    const double s = group_sum(eam_rho_part(q, ii, S.nbr + (int64_t)ii * SW_MAXN, S.nnbr[ii], sub, tpa, A.box,
                                             A.rc2, A.rho), tpa);
     if (i < n && sub == 0) {
       double f, df;
@@ -157,7 +174,7 @@ __device__ void sw_eam(const SweepArgs& A, const Slot& S, const double* q, doubl
     const int i = base + gi0;
     const int ii = i < n ? i : n - 1;
     double gg[3] = {0.0, 0.0, 0.0}, e = 0.0, v[6];
-    eam_force_part<false>(q, fp, ii, S.cand + (int64_t)ii * SW_MAXN, S.ncand[ii], sub, tpa, A.box, A.rc2, A.rho,
+    eam_force_part<false>(q, fp, ii, S.nbr + (int64_t)ii * SW_MAXN, S.nnbr[ii], sub, tpa, A.box, A.rc2, A.rho,
                           A.phi, gg, &e, v);
     gg[0] = group_sum(gg[0], tpa);
     gg[1] = group_sum(gg[1], tpa);
@@ -184,7 +201,7 @@ __device__ __forceinline__ void sw_force(const SweepArgs& A, const Slot& S, cons
 __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(const SweepArgs A) {
   extern __shared__ double sm[];
   Slot S{A.Q, A.P, A.prevQ, A.baseQ, A.baseP, A.jumpQ, A.jumpP, A.noise, A.hist, A.acc, A.out,
-         A.m0, A.m1, A.include_m0, A.cand, A.ncand};
+         A.m0, A.m1, A.include_m0, A.cand, A.ncand, A.cand, A.ncand};
   if (A.b_ridx) {
     // replica slot: offset every per-replica array, take this slot's slab
     const int slot = blockIdx.x;
@@ -203,10 +220,13 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(const SweepArgs A) {
     S.m0 = A.b_m0[slot];
     S.m1 = A.b_m1[slot];
     S.include_m0 = A.b_inc[slot];
-    if (!A.use_ew) {
-      S.cand += (int64_t)slot * ((int64_t)A.n_atoms * (SW_MAXN + 1) + 8);
-      S.ncand = S.cand + (int64_t)A.n_atoms * SW_MAXN;
-    }
+    if (!A.use_ew) S.cand += (int64_t)slot * 2 * ((int64_t)A.n_atoms * (SW_MAXN + 1) + 8);
+  }
+  if (!A.use_ew) {
+    // per slot: [candidates][counts][exact list][counts]
+    S.ncand = S.cand + (int64_t)A.n_atoms * SW_MAXN;
+    S.nbr = S.ncand + A.n_atoms + 8;
+    S.nnbr = S.nbr + (int64_t)A.n_atoms * SW_MAXN;
   }
   const int64_t d = A.d;
   double* q = sm;
@@ -368,7 +388,7 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
   A.dt = dt; A.h = h; A.hg = hg; A.expl = expl;
   cudaStream_t st = ctx->stream;
   // device scratch: amp, acc, out, (EAM lists)
-  size_t lists = ew ? 0 : sizeof(int32_t) * ((size_t)n * (SW_MAXN + 1) + 8) + 128;
+  size_t lists = ew ? 0 : 2 * sizeof(int32_t) * ((size_t)n * (SW_MAXN + 1) + 8) + 128;
   PL_TRY(ctx->work[4].reserve(sizeof(double) * (L + 1 + 2) + sizeof(int64_t) * 4 + 64 + lists));
   char* w = (char*)ctx->work[4].ptr;
   double* amp = (double*)w;
@@ -440,7 +460,7 @@ int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, in
   A.s_noise = N * (int64_t)(L + 1) * d;
   A.s_hist = N;
   cudaStream_t st = ctx->stream;
-  const size_t per_slot_lists = ew ? 0 : sizeof(int32_t) * ((size_t)n * (SW_MAXN + 1) + 8);
+  const size_t per_slot_lists = ew ? 0 : 2 * sizeof(int32_t) * ((size_t)n * (SW_MAXN + 1) + 8);
   const size_t hdr = sizeof(double) * (L + 1) + sizeof(double) * 2 * R_act + sizeof(int64_t) * 4 * R_act +
                      sizeof(int64_t) * 2 * R_act + sizeof(int32_t) * 2 * R_act + 256;
   PL_TRY(ctx->work[4].reserve(hdr + per_slot_lists * R_act + 256));
