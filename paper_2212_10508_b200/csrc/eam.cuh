@@ -43,20 +43,37 @@ __host__ __device__ inline int eam_tpa(int n, int threads) {
   return best;
 }
 
-// partial density of atom i over EXACT-list entries sub, sub+tpa, ... (the
-// persistent sweep compacts its Verlet candidates to the exact list each step,
-// so both paths see the same entries in the same lanes)
+// pair geometry (r_j - r_i, |r|) of list entry k: recomputed (batched path) or
+// read from the cache the persistent sweep fills once per step; both give the
+// same bits (pair_vec, r2_exact, __dsqrt_rn)
+__device__ __forceinline__ void pair_geo(const double* qb, int i, int j, const Box& box, const double4* cache,
+                                         int k, double& dx, double& dy, double& dz, double& r2, double& r) {
+  if (cache) {
+    const double4 c = cache[k];
+    dx = c.x;
+    dy = c.y;
+    dz = c.z;
+    r = c.w;
+    r2 = 0.0;  // unused: cached entries are already within rc
+  } else {
+    pair_vec(qb, i, j, box, dx, dy, dz);
+    r2 = r2_exact(dx, dy, dz);
+    r = __dsqrt_rn(r2);
+  }
+}
+
+// partial density of atom i over EXACT-list entries sub, sub+tpa, ...
 __device__ __forceinline__ double eam_rho_part(const double* qb, int i, const int32_t* list, int nl, int sub,
-                                               int tpa, const Box& box, double rc2, const Table& rho) {
+                                               int tpa, const Box& box, double rc2, const Table& rho,
+                                               const double4* cache = nullptr) {
   double s = 0.0;
   for (int k = sub; k < nl; k += tpa) {
     const int j = list[k];
-    double dx, dy, dz;
-    pair_vec(qb, i, j, box, dx, dy, dz);
-    const double r2 = r2_exact(dx, dy, dz);
-    if (!(r2 < rc2)) continue;
+    double dx, dy, dz, r2, r;
+    pair_geo(qb, i, j, box, cache, k, dx, dy, dz, r2, r);
+    if (!cache && !(r2 < rc2)) continue;
     double f, df;
-    tab_eval(rho, __dsqrt_rn(r2), f, df);
+    tab_eval(rho, r, f, df);
     s = __dadd_rn(s, f);
   }
   return s;
@@ -73,15 +90,13 @@ template <bool EV>
 __device__ __forceinline__ void eam_force_part(const double* qb, const double* fpb, int i, const int32_t* list,
                                                int nl, int sub, int tpa, const Box& box, double rc2,
                                                const Table& rho, const Table& phi, double* g, double* e,
-                                               double* v) {
+                                               double* v, const double4* cache = nullptr) {
   const double fpi = fpb[i];
   for (int k = sub; k < nl; k += tpa) {
     const int j = list[k];
-    double dx, dy, dz;
-    pair_vec(qb, i, j, box, dx, dy, dz);
-    const double r2 = r2_exact(dx, dy, dz);
-    if (!(r2 < rc2)) continue;
-    const double r = __dsqrt_rn(r2);
+    double dx, dy, dz, r2, r;
+    pair_geo(qb, i, j, box, cache, k, dx, dy, dz, r2, r);
+    if (!cache && !(r2 < rc2)) continue;
     double rf, drf, pf, dpf;
     tab_eval(rho, r, rf, drf);
     tab_eval(phi, r, pf, dpf);

@@ -48,6 +48,7 @@ struct SweepArgs {
   Table rho, phi, F;
   int32_t* cand;    // [n_atoms][SW_MAXN] Verlet candidates (rc + skin)
   int32_t* ncand;   // [n_atoms]
+  double4* geo;     // [slots][n_atoms][SW_MAXN] pair geometry cache
   int* overflow;
   // elementwise
   EwProg ew;
@@ -96,6 +97,7 @@ struct Slot {  // per-CTA (replica slot) view of the arrays, kept in registers
   int32_t* ncand;
   int32_t* nbr;   // exact list of the current step (compacted candidates)
   int32_t* nnbr;
+  double4* geo;   // cached (dx, dy, dz, r) of the exact-list pairs
 };
 
 // Verlet candidate lists (ascending j, rc + skin) of the current positions
@@ -140,30 +142,52 @@ __device__ void sw_eam(const SweepArgs& A, const Slot& S, const double* q, doubl
     sw_build(A, S, q, qref);
     __syncthreads();
   }
-  // exact list of this step: candidates filtered in order (same entries, same
-  // lane partition as k_eam_density / k_eam_force)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int nc = S.ncand[i];
-    const int32_t* cl = S.cand + (int64_t)i * SW_MAXN;
-    int32_t* el = S.nbr + (int64_t)i * SW_MAXN;
-    int c = 0;
-    for (int k = 0; k < nc; ++k) {
-      double dx, dy, dz;
-      pair_vec(q, i, cl[k], A.box, dx, dy, dz);
-      if (r2_exact(dx, dy, dz) < A.rc2) el[c++] = cl[k];
-    }
-    S.nnbr[i] = c;
-  }
-  __syncthreads();
+  // exact list of this step: tpa lanes per atom filter the candidates in
+  // chunks, ballots keep the ascending-j order, and the pair geometry of every
+  // kept pair is cached for both passes
   const int tpa = A.tpa;
   const int groups = blockDim.x / tpa;
   const int gi0 = threadIdx.x / tpa, sub = threadIdx.x % tpa;
+  const int lane = threadIdx.x & 31;
+  const unsigned gmask = (tpa == 32 ? 0xffffffffu : ((1u << tpa) - 1u)) << (lane & ~(tpa - 1));
   for (int base = 0; base < n; base += groups) {
     const int i = base + gi0;
-    const int ii = i < n ? i : n - 1;
-    const double s = group_sum(eam_rho_part(q, ii, S.nbr + (int64_t)ii * SW_MAXN, S.nnbr[ii], sub, tpa, A.box,
-                                            A.rc2, A.rho), tpa);
-    if (i < n && sub == 0) {
+    const bool live = i < n;
+    const int nc = live ? S.ncand[i] : 0;
+    const int32_t* cl = S.cand + (int64_t)(live ? i : 0) * SW_MAXN;
+    int32_t* el = S.nbr + (int64_t)(live ? i : 0) * SW_MAXN;
+    double4* geo = S.geo + (int64_t)(live ? i : 0) * SW_MAXN;
+    int c = 0;
+    for (int k0 = 0; k0 < SW_MAXN; k0 += tpa) {
+      const int k = k0 + sub;
+      bool keep = false;
+      double dx = 0.0, dy = 0.0, dz = 0.0, r2 = 0.0;
+      int j = 0;
+      if (k < nc) {
+        j = cl[k];
+        pair_vec(q, i, j, A.box, dx, dy, dz);
+        r2 = r2_exact(dx, dy, dz);
+        keep = r2 < A.rc2;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep) & gmask;
+      if (keep) {
+        const int pos = c + __popc(bal & ((1u << lane) - 1u));
+        el[pos] = j;
+        geo[pos] = make_double4(dx, dy, dz, __dsqrt_rn(r2));
+      }
+      c += __popc(bal);
+      if (!__any_sync(0xffffffffu, k0 + tpa < nc)) break;
+    }
+    if (live && sub == 0) S.nnbr[i] = c;
+  }
+  __syncthreads();
+  for (int base = 0; base < n; base += groups) {
+    const int i = base + gi0;
+    const bool live = i < n;
+    const int ii = live ? i : 0;
+    const double s = group_sum(eam_rho_part(q, ii, S.nbr + (int64_t)ii * SW_MAXN, live ? S.nnbr[ii] : 0, sub, tpa,
+                                            A.box, A.rc2, A.rho, S.geo + (int64_t)ii * SW_MAXN), tpa);
+    if (live && sub == 0) {
       double f, df;
       tab_eval(A.F, s, f, df);
       fp[i] = df;
@@ -172,14 +196,15 @@ __device__ void sw_eam(const SweepArgs& A, const Slot& S, const double* q, doubl
   __syncthreads();
   for (int base = 0; base < n; base += groups) {
     const int i = base + gi0;
-    const int ii = i < n ? i : n - 1;
+    const bool live = i < n;
+    const int ii = live ? i : 0;
     double gg[3] = {0.0, 0.0, 0.0}, e = 0.0, v[6];
-    eam_force_part<false>(q, fp, ii, S.nbr + (int64_t)ii * SW_MAXN, S.nnbr[ii], sub, tpa, A.box, A.rc2, A.rho,
-                          A.phi, gg, &e, v);
+    eam_force_part<false>(q, fp, ii, S.nbr + (int64_t)ii * SW_MAXN, live ? S.nnbr[ii] : 0, sub, tpa, A.box, A.rc2,
+                          A.rho, A.phi, gg, &e, v, S.geo + (int64_t)ii * SW_MAXN);
     gg[0] = group_sum(gg[0], tpa);
     gg[1] = group_sum(gg[1], tpa);
     gg[2] = group_sum(gg[2], tpa);
-    if (i < n && sub == 0) {
+    if (live && sub == 0) {
       g[3 * i] = gg[0];
       g[3 * i + 1] = gg[1];
       g[3 * i + 2] = gg[2];
@@ -198,10 +223,10 @@ __device__ __forceinline__ void sw_force(const SweepArgs& A, const Slot& S, cons
   }
 }
 
-__global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(const SweepArgs A) {
+__global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(const __grid_constant__ SweepArgs A) {
   extern __shared__ double sm[];
   Slot S{A.Q, A.P, A.prevQ, A.baseQ, A.baseP, A.jumpQ, A.jumpP, A.noise, A.hist, A.acc, A.out,
-         A.m0, A.m1, A.include_m0, A.cand, A.ncand, A.cand, A.ncand};
+         A.m0, A.m1, A.include_m0, A.cand, A.ncand, A.cand, A.ncand, A.geo};
   if (A.b_ridx) {
     // replica slot: offset every per-replica array, take this slot's slab
     const int slot = blockIdx.x;
@@ -220,7 +245,10 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep_cta(const SweepArgs A) {
     S.m0 = A.b_m0[slot];
     S.m1 = A.b_m1[slot];
     S.include_m0 = A.b_inc[slot];
-    if (!A.use_ew) S.cand += (int64_t)slot * 2 * ((int64_t)A.n_atoms * (SW_MAXN + 1) + 8);
+    if (!A.use_ew) {
+      S.cand += (int64_t)slot * 2 * ((int64_t)A.n_atoms * (SW_MAXN + 1) + 8);
+      S.geo += (int64_t)slot * A.n_atoms * SW_MAXN;
+    }
   }
   if (!A.use_ew) {
     // per slot: [candidates][counts][exact list][counts]
@@ -413,6 +441,8 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
     A.cand = (int32_t*)(((uintptr_t)(A.overflow + 4) + 15) & ~(uintptr_t)15);
     A.ncand = A.cand + (size_t)n * SW_MAXN;
     A.tpa = eam_tpa(n, SW_THREADS);
+    PL_TRY(ctx->work[7].reserve(sizeof(double4) * (size_t)n * SW_MAXN));
+    A.geo = (double4*)ctx->work[7].ptr;
     PL_CUDA(cudaMemsetAsync(A.overflow, 0, sizeof(int), st));
   }
   double init[2] = {h_state[0], h_state[1]};
@@ -489,6 +519,8 @@ int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, in
     A.ncand = A.cand + (size_t)n * SW_MAXN;  // slot 0; the kernel offsets per slot
     A.overflow = ovf;
     A.tpa = eam_tpa(n, SW_THREADS);
+    PL_TRY(ctx->work[7].reserve(sizeof(double4) * (size_t)n * SW_MAXN * R_act));
+    A.geo = (double4*)ctx->work[7].ptr;
     PL_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
   }
   PL_CUDA(cudaMemcpyAsync(amp, h_amp, sizeof(double) * (L + 1), cudaMemcpyHostToDevice, st));
