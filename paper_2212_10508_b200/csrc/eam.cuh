@@ -22,7 +22,7 @@ __device__ __forceinline__ void tab_eval(const Table& T, double x, double& f, do
   int k = (int)p;
   k = k < 0 ? 0 : (k > T.n - 1 ? T.n - 1 : k);
   const double t = __dsub_rn(p, (double)k);
-  const double4 c = *reinterpret_cast<const double4*>(T.c + 4 * (int64_t)k);
+  const double4 c = __ldg(reinterpret_cast<const double4*>(T.c + 4 * (int64_t)k));
   f = fma(t, fma(t, fma(t, c.w, c.z), c.y), c.x);
   df = __dmul_rn(fma(t, fma(t, __dmul_rn(3.0, c.w), __dmul_rn(2.0, c.z)), c.y), T.inv_dx);
 }
@@ -67,6 +67,9 @@ __device__ __forceinline__ double eam_rho_part(const double* qb, int i, const in
                                                int tpa, const Box& box, double rc2, const Table& rho,
                                                const double4* cache = nullptr) {
   double s = 0.0;
+  // unrolled so several independent table loads are in flight (the 5000-knot
+  // tables do not fit in L1); the sum order is unchanged
+#pragma unroll 4
   for (int k = sub; k < nl; k += tpa) {
     const int j = list[k];
     double dx, dy, dz, r2, r;
@@ -92,6 +95,7 @@ __device__ __forceinline__ void eam_force_part(const double* qb, const double* f
                                                const Table& rho, const Table& phi, double* g, double* e,
                                                double* v, const double4* cache = nullptr) {
   const double fpi = fpb[i];
+#pragma unroll 4
   for (int k = sub; k < nl; k += tpa) {
     const int j = list[k];
     double dx, dy, dz, r2, r;
