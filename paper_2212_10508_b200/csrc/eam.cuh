@@ -22,7 +22,9 @@ __device__ __forceinline__ void tab_eval(const Table& T, double x, double& f, do
   int k = (int)p;
   k = k < 0 ? 0 : (k > T.n - 1 ? T.n - 1 : k);
   const double t = __dsub_rn(p, (double)k);
-  const double4 c = __ldg(reinterpret_cast<const double4*>(T.c + 4 * (int64_t)k));
+  const double2 c01 = __ldg(reinterpret_cast<const double2*>(T.c + 4 * (int64_t)k));
+  const double2 c23 = __ldg(reinterpret_cast<const double2*>(T.c + 4 * (int64_t)k + 2));
+  const double4 c = make_double4(c01.x, c01.y, c23.x, c23.y);
   f = fma(t, fma(t, fma(t, c.w, c.z), c.y), c.x);
   df = __dmul_rn(fma(t, fma(t, __dmul_rn(3.0, c.w), __dmul_rn(2.0, c.z)), c.y), T.inv_dx);
 }
