@@ -16,6 +16,8 @@
 
 namespace pl {
 
+int eam_tpa_for(int n);
+
 constexpr int EAM_MAXN = 96;
 
 // tpa threads per atom (eam_tpa rule), one atom per group, groups strided over
@@ -120,7 +122,7 @@ int compute_eam(pl_pot* pot, int64_t B, const double* q, double* energy, double*
   Box box = make_box(pot->box);
   Table trho{pot->d_rho, pot->n_r, pot->dr, 1.0 / pot->dr}, tphi{pot->d_phi, pot->n_r, pot->dr, 1.0 / pot->dr},
       tF{pot->d_F, pot->n_rho, pot->drho, 1.0 / pot->drho};
-  const int tpa = eam_tpa(N, 1024);  // the persistent sweep's rule (same reduction tree)
+  const int tpa = eam_tpa_for(N);  // the cluster sweep's rule (same lane partition and reduction tree)
   const double rc2 = pot->rcut * pot->rcut;
   unsigned g = (unsigned)((na * tpa + 127) / 128);
   prof_mark(ctx->stream, ST_EAM, true);

@@ -101,6 +101,25 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
               const double* mass, double dt, double h, double hg, double expl, double* h_state,
               int64_t* h_out4, double* d_hist);
 
+int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, int R_act, const int32_t* h_ridx,
+                        const int64_t* h_m0, const int64_t* h_m1, const int32_t* h_inc, int mode, double* Q,
+                        double* P, double* baseQ, double* baseP, const double* jumpQ, const double* jumpP,
+                        const double* noise, const double* h_amp, const double* mass, double dt, double h,
+                        double hg, double expl, double* h_state, int64_t* h_out4, double* d_hist);
+
+// one-slot cluster sweep (EAM coarse); -1 when not applicable
+static int sweep_cluster_one(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1, int inc,
+                             int mode, double* Q, double* P, double* baseQ, double* baseP, const double* jumpQ,
+                             const double* jumpP, const double* noise, const double* h_amp, const double* mass,
+                             double dt, double h, double hg, double expl, double* h_state, int64_t* o4,
+                             double* d_hist) {
+  if (coarse->kind != POT_EAM || getenv("PL_SWEEP_NOCLUSTER")) return -1;
+  const int32_t ridx = 0;
+  const int32_t incl = inc;
+  return sweep_cluster_batch(ctx, coarse, d, L, m1, 1, &ridx, &m0, &m1, &incl, mode, Q, P, baseQ, baseP, jumpQ,
+                             jumpP, noise, h_amp, mass, dt, h, hg, expl, h_state, o4, d_hist);
+}
+
 static int cta_status(const int64_t* o4, int64_t* h_out, int32_t* h_blowup) {
   if (o4[3] == 1) {
     h_out[0] = o4[1];
@@ -125,9 +144,12 @@ int bootstrap(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
   if (coarse->dim && coarse->dim != d) return fail(PL_EARG, "potential dimension mismatch");
   int64_t o4[4];
   double state[2] = {0.0, 0.0};
-  PL_TRY(ctx->work[5].reserve(sizeof(double) * (m1 - m0 + 1)));
-  int rc = sweep_cta(ctx, coarse, d, L, m0, m1, 0, 1, Q, P, Q, baseQ, baseP, baseQ, baseP, noise_all, h_amp,
-                     mass, dt, h, hg, 0.0, state, o4, (double*)ctx->work[5].ptr);
+  PL_TRY(ctx->work[6].reserve(sizeof(double) * (m1 - m0 + 1)));
+  int rc = sweep_cluster_one(ctx, coarse, d, L, m0, m1, 0, 1, Q, P, baseQ, baseP, baseQ, baseP, noise_all, h_amp,
+                             mass, dt, h, hg, 0.0, state, o4, (double*)ctx->work[6].ptr);
+  if (rc == -1)
+    rc = sweep_cta(ctx, coarse, d, L, m0, m1, 0, 1, Q, P, Q, baseQ, baseP, baseQ, baseP, noise_all, h_amp, mass, dt,
+                   h, hg, 0.0, state, o4, (double*)ctx->work[6].ptr);
   if (rc != -1) {
     PL_TRY(rc);
     return cta_status(o4, h_out, h_blowup);
@@ -169,8 +191,11 @@ int sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1,
   if (coarse->dim && coarse->dim != d) return fail(PL_EARG, "potential dimension mismatch");
   if (!getenv("PL_SWEEP_GENERIC")) {
     int64_t o4[4];
-    int rc = sweep_cta(ctx, coarse, d, L, m0, m1, include_m0, 0, traj_q, traj_p, prev_q, base_q, base_p,
-                       jump_q, jump_p, noise_all, h_amp, mass, dt, h, hg, expl, h_state, o4, d_hist);
+    int rc = sweep_cluster_one(ctx, coarse, d, L, m0, m1, include_m0, 0, traj_q, traj_p, base_q, base_p, jump_q,
+                               jump_p, noise_all, h_amp, mass, dt, h, hg, expl, h_state, o4, d_hist);
+    if (rc == -1)
+      rc = sweep_cta(ctx, coarse, d, L, m0, m1, include_m0, 0, traj_q, traj_p, prev_q, base_q, base_p, jump_q,
+                     jump_p, noise_all, h_amp, mass, dt, h, hg, expl, h_state, o4, d_hist);
     if (rc != -1) {
       PL_TRY(rc);
       return cta_status(o4, h_out, h_blowup);

@@ -13,6 +13,8 @@
 // Integrator arithmetic = integrator.cu (explicit round-to-nearest, numpy
 // order); EAM sums in neighbour order; every reduction in a fixed tree:
 // the sweep is bitwise deterministic.
+#include <cstdlib>
+
 #include "eam.cuh"
 #include "neigh.cuh"
 #include "pl_common.cuh"
@@ -467,6 +469,12 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
   return PL_OK;
 }
 
+int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, int R_act, const int32_t* h_ridx,
+                        const int64_t* h_m0, const int64_t* h_m1, const int32_t* h_inc, int mode, double* Q,
+                        double* P, double* baseQ, double* baseP, const double* jumpQ, const double* jumpP,
+                        const double* noise, const double* h_amp, const double* mass, double dt, double h,
+                        double hg, double expl, double* h_state, int64_t* h_out4, double* d_hist);
+
 // R_act replica slots in one launch (grid = R_act CTAs); arrays carry a leading
 // replica dimension: Q/P (R, N+1, d), base/jump (R, N, d), noise (R, N, L+1, d),
 // d_hist (R, N).  h_state (2 R_act) and h_out4 (4 R_act) per slot.
@@ -476,6 +484,12 @@ int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, in
                     const double* h_amp, const double* mass, double dt, double h, double hg, double expl,
                     double* h_state, int64_t* h_out4, double* d_hist) {
   if (R_act <= 0) return PL_OK;
+  if (!getenv("PL_SWEEP_NOCLUSTER")) {
+    const int rc = sweep_cluster_batch(ctx, coarse, d, L, N, R_act, h_ridx, h_m0, h_m1, h_inc, mode, Q, P, baseQ,
+                                       baseP, jumpQ, jumpP, noise, h_amp, mass, dt, h, hg, expl, h_state, h_out4,
+                                       d_hist);
+    if (rc != -1) return rc;
+  }
   SweepArgs A{};
   const bool ew = is_elementwise(coarse);
   if (!ew && coarse->kind != POT_EAM) return fail(PL_EARG, "batched sweep needs an EAM or elementwise coarse potential");
