@@ -143,6 +143,12 @@ __constant__ int c_yi5_cgoff[130];    // triple id -> offset of its block in c_c
 constexpr int YI6_WARPS = 16;
 __constant__ int c_yi6_gseg[YI6_WARPS + 1];
 __constant__ int c_yi6_groups[32];
+// box-form Z/Y kernel (snap_yi8.cu, own constant bank)
+cudaError_t snap_box_setup(const double* box, int nbox, const int* off, const int* code, const int* iseg,
+                           const int* items, int nitems);
+int snap_box_variants(int* nw);
+cudaError_t snap_box_launch(int nw, cudaStream_t st, int64_t natoms, double beta0, const double* coef,
+                            const void* utot, void* ylist, double* eatom);
 
 // ------------------------------------------------------------------ host setup
 static double fact(int n) {
@@ -297,6 +303,72 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     std::vector<int> groups, gseg, groups16, gseg16;
     lpt(8, groups, gseg);
     lpt(YI6_WARPS, groups16, gseg16);
+    {  // box kernel (snap_yi8.cu): every (X+1)(Y+1) product of each admissible mb1
+      auto rows6 = rows;
+      rows.clear();
+      for (int J = 0; J <= tj; ++J)
+        for (int mb = 0; 2 * mb <= J; ++mb) {
+          double c = 0.0;
+          for (int tid : byJ[J]) {
+            int x = code[tid] / 100, y = (code[tid] / 10) % 10, sh = (x + y - J) / 2;
+            for (int mb1 = 0; mb1 <= x; ++mb1)
+              if (mb + sh - mb1 >= 0 && mb + sh - mb1 <= y) c += 7.0 * (x + 1) * (y + 1) + 2.0 * (x + y + 2) + 12.0;
+            c += 60.0;
+          }
+          rows.push_back({c, (J << 8) | mb});
+        }
+      std::sort(rows.begin(), rows.end(), [](auto& a, auto& b) { return a.first > b.first; });
+      // rows -> warps (LPT), then each warp's (row, triple) items in ascending X
+      auto itemize = [&](int NW, std::vector<int>& iseg, std::vector<int>& items) {
+        std::vector<int> g, sg;
+        lpt(NW, g, sg);
+        iseg.assign(NW + 1, 0);
+        items.clear();
+        for (int w = 0; w < NW; ++w) {
+          iseg[w] = (int)items.size();
+          std::vector<std::pair<int, int>> mine;  // (sort key, item)
+          for (int gi = sg[w]; gi < sg[w + 1]; ++gi) {
+            const int J = g[gi] >> 8, mb = g[gi] & 0xff;
+            for (int tid : byJ[J]) {
+              const int x = code[tid] / 100, y = (code[tid] / 10) % 10;
+              mine.push_back({x * 10000 + y * 100 + J * 10 + mb, (tid << 16) | (J << 8) | mb});
+            }
+          }
+          std::sort(mine.begin(), mine.end());
+          for (auto& m : mine) items.push_back(m.second);
+        }
+        iseg[NW] = (int)items.size();
+      };
+      int box_nw[8];
+      const int box_nv = snap_box_variants(box_nw);
+      std::vector<int> iseg_all(box_nv * 17, 0), items_all;
+      for (int v = 0; v < box_nv; ++v) {
+        std::vector<int> is, it;
+        itemize(box_nw[v], is, it);
+        std::copy(is.begin(), is.end(), iseg_all.begin() + v * 17);
+        items_all.insert(items_all.end(), it.begin(), it.end());
+      }
+      const int n_items = (int)items_all.size() / box_nv;
+      rows = rows6;
+      static bool box_done = false;
+      if (!box_done) {
+        std::vector<double> box;
+        std::vector<int> boff;
+        for (int c : code) {
+          const int x = c / 100, y = (c / 10) % 10, J = c % 10, sh = (x + y - J) / 2;
+          boff.push_back((int)box.size());
+          for (int b = 0; b <= y; ++b)
+            for (int a = 0; a <= x; ++a) {
+              const int ma = a + b - sh;
+              box.push_back(ma >= 0 && ma <= J ? clebsch(x, 2 * a - x, y, 2 * b - y, J, 2 * ma - J) : 0.0);
+            }
+        }
+        if ((int)code.size() != yi5::NT) return fail(PL_EARG, "SNAP box tables: unexpected triple count");
+        PL_CUDA(snap_box_setup(box.data(), (int)box.size(), boff.data(), code.data(), iseg_all.data(),
+                               items_all.data(), n_items));
+        box_done = true;
+      }
+    }
     PL_CUDA(cudaMemcpyToSymbol(c_yi6_gseg, gseg16.data(), sizeof(int) * gseg16.size()));
     PL_CUDA(cudaMemcpyToSymbol(c_yi6_groups, groups16.data(), sizeof(int) * groups16.size()));
     std::vector<double> cb2(cy);
@@ -2117,9 +2189,15 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   prof_mark(ctx->stream, ST_YI, true);
   static const int yi_var = [] {
     const char* e = getenv("PL_SNAP_YI");
-    return e ? atoi(e) : 6;
+    return e ? atoi(e) : 8;
   }();
-  if (S->yi_reg && yi_var == 7) {
+  static const int box_nw = [] {
+    const char* e = getenv("PL_SNAP_BOXW");
+    return e ? atoi(e) : 12;
+  }();
+  if (S->yi_reg && yi_var == 8) {
+    PL_CUDA(snap_box_launch(box_nw, ctx->stream, na, D.beta0, D.yi5, buf.utot, buf.y, buf.eatom));
+  } else if (S->yi_reg && yi_var == 7) {
     size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI6_WARPS * 9 * YI_ATOMS +
                 sizeof(double) * YI6_WARPS * YI_ATOMS;
     k_snap_yi_seven<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI6_WARPS * 32, sm, ctx->stream>>>(
@@ -2226,7 +2304,7 @@ extern "C" int pl_snap_info(pl_pot* pot, int32_t* h_counts, double* h_flops) {
   h_counts[4] = S->nunits;
   // FLOPs of the kernel variants that compute_snap actually launches
   const char* ey = getenv("PL_SNAP_YI");
-  const int yv = ey ? atoi(ey) : 6;
+  const int yv = ey ? atoi(ey) : 8;
   const char* ea = getenv("PL_SNAP_ADJ");
   const char* er = getenv("PL_SNAP_RR");
   const bool rr = !(er && er[0] == '0') && S->tj == 8;

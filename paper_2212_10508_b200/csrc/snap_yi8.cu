@@ -1,0 +1,231 @@
+// SNAP Z/Y contraction, twojmax = 8, "box" form (k_snap_yi_box).
+//
+// Lanes = atoms (32 per CTA, U^J of all layers expanded to full matrices in
+// shared memory, as k_snap_yi_six); warps own (J, mb) half rows by an LPT
+// schedule.  For every triple (X, Y, J) of a row and every admissible mb1,
+// both U columns U^X[.][mb1] and U^Y[.][mb2] are loaded into registers (the
+// b-side CG factor C(mb, mb1) folded into U^Y) and ALL (X+1)(Y+1) products are
+// accumulated on their anti-diagonal s = ma1 + ma2 (compile-time register
+// index), weighted by the box table C(ma = s - SH, ma1) that is zero outside
+// the CG band.  The code per (X, Y) is one branch-free block of independent
+// FMA chains with constant-bank coefficients at compile-time offsets; the
+// corner products it spends on zeros (~40%) are cheaper than the per-product
+// index arithmetic and predication of the banded loops (k_snap_yi_six).  The
+// diagonals are mapped to the z row (runtime shift SH) through the warp's
+// shared strip once per (triple, row).
+//
+// Separate translation unit: the box table (32.8 KB) has its own constant
+// bank next to snap.cu's CG blocks.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pl {
+
+namespace yib {
+constexpr int TJ = 8;
+constexpr int NT = 125;        // (X >= Y, J) triples at twojmax 8
+constexpr int NFULL = 285;     // sum (J+1)^2
+constexpr int NHALF = 155;     // sum (J+1)(J/2+1)
+constexpr int ATOMS = 32;
+constexpr int BOX_MAX = 4098;  // sum over triples of (X+1)(Y+1)
+constexpr int foff(int J) { return J * (J + 1) * (2 * J + 1) / 6; }
+constexpr int hoff(int J) {
+  int h = 0;
+  for (int j = 0; j < J; ++j) h += (j + 1) * (j / 2 + 1);
+  return h;
+}
+}  // namespace yib
+
+__constant__ double c_box[yib::BOX_MAX];  // per triple: [Y+1][X+1]
+__constant__ int c_box_off[yib::NT];
+__constant__ int c_box_code[yib::NT];         // X*100 + Y*10 + J
+constexpr int BOX_MAX_ITEMS = 400;            // (row, triple) pairs: 375 at twojmax 8
+// warps per CTA of the compiled variants (the host builds one schedule each)
+// (3 warps per SM sub-partition leave 168 registers per thread; 4 would force 128
+// and spill the X = 8 instantiation)
+constexpr int BOX_NV = 2;
+constexpr int BOX_NW[BOX_NV] = {12, 8};
+__constant__ int c_box_iseg[BOX_NV][17];                 // items of warp w: [iseg[w], iseg[w+1])
+__constant__ int c_box_items[BOX_NV][BOX_MAX_ITEMS];     // tid << 16 | J << 8 | mb
+
+struct Cx {
+  double re, im;
+};
+
+template <int X>
+__device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int J, int SH, int jtop, int mb, int boff,
+                                      double cy, double be, Cx* __restrict__ yrow, const Cx* __restrict__ urow,
+                                      double& esum) {
+  constexpr int S = X + yib::TJ;
+  constexpr int FX = yib::foff(X);
+  Cx d[S + 1];
+#pragma unroll
+  for (int s = 0; s <= S; ++s) d[s] = Cx{0.0, 0.0};
+  const double* cb = c_box + boff;  // [Y+1][X+1]: cb[b * (X + 1) + a] = C(ma = a + b - SH, ma1 = a)
+  const int FY = yib::foff(Y);
+  const int lo = max(0, mb + SH - Y), hi = min(X, mb + SH);
+#pragma unroll 1
+  for (int mb1 = lo; mb1 <= hi; ++mb1) {
+    const int mb2 = mb + SH - mb1;
+    const double cbv = cb[mb2 * (X + 1) + mb1];  // C(mb, mb1)
+    const Cx* px = Ul + (FX + mb1 * (X + 1)) * yib::ATOMS;
+    const Cx* py = Ul + (FY + mb2 * (Y + 1)) * yib::ATOMS;
+    Cx ux[X + 1];
+#pragma unroll
+    for (int a = 0; a <= X; ++a) ux[a] = px[a * yib::ATOMS];
+    // element b of the U^Y column times row block b of the box: X+1 independent
+    // diagonals (skipping the zero corners per product costs more than it saves)
+#pragma unroll
+    for (int b = 0; b <= yib::TJ; ++b) {
+      if (b > Y) break;
+      const Cx v = py[b * yib::ATOMS];
+      const Cx uy{cbv * v.re, cbv * v.im};
+#pragma unroll
+      for (int a = 0; a <= X; ++a) {
+        const double c = cb[b * (X + 1) + a];
+        const double tr = c * ux[a].re, ti = c * ux[a].im;
+        d[a + b].re = fma(tr, uy.re, d[a + b].re);
+        d[a + b].im = fma(tr, uy.im, d[a + b].im);
+        d[a + b].re = fma(-ti, uy.im, d[a + b].re);
+        d[a + b].im = fma(ti, uy.re, d[a + b].im);
+      }
+    }
+  }
+  // diagonal s -> element ma = s - SH of the Y row (the warp owns the row) and the energy
+  Cx* yo = yrow - SH * yib::ATOMS;
+  const Cx* uo = urow - SH * yib::ATOMS;
+#pragma unroll
+  for (int s = 0; s <= S; ++s) {
+    if (s >= SH && s <= SH + jtop) {
+      Cx y = yo[s * yib::ATOMS];
+      y.re = fma(cy, d[s].re, y.re);
+      y.im = fma(cy, d[s].im, y.im);
+      yo[s * yib::ATOMS] = y;
+      if (be != 0.0) {
+        const int ma = s - SH;
+        const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+        const Cx u = uo[s * yib::ATOMS];
+        esum = fma(be * w, fma(u.re, d[s].re, u.im * d[s].im), esum);
+      }
+    }
+  }
+}
+
+constexpr int box_regs(int nw) { return nw <= 8 ? 255 : 168; }
+
+template <int NW, int V>
+__global__ void __maxnreg__(box_regs(NW))
+k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, const Cx* __restrict__ utot,
+              Cx* __restrict__ ylist, double* __restrict__ eatom) {
+  extern __shared__ double smem[];
+  Cx* Uf = reinterpret_cast<Cx*>(smem);                 // [NFULL][32] full U matrices
+  Cx* Ys = Uf + yib::NFULL * yib::ATOMS;               // [NHALF][32] Y half rows
+  double* epart = reinterpret_cast<double*>(Ys + yib::NHALF * yib::ATOMS);  // [NW][32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t a0 = (int64_t)blockIdx.x * yib::ATOMS;
+  const int na_blk = (int)min((int64_t)yib::ATOMS, natoms - a0);
+  for (int t = threadIdx.x; t < yib::NFULL * yib::ATOMS; t += blockDim.x) {
+    const int at = t & (yib::ATOMS - 1), f = t >> 5;
+    int J = 0;
+    while (J < yib::TJ && f >= yib::foff(J + 1)) ++J;
+    const int e = f - yib::foff(J), mb = e / (J + 1), ma = e - mb * (J + 1);
+    Cx v{0.0, 0.0};
+    if (at < na_blk) {
+      const Cx* ua = utot + (a0 + at) * yib::NHALF + yib::hoff(J);
+      if (2 * mb <= J) {
+        v = ua[mb * (J + 1) + ma];
+      } else {
+        const Cx w = ua[(J - mb) * (J + 1) + (J - ma)];
+        v = ((ma + mb) & 1) ? Cx{-w.re, w.im} : Cx{w.re, -w.im};
+      }
+    }
+    Uf[f * yib::ATOMS + at] = v;
+  }
+  for (int t = threadIdx.x; t < yib::NHALF * yib::ATOMS; t += blockDim.x) Ys[t] = Cx{0.0, 0.0};
+  __syncthreads();
+  const Cx* Ul = Uf + lane;
+  const int* iseg = c_box_iseg[V];
+  const int* items = c_box_items[V];
+  double esum = 0.0;
+  // the warp's (row, triple) items in ascending X: all warps sweep the X
+  // instantiations in the same order, so the live code stays small
+  for (int it = iseg[warp]; it < iseg[warp + 1]; ++it) {
+    const int item = items[it];
+    const int tid = item >> 16, J = (item >> 8) & 0xff, mb = item & 0xff;
+    const int code = c_box_code[tid];
+    const int X = code / 100, Y = (code / 10) % 10;
+    const int SH = (X + Y - J) / 2;
+    const int jtop = (2 * mb == J) ? J / 2 : J;
+    const int boff = c_box_off[tid];
+    const double cy = coef[tid], be = coef[yib::NT + tid];
+    Cx* yrow = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + lane;
+    const Cx* urow = Ul + (yib::foff(J) + mb * (J + 1)) * yib::ATOMS;
+    switch (X) {
+      case 0: box_x<0>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      case 1: box_x<1>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      case 2: box_x<2>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      case 3: box_x<3>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      case 4: box_x<4>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      case 5: box_x<5>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      case 6: box_x<6>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      case 7: box_x<7>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      default: box_x<8>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+    }
+  }
+  epart[warp * yib::ATOMS + lane] = esum;
+  __syncthreads();
+  for (int t = threadIdx.x; t < na_blk * yib::NHALF; t += blockDim.x) {
+    const int at = t / yib::NHALF, h = t - at * yib::NHALF;
+    ylist[(a0 + at) * yib::NHALF + h] = Ys[h * yib::ATOMS + at];
+  }
+  if (warp == 0 && lane < na_blk) {
+    double e = beta0;
+    for (int w = 0; w < NW; ++w) e += epart[w * yib::ATOMS + lane];
+    eatom[a0 + lane] = e;
+  }
+}
+
+// Upload the box table and the per-warp item lists (process-wide; twojmax 8 only).
+// iseg: [BOX_NV][17], items: [BOX_NV][nitems]
+cudaError_t snap_box_setup(const double* box, int nbox, const int* off, const int* code, const int* iseg,
+                           const int* items, int nitems) {
+  if (nbox > yib::BOX_MAX || nitems > BOX_MAX_ITEMS) return cudaErrorInvalidValue;
+  cudaError_t e;
+  if ((e = cudaMemcpyToSymbol(c_box, box, sizeof(double) * nbox)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_box_off, off, sizeof(int) * yib::NT)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_box_code, code, sizeof(int) * yib::NT)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_box_iseg, iseg, sizeof(int) * BOX_NV * 17)) != cudaSuccess) return e;
+  for (int v = 0; v < BOX_NV; ++v)
+    if ((e = cudaMemcpyToSymbol(c_box_items, items + (size_t)v * nitems, sizeof(int) * nitems,
+                                sizeof(int) * BOX_MAX_ITEMS * v)) != cudaSuccess)
+      return e;
+  return cudaSuccess;
+}
+
+int snap_box_variants(int* nw) {
+  for (int v = 0; v < BOX_NV; ++v) nw[v] = BOX_NW[v];
+  return BOX_NV;
+}
+
+template <int NW, int V>
+static cudaError_t box_launch(cudaStream_t st, unsigned grid, int64_t natoms, double beta0, const double* coef,
+                              const void* utot, void* ylist, double* eatom) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_snap_yi_box<NW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * NW * yib::ATOMS;
+  k_snap_yi_box<NW, V><<<grid, NW * 32, sm, st>>>(natoms, beta0, coef, (const Cx*)utot, (Cx*)ylist, eatom);
+  return cudaGetLastError();
+}
+
+// nw: warps per CTA (one of BOX_NW)
+cudaError_t snap_box_launch(int nw, cudaStream_t st, int64_t natoms, double beta0, const double* coef,
+                            const void* utot, void* ylist, double* eatom) {
+  const unsigned grid = (unsigned)((natoms + yib::ATOMS - 1) / yib::ATOMS);
+  if (nw == 8) return box_launch<8, 1>(st, grid, natoms, beta0, coef, utot, ylist, eatom);
+  return box_launch<12, 0>(st, grid, natoms, beta0, coef, utot, ylist, eatom);
+}
+
+}  // namespace pl
