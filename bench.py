@@ -389,9 +389,32 @@ def parareal_run():
         return {"error": f"{type(exc).__name__}: {exc}"}
     torch.cuda.synchronize()
     wall = time.perf_counter() - t
+    # measured per-window costs C_f / C_c (one window, device-resident, CUDA events)
+    # and the reference cost model's gain Gamma (accounting.py:141-159)
+    from paper_2212_10508_b200 import accounting
+    from paper_2212_10508_b200.integrator import WindowKernel
+
+    def window_ms(pot, reps=5):
+        k = WindowKernel(pot, params, sched, 3 * n)
+        Q0 = torch.from_numpy(q0[None].copy()).to(k.device)
+        P0 = torch.from_numpy(init.p[None].copy()).to(k.device)
+        noise = k.noise([plan.window_seeds[0]])
+        k.run(Q0, P0, noise)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        for _ in range(reps):
+            k.run(Q0, P0, noise)
+        ev[1].record()
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / reps
+
+    cf, cc = window_ms(snap), window_ms(eam)
+    g = accounting.adaptive_gain(res.slabs, N, cf, cc)
     return {"config": "PR1: 129 atoms, 16 slices x 100, SNAP fine / EAM coarse, delta_conv 1e-10, "
                       "delta_expl 0.35", "wall_s": wall, "n_slab": res.n_slab,
-            "sum_k": res.total_iterations, "converged": res.converged}
+            "sum_k": res.total_iterations, "converged": res.converged,
+            "cf_ms": cf, "cc_ms": cc, "gain_model": g.gain, "gain_ideal": g.ideal_gain,
+            "sequential_fine_s": N * cf / 1e3, "speedup_vs_sequential_fine": (N * cf / 1e3) / wall}
 
 
 def main():

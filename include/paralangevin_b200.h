@@ -122,6 +122,31 @@ int pl_propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L,
                          const double* h_amp, const double* d_mass, double dt, double half_dt,
                          double half_dt_gamma, double* d_q1, double* d_p1, int32_t* d_blowup);
 
+/* Same propagation, also accumulating the full-step momentum moments of the
+ * kinetic-temperature measurement (integrator.py:350-365 _measure_chain,
+ * 430-482 measure_kinetic_temperature): for every window w, substep
+ * l = 1..L and component c,
+ *   d_s1[(w*L + l-1)*d + c] += p_l,   d_s2[...] += p_l * p_l   (numpy order).
+ * d_s1 / d_s2 are W x L x d device arrays owned by the caller (zero them
+ * before the first window that counts). */
+int pl_propagate_windows_moments(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L,
+                                 const double* d_q0, const double* d_p0, const double* d_noise,
+                                 const double* h_amp, const double* d_mass, double dt, double half_dt,
+                                 double half_dt_gamma, double* d_q1, double* d_p1, int32_t* d_blowup,
+                                 double* d_s1, double* d_s2);
+
+/* ---- batched local minimisation (potentials.py:231-287) ---------------- */
+/* B independent steepest descents with Armijo backtracking, the reference's
+ * _descend: from x (B x d, device, overwritten with the result) until
+ * sqrt(|grad|^2) <= tol, the step doubling (cap 1e3) per iteration and halving
+ * per rejected trial, acceptance E_trial <= E - 0.5*step*|grad|^2 (a trial the
+ * potential rejects counts as +inf).  h_status[b]: 0 converged, 1 line search
+ * stalled (step < 1e-18), 2 no convergence within max_iter (the two cases
+ * where the reference raises MinimizationError); h_iters[b] = accepted steps;
+ * h_energy (optional) = final energies.  Synchronous. */
+int pl_minimize(pl_ctx* ctx, pl_pot* pot, int64_t B, int64_t d, double* d_x, double tol, int64_t max_iter,
+                int32_t* h_status, int64_t* h_iters, double* h_energy);
+
 /* ---- parareal corrected sweep (parareal.py:289-299, 195-198, 425-445) -- */
 /* Trajectory nodes live in two (N+1) x d arrays: d_traj_q, d_traj_p.  Window
  * quantities (indexed by the absolute 0-based window m) live in N x d arrays:

@@ -56,6 +56,9 @@ SIGNATURES = {
     "pl_compute": (C.c_int, [vp, vp, i64, i64, vp, vp, vp, vp]),
     "pl_propagate_windows": (C.c_int, [vp, vp, i64, i64, C.c_int, vp, vp, vp, pd, vp, dbl, dbl,
                                        dbl, vp, vp, vp]),
+    "pl_propagate_windows_moments": (C.c_int, [vp, vp, i64, i64, C.c_int, vp, vp, vp, pd, vp, dbl, dbl,
+                                               dbl, vp, vp, vp, vp, vp]),
+    "pl_minimize": (C.c_int, [vp, vp, i64, i64, vp, dbl, i64, pi32, pi64, pd]),
     "pl_sweep": (C.c_int, [vp, vp, i64, C.c_int, i64, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp,
                            vp, pd, vp, dbl, dbl, dbl, dbl, pd, vp, pi64, pi32]),
     "pl_sub": (C.c_int, [vp, i64, vp, vp, vp]),

@@ -36,8 +36,10 @@ int gaussian_streams(pl_ctx* ctx, const uint64_t* seeds, int64_t n_rows, int64_t
 int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, const double* q0,
                       const double* p0, const double* noise, const double* h_amp,
                       const double* mass, double dt, double h, double hg, double* q1, double* p1,
-                      int32_t* blow);
+                      int32_t* blow, double* s1 = nullptr, double* s2 = nullptr);
 int lj_check(pl_pot* pot);
+int minimize(pl_ctx* ctx, pl_pot* pot, int64_t B, int64_t d, double* x, double tol, int64_t max_iter,
+             int32_t* h_status, int64_t* h_iters, double* h_energy);
 int eam_prepare(pl_pot* pot, const double* rho, const double* phi, const double* F);
 int sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1, int include_m0,
           double* traj_q, double* traj_p, const double* prev_q, double* base_q, double* base_p,
@@ -298,6 +300,23 @@ int pl_propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L,
     return fail(PL_EARG, "NULL argument");
   return propagate_windows(ctx, pot, W, d, L, d_q0, d_p0, d_noise, h_amp, d_mass, dt, half_dt,
                            half_dt_gamma, d_q1, d_p1, d_blowup);
+}
+
+int pl_minimize(pl_ctx* ctx, pl_pot* pot, int64_t B, int64_t d, double* d_x, double tol, int64_t max_iter,
+                int32_t* h_status, int64_t* h_iters, double* h_energy) {
+  if (!ctx || !pot || !d_x || !h_status || !h_iters) return fail(PL_EARG, "NULL argument");
+  return minimize(ctx, pot, B, d, d_x, tol, max_iter, h_status, h_iters, h_energy);
+}
+
+int pl_propagate_windows_moments(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L,
+                                 const double* d_q0, const double* d_p0, const double* d_noise,
+                                 const double* h_amp, const double* d_mass, double dt, double half_dt,
+                                 double half_dt_gamma, double* d_q1, double* d_p1, int32_t* d_blowup,
+                                 double* d_s1, double* d_s2) {
+  if (!ctx || !pot || !d_q0 || !d_p0 || !d_noise || !h_amp || !d_q1 || !d_p1 || !d_blowup || !d_s1 || !d_s2)
+    return fail(PL_EARG, "NULL argument");
+  return propagate_windows(ctx, pot, W, d, L, d_q0, d_p0, d_noise, h_amp, d_mass, dt, half_dt, half_dt_gamma,
+                           d_q1, d_p1, d_blowup, d_s1, d_s2);
 }
 
 int pl_sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1, int include_m0,

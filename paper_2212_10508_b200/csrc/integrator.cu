@@ -50,12 +50,20 @@ __device__ __forceinline__ void record_blowup(int32_t* blow, int64_t w, int s) {
 
 __device__ __forceinline__ bool bounded(double a) { return fabs(a) <= BLOWUP_LIMIT; }
 
+// running momentum moments of the full steps (integrator.py:359-361: s1 += p,
+// s2 += p * p, numpy order), one slot per (window, substep, component)
+__device__ __forceinline__ void moment(double* s1, double* s2, int64_t k, double p) {
+  s1[k] = add(s1[k], p);
+  s2[k] = add(s2[k], mul(p, p));
+}
+
 // ------------------------------------------------------------ elementwise
 __global__ void k_window_ew(EwProg P, int64_t W, int64_t d, StepConsts K,
                             const double* __restrict__ amp, const double* __restrict__ q0,
                             const double* __restrict__ p0, const double* __restrict__ noise,
                             const double* __restrict__ mass, double* __restrict__ q1,
-                            double* __restrict__ p1, int32_t* __restrict__ blow) {
+                            double* __restrict__ p1, int32_t* __restrict__ blow, double* __restrict__ s1,
+                            double* __restrict__ s2) {
   int64_t n = W * d;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -77,6 +85,7 @@ __global__ void k_window_ew(EwProg P, int64_t W, int64_t d, StepConsts K,
       al = mul(amp[s], sm);
       p = add(sub(sub(ph, mul(K.h, grad)), mul(K.hg, ph)), mul(al, gl));
       if (!failed && !(bounded(q) && bounded(p))) failed = s;
+      if (s1) moment(s1, s2, (w * K.L + (s - 1)) * d + i, p);
       pref = ph;
     }
     q1[t] = q;
@@ -92,7 +101,8 @@ k_window_lj(int64_t W, int n, double eps, double sigma, StepConsts K,
             const double* __restrict__ amp, const double* __restrict__ q0,
             const double* __restrict__ p0, const double* __restrict__ noise,
             const double* __restrict__ mass, double* __restrict__ q1, double* __restrict__ p1,
-            int32_t* __restrict__ blow, int* __restrict__ coincident) {
+            int32_t* __restrict__ blow, int* __restrict__ coincident, double* __restrict__ s1,
+            double* __restrict__ s2) {
   extern __shared__ double sm_[];
   const int d = n * D;
   double* sq = sm_;          // positions
@@ -143,6 +153,7 @@ k_window_lj(int64_t W, int n, double eps, double sigma, StepConsts K,
         double al = mul(amp[s], smm);
         p[k] = add(sub(sub(ph[k], mul(K.h, sg[t])), mul(K.hg, ph[k])), mul(al, gw[(int64_t)s * d + t]));
         if (!(bounded(sq[t]) && bounded(p[k]))) f = 1;
+        if (s1) moment(s1, s2, (w * K.L + (s - 1)) * d + t, p[k]);
         pref[k] = ph[k];
       }
     }
@@ -183,7 +194,7 @@ __global__ void k_close(int64_t W, int64_t d, int s, StepConsts K, const double*
                         const double* __restrict__ noise, const double* __restrict__ mass,
                         const double* __restrict__ grad, const double* __restrict__ ph,
                         const double* __restrict__ q, double* __restrict__ p,
-                        int32_t* __restrict__ blow) {
+                        int32_t* __restrict__ blow, double* __restrict__ s1, double* __restrict__ s2) {
   int64_t n = W * d;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -195,6 +206,7 @@ __global__ void k_close(int64_t W, int64_t d, int s, StepConsts K, const double*
     double pn = add(sub(sub(h, mul(K.h, grad[t])), mul(K.hg, h)), mul(al, gl));
     p[t] = pn;
     if (!(bounded(q[t]) && bounded(pn))) record_blowup(blow, w, s);
+    if (s1) moment(s1, s2, (w * K.L + (s - 1)) * d + i, pn);
   }
 }
 
@@ -207,7 +219,7 @@ static unsigned grid_for(int64_t n, int threads = 256) {
 int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, const double* q0,
                       const double* p0, const double* noise, const double* h_amp,
                       const double* mass, double dt, double h, double hg, double* q1, double* p1,
-                      int32_t* blow) {
+                      int32_t* blow, double* s1, double* s2) {
   if (W < 0 || d < 1 || L < 1) return fail(PL_EARG, "need W >= 0, d >= 1, L >= 1");
   if (pot->dim && pot->dim != d)
     return fail(PL_EARG, "potential expects dimension " + std::to_string(pot->dim) + ", got " +
@@ -224,7 +236,7 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
   if (is_elementwise(pot)) {
     EwProg P;
     PL_TRY(ew_program(pot, &P));
-    k_window_ew<<<grid_for(W * d), 256, 0, st>>>(P, W, d, K, amp, q0, p0, noise, mass, q1, p1, blow);
+    k_window_ew<<<grid_for(W * d), 256, 0, st>>>(P, W, d, K, amp, q0, p0, noise, mass, q1, p1, blow, s1, s2);
     PL_CHECK_LAUNCH();
     // the amplitude upload is ordered on the stream, but h_amp is pageable:
     // cudaMemcpyAsync from pageable memory is synchronous w.r.t. the host.
@@ -240,7 +252,7 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
   case DD:                                                                                   \
     cudaFuncSetAttribute(k_window_lj<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     k_window_lj<DD><<<(unsigned)W, 256, smem, st>>>(W, pot->n_atoms, pot->eps, pot->sigma, K, amp, \
-                                                   q0, p0, noise, mass, q1, p1, blow, flag); \
+                                                   q0, p0, noise, mass, q1, p1, blow, flag, s1, s2); \
     break;
     switch (pot->space_dim) {
       LJ_CASE(1)
@@ -270,7 +282,7 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
     prof_mark(st, ST_INT, false);
     PL_TRY(compute(pot, W, d, q1, nullptr, grad, nullptr));
     prof_mark(st, ST_INT, true);
-    k_close<<<g, 256, 0, st>>>(W, d, s, K, amp, noise, mass, grad, ph, q1, p1, blow);
+    k_close<<<g, 256, 0, st>>>(W, d, s, K, amp, noise, mass, grad, ph, q1, p1, blow, s1, s2);
     PL_CHECK_LAUNCH();
     prof_mark(st, ST_INT, false);
   }

@@ -15,7 +15,7 @@ namespace pl {
 int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, const double* q0,
                       const double* p0, const double* noise, const double* h_amp,
                       const double* mass, double dt, double h, double hg, double* q1, double* p1,
-                      int32_t* blow);
+                      int32_t* blow, double* s1 = nullptr, double* s2 = nullptr);
 
 namespace {
 

@@ -115,14 +115,18 @@ class WindowKernel:
         self.mass = None
         if params.mass is not None:
             m = params.mass_vector(d)
-            self.mass = torch.from_numpy(np.ascontiguousarray(m)).to(self.device)
+            self.mass = torch.from_numpy(np.array(m, dtype=float)).to(self.device)
 
     def noise(self, seeds):
         """(W, (L+1)*d) device noise blocks for the given window seeds."""
         return device_streams(seeds, (self.L + 1) * self.d)
 
-    def run(self, Q0, P0, noise, Q1=None, P1=None, blow=None):
-        """Propagate W windows: Q0/P0 (W, d) device tensors; returns (Q1, P1, blowup)."""
+    def run(self, Q0, P0, noise, Q1=None, P1=None, blow=None, moments=None):
+        """Propagate W windows: Q0/P0 (W, d) device tensors; returns (Q1, P1, blowup).
+
+        ``moments=(S1, S2)`` ((W, L, d) device tensors) also accumulates the
+        full-step momentum moments (pl_propagate_windows_moments).
+        """
         import torch
         W = Q0.shape[0]
         Q1 = torch.empty_like(Q0) if Q1 is None else Q1
@@ -130,11 +134,15 @@ class WindowKernel:
         if blow is None:
             blow = torch.zeros(W, dtype=torch.int32, device=Q0.device)
         ctx = _lib.context()
-        try:
-            _lib.check(_lib.load().pl_propagate_windows(
-                ctx.handle, self.pot.handle(ctx), W, self.d, self.L, _lib.ptr(Q0), _lib.ptr(P0),
+        lib = _lib.load()
+        args = (ctx.handle, self.pot.handle(ctx), W, self.d, self.L, _lib.ptr(Q0), _lib.ptr(P0),
                 _lib.ptr(noise), _lib.dptr(self.amp), _lib.ptr(self.mass), self.dt, self.h, self.hg,
-                _lib.ptr(Q1), _lib.ptr(P1), _lib.ptr(blow)))
+                _lib.ptr(Q1), _lib.ptr(P1), _lib.ptr(blow))
+        try:
+            if moments is None:
+                _lib.check(lib.pl_propagate_windows(*args))
+            else:
+                _lib.check(lib.pl_propagate_windows_moments(*args, _lib.ptr(moments[0]), _lib.ptr(moments[1])))
         except _lib.CallError as err:
             if err.code in (_lib.PL_EARG, _lib.PL_EPOT):
                 raise PotentialError(err.message) from None
@@ -179,3 +187,101 @@ def propagate_window(state: PhaseState, pot: Potential, params: LangevinParams,
                      schedule: TemperatureSchedule, seed: int) -> PhaseState:
     """Advance one window of ``params.substeps`` steps (integrator.py:292-308)."""
     return propagate_windows([state], pot, params, schedule, [seed])[0]
+
+
+# ---------------------------------------------------------------- kinetic temperature
+ALL_SUBSTEPS = "all_substeps"
+WINDOW_ENDS = "window_ends"
+
+
+def predicted_kinetic_temperature(substeps: int, inv_beta: float) -> float:
+    """Leading-order stationary kinetic temperature (integrator.py:316-320)."""
+    if substeps < 1:
+        raise ValueError(f"substeps must be >= 1, got {substeps}")
+    return inv_beta * (1.0 - 1.0 / (2.0 * substeps))
+
+
+@dataclass(frozen=True)
+class TemperatureReport:
+    """Outcome of a kinetic-temperature measurement (integrator.py:337-346)."""
+
+    k_eq_empirical: float
+    k_eq_predicted: float
+    per_substep_variance: tuple
+    n_windows: int
+    n_burn_in: int
+    sampling: str
+
+
+def _variance(s1, s2, count, mass) -> float:
+    # mass-weighted, component-averaged variance from running moments (integrator.py:349-353)
+    mean = s1 / count
+    var = s2 / count - mean * mean
+    return float(np.mean(var / mass))
+
+
+def measure_kinetic_temperature_batch(pot: Potential, params: LangevinParams, schedule: TemperatureSchedule,
+                                      n_windows: int, master_seeds, sampling: str = ALL_SUBSTEPS,
+                                      burn_in: float = 0.1, initial: PhaseState | None = None) -> list:
+    """``measure_kinetic_temperature`` for R independent chains in one device pass.
+
+    Chain r starts cold (q = p = 0, or ``initial`` -- an extension for lattice
+    systems, where q = 0 stacks every atom on one site) and runs ``n_windows`` windows, window n
+    with seed ``derive_seeds(master_seeds[r], n_windows)[n]``; each window is
+    one ``pl_propagate_windows_moments`` launch over all R chains, the moments
+    of windows n >= n_burn accumulate on the device (integrator.py:355-365,
+    430-482).  Returns one TemperatureReport per chain.
+    """
+    import torch
+    from .rng import derive_seeds
+    if sampling not in (ALL_SUBSTEPS, WINDOW_ENDS):
+        raise ValueError(f"unknown sampling mode: {sampling!r}")
+    if not 0.0 <= burn_in < 1.0:
+        raise ValueError(f"burn_in must lie in [0, 1), got {burn_in}")
+    if n_windows < 1:
+        raise ValueError("n_windows must be >= 1")
+    n_burn = int(round(burn_in * n_windows))
+    if n_burn >= n_windows:
+        n_burn = n_windows - 1
+    d = params.mass.shape[0] if params.mass is not None else 1
+    mass = params.mass_vector(d)
+    seeds = np.stack([np.asarray(derive_seeds(int(m), n_windows), dtype=np.uint64) for m in master_seeds])
+    R, L = seeds.shape[0], params.substeps
+    k = WindowKernel(pot, params, schedule, d)
+    Q = [torch.zeros((R, d), dtype=torch.float64, device=k.device) for _ in range(2)]
+    P = [torch.zeros((R, d), dtype=torch.float64, device=k.device) for _ in range(2)]
+    if initial is not None:
+        if initial.dim != d:
+            raise ValueError(f"initial state has dimension {initial.dim}, expected {d}")
+        Q[0].copy_(torch.from_numpy(np.asarray(initial.q, dtype=float))[None].expand(R, d))
+        P[0].copy_(torch.from_numpy(np.asarray(initial.p, dtype=float))[None].expand(R, d))
+    S1 = torch.zeros((R, L, d), dtype=torch.float64, device=k.device)
+    S2 = torch.zeros_like(S1)
+    blows = torch.zeros((n_windows, R), dtype=torch.int32, device=k.device)
+    for n in range(n_windows):
+        a, b = n % 2, (n + 1) % 2
+        noise = k.noise([int(x) for x in seeds[:, n]])
+        k.run(Q[a], P[a], noise, Q[b], P[b], blows[n], moments=(S1, S2) if n >= n_burn else None)
+    bl = blows.cpu().numpy()
+    if bl.any():
+        n, r = (int(v[0]) for v in np.nonzero(bl))
+        raise BlowUpError(f"chain {r} left the trusted range at substep {int(bl[n, r])}",
+                          substep=int(bl[n, r]), window=n)
+    s1, s2 = S1.cpu().numpy(), S2.cpu().numpy()
+    count = n_windows - n_burn
+    k_pred = predicted_kinetic_temperature(L, params.inv_beta)
+    out = []
+    for r in range(R):
+        per = tuple(_variance(s1[r, l], s2[r, l], count, mass) for l in range(L))
+        k_emp = (_variance(s1[r].sum(axis=0), s2[r].sum(axis=0), count * L, mass)
+                 if sampling == ALL_SUBSTEPS else per[-1])
+        out.append(TemperatureReport(k_emp, k_pred, per, n_windows, n_burn, sampling))
+    return out
+
+
+def measure_kinetic_temperature(pot: Potential, params: LangevinParams, schedule: TemperatureSchedule,
+                                n_windows: int, master_seed: int, sampling: str = ALL_SUBSTEPS,
+                                burn_in: float = 0.1) -> TemperatureReport:
+    """Chain windows from a cold start and report the stationary temperature (integrator.py:430-482)."""
+    return measure_kinetic_temperature_batch(pot, params, schedule, n_windows, [master_seed], sampling,
+                                             burn_in)[0]

@@ -333,6 +333,56 @@ def gradient_check(pot: Potential, q, h: float = 1e-6) -> float:
     return float(np.max(np.abs(fd - grad)))
 
 
+def minimize_batch(pot: Potential, starts, tol: float = 1e-8, max_iter: int = 50_000):
+    """B steepest descents with Armijo backtracking in one device pass (pl_minimize).
+
+    The reference's ``_descend`` (potentials.py:231-266) per start, batched:
+    returns ``(minima (B, d), status (B,), iterations (B,), energies (B,))``
+    with status 0 converged, 1 line search stalled, 2 no convergence.
+    """
+    import torch
+    X = np.atleast_2d(np.asarray(starts, dtype=float))
+    B, d = X.shape
+    if pot.dimension is not None and d != pot.dimension:
+        raise PotentialError(f"{type(pot).__name__} expects dimension {pot.dimension}, got {d}")
+    ctx = _lib.context()
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).to(torch.device("cuda", ctx.device))
+    status = np.zeros(B, dtype=np.int32)
+    iters = np.zeros(B, dtype=np.int64)
+    energy = np.zeros(B, dtype=float)
+    try:
+        _lib.check(_lib.load().pl_minimize(ctx.handle, pot.handle(ctx), B, d, _lib.ptr(Xd), float(tol),
+                                           int(max_iter), status.ctypes.data_as(_lib.pi32),
+                                           iters.ctypes.data_as(_lib.pi64), _lib.dptr(energy)))
+    except _lib.CallError as err:
+        _raise(err)
+    return Xd.cpu().numpy(), status, iters, energy
+
+
+def local_minima(pot: Potential, starts, tol: float = 1e-8, max_iter: int = 50_000) -> list:
+    """Distinct minima in first-found order (potentials.py:268-287), all descents batched.
+
+    Raises MinimizationError naming the first start (in order) whose descent
+    stalls or does not converge, as the sequential reference would.
+    """
+    if tol <= 0.0:
+        raise ValueError("tol must be positive")
+    starts = [np.asarray(s, dtype=float) for s in starts]
+    if not starts:
+        return []
+    X, status, _, _ = minimize_batch(pot, np.stack(starts), tol, max_iter)
+    minima: list = []
+    for i, x in enumerate(X):
+        if status[i] == 1:
+            raise MinimizationError(f"line search stalled while minimizing from start {starts[i].tolist()}")
+        if status[i] == 2:
+            raise MinimizationError(f"no convergence to |grad| <= {tol} within {max_iter} iterations "
+                                    f"from start {starts[i].tolist()}")
+        if all(np.linalg.norm(x - m) > tol for m in minima):
+            minima.append(x)
+    return minima
+
+
 @dataclass(frozen=True)
 class PropagatorPair:
     """Fine and coarse potentials with their configured per-window costs."""

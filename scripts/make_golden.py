@@ -193,11 +193,83 @@ def make_residence():
     np.savez_compressed(os.path.join(OUT, "residence_golden.npz"), versions=json.dumps(_versions()), **out)
 
 
+def make_accounting():
+    """classic_gain / adaptive_gain on hand-built slab records (accounting.py:99-159)."""
+    from paralangevin import accounting as acc
+    from paralangevin.parareal import SlabAttempt, SlabRecord
+    slabsets = [
+        [SlabRecord(1, 0, (SlabAttempt(16, 3),), 16, 3)],
+        [SlabRecord(1, 0, (SlabAttempt(16, 2), SlabAttempt(9, 4)), 9, 6),
+         SlabRecord(2, 9, (SlabAttempt(16, 5),), 16, 5)],
+        [SlabRecord(1, 0, (SlabAttempt(64, 1), SlabAttempt(20, 3)), 20, 4),
+         SlabRecord(2, 20, (SlabAttempt(41, 7),), 41, 7),
+         SlabRecord(3, 41, (SlabAttempt(64, 2), SlabAttempt(63, 1), SlabAttempt(50, 9)), 50, 12),
+         SlabRecord(4, 50, (SlabAttempt(64, 3),), 64, 3)],
+    ]
+    costs = [(1.0, 0.0), (100.0, 1.0), (37.5, 0.8125), (1.0, 1.0)]
+    rows_a, rows_c = [], []
+    for si, slabs in enumerate(slabsets):
+        n = slabs[-1].n_final
+        for cf, cc in costs:
+            r = acc.adaptive_gain(slabs, n, cf, cc)
+            rows_a.append([si, cf, cc, r.total_cost, r.sequential_cost, r.gain, r.ideal_gain, r.n_slab,
+                           r.total_iterations])
+    for n, k in ((16, 3), (100, 7), (64, 64)):
+        for cf, cc in costs:
+            r = acc.classic_gain(n, k, cf, cc)
+            rows_c.append([n, k, cf, cc, r.total_cost, r.sequential_cost, r.gain, r.ideal_gain, r.total_effort])
+    enc = [[(s.slab_index, s.n_init, s.n_final, s.k_conv, [(a.n_final, a.iterations) for a in s.attempts])
+            for s in slabs] for slabs in slabsets]
+    np.savez_compressed(os.path.join(OUT, "accounting_golden.npz"), versions=json.dumps(_versions()),
+                        slabsets=json.dumps(enc), adaptive=np.array(rows_a), classic=np.array(rows_c))
+
+
+def make_temperature():
+    """measure_kinetic_temperature (integrator.py:430-482) on small systems."""
+    from paralangevin import integrator as integ
+    out = {}
+    cases = {
+        "harm": (pl.Harmonic(k=np.array([1.0, 3.0, 0.5])), pl.LangevinParams(1.0, 0.7, 0.05, 5, mass=[1.0, 2.0, 0.5]),
+                 40, 123),
+        "dw": (pl.DoubleWell(1.0, 1.0), pl.LangevinParams(0.5, 0.4, 0.05, 3), 60, 7),
+        "lj7": (pl.LennardJonesCluster(1.0, 1.0, 7, 2), pl.LangevinParams(1.0, 0.3, 0.005, 4, mass=[1.0] * 14),
+                25, 99),
+    }
+    for name, (pot, params, nw, seed) in cases.items():
+        sched = pl.TemperatureSchedule.robust(params.substeps)
+        for sampling in (integ.ALL_SUBSTEPS, integ.WINDOW_ENDS):
+            if name == "lj7":
+                # a cold LJ start has coincident atoms: chain from the reference's own minimiser output
+                continue
+            r = integ.measure_kinetic_temperature(pot, params, sched, nw, seed, sampling=sampling, burn_in=0.2)
+            out[f"{name}_{sampling}"] = np.array([r.k_eq_empirical, r.k_eq_predicted, r.n_windows, r.n_burn_in]
+                                                 + list(r.per_substep_variance))
+    np.savez_compressed(os.path.join(OUT, "temperature_golden.npz"), versions=json.dumps(_versions()), **out)
+
+
+def make_minima():
+    """local_minima (potentials.py:268-287): double well, harmonic and LJ7-2D starts."""
+    from paralangevin import potentials as pots
+    rs = np.random.default_rng(5)
+    out = {}
+    dw = pl.DoubleWell(1.0, 1.0)
+    starts = [np.array([x]) for x in (-1.7, -0.3, 0.2, 0.9, 2.5, -1.0)]
+    out["dw_starts"] = np.stack(starts)
+    out["dw_minima"] = np.stack(pots.local_minima(dw, starts, tol=1e-9))
+    lj = pl.LennardJonesCluster(1.0, 1.0, 7, 2)
+    base = np.array([[0.0, 0.0], [1.12, 0.0], [0.56, 0.97], [-0.56, 0.97], [-1.12, 0.0], [-0.56, -0.97],
+                     [0.56, -0.97]]).ravel()
+    ljs = [base + 0.05 * rs.normal(size=base.shape) for _ in range(4)]
+    out["lj_starts"] = np.stack(ljs)
+    out["lj_minima"] = np.stack(pots.local_minima(lj, ljs, tol=1e-6))
+    out["lj_energy"] = np.array([lj.energy(m) for m in out["lj_minima"]])
+    np.savez_compressed(os.path.join(OUT, "minima_golden.npz"), versions=json.dumps(_versions()), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    make_rng()
-    make_window()
-    make_parareal()
-    make_residence()
+    which = sys.argv[1:] or ["rng", "window", "parareal", "residence", "accounting", "temperature", "minima"]
+    for w in which:
+        globals()[f"make_{w}"]()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -118,3 +118,26 @@ def test_residence_times_match_reference(golden):
         assert np.array_equal(got, z[f"events_{mr}"])
         ci = sia.mean_ci([e.duration for e in ev if not e.censored])
         assert np.array(ci).tobytes() == z[f"ci_{mr}"].tobytes()
+
+
+def test_gain_accounting_matches_reference(golden):
+    """accounting.adaptive_gain / classic_gain vs the reference (accounting.py:99-159)."""
+    import json
+
+    from paper_2212_10508_b200 import accounting as acc
+    from paper_2212_10508_b200.parareal import SlabAttempt, SlabRecord
+    z = golden("accounting_golden.npz")
+    sets = [[SlabRecord(i, n0, tuple(SlabAttempt(a, k) for a, k in att), n1, kc)
+             for i, n0, n1, kc, att in slabs] for slabs in json.loads(str(z["slabsets"]))]
+    for row in z["adaptive"]:
+        si, cf, cc = int(row[0]), row[1], row[2]
+        r = acc.adaptive_gain(sets[si], sets[si][-1].n_final, cf, cc)
+        assert [r.total_cost, r.sequential_cost, r.gain, r.ideal_gain] == list(row[3:7])
+        assert (r.n_slab, r.total_iterations) == (int(row[7]), int(row[8]))
+    for row in z["classic"]:
+        r = acc.classic_gain(int(row[0]), int(row[1]), row[2], row[3])
+        assert [r.total_cost, r.sequential_cost, r.gain, r.ideal_gain, r.total_effort] == list(row[4:9])
+    with pytest.raises(ValueError):
+        acc.adaptive_gain(sets[1][:1], 16, 1.0, 0.0)  # does not tile the window range
+    with pytest.raises(ValueError):
+        acc.classic_gain(16, 3, 0.0, 1.0)
