@@ -220,7 +220,7 @@ def run_ours(args, rank, world, local_rank):
     roof = {"bound": "fp64", "kernel": f"k_{dom}", "achieved": round(achieved, 3),
             "peak": round(peak, 3), "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
             "peak_source": "measured DFMA (pl_fp64_peak) on this B200; FP64 absent from MEASURED_PEAKS.json",
-            "traffic": None,
+            "traffic": ncu_traffic(f"k_{dom}"),
             "flops_per_launch": fl[{"snap_ui": "ui", "snap_yi": "yi", "snap_deidrj": "deidrj"}[dom]],
             "snap_all_kernels_tflops": round(snap_flops_total / (snap_ms * 1e-3) / 1e12, 3),
             "stage_share": {k_: round(v, 4) for k_, v in share.items()},
@@ -362,6 +362,17 @@ def run_reference(args, rank, world):
                                        "(reference path restated in oracle/: BBK integrator + C SNAP)"},
             "e2e": {"value": v, "unit": "atom-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
+    ncu --set full capture of this config (profiles/r1_traffic.json), else None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")) as f:
+            t = json.load(f)
+        return t["kernels"].get(kernel)
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 # ---------------------------------------------------------------- parareal wall-clock (PR1)

@@ -9,7 +9,7 @@ import sys
 from collections import defaultdict
 
 METRICS = [
-    ("gpu__time_duration.sum", "duration (ns)"),
+    ("gpu__time_duration.sum", "duration"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
@@ -47,13 +47,14 @@ def launches(path):
 def full(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
         d = {"kernel": r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")}
         for m, name in METRICS:
             if m in hdr:
-                d[name] = r[hdr.index(m)]
+                u = units[hdr.index(m)]
+                d[name] = r[hdr.index(m)] + (f" {u}" if u else "")
         res.append(d)
     return res
 
