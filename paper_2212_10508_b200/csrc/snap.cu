@@ -145,10 +145,10 @@ __constant__ int c_yi6_gseg[YI6_WARPS + 1];
 __constant__ int c_yi6_groups[32];
 // box-form Z/Y kernel (snap_yi8.cu, own constant bank)
 cudaError_t snap_box_setup(const double* box, int nbox, const int* off, const int* code, const int* iseg,
-                           const int* items, int nitems);
-int snap_box_variants(int* nw);
+                           const int* items, int nitems, const int* rowsplit);
+int snap_box_variants(int* nw, int* ns);
 cudaError_t snap_box_launch(int nw, cudaStream_t st, int64_t natoms, double beta0, const double* coef,
-                            const void* utot, void* ylist, double* eatom);
+                            const void* utot, void* ylist, double* eatom, double* erow_g);
 
 // ------------------------------------------------------------------ host setup
 static double fact(int n) {
@@ -318,17 +318,27 @@ int snap_prepare(pl_pot* pot, const double* beta) {
           rows.push_back({c, (J << 8) | mb});
         }
       std::sort(rows.begin(), rows.end(), [](auto& a, auto& b) { return a.first > b.first; });
-      // rows -> warps (LPT), then each warp's (row, triple) items in ascending X
-      auto itemize = [&](int NW, std::vector<int>& iseg, std::vector<int>& items) {
+      // rows -> NW*S virtual warps (LPT; virtual warp w runs on CTA w / NW of the
+      // block), then each warp's (row, triple) items in ascending X
+      auto row_index = [](int J, int mb) {
+        int r = 0;
+        for (int j = 0; j < J; ++j) r += j / 2 + 1;
+        return r + mb;
+      };
+      auto itemize = [&](int NW, int NS, std::vector<int>& iseg, std::vector<int>& items,
+                         std::vector<int>& rowsplit) {
         std::vector<int> g, sg;
-        lpt(NW, g, sg);
-        iseg.assign(NW + 1, 0);
+        const int NV = NW * NS;
+        lpt(NV, g, sg);
+        iseg.assign(26, 0);
+        rowsplit.assign(25, 0);
         items.clear();
-        for (int w = 0; w < NW; ++w) {
+        for (int w = 0; w < NV; ++w) {
           iseg[w] = (int)items.size();
           std::vector<std::pair<int, int>> mine;  // (sort key, item)
           for (int gi = sg[w]; gi < sg[w + 1]; ++gi) {
             const int J = g[gi] >> 8, mb = g[gi] & 0xff;
+            rowsplit[row_index(J, mb)] = w / NW;
             for (int tid : byJ[J]) {
               const int x = code[tid] / 100, y = (code[tid] / 10) % 10;
               mine.push_back({x * 10000 + y * 100 + J * 10 + mb, (tid << 16) | (J << 8) | mb});
@@ -337,15 +347,16 @@ int snap_prepare(pl_pot* pot, const double* beta) {
           std::sort(mine.begin(), mine.end());
           for (auto& m : mine) items.push_back(m.second);
         }
-        iseg[NW] = (int)items.size();
+        for (int w = NV; w < 26; ++w) iseg[w] = (int)items.size();
       };
-      int box_nw[8];
-      const int box_nv = snap_box_variants(box_nw);
-      std::vector<int> iseg_all(box_nv * 17, 0), items_all;
+      int box_nw[8], box_ns[8];
+      const int box_nv = snap_box_variants(box_nw, box_ns);
+      std::vector<int> iseg_all(box_nv * 26, 0), items_all, rowsplit_all(box_nv * 25, 0);
       for (int v = 0; v < box_nv; ++v) {
-        std::vector<int> is, it;
-        itemize(box_nw[v], is, it);
-        std::copy(is.begin(), is.end(), iseg_all.begin() + v * 17);
+        std::vector<int> is, it, rs;
+        itemize(box_nw[v], box_ns[v], is, it, rs);
+        std::copy(is.begin(), is.end(), iseg_all.begin() + v * 26);
+        std::copy(rs.begin(), rs.end(), rowsplit_all.begin() + v * 25);
         items_all.insert(items_all.end(), it.begin(), it.end());
       }
       const int n_items = (int)items_all.size() / box_nv;
@@ -365,7 +376,7 @@ int snap_prepare(pl_pot* pot, const double* beta) {
         }
         if ((int)code.size() != yi5::NT) return fail(PL_EARG, "SNAP box tables: unexpected triple count");
         PL_CUDA(snap_box_setup(box.data(), (int)box.size(), boff.data(), code.data(), iseg_all.data(),
-                               items_all.data(), n_items));
+                               items_all.data(), n_items, rowsplit_all.data()));
         box_done = true;
       }
     }
@@ -2141,13 +2152,15 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   int64_t na = B * N;
   if (na > 0x7fffffff) return fail(PL_EARG, "too many atoms in one batch");
   PL_TRY(build_neighbours(pot, B, q, pot->rcut, SNAP_MAXN, &nl));
-  size_t bytes = sizeof(C2) * 2 * na * S->nhalf + sizeof(double) * na * (1 + 3 * SNAP_MAXN + 6);
+  // + 25 x na doubles: per-row energies of the split Y kernel (small batches)
+  size_t bytes = sizeof(C2) * 2 * na * S->nhalf + sizeof(double) * na * (1 + 3 * SNAP_MAXN + 6 + 25);
   PL_TRY(pot->work[2].reserve(bytes));
   buf.utot = (C2*)pot->work[2].ptr;
   buf.y = buf.utot + na * S->nhalf;
   buf.eatom = (double*)(buf.y + na * S->nhalf);
   buf.dedr = buf.eatom + na;
   buf.vatom = buf.dedr + na * 3 * SNAP_MAXN;
+  double* erow = buf.vatom + na * 6;
   Box box = make_box(pot->box);
   size_t s1 = ui_smem(D), s2 = yi_smem(D), s3 = de_smem(D);
   static thread_local bool attr_done = false;
@@ -2196,7 +2209,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     return e ? atoi(e) : 12;
   }();
   if (S->yi_reg && yi_var == 8) {
-    PL_CUDA(snap_box_launch(box_nw, ctx->stream, na, D.beta0, D.yi5, buf.utot, buf.y, buf.eatom));
+    PL_CUDA(snap_box_launch(box_nw, ctx->stream, na, D.beta0, D.yi5, buf.utot, buf.y, buf.eatom, erow));
   } else if (S->yi_reg && yi_var == 7) {
     size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI6_WARPS * 9 * YI_ATOMS +
                 sizeof(double) * YI6_WARPS * YI_ATOMS;

@@ -29,6 +29,7 @@ constexpr int NHALF = 155;     // sum (J+1)(J/2+1)
 constexpr int ATOMS = 32;
 constexpr int BOX_MAX = 4098;  // sum over triples of (X+1)(Y+1)
 constexpr int foff(int J) { return J * (J + 1) * (2 * J + 1) / 6; }
+constexpr int rowoff(int J) { return (J / 2 + 1) * (J / 2 + 1) - (J % 2 == 0 ? J / 2 + 1 : 0); }  // rows of layers < J
 constexpr int hoff(int J) {
   int h = 0;
   for (int j = 0; j < J; ++j) h += (j + 1) * (j / 2 + 1);
@@ -40,13 +41,17 @@ __constant__ double c_box[yib::BOX_MAX];  // per triple: [Y+1][X+1]
 __constant__ int c_box_off[yib::NT];
 __constant__ int c_box_code[yib::NT];         // X*100 + Y*10 + J
 constexpr int BOX_MAX_ITEMS = 400;            // (row, triple) pairs: 375 at twojmax 8
-// warps per CTA of the compiled variants (the host builds one schedule each)
-// (3 warps per SM sub-partition leave 168 registers per thread; 4 would force 128
-// and spill the X = 8 instantiation)
-constexpr int BOX_NV = 2;
-constexpr int BOX_NW[BOX_NV] = {12, 8};
-__constant__ int c_box_iseg[BOX_NV][17];                 // items of warp w: [iseg[w], iseg[w+1])
+// compiled variants: (warps per CTA, CTAs per 32-atom block).  A block's
+// (J, mb) rows are split over S CTAs when the batch has fewer blocks than SMs
+// (latency of small systems); each row stays with one warp.  (3 warps per SM
+// sub-partition leave 168 registers per thread; 4 would force 128 and spill.)
+constexpr int BOX_NV = 3;
+constexpr int BOX_NW[BOX_NV] = {12, 8, 12};
+constexpr int BOX_NS[BOX_NV] = {1, 1, 2};
+constexpr int BOX_ROWS = 25;                              // (J, mb <= J/2) half rows at twojmax 8
+__constant__ int c_box_iseg[BOX_NV][BOX_ROWS + 1];        // items of virtual warp w: [iseg[w], iseg[w+1])
 __constant__ int c_box_items[BOX_NV][BOX_MAX_ITEMS];     // tid << 16 | J << 8 | mb
+__constant__ int c_box_rowsplit[BOX_NV][BOX_ROWS];       // CTA of the block that owns row r
 
 struct Cx {
   double re, im;
@@ -113,16 +118,18 @@ __device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int J, i
 
 constexpr int box_regs(int nw) { return nw <= 8 ? 255 : 168; }
 
-template <int NW, int V>
+template <int NW, int V, int S>
 __global__ void __maxnreg__(box_regs(NW))
 k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, const Cx* __restrict__ utot,
-              Cx* __restrict__ ylist, double* __restrict__ eatom) {
+              Cx* __restrict__ ylist, double* __restrict__ eatom, double* __restrict__ erow_g) {
   extern __shared__ double smem[];
   Cx* Uf = reinterpret_cast<Cx*>(smem);                 // [NFULL][32] full U matrices
   Cx* Ys = Uf + yib::NFULL * yib::ATOMS;               // [NHALF][32] Y half rows
-  double* epart = reinterpret_cast<double*>(Ys + yib::NHALF * yib::ATOMS);  // [NW][32]
+  double* erow = reinterpret_cast<double*>(Ys + yib::NHALF * yib::ATOMS);  // [ROWS][32] energy per row
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t a0 = (int64_t)blockIdx.x * yib::ATOMS;
+  const int64_t blk = blockIdx.x / S;
+  const int split = (int)(blockIdx.x - blk * S);
+  const int64_t a0 = blk * yib::ATOMS;
   const int na_blk = (int)min((int64_t)yib::ATOMS, natoms - a0);
   for (int t = threadIdx.x; t < yib::NFULL * yib::ATOMS; t += blockDim.x) {
     const int at = t & (yib::ATOMS - 1), f = t >> 5;
@@ -142,15 +149,14 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
     Uf[f * yib::ATOMS + at] = v;
   }
   for (int t = threadIdx.x; t < yib::NHALF * yib::ATOMS; t += blockDim.x) Ys[t] = Cx{0.0, 0.0};
+  for (int t = threadIdx.x; t < BOX_ROWS * yib::ATOMS; t += blockDim.x) erow[t] = 0.0;
   __syncthreads();
   const Cx* Ul = Uf + lane;
-  const int* iseg = c_box_iseg[V];
-  const int* items = c_box_items[V];
-  double esum = 0.0;
+  const int vw = split * NW + warp;  // virtual warp of the block's schedule
   // the warp's (row, triple) items in ascending X: all warps sweep the X
   // instantiations in the same order, so the live code stays small
-  for (int it = iseg[warp]; it < iseg[warp + 1]; ++it) {
-    const int item = items[it];
+  for (int it = c_box_iseg[V][vw]; it < c_box_iseg[V][vw + 1]; ++it) {
+    const int item = c_box_items[V][it];
     const int tid = item >> 16, J = (item >> 8) & 0xff, mb = item & 0xff;
     const int code = c_box_code[tid];
     const int X = code / 100, Y = (code / 10) % 10;
@@ -160,6 +166,7 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
     const double cy = coef[tid], be = coef[yib::NT + tid];
     Cx* yrow = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + lane;
     const Cx* urow = Ul + (yib::foff(J) + mb * (J + 1)) * yib::ATOMS;
+    double esum = 0.0;
     switch (X) {
       case 0: box_x<0>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
       case 1: box_x<1>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
@@ -171,30 +178,57 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
       case 7: box_x<7>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
       default: box_x<8>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
     }
+    // energy per row, items of a row in one fixed order whatever the schedule
+    erow[(yib::rowoff(J) + mb) * yib::ATOMS + lane] += esum;
   }
-  epart[warp * yib::ATOMS + lane] = esum;
   __syncthreads();
+  // rows owned by this CTA -> global (all rows when S = 1)
   for (int t = threadIdx.x; t < na_blk * yib::NHALF; t += blockDim.x) {
     const int at = t / yib::NHALF, h = t - at * yib::NHALF;
+    if (S > 1) {
+      int J = 0;
+      while (J < yib::TJ && h >= yib::hoff(J + 1)) ++J;
+      const int r = yib::rowoff(J) + (h - yib::hoff(J)) / (J + 1);
+      if (c_box_rowsplit[V][r] != split) continue;
+    }
     ylist[(a0 + at) * yib::NHALF + h] = Ys[h * yib::ATOMS + at];
   }
-  if (warp == 0 && lane < na_blk) {
-    double e = beta0;
-    for (int w = 0; w < NW; ++w) e += epart[w * yib::ATOMS + lane];
-    eatom[a0 + lane] = e;
+  if (S == 1) {
+    if (warp == 0 && lane < na_blk) {
+      double e = beta0;
+      for (int r = 0; r < BOX_ROWS; ++r) e += erow[r * yib::ATOMS + lane];
+      eatom[a0 + lane] = e;
+    }
+  } else {
+    for (int t = threadIdx.x; t < BOX_ROWS * na_blk; t += blockDim.x) {
+      const int r = t / na_blk, at = t - r * na_blk;
+      if (c_box_rowsplit[V][r] == split) erow_g[(int64_t)r * natoms + a0 + at] = erow[r * yib::ATOMS + at];
+    }
   }
 }
 
-// Upload the box table and the per-warp item lists (process-wide; twojmax 8 only).
-// iseg: [BOX_NV][17], items: [BOX_NV][nitems]
+// split mode: E_i = beta0 + sum over rows in row order (the S = 1 arithmetic)
+__global__ void k_box_energy(int64_t natoms, double beta0, const double* __restrict__ erow_g,
+                             double* __restrict__ eatom) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < natoms; a += (int64_t)gridDim.x * blockDim.x) {
+    double e = beta0;
+    for (int r = 0; r < BOX_ROWS; ++r) e += erow_g[(int64_t)r * natoms + a];
+    eatom[a] = e;
+  }
+}
+
+// Upload the box table, the per-virtual-warp item lists and the row owners
+// (process-wide; twojmax 8 only).  iseg: [BOX_NV][ROWS+1], items: [BOX_NV][nitems],
+// rowsplit: [BOX_NV][ROWS].
 cudaError_t snap_box_setup(const double* box, int nbox, const int* off, const int* code, const int* iseg,
-                           const int* items, int nitems) {
+                           const int* items, int nitems, const int* rowsplit) {
   if (nbox > yib::BOX_MAX || nitems > BOX_MAX_ITEMS) return cudaErrorInvalidValue;
   cudaError_t e;
   if ((e = cudaMemcpyToSymbol(c_box, box, sizeof(double) * nbox)) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_box_off, off, sizeof(int) * yib::NT)) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_box_code, code, sizeof(int) * yib::NT)) != cudaSuccess) return e;
-  if ((e = cudaMemcpyToSymbol(c_box_iseg, iseg, sizeof(int) * BOX_NV * 17)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_box_iseg, iseg, sizeof(int) * BOX_NV * (BOX_ROWS + 1))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_box_rowsplit, rowsplit, sizeof(int) * BOX_NV * BOX_ROWS)) != cudaSuccess) return e;
   for (int v = 0; v < BOX_NV; ++v)
     if ((e = cudaMemcpyToSymbol(c_box_items, items + (size_t)v * nitems, sizeof(int) * nitems,
                                 sizeof(int) * BOX_MAX_ITEMS * v)) != cudaSuccess)
@@ -202,30 +236,39 @@ cudaError_t snap_box_setup(const double* box, int nbox, const int* off, const in
   return cudaSuccess;
 }
 
-int snap_box_variants(int* nw) {
-  for (int v = 0; v < BOX_NV; ++v) nw[v] = BOX_NW[v];
+// (warps, splits) of every variant; returns the count
+int snap_box_variants(int* nw, int* ns) {
+  for (int v = 0; v < BOX_NV; ++v) {
+    nw[v] = BOX_NW[v];
+    ns[v] = BOX_NS[v];
+  }
   return BOX_NV;
 }
 
-template <int NW, int V>
-static cudaError_t box_launch(cudaStream_t st, unsigned grid, int64_t natoms, double beta0, const double* coef,
-                              const void* utot, void* ylist, double* eatom) {
+template <int NW, int V, int S>
+static cudaError_t box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const void* utot,
+                              void* ylist, double* eatom, double* erow_g) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_snap_yi_box<NW, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_snap_yi_box<NW, V, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * NW * yib::ATOMS;
-  k_snap_yi_box<NW, V><<<grid, NW * 32, sm, st>>>(natoms, beta0, coef, (const Cx*)utot, (Cx*)ylist, eatom);
+  const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * BOX_ROWS * yib::ATOMS;
+  const unsigned grid = (unsigned)(S * ((natoms + yib::ATOMS - 1) / yib::ATOMS));
+  k_snap_yi_box<NW, V, S><<<grid, NW * 32, sm, st>>>(natoms, beta0, coef, (const Cx*)utot, (Cx*)ylist, eatom,
+                                                     erow_g);
+  if (S > 1) k_box_energy<<<(unsigned)((natoms + 255) / 256), 256, 0, st>>>(natoms, beta0, erow_g, eatom);
   return cudaGetLastError();
 }
 
-// nw: warps per CTA (one of BOX_NW)
+// nw: warps per CTA (12 or 8); split rows over 2 CTAs per block when the
+// batch has fewer blocks than SMs (erow_g: 25 x natoms doubles of scratch)
 cudaError_t snap_box_launch(int nw, cudaStream_t st, int64_t natoms, double beta0, const double* coef,
-                            const void* utot, void* ylist, double* eatom) {
-  const unsigned grid = (unsigned)((natoms + yib::ATOMS - 1) / yib::ATOMS);
-  if (nw == 8) return box_launch<8, 1>(st, grid, natoms, beta0, coef, utot, ylist, eatom);
-  return box_launch<12, 0>(st, grid, natoms, beta0, coef, utot, ylist, eatom);
+                            const void* utot, void* ylist, double* eatom, double* erow_g) {
+  const int64_t blocks = (natoms + yib::ATOMS - 1) / yib::ATOMS;
+  if (nw == 8) return box_launch<8, 1, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
+  if (blocks < 148 && erow_g) return box_launch<12, 2, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
+  return box_launch<12, 0, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
 }
 
 }  // namespace pl
