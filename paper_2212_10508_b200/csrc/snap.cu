@@ -1863,7 +1863,16 @@ k_snap_deidrj_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
 // operations than propagating the three dU/dr_k.
 constexpr int ADJ_WARPS = 2;
 
-template <int TJ>
+// RC (recompute): only the even layers' rows are stored; the odd layer J-1
+// needed by the backward step at even J is rebuilt from the stored layer J-2
+// with the same row_step (bitwise the forward value).  25 instead of 45 slots
+// per lane: 12.8 KB instead of 23 KB of history per warp, 1.5x the warps per SM.
+template <int J, bool RC>
+__device__ __forceinline__ constexpr int adj_slot() {
+  return RC ? (J / 2) * (J / 2) : J * (J + 1) / 2;
+}
+
+template <int TJ, bool RC>
 struct AdjLayers {
   // forward: layer J from J-1 (in place), store the row, accumulate F
   template <int J>
@@ -1879,7 +1888,7 @@ struct AdjLayers {
       const C2* yr = Y + c_hoff[J] + mb * (J + 1);
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
-        hist[(J * (J + 1) / 2 + ma) * 32 + lane] = u[ma];
+        if (!RC || J % 2 == 0) hist[(adj_slot<J, RC>() + ma) * 32 + lane] = u[ma];
         const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
         F += w * (u[ma].re * yr[ma].re + u[ma].im * yr[ma].im);
       }
@@ -1894,18 +1903,34 @@ struct AdjLayers {
     if constexpr (J > 0) {
       const bool active = 2 * mb <= J;
       const bool born = (J % 2 == 0) && (2 * mb == J);  // row mb of layer J-1 is virtual
-      if (active) {
-        // U^{J-1} row mb (stored, or the symmetric image of row mb-1 of the lane below)
-        C2 up[TJ + 1];
+      // U^{J-1} row mb (stored, rebuilt, or the symmetric image of row mb-1 of the lane below)
+      C2 up[TJ + 1];
+      if (!RC || (J - 1) % 2 == 0) {
+        if (active) {
 #pragma unroll
-        for (int x = 0; x < J; ++x) {
-          if (!born) {
-            up[x] = hist[((J - 1) * J / 2 + x) * 32 + lane];
-          } else {
-            const C2 v = hist[((J - 1) * J / 2 + (J - 1 - x)) * 32 + lane - 1];
-            up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+          for (int x = 0; x < J; ++x) {
+            if (!born) {
+              up[x] = hist[(adj_slot<J - 1, RC>() + x) * 32 + lane];
+            } else {
+              const C2 v = hist[(adj_slot<J - 1, RC>() + (J - 1 - x)) * 32 + lane - 1];
+              up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+            }
           }
         }
+      } else if constexpr (J >= 2) {
+        // J even: rebuild odd layer J-1 from stored layer J-2 (every lane: the born
+        // lane takes row mb-1 from the lane below by shuffle)
+#pragma unroll
+        for (int x = 0; x <= J - 2; ++x) up[x] = hist[(adj_slot<J - 2, RC>() + x) * 32 + lane];
+        C2 dnone[TJ + 1];
+        row_step<TJ, J - 1, false>(up, dnone, g, mb, rp);
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          const C2 v = shfl_up_c2(up[J - 1 - x], 1);
+          if (born) up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+        }
+      }
+      if (active) {
 #pragma unroll
         for (int ma = 0; ma <= J; ++ma) {
           if (ma < J) {
@@ -1964,13 +1989,13 @@ struct AdjLayers {
   }
 };
 
-template <int TJ>
-__global__ void __launch_bounds__(ADJ_WARPS * 32)
+template <int TJ, bool RC>
+__global__ void __launch_bounds__(ADJ_WARPS * 32, RC ? 6 : 1)
 k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
                   const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
                   const C2* __restrict__ ylist, double* __restrict__ dedr) {
   constexpr int R = TJ / 2 + 1, P = 32 / R;
-  constexpr int NSLOT = (TJ + 1) * (TJ + 2) / 2;
+  constexpr int NSLOT = RC ? (TJ / 2 + 1) * (TJ / 2 + 1) : (TJ + 1) * (TJ + 2) / 2;
   extern __shared__ double smem[];
   double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
   const int nh = D.nhalf;
@@ -2010,7 +2035,7 @@ k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __res
     for (int e = 0; e <= TJ; ++e) u[e] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
     double F = 0.0;
-    AdjLayers<TJ>::template fwd<TJ>(u, g, mb, rp, Y, hist, lane, F);
+    AdjLayers<TJ, RC>::template fwd<TJ>(u, g, mb, rp, Y, hist, lane, F);
     __syncwarp();
     // adjoint of the top layer: its direct term
     C2 G[TJ + 1];
@@ -2025,7 +2050,7 @@ k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __res
       }
     }
     C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
-    AdjLayers<TJ>::template bwd<TJ>(G, g, mb, rp, Y, hist, lane, Sa, Sb);
+    AdjLayers<TJ, RC>::template bwd<TJ>(G, g, mb, rp, Y, hist, lane, Sa, Sb);
     __syncwarp();
     // fixed-order sums over the R row lanes of the pair
 #pragma unroll
@@ -2176,7 +2201,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_yi_six, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
     cudaFuncSetAttribute(k_snap_yi_seven, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_adj<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_adj<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_adj<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
   // register-resident kernels are instantiated for twojmax = 8 (PL_SNAP_RR=0 selects the
@@ -2243,9 +2269,17 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     const char* e = getenv("PL_SNAP_ADJ");
     return !(e && e[0] == '0');
   }();
-  if (rr && adj_env) {
+  static const bool adj_rc = [] {
+    const char* e = getenv("PL_SNAP_ADJ");
+    return e && e[0] == '3';  // 3: store even layers only, rebuild odd ones (bitwise equal, measured slower)
+  }();
+  if (rr && adj_env && adj_rc) {
+    size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + 25 * 32);
+    k_snap_deidrj_adj<8, true><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
+        D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
+  } else if (rr && adj_env) {
     size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + 45 * 32);
-    k_snap_deidrj_adj<8><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
+    k_snap_deidrj_adj<8, false><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
         D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
   } else if (rr) {
     size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * D.nhalf;
