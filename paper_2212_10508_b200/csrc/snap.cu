@@ -1726,10 +1726,13 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
   const int nh = D.nhalf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  C2* part = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * P * nh;
+  // pair-slot stride nh + 2 (= 5 mod 8 complex at twojmax 8): the 8 lanes of a
+  // 128-bit shared-memory phase hit distinct bank groups in the top layer
+  const int ps = nh + 2;
+  C2* part = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * P * ps;
   stage_rootpq(rp);
   const int64_t atom = (int64_t)blockIdx.x * RR_WARPS + warp;
-  for (int t = lane; t < P * nh; t += 32) part[t] = C2{0.0, 0.0};
+  for (int t = lane; t < P * ps; t += 32) part[t] = C2{0.0, 0.0};
   __syncthreads();
   if (atom >= natoms) return;
   const int64_t b = atom / N;
@@ -1760,7 +1763,7 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
 #pragma unroll
     for (int k = 0; k <= TJ; ++k) u[k] = du[k] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
-    C2* mypart = part + p * nh;
+    C2* mypart = part + p * ps;
     if (valid && mb == 0) mypart[0].re += fc;  // J = 0
     // every lane runs the recursion (shuffles need the full warp); only valid
     // lanes accumulate, each into its own pair slot
@@ -1773,8 +1776,8 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
     C2 acc{0.0, 0.0};
 #pragma unroll
     for (int pp = 0; pp < P; ++pp) {
-      acc.re += part[pp * nh + t].re;
-      acc.im += part[pp * nh + t].im;
+      acc.re += part[pp * ps + t].re;
+      acc.im += part[pp * ps + t].im;
     }
     int J = 0;
     while (J < TJ && t >= c_hoff[J + 1]) ++J;
@@ -2216,7 +2219,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   const unsigned rr_grid = (unsigned)((na + RR_WARPS - 1) / RR_WARPS);
   prof_mark(ctx->stream, ST_UI, true);
   if (rr) {
-    size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * (32 / 5) * D.nhalf;
+    size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * (32 / 5) * (D.nhalf + 2);
     k_snap_ui_rr<8><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
                                                                  buf.utot);
   } else {
