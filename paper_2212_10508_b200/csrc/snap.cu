@@ -284,14 +284,62 @@ int snap_prepare(pl_pot* pot, const double* beta) {
         rows.push_back({c, (J << 8) | mb});
       }
     std::sort(rows.begin(), rows.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    // rows -> NW warps: LPT, then deterministic local search (single moves and
+    // pairwise swaps) that lowers the makespan, ties broken by the sum of
+    // squared loads.  For 25 rows on 12 warps LPT reaches ~83 % balance, the
+    // search ~96 % (cost model).
     auto lpt = [&](int NW, std::vector<int>& groups, std::vector<int>& gseg) {
-      std::vector<std::vector<int>> wr(NW);
+      const int nr = (int)rows.size();
+      std::vector<int> asg(nr);
       std::vector<double> wl(NW, 0.0);
-      for (auto& r : rows) {
+      for (int i = 0; i < nr; ++i) {
         int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
-        wr[w].push_back(r.second);
-        wl[w] += r.first;
+        asg[i] = w;
+        wl[w] += rows[i].first;
       }
+      auto score = [&](const std::vector<double>& l) {
+        double mx = 0.0, sq = 0.0;
+        for (double v : l) {
+          mx = std::max(mx, v);
+          sq += v * v;
+        }
+        return std::make_pair(mx, sq);
+      };
+      for (bool improved = true; improved;) {
+        improved = false;
+        auto cur = score(wl);
+        for (int i = 0; i < nr; ++i)
+          for (int w = 0; w < NW; ++w) {
+            if (w == asg[i]) continue;
+            std::vector<double> nl(wl);
+            nl[asg[i]] -= rows[i].first;
+            nl[w] += rows[i].first;
+            auto sc = score(nl);
+            if (sc < cur) {
+              wl = nl;
+              asg[i] = w;
+              cur = sc;
+              improved = true;
+            }
+          }
+        for (int i = 0; i < nr; ++i)
+          for (int j = i + 1; j < nr; ++j) {
+            const int a = asg[i], b = asg[j];
+            if (a == b) continue;
+            std::vector<double> nl(wl);
+            nl[a] += rows[j].first - rows[i].first;
+            nl[b] += rows[i].first - rows[j].first;
+            auto sc = score(nl);
+            if (sc < cur) {
+              wl = nl;
+              std::swap(asg[i], asg[j]);
+              cur = sc;
+              improved = true;
+            }
+          }
+      }
+      std::vector<std::vector<int>> wr(NW);
+      for (int i = 0; i < nr; ++i) wr[asg[i]].push_back(rows[i].second);
       gseg.assign(NW + 1, 0);
       groups.clear();
       for (int w = 0; w < NW; ++w) {
