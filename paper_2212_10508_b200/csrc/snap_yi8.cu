@@ -58,9 +58,8 @@ struct Cx {
 };
 
 template <int X>
-__device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int J, int SH, int jtop, int mb, int boff,
-                                      double cy, double be, Cx* __restrict__ yrow, const Cx* __restrict__ urow,
-                                      double& esum) {
+__device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int SH, int jtop, int mb, int boff,
+                                      double cy, Cx* __restrict__ yrow) {
   constexpr int S = X + yib::TJ;
   constexpr int FX = yib::foff(X);
   Cx d[S + 1];
@@ -96,9 +95,8 @@ __device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int J, i
       }
     }
   }
-  // diagonal s -> element ma = s - SH of the Y row (the warp owns the row) and the energy
+  // diagonal s -> element ma = s - SH of the Y row (the warp owns the row)
   Cx* yo = yrow - SH * yib::ATOMS;
-  const Cx* uo = urow - SH * yib::ATOMS;
 #pragma unroll
   for (int s = 0; s <= S; ++s) {
     if (s >= SH && s <= SH + jtop) {
@@ -106,12 +104,6 @@ __device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int J, i
       y.re = fma(cy, d[s].re, y.re);
       y.im = fma(cy, d[s].im, y.im);
       yo[s * yib::ATOMS] = y;
-      if (be != 0.0) {
-        const int ma = s - SH;
-        const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
-        const Cx u = uo[s * yib::ATOMS];
-        esum = fma(be * w, fma(u.re, d[s].re, u.im * d[s].im), esum);
-      }
     }
   }
 }
@@ -163,23 +155,38 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
     const int SH = (X + Y - J) / 2;
     const int jtop = (2 * mb == J) ? J / 2 : J;
     const int boff = c_box_off[tid];
-    const double cy = coef[tid], be = coef[yib::NT + tid];
+    const double cy = coef[tid];
     Cx* yrow = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + lane;
-    const Cx* urow = Ul + (yib::foff(J) + mb * (J + 1)) * yib::ATOMS;
-    double esum = 0.0;
     switch (X) {
-      case 0: box_x<0>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
-      case 1: box_x<1>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
-      case 2: box_x<2>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
-      case 3: box_x<3>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
-      case 4: box_x<4>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
-      case 5: box_x<5>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
-      case 6: box_x<6>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
-      case 7: box_x<7>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
-      default: box_x<8>(Ul, Y, J, SH, jtop, mb, boff, cy, be, yrow, urow, esum); break;
+      case 0: box_x<0>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      case 1: box_x<1>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      case 2: box_x<2>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      case 3: box_x<3>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      case 4: box_x<4>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      case 5: box_x<5>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      case 6: box_x<6>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      case 7: box_x<7>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      default: box_x<8>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
     }
-    // energy per row, items of a row in one fixed order whatever the schedule
-    erow[(yib::rowoff(J) + mb) * yib::ATOMS + lane] += esum;
+  }
+  __syncthreads();
+  // energy: E - beta0 is cubic in U and Y = dE/dU, so E = beta0 + (1/3) sum_J <U^J, Y^J>
+  // (half rows with the full-matrix weights); per row, rows summed in row order
+  for (int t = threadIdx.x; t < BOX_ROWS * yib::ATOMS; t += blockDim.x) {
+    const int r = t >> 5, at = t & 31;
+    if (S > 1 && c_box_rowsplit[V][r] != split) continue;
+    int J = 0;
+    while (J < yib::TJ && r >= yib::rowoff(J + 1)) ++J;
+    const int mb = r - yib::rowoff(J);
+    const Cx* u = Uf + (yib::foff(J) + mb * (J + 1)) * yib::ATOMS + at;
+    const Cx* y = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + at;
+    double e = 0.0;
+    for (int ma = 0; ma <= J; ++ma) {
+      const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+      const Cx uu = u[ma * yib::ATOMS], yy = y[ma * yib::ATOMS];
+      e = fma(w, fma(uu.re, yy.re, uu.im * yy.im), e);
+    }
+    erow[t] = e * (1.0 / 3.0);
   }
   __syncthreads();
   // rows owned by this CTA -> global (all rows when S = 1)
