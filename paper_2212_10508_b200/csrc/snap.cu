@@ -1914,24 +1914,30 @@ k_snap_deidrj_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
 // operations than propagating the three dU/dr_k.
 constexpr int ADJ_WARPS = 2;
 
-// RC (recompute): only the even layers' rows are stored; the odd layer J-1
-// needed by the backward step at even J is rebuilt from the stored layer J-2
-// with the same row_step (bitwise the forward value).  25 instead of 45 slots
-// per lane: 12.8 KB instead of 23 KB of history per warp, 1.5x the warps per SM.
-template <int J, bool RC>
-__device__ __forceinline__ constexpr int adj_slot() {
-  return RC ? (J / 2) * (J / 2) : J * (J + 1) / 2;
+// Forward-row history layouts: HL = 0 [slot (J, x)][lane] (23 KB per warp);
+// HL = 1 [half index (J, row, x)][pair slot] (155 x 7 complex, 17.4 KB per warp:
+// only the rows that exist are stored; slot 6 is the scratch of the two lanes
+// without a pair), which leaves room for more warps per SM.
+constexpr int ADJ_P = 7;  // pair slots per warp (32 / 5 rows = 6, + 1)
+
+template <int HL, int J>
+__device__ __forceinline__ int hpos(int x, int row, int mb, int lane, int p) {
+  if constexpr (HL == 0) {
+    return (J * (J + 1) / 2 + x) * 32 + lane + (row - mb);  // row mb - 1 is the lane below
+  } else {
+    return (yi5::hoff(J) + row * (J + 1) + x) * ADJ_P + p;
+  }
 }
 
-template <int TJ, bool RC>
+template <int TJ, int HL>
 struct AdjLayers {
   // forward: layer J from J-1 (in place), store the row, accumulate F
   template <int J>
   __device__ __forceinline__ static void fwd(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb,
                                              const double (*rp)[SNAP_JMAX + 2], const C2* Y, C2* hist,
-                                             int lane, double& F) {
+                                             int lane, int p, double& F) {
     if constexpr (J > 0) {
-      fwd<J - 1>(u, g, mb, rp, Y, hist, lane, F);
+      fwd<J - 1>(u, g, mb, rp, Y, hist, lane, p, F);
       C2 du[TJ + 1];
       row_step<TJ, J, false>(u, du, g, mb, rp);
     }
@@ -1939,7 +1945,7 @@ struct AdjLayers {
       const C2* yr = Y + c_hoff[J] + mb * (J + 1);
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
-        if (!RC || J % 2 == 0) hist[(adj_slot<J, RC>() + ma) * 32 + lane] = u[ma];
+        hist[hpos<HL, J>(ma, mb, mb, lane, p)] = u[ma];
         const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
         F += w * (u[ma].re * yr[ma].re + u[ma].im * yr[ma].im);
       }
@@ -1950,35 +1956,21 @@ struct AdjLayers {
   template <int J>
   __device__ __forceinline__ static void bwd(C2 (&G)[TJ + 1], const RowGeom<TJ>& g, int mb,
                                              const double (*rp)[SNAP_JMAX + 2], const C2* Y, const C2* hist,
-                                             int lane, C2& Sa, C2& Sb) {
+                                             int lane, int p, C2& Sa, C2& Sb) {
     if constexpr (J > 0) {
       const bool active = 2 * mb <= J;
       const bool born = (J % 2 == 0) && (2 * mb == J);  // row mb of layer J-1 is virtual
-      // U^{J-1} row mb (stored, rebuilt, or the symmetric image of row mb-1 of the lane below)
+      // U^{J-1} row mb (stored, or the symmetric image of row mb-1 of the same pair)
       C2 up[TJ + 1];
-      if (!RC || (J - 1) % 2 == 0) {
-        if (active) {
-#pragma unroll
-          for (int x = 0; x < J; ++x) {
-            if (!born) {
-              up[x] = hist[(adj_slot<J - 1, RC>() + x) * 32 + lane];
-            } else {
-              const C2 v = hist[(adj_slot<J - 1, RC>() + (J - 1 - x)) * 32 + lane - 1];
-              up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
-            }
-          }
-        }
-      } else if constexpr (J >= 2) {
-        // J even: rebuild odd layer J-1 from stored layer J-2 (every lane: the born
-        // lane takes row mb-1 from the lane below by shuffle)
-#pragma unroll
-        for (int x = 0; x <= J - 2; ++x) up[x] = hist[(adj_slot<J - 2, RC>() + x) * 32 + lane];
-        C2 dnone[TJ + 1];
-        row_step<TJ, J - 1, false>(up, dnone, g, mb, rp);
+      if (active) {
 #pragma unroll
         for (int x = 0; x < J; ++x) {
-          const C2 v = shfl_up_c2(up[J - 1 - x], 1);
-          if (born) up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+          if (!born) {
+            up[x] = hist[hpos<HL, J - 1>(x, mb, mb, lane, p)];
+          } else {
+            const C2 v = hist[hpos<HL, J - 1>(J - 1 - x, mb - 1, mb, lane, p)];
+            up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+          }
         }
       }
       if (active) {
@@ -2035,25 +2027,24 @@ struct AdjLayers {
           G[x].im += w * yr[x].im;
         }
       }
-      bwd<J - 1>(G, g, mb, rp, Y, hist, lane, Sa, Sb);
+      bwd<J - 1>(G, g, mb, rp, Y, hist, lane, p, Sa, Sb);
     }
   }
 };
 
-template <int TJ, bool RC>
-__global__ void __launch_bounds__(ADJ_WARPS * 32, RC ? 6 : 1)
+template <int TJ, int HL>
+__global__ void __launch_bounds__(ADJ_WARPS * 32)
 k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
                   const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
                   const C2* __restrict__ ylist, double* __restrict__ dedr) {
   constexpr int R = TJ / 2 + 1, P = 32 / R;
-  constexpr int NSLOT = RC ? (TJ / 2 + 1) * (TJ / 2 + 1) : (TJ + 1) * (TJ + 2) / 2;
+  constexpr int HIST = HL == 0 ? (TJ + 1) * (TJ + 2) / 2 * 32 : yi5::hoff(TJ + 1) * ADJ_P;  // complex per warp
   extern __shared__ double smem[];
   double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
   const int nh = D.nhalf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   C2* Y = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * nh;
-  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + ADJ_WARPS * nh +
-             warp * NSLOT * 32;
+  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + ADJ_WARPS * nh + warp * HIST;
   stage_rootpq(rp);
   const int64_t atom = (int64_t)blockIdx.x * ADJ_WARPS + warp;
   if (atom < natoms)
@@ -2064,6 +2055,7 @@ k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __res
   const int i = (int)(atom - b * N);
   const double* qb = q + b * (int64_t)N * 3;
   const int p = lane / R, mb = lane - p * R;
+  const int pc = p;  // lanes 30, 31 (no pair) write their own scratch slot 6
   const bool lane_ok = lane < P * R;
   const int n = cnt[atom];
   const int32_t* nb = nbr + atom * maxn;
@@ -2086,7 +2078,7 @@ k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __res
     for (int e = 0; e <= TJ; ++e) u[e] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
     double F = 0.0;
-    AdjLayers<TJ, RC>::template fwd<TJ>(u, g, mb, rp, Y, hist, lane, F);
+    AdjLayers<TJ, HL>::template fwd<TJ>(u, g, mb, rp, Y, hist, lane, pc, F);
     __syncwarp();
     // adjoint of the top layer: its direct term
     C2 G[TJ + 1];
@@ -2101,7 +2093,7 @@ k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __res
       }
     }
     C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
-    AdjLayers<TJ, RC>::template bwd<TJ>(G, g, mb, rp, Y, hist, lane, Sa, Sb);
+    AdjLayers<TJ, HL>::template bwd<TJ>(G, g, mb, rp, Y, hist, lane, pc, Sa, Sb);
     __syncwarp();
     // fixed-order sums over the R row lanes of the pair
 #pragma unroll
@@ -2252,8 +2244,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_yi_six, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
     cudaFuncSetAttribute(k_snap_yi_seven, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_adj<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_adj<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_adj<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_adj<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
   // register-resident kernels are instantiated for twojmax = 8 (PL_SNAP_RR=0 selects the
@@ -2320,17 +2312,17 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     const char* e = getenv("PL_SNAP_ADJ");
     return !(e && e[0] == '0');
   }();
-  static const bool adj_rc = [] {
+  static const int adj_hl = [] {
     const char* e = getenv("PL_SNAP_ADJ");
-    return e && e[0] == '3';  // 3: store even layers only, rebuild odd ones (bitwise equal, measured slower)
+    return (e && e[0] == '4') ? 1 : 0;  // 4: compact [half][pair] history (bitwise equal, measured slower)
   }();
-  if (rr && adj_env && adj_rc) {
-    size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + 25 * 32);
-    k_snap_deidrj_adj<8, true><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
+  if (rr && adj_env && adj_hl == 1) {
+    size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + yi5::hoff(9) * ADJ_P);
+    k_snap_deidrj_adj<8, 1><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
         D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
   } else if (rr && adj_env) {
     size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + 45 * 32);
-    k_snap_deidrj_adj<8, false><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
+    k_snap_deidrj_adj<8, 0><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
         D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
   } else if (rr) {
     size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * D.nhalf;
