@@ -1743,8 +1743,24 @@ struct Layers {
       C2* pr = part + c_hoff[J] + mb * (J + 1);
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
-        pr[ma].re += fc * u[ma].re;
-        pr[ma].im += fc * u[ma].im;
+        pr[ma].re = fma(fc, u[ma].re, pr[ma].re);
+        pr[ma].im = fma(fc, u[ma].im, pr[ma].im);
+      }
+    }
+  }
+  // same recursion, the lane's row accumulated in registers over its pairs
+  // (acc[J(J+1)/2 + ma]); one shared-memory write per element at the end
+  __device__ __forceinline__ static void ui_reg(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                                const double (*rp)[SNAP_JMAX + 2], bool on, double fc,
+                                                C2 (&acc)[(TJ + 1) * (TJ + 2) / 2]) {
+    Layers<TJ, J - 1>::ui_reg(u, du, g, mb, rp, on, fc, acc);
+    row_step<TJ, J, false>(u, du, g, mb, rp);
+    if (on && 2 * mb <= J) {
+#pragma unroll
+      for (int ma = 0; ma <= J; ++ma) {
+        C2& a = acc[J * (J + 1) / 2 + ma];
+        a.re = fma(fc, u[ma].re, a.re);
+        a.im = fma(fc, u[ma].im, a.im);
       }
     }
   }
@@ -1755,6 +1771,9 @@ struct Layers<TJ, 0> {
                                             const double (*)[SNAP_JMAX + 2], const C2*, double, double, double&) {}
   __device__ __forceinline__ static void ui(C2 (&)[TJ + 1], C2 (&)[TJ + 1], const RowGeom<TJ>&, int,
                                             const double (*)[SNAP_JMAX + 2], C2*, double) {}
+  __device__ __forceinline__ static void ui_reg(C2 (&)[TJ + 1], C2 (&)[TJ + 1], const RowGeom<TJ>&, int,
+                                                const double (*)[SNAP_JMAX + 2], bool, double,
+                                                C2 (&)[(TJ + 1) * (TJ + 2) / 2]) {}
 };
 
 constexpr int RR_WARPS = 4;  // warps per CTA of the register-resident kernels (one atom per warp)
@@ -1764,7 +1783,7 @@ __device__ __forceinline__ void stage_rootpq(double (*rp)[SNAP_JMAX + 2]) {
     rp[t / (SNAP_JMAX + 2)][t % (SNAP_JMAX + 2)] = c_rootpq[t / (SNAP_JMAX + 2)][t % (SNAP_JMAX + 2)];
 }
 
-template <int TJ>
+template <int TJ, bool REG>
 __global__ void __launch_bounds__(RR_WARPS * 32)
 k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
              const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
@@ -1790,6 +1809,11 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   const bool lane_ok = lane < P * R;
   const int n = cnt[atom];
   const int32_t* nb = nbr + atom * maxn;
+  C2 acc[(TJ + 1) * (TJ + 2) / 2];
+  if (REG) {
+#pragma unroll
+    for (int k = 0; k < (TJ + 1) * (TJ + 2) / 2; ++k) acc[k] = C2{0.0, 0.0};
+  }
   for (int s0 = 0; s0 < n; s0 += P) {
     const int s = s0 + p;
     const bool valid = lane_ok && s < n;
@@ -1811,11 +1835,24 @@ k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
 #pragma unroll
     for (int k = 0; k <= TJ; ++k) u[k] = du[k] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
+    if (REG) {
+      if (valid && mb == 0) acc[0].re += fc;  // J = 0
+      Layers<TJ, TJ>::ui_reg(u, du, g, mb, rp, valid, fc, acc);
+    } else {
+      C2* mypart = part + p * ps;
+      if (valid && mb == 0) mypart[0].re += fc;  // J = 0
+      // every lane runs the recursion (shuffles need the full warp); only valid
+      // lanes accumulate, each into its own pair slot
+      Layers<TJ, TJ>::ui(u, du, g, mb, rp, valid ? mypart : nullptr, fc);
+    }
+  }
+  if (REG && lane_ok) {  // each lane owns its (pair slot, row): plain stores
     C2* mypart = part + p * ps;
-    if (valid && mb == 0) mypart[0].re += fc;  // J = 0
-    // every lane runs the recursion (shuffles need the full warp); only valid
-    // lanes accumulate, each into its own pair slot
-    Layers<TJ, TJ>::ui(u, du, g, mb, rp, valid ? mypart : nullptr, fc);
+#pragma unroll
+    for (int J = 0; J <= TJ; ++J)
+      if (2 * mb <= J)
+#pragma unroll
+        for (int ma = 0; ma <= J; ++ma) mypart[c_hoff[J] + mb * (J + 1) + ma] = acc[J * (J + 1) / 2 + ma];
   }
   __syncwarp();
   // fixed-order sum over the P pair slots + self term
@@ -2237,7 +2274,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_yi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_bispectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_ui_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_ui_rr<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_ui_rr<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_yi_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_snap_yi_half, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
     cudaFuncSetAttribute(k_snap_yi_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -2260,8 +2298,16 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   prof_mark(ctx->stream, ST_UI, true);
   if (rr) {
     size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * (32 / 5) * (D.nhalf + 2);
-    k_snap_ui_rr<8><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
-                                                                 buf.utot);
+    static const bool ui_reg = [] {
+      const char* e = getenv("PL_SNAP_UI");
+      return !(e && e[0] == '0');  // 0: accumulate through shared memory every pair
+    }();
+    if (ui_reg)
+      k_snap_ui_rr<8, true><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
+                                                                          nl.maxn, buf.utot);
+    else
+      k_snap_ui_rr<8, false><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
+                                                                           nl.maxn, buf.utot);
   } else {
     k_snap_ui<<<(unsigned)na, UI_WARPS * 32, s1, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
                                                                  buf.utot);
