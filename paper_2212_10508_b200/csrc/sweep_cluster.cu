@@ -16,6 +16,7 @@
 // atom, same lane partition): coarse windows are bitwise those of
 // k_eam_density / k_eam_force + k_open / k_close.
 #include <cooperative_groups.h>
+#include <stdlib.h>
 
 #include "eam.cuh"
 #include "neigh.cuh"
@@ -32,9 +33,19 @@ constexpr double CL_SKIN = 0.4;
 
 // cluster size and threads per atom of an n-atom system (also used by the
 // batched EAM kernels so both paths share the lane partition)
-__host__ __device__ inline void cluster_layout(int n, int& C, int& tpa) {
+static int cluster_own_max() {  // atoms per CTA before the cluster grows (env PL_SWEEP_OWN, default 32: 15.0 vs 17.2 us per substep at 129 atoms)
+  static const int v = [] {
+    const char* e = getenv("PL_SWEEP_OWN");
+    const int x = e ? atoi(e) : 32;
+    return x < 8 ? 8 : x;
+  }();
+  return v;
+}
+
+inline void cluster_layout(int n, int& C, int& tpa) {
+  const int own_max = cluster_own_max();
   C = 1;
-  while (C < 16 && (n + C - 1) / C > 64) C *= 2;
+  while (C < 16 && (n + C - 1) / C > own_max) C *= 2;
   const int own = (n + C - 1) / C;
   tpa = 1;
   while (tpa < 32 && own * tpa * 2 <= CL_THREADS) tpa *= 2;
@@ -68,7 +79,8 @@ struct ClArgs {
 };
 
 struct ClSmem {  // carve-up of the dynamic shared memory of one CTA
-  double* q;       // 3n full positions
+  double* q;       // 3n full positions (two buffers: substeps alternate)
+  double* q2;
   double* fp;      // n full F'
   double* p;       // own momenta
   double* ph;      // own half-step momenta
@@ -82,7 +94,7 @@ struct ClSmem {  // carve-up of the dynamic shared memory of one CTA
 };
 
 __host__ __device__ inline size_t cl_smem_bytes(int n, int own) {
-  return sizeof(double) * (3 * (size_t)n + n + 4 * 3 * (size_t)own + (size_t)own * CL_MAXN) +
+  return sizeof(double) * (6 * (size_t)n + n + 4 * 3 * (size_t)own + (size_t)own * CL_MAXN) +
          sizeof(int32_t) * ((size_t)own * CL_MAXC + own + (size_t)own * CL_MAXN + own) + 64;
 }
 
@@ -127,7 +139,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
   // shared memory carve-up
   ClSmem M;
   M.q = sm;
-  M.fp = M.q + 3 * n;
+  M.q2 = M.q + 3 * n;
+  M.fp = M.q2 + 3 * n;
   M.p = M.fp + n;
   M.ph = M.p + 3 * own;
   M.g = M.ph + 3 * own;
@@ -143,36 +156,33 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
   const int lane = threadIdx.x & 31;
   const unsigned gmask = (tpa == 32 ? 0xffffffffu : ((1u << tpa) - 1u)) << (lane & ~(tpa - 1));
 
-  auto push_q_slice = [&]() {  // own positions -> every peer's q
+  // positions of the current substep (q) and the buffer the next open writes
+  // (qn): a peer still reading q in its force pass never sees our next slice,
+  // so one cluster barrier per position exchange suffices
+  double* q = M.q;
+  double* qn = M.q2;
+  auto push_q_slice = [&]() {  // own positions -> every peer's current buffer
     for (int pr = 0; pr < C; ++pr) {
-      double* dst = cl.map_shared_rank(M.q, pr);
-      for (int t = threadIdx.x; t < dn; t += blockDim.x) dst[c0 + t] = M.q[c0 + t];
+      double* dst = cl.map_shared_rank(q, pr);
+      for (int t = threadIdx.x; t < dn; t += blockDim.x) dst[c0 + t] = q[c0 + t];
     }
   };
 
   // ---------------------------------------------------------------- force
-  auto eam_force = [&](bool force_rebuild) {
-    // rebuild: own atoms' candidates from the full positions
-    int moved = 0;
-    if (!force_rebuild)
-      for (int i = threadIdx.x; i < nown; i += blockDim.x) {
-        const double dx = M.q[c0 + 3 * i] - M.qref[3 * i], dy = M.q[c0 + 3 * i + 1] - M.qref[3 * i + 1];
-        const double dz = M.q[c0 + 3 * i + 2] - M.qref[3 * i + 2];
-        if (!(dx * dx + dy * dy + dz * dz <= 0.25 * CL_SKIN * CL_SKIN)) moved = 1;
-      }
-    moved = __syncthreads_or(moved);
-    const bool any = force_rebuild || cluster_sum(cl, moved ? 1.0 : 0.0, slots_c, C, rank) > 0.0;
+  auto eam_force = [&](bool any) {
+    // rebuild (any CTA saw an atom move by more than half the skin): own atoms'
+    // candidates from the full positions
     if (any) {
       for (int i = threadIdx.x; i < nown; i += blockDim.x) {
         const int ai = a0 + i;
-        const double xi = M.q[3 * ai], yi = M.q[3 * ai + 1], zi = M.q[3 * ai + 2];
+        const double xi = q[3 * ai], yi = q[3 * ai + 1], zi = q[3 * ai + 2];
         int c = 0;
         int32_t* my = M.cand + (size_t)i * CL_MAXC;
         for (int j = 0; j < n; ++j) {
           if (j == ai) continue;
-          const double dx = min_image(sub(M.q[3 * j], xi), A.box.L[0], A.box.inv[0]);
-          const double dy = min_image(sub(M.q[3 * j + 1], yi), A.box.L[1], A.box.inv[1]);
-          const double dz = min_image(sub(M.q[3 * j + 2], zi), A.box.L[2], A.box.inv[2]);
+          const double dx = min_image(sub(q[3 * j], xi), A.box.L[0], A.box.inv[0]);
+          const double dy = min_image(sub(q[3 * j + 1], yi), A.box.L[1], A.box.inv[1]);
+          const double dz = min_image(sub(q[3 * j + 2], zi), A.box.L[2], A.box.inv[2]);
           if (r2_exact(dx, dy, dz) < A.rl2) {
             if (c < CL_MAXC) my[c] = j;
             ++c;
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
         if (k < nc) {
           j = M.cand[(size_t)ii * CL_MAXC + k];
           double dx, dy, dz;
-          pair_vec(M.q, ai, j, A.box, dx, dy, dz);
+          pair_vec(q, ai, j, A.box, dx, dy, dz);
           r2 = r2_exact(dx, dy, dz);
           keep = r2 < A.rc2;
         }
@@ -260,7 +270,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
       for (int k = sl; k < nl; k += tpa) {
         const int j = M.nbr[(size_t)ii * CL_MAXN + k];
         double dx, dy, dz;
-        pair_vec(M.q, ai, j, A.box, dx, dy, dz);
+        pair_vec(q, ai, j, A.box, dx, dy, dz);
         const double rr = M.rr[(size_t)ii * CL_MAXN + k];
         double rf, drf, pf, dpf;
         tab_eval(A.rho, rr, rf, drf);
@@ -284,13 +294,13 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
 
   // ---------------------------------------------------------------- sweep
   double num = A.acc[2 * slot], den = A.acc[2 * slot + 1];
-  for (int64_t t = threadIdx.x; t < 3 * (int64_t)n; t += blockDim.x) M.q[t] = Q[m0 * d + t];
+  for (int64_t t = threadIdx.x; t < 3 * (int64_t)n; t += blockDim.x) q[t] = Q[m0 * d + t];
   for (int t = threadIdx.x; t < dn; t += blockDim.x) M.p[t] = P[m0 * d + c0 + t];
   __syncthreads();
   cl.sync();
   if (A.b_inc[slot]) {
     double s2 = 0.0;
-    for (int t = threadIdx.x; t < dn; t += blockDim.x) s2 += M.q[c0 + t] * M.q[c0 + t];
+    for (int t = threadIdx.x; t < dn; t += blockDim.x) s2 += q[c0 + t] * q[c0 + t];
     for (int off = 16; off > 0; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
     if (lane == 0) red[threadIdx.x >> 5] = s2;
     __syncthreads();
@@ -315,14 +325,27 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
         const double pref = (s == 1) ? M.p[t] : M.ph[t];
         const double hv = add(sub(sub(M.p[t], mul(A.h, M.g[t])), mul(A.hg, pref)), mul(al, G[(int64_t)(s - 1) * d + gc]));
         M.ph[t] = hv;
-        M.q[gc] = add(M.q[gc], mul(A.dt, dvd(hv, mm)));
+        qn[gc] = add(q[gc], mul(A.dt, dvd(hv, mm)));
       }
-      // peers may still be in the previous force pass, reading their copy of
-      // our slice: wait for the whole cluster before overwriting it
-      cl.sync();
+      __syncthreads();
+      {  // swap buffers; own moved-by-half-skin flag travels with the slice
+        double* tq = q;
+        q = qn;
+        qn = tq;
+      }
+      int moved = 0;
+      for (int i = threadIdx.x; i < nown; i += blockDim.x) {
+        const double dx = q[c0 + 3 * i] - M.qref[3 * i], dy = q[c0 + 3 * i + 1] - M.qref[3 * i + 1];
+        const double dz = q[c0 + 3 * i + 2] - M.qref[3 * i + 2];
+        if (!(dx * dx + dy * dy + dz * dz <= 0.25 * CL_SKIN * CL_SKIN)) moved = 1;
+      }
+      moved = __syncthreads_or(moved);
       push_q_slice();
+      if (threadIdx.x < (unsigned)C) cl.map_shared_rank(slots_c, (int)threadIdx.x)[rank] = moved ? 1.0 : 0.0;
       cl.sync();
-      eam_force(false);
+      bool any = false;
+      for (int rr_ = 0; rr_ < C; ++rr_) any = any || slots_c[rr_] > 0.0;
+      eam_force(any);
       int bad = 0;
       for (int t = threadIdx.x; t < dn; t += blockDim.x) {  // close + blow-up check
         const int gc = c0 + t;
@@ -331,13 +354,13 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
         const double hv = M.ph[t];
         const double pn = add(sub(sub(hv, mul(A.h, M.g[t])), mul(A.hg, hv)), mul(al, G[(int64_t)s * d + gc]));
         M.p[t] = pn;
-        if (!(fabs(M.q[gc]) <= BLOWUP_LIMIT && fabs(pn) <= BLOWUP_LIMIT)) bad = 1;
+        if (!(fabs(q[gc]) <= BLOWUP_LIMIT && fabs(pn) <= BLOWUP_LIMIT)) bad = 1;
       }
       if (__syncthreads_or(bad) && threadIdx.x == 0 && s_fail == 0) s_fail = s;
     }
     __syncthreads();
     for (int t = threadIdx.x; t < dn; t += blockDim.x) {
-      baseQ[m * d + c0 + t] = M.q[c0 + t];
+      baseQ[m * d + c0 + t] = q[c0 + t];
       baseP[m * d + c0 + t] = M.p[t];
     }
     // first failing substep over the cluster (0 = none): min over ranks
@@ -364,7 +387,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
     }
     if (A.mode == 1) {
       for (int t = threadIdx.x; t < dn; t += blockDim.x) {
-        Q[(m + 1) * d + c0 + t] = M.q[c0 + t];
+        Q[(m + 1) * d + c0 + t] = q[c0 + t];
         P[(m + 1) * d + c0 + t] = M.p[t];
       }
       ++done;
@@ -375,11 +398,11 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
     for (int t = threadIdx.x; t < dn; t += blockDim.x) {
       const int gc = c0 + t;
       const double pv = Q[(m + 1) * d + gc];  // prev[m+1], read before cur[m+1] overwrites it
-      const double cq = add(M.q[gc], jumpQ[m * d + gc]);
+      const double cq = add(q[gc], jumpQ[m * d + gc]);
       const double cp = add(M.p[t], jumpP[m * d + gc]);
       Q[(m + 1) * d + gc] = cq;
       P[(m + 1) * d + gc] = cp;
-      M.q[gc] = cq;
+      q[gc] = cq;
       M.p[t] = cp;
       if (!isfinite(cq) || !isfinite(cp)) nonfinite = 1;
       const double e = sub(cq, pv);
