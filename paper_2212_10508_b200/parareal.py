@@ -233,6 +233,60 @@ def _call(prop, state, m, iteration):
         raise
 
 
+class _FineCache:
+    """Fine-window results keyed by their exact start state.
+
+    Behind the parareal exactness front prev[m] stops changing bit for bit, so
+    F(prev[m]) is the previous iteration's value: a row is re-propagated only
+    when its start (q, p) differs in any bit from the cached input (the fine
+    propagator is deterministic, so results are identical to recomputing).
+    The reference recomputes every slab window each iteration
+    (parareal.py:270-286); the gain model still charges them (accounting.py).
+    Disable with PL_PARAREAL_NOCACHE=1.
+    """
+
+    def __init__(self, rows: int, d: int, device):
+        import os
+
+        import torch
+        f64 = dict(dtype=torch.float64, device=device)
+        self.inQ = torch.zeros((rows, d), **f64)
+        self.inP = torch.zeros((rows, d), **f64)
+        self.outQ = torch.zeros((rows, d), **f64)
+        self.outP = torch.zeros((rows, d), **f64)
+        self.valid = torch.zeros(rows, dtype=torch.bool, device=device)
+        self.enabled = os.environ.get("PL_PARAREAL_NOCACHE", "0") in ("", "0")
+        self.propagated = 0  # rows actually propagated (diagnostics)
+
+    def run(self, rows, Qs, Ps, noise_of, run_fn):
+        """rows: LongTensor of cache rows; Qs/Ps their start states; noise_of(pos)
+        the noise rows of positions ``pos`` of ``rows``.  run_fn(Q, P, N) ->
+        (FQ, FP, blow) propagates a (sub)batch.  Returns
+        (FQ, FP, blow, positions) for all rows; blow/positions refer to the
+        propagated subset (positions index into ``rows``)."""
+        import torch
+        if self.enabled:
+            same = self.valid.index_select(0, rows)
+            same &= (Qs.view(torch.int64) == self.inQ.index_select(0, rows).view(torch.int64)).all(dim=1)
+            same &= (Ps.view(torch.int64) == self.inP.index_select(0, rows).view(torch.int64)).all(dim=1)
+            pos = torch.nonzero(~same).squeeze(1)
+        else:
+            pos = torch.arange(rows.numel(), device=rows.device)
+        blow = torch.zeros(0, dtype=torch.int32, device=rows.device)
+        if pos.numel():
+            sub = rows.index_select(0, pos)
+            q0, p0 = Qs.index_select(0, pos), Ps.index_select(0, pos)
+            FQ, FP, blow = run_fn(q0, p0, noise_of(pos).contiguous())
+            self.inQ.index_copy_(0, sub, q0)
+            self.inP.index_copy_(0, sub, p0)
+            self.outQ.index_copy_(0, sub, FQ)
+            self.outP.index_copy_(0, sub, FP)
+            ok = (blow == 0)
+            self.valid.index_copy_(0, sub, ok)
+            self.propagated += int(pos.numel())
+        return self.outQ.index_select(0, rows), self.outP.index_select(0, rows), blow, pos
+
+
 class _DeviceRun:
     """Device-resident trajectory + cached coarse outputs for one engine run."""
 
@@ -259,6 +313,7 @@ class _DeviceRun:
         self.hist = torch.zeros(n, **f64)
         self.noise_f = fine.noise_all()
         self.noise_c = coarse.noise_all()
+        self.fcache = _FineCache(n, d, dev)
 
     def bootstrap(self, n_init: int) -> None:
         """cur[m+1] = C(cur[m]) for m = n_init..N-1 (parareal.py:404-405); caches base."""
@@ -285,19 +340,25 @@ class _DeviceRun:
         all-gather of the endpoints gives every rank the full set
         (distributed.sharded_fine).
         """
+        import torch
         W = n_final - n_init
 
-        def run_block(lo, hi):
-            return self.fine.kernel.run(self.Q[lo:hi], self.P[lo:hi], self.noise_f[lo:hi])
+        def run_fn(q0, p0, nz):
+            def run_block(lo, hi):
+                return self.fine.kernel.run(q0[lo:hi].contiguous(), p0[lo:hi].contiguous(), nz[lo:hi])
+            return sharded_fine(run_block, 0, q0.shape[0])
 
-        FQ, FP, blow = sharded_fine(run_block, n_init, n_final)
+        rows = torch.arange(n_init, n_final, device=self.Q.device)
+        nz = self.noise_f[n_init:n_final]
+        FQ, FP, blow, pos = self.fcache.run(rows, self.Q[n_init:n_final], self.P[n_init:n_final],
+                                            lambda p_: nz.index_select(0, p_), run_fn)
         b = blow.cpu().numpy()
         bad = np.nonzero(b)[0]
         if bad.size:
-            i = int(bad[0])
+            i = int(pos[int(bad[0])])
             raise BlowUpError(
-                f"state left the trusted range (|component| > 1e+12 or non-finite) at substep {b[i]}",
-                substep=int(b[i]), window=n_init + i + 1, iteration=iteration)
+                f"state left the trusted range (|component| > 1e+12 or non-finite) at substep {b[bad[0]]}",
+                substep=int(b[bad[0]]), window=n_init + i + 1, iteration=iteration)
         lib, ctx = _lib.load(), _lib.context()
         n = W * self.d
         _lib.check(lib.pl_sub(ctx.handle, n, _lib.ptr(FQ), _lib.ptr(self.baseQ[n_init:n_final]),
@@ -512,6 +573,7 @@ class _BatchRun:
         self.hist = torch.zeros((R, n), **f64)
         seeds = np.concatenate([np.asarray(p.window_seeds[:n], dtype=np.uint64) for p in plans])
         self.noise = self.fk.noise(seeds).reshape(R, n, (L + 1) * d)
+        self.fcache = _FineCache(R * n, d, dev)
 
     def _batch_call(self, slots, mode, expl):
         import numpy as np_
@@ -553,16 +615,19 @@ class _BatchRun:
                               dtype=torch.long, device=self.Q.device)
         Qs = self.Q.view(-1, d).index_select(0, rows_q)
         Ps = self.P.view(-1, d).index_select(0, rows_q)
-        Ns = self.noise.view(-1, self.noise.shape[-1]).index_select(0, rows_w)
+        Ns = self.noise.view(-1, self.noise.shape[-1])
 
-        def run_block(lo, hi):
-            return self.fk.run(Qs[lo:hi].contiguous(), Ps[lo:hi].contiguous(), Ns[lo:hi].contiguous())
+        def run_fn(q0, p0, nz):
+            def run_block(lo, hi):
+                return self.fk.run(q0[lo:hi].contiguous(), p0[lo:hi].contiguous(), nz[lo:hi].contiguous())
+            return sharded_fine(run_block, 0, q0.shape[0])
 
-        FQ, FP, blow = sharded_fine(run_block, 0, rows_w.numel())
+        FQ, FP, blow, pos = self.fcache.run(rows_w, Qs, Ps, lambda p_: Ns.index_select(0, rows_w.index_select(0, p_)),
+                                            run_fn)
         b = blow.cpu().numpy()
         if b.any():
             i = int(np.nonzero(b)[0][0])
-            raise BlowUpError(f"fine window blew up at substep {int(b[i])} (batch row {i})",
+            raise BlowUpError(f"fine window blew up at substep {int(b[i])} (batch row {int(pos[i])})",
                               substep=int(b[i]))
         lib, ctx = _lib.load(), _lib.context()
         bq = self.baseQ.view(-1, d).index_select(0, rows_w)
