@@ -266,9 +266,26 @@ def make_minima():
     np.savez_compressed(os.path.join(OUT, "minima_golden.npz"), versions=json.dumps(_versions()), **out)
 
 
+def make_reports():
+    """The reference's own report files (cli._run_parareal: trajectory.csv,
+    history.csv, result.json) for configs/adaptive.json and configs/parareal.json."""
+    import tempfile
+    from paralangevin import cli
+    out = {}
+    for name in ("adaptive", "parareal"):
+        cfg = cli.validate_config(os.path.join(CFG, f"{name}.json"))
+        with tempfile.TemporaryDirectory() as tmp:
+            outputs = []
+            cli._run_parareal(cfg, __import__("pathlib").Path(tmp), 1, outputs)
+            for f in ("trajectory.csv", "history.csv", "result.json"):
+                out[f"{name}_{f.replace('.', '_')}"] = np.array(open(os.path.join(tmp, f)).read())
+    np.savez_compressed(os.path.join(OUT, "reports_golden.npz"), versions=json.dumps(_versions()), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["rng", "window", "parareal", "residence", "accounting", "temperature", "minima"]
+    which = sys.argv[1:] or ["rng", "window", "parareal", "residence", "accounting", "temperature", "minima",
+                             "reports"]
     for w in which:
         globals()[f"make_{w}"]()
     for f in sorted(os.listdir(OUT)):

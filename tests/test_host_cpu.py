@@ -141,3 +141,32 @@ def test_gain_accounting_matches_reference(golden):
         acc.adaptive_gain(sets[1][:1], 16, 1.0, 0.0)  # does not tile the window range
     with pytest.raises(ValueError):
         acc.classic_gain(16, 3, 0.0, 1.0)
+
+
+@pytest.mark.parametrize("name", ["adaptive", "parareal"])
+def test_report_files_match_reference(golden, tmp_path, name):
+    """trajectory.csv / history.csv / result.json byte-identical to the reference's
+    own report writers (cli.py:888-930) for the reference's parareal result."""
+    from paper_2212_10508_b200 import reports
+    from paper_2212_10508_b200.model import LangevinParams, NodeTrajectory
+    from paper_2212_10508_b200.parareal import PararealConfig, PararealResult, SlabAttempt, SlabRecord
+    z, ref = golden("parareal_golden.npz"), golden("reports_golden.npz")
+    cfg = z[f"{name}_cfg"]
+    slabs, by = [], {}
+    for si, n0, n1, kc, af, ai in z[f"{name}_slabs"]:
+        by.setdefault((int(si), int(n0), int(n1), int(kc)), []).append(SlabAttempt(int(af), int(ai)))
+    for (si, n0, n1, kc), att in sorted(by.items()):
+        slabs.append(SlabRecord(si, n0, tuple(att), n1, kc))
+    res = PararealResult(trajectory=NodeTrajectory.from_arrays(z[f"{name}_Q"], z[f"{name}_P"]), slabs=slabs,
+                         error_history=[tuple(r) for r in z[f"{name}_hist"]],
+                         converged=bool(z[f"{name}_converged"]))
+    params = LangevinParams(cfg[0], cfg[1], cfg[2], int(cfg[3]))
+    config = PararealConfig(int(cfg[5]), cfg[6], cfg[7] if name == "adaptive" else None)
+
+    class Pair:
+        cost_fine, cost_coarse = 175.0, 1.0
+
+    exp = "parareal_adaptive" if name == "adaptive" else "parareal_classic"
+    paths = reports.write_parareal_report(tmp_path, res, exp, params, config, Pair)
+    for p in paths:
+        assert p.read_text() == str(ref[f"{name}_{p.name.replace('.', '_')}"]), p.name
