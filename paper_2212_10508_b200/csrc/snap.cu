@@ -2155,6 +2155,265 @@ k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __res
   }
 }
 
+// ------------------------------------------------------------------ reverse-mode dE/dr, 4 lanes per pair
+// twojmax 8: lanes own half rows 0..3 of a pair (8 pairs per warp instead of 6);
+// row 4 exists only in layer 8, where it is born from row 3 of layer 7, so the
+// row-3 lane carries it (forward step, direct term, adjoint, and the adjoint of
+// the virtual row flowing back to row 3 stay inside that lane).  Balances the
+// lanes (rows 0..4 carry 45, 42, 35, 24, 9 elements; the row-3 lane now 33) and
+// stores only layers 0..7 (the backward never reads layer 8): 18.4 KB per warp.
+template <int TJ, int J>
+__device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                           const double (*rp)[SNAP_JMAX + 2]) {
+#pragma unroll
+  for (int ma = J; ma >= 0; --ma) {
+    C2 nu{0.0, 0.0};
+    if (ma < J) {
+      const double A = rp[J - ma][J - mb];
+      const C2 t = cmulc(g.a, u[ma]);
+      nu.re += A * t.re;
+      nu.im += A * t.im;
+    }
+    if (ma > 0) {
+      const double Bc = rp[ma][J - mb];
+      const C2 t = cmulc(g.b, u[ma - 1]);
+      nu.re -= Bc * t.re;
+      nu.im -= Bc * t.im;
+    }
+    u[ma] = nu;
+  }
+}
+
+__device__ __forceinline__ double half_w(int J, int mb, int ma) {
+  return (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
+}
+
+struct AdjR4 {
+  static constexpr int TJ = 8;
+  // forward: layer J from J-1 (in place), store rows of layers <= 7, accumulate F
+  template <int J>
+  __device__ __forceinline__ static void fwd(C2 (&u)[TJ + 1], C2 (&u4)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                             const double (*rp)[SNAP_JMAX + 2], const C2* Y, C2* hist, int lane,
+                                             double& F) {
+    if constexpr (J > 0) {
+      fwd<J - 1>(u, u4, g, mb, rp, Y, hist, lane, F);
+      if constexpr (J == TJ) {
+        // virtual row 4 of layer 7 = born image of this lane's row 3 of layer 7
+#pragma unroll
+        for (int i = 0; i < J; ++i) {
+          const int x = J - 1 - i;
+          const C2 v = u[i];
+          u4[x] = ((x + J / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+        }
+        u4[J] = C2{0.0, 0.0};
+      }
+      C2 du[TJ + 1];
+      row_step<TJ, J, false>(u, du, g, mb, rp);  // rows 1..3 are born at J = 2, 4, 6 from the lane below
+      if constexpr (J == TJ) row_update<TJ, TJ>(u4, g, TJ / 2, rp);
+    }
+    if (2 * mb <= J) {
+      const C2* yr = Y + c_hoff[J] + mb * (J + 1);
+#pragma unroll
+      for (int ma = 0; ma <= J; ++ma) {
+        if constexpr (J < TJ) hist[(J * (J + 1) / 2 + ma) * 32 + lane] = u[ma];
+        F += half_w(J, mb, ma) * (u[ma].re * yr[ma].re + u[ma].im * yr[ma].im);
+      }
+    }
+    if constexpr (J == TJ) {
+      if (mb == TJ / 2 - 1) {
+        const C2* yr = Y + c_hoff[J] + (TJ / 2) * (J + 1);
+#pragma unroll
+        for (int ma = 0; ma <= J; ++ma) F += half_w(J, TJ / 2, ma) * (u4[ma].re * yr[ma].re + u4[ma].im * yr[ma].im);
+      }
+    }
+  }
+
+  // Sa/Sb of one row at layer J, then its adjoint to layer J-1 (in place)
+  template <int J>
+  __device__ __forceinline__ static void row_adj(C2 (&G)[TJ + 1], const C2 (&up)[TJ + 1], const RowGeom<TJ>& g,
+                                                 int mb, const double (*rp)[SNAP_JMAX + 2], C2& Sa, C2& Sb) {
+#pragma unroll
+    for (int ma = 0; ma <= J; ++ma) {
+      if (ma < J) {
+        const double A = rp[J - ma][J - mb];
+        const C2 t = cmulc(up[ma], G[ma]);
+        Sa.re += A * t.re;
+        Sa.im += A * t.im;
+      }
+      if (ma > 0) {
+        const double Bc = rp[ma][J - mb];
+        const C2 t = cmulc(up[ma - 1], G[ma]);
+        Sb.re -= Bc * t.re;
+        Sb.im -= Bc * t.im;
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < J; ++x) {
+      const double A = rp[J - x][J - mb];
+      const double Bc = rp[x + 1][J - mb];
+      const C2 t1 = cmul(g.a, G[x]);
+      const C2 t2 = cmul(g.b, G[x + 1]);
+      G[x] = C2{A * t1.re - Bc * t2.re, A * t1.im - Bc * t2.im};
+    }
+    G[J] = C2{0.0, 0.0};
+  }
+
+  template <int J>
+  __device__ __forceinline__ static void bwd(C2 (&G)[TJ + 1], C2 (&G4)[TJ + 1], const RowGeom<TJ>& g, int mb,
+                                             const double (*rp)[SNAP_JMAX + 2], const C2* Y, const C2* hist, int lane,
+                                             C2& Sa, C2& Sb) {
+    if constexpr (J > 0) {
+      const bool active = 2 * mb <= J;
+      const bool born = (J % 2 == 0) && (J < TJ) && (2 * mb == J);  // rows 1..3: virtual in layer J-1
+      C2 up[TJ + 1];
+      if (active) {
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          if (!born) {
+            up[x] = hist[((J - 1) * J / 2 + x) * 32 + lane];
+          } else {
+            const C2 v = hist[((J - 1) * J / 2 + (J - 1 - x)) * 32 + lane - 1];
+            up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+          }
+        }
+        row_adj<J>(G, up, g, mb, rp, Sa, Sb);
+      }
+      if constexpr (J == TJ) {
+        // row 4 (row-3 lane): its layer-7 image comes from this lane's own row 3
+        if (mb == TJ / 2 - 1) {
+          C2 up4[TJ + 1];
+#pragma unroll
+          for (int x = 0; x < J; ++x) {
+            const C2 v = hist[((J - 1) * J / 2 + (J - 1 - x)) * 32 + lane];
+            up4[x] = ((x + TJ / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+          }
+          row_adj<J>(G4, up4, g, TJ / 2, rp, Sa, Sb);
+          // adjoint of the virtual row 4 of layer 7 flows to row 3
+#pragma unroll
+          for (int x = 0; x < J; ++x) {
+            const C2 v = G4[x];
+            const int xs = J - 1 - x;
+            const bool neg = ((x + TJ / 2) & 1) != 0;
+            G[xs].re += neg ? -v.re : v.re;
+            G[xs].im += neg ? v.im : -v.im;
+          }
+        }
+      } else if constexpr (J % 2 == 0) {
+        // rows 1..3 born at J: their adjoint flows to the lane below (same pair)
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          const C2 v = C2{__shfl_down_sync(0xffffffffu, G[x].re, 1), __shfl_down_sync(0xffffffffu, G[x].im, 1)};
+          if (2 * (mb + 1) == J) {
+            const int xs = J - 1 - x;
+            const bool neg = ((x + mb + 1) & 1) != 0;
+            G[xs].re += neg ? -v.re : v.re;
+            G[xs].im += neg ? v.im : -v.im;
+          }
+        }
+        if (born) {
+#pragma unroll
+          for (int x = 0; x <= J; ++x) G[x] = C2{0.0, 0.0};
+        }
+      }
+      if (2 * mb <= J - 1) {
+        const C2* yr = Y + c_hoff[J - 1] + mb * J;
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          const double w = half_w(J - 1, mb, x);
+          G[x].re += w * yr[x].re;
+          G[x].im += w * yr[x].im;
+        }
+      }
+      bwd<J - 1>(G, G4, g, mb, rp, Y, hist, lane, Sa, Sb);
+    }
+  }
+};
+
+constexpr int ADJ4_WARPS = 2;
+constexpr int ADJ4_SLOTS = 36;  // layers 0..7
+
+__global__ void __launch_bounds__(ADJ4_WARPS * 32)
+k_snap_deidrj_adj4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+                   const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+                   const C2* __restrict__ ylist, double* __restrict__ dedr) {
+  constexpr int TJ = 8, R = 4, P = 8;
+  extern __shared__ double smem[];
+  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  C2* Y = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * nh;
+  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + ADJ4_WARPS * nh +
+             warp * ADJ4_SLOTS * 32;
+  stage_rootpq(rp);
+  const int64_t atom = (int64_t)blockIdx.x * ADJ4_WARPS + warp;
+  if (atom < natoms)
+    for (int t = lane; t < nh; t += 32) Y[t] = ylist[atom * nh + t];
+  __syncthreads();
+  if (atom >= natoms) return;
+  const int64_t b = atom / N;
+  const int i = (int)(atom - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const int p = lane / R, mb = lane - p * R;
+  const int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  for (int s0 = 0; s0 < n; s0 += P) {
+    const int s = s0 + p;
+    const bool valid = s < n;
+    PairGeom pg;
+    if (valid) {
+      double dx, dy, dz;
+      pair_vec(qb, i, nb[s], box, dx, dy, dz);
+      pair_geom(D, dx, dy, dz, pg, true);
+    } else {
+      pair_geom(D, 1.0, 0.0, 0.0, pg, true);
+      pg.fc = 0.0;
+      pg.dfc = 0.0;
+    }
+    RowGeom<TJ> g{pg.a, pg.b, C2{0.0, 0.0}, C2{0.0, 0.0}};
+    C2 u[TJ + 1], u4[TJ + 1];
+#pragma unroll
+    for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
+    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
+    double F = 0.0;
+    AdjR4::fwd<TJ>(u, u4, g, mb, rp, Y, hist, lane, F);
+    __syncwarp();
+    C2 G[TJ + 1], G4[TJ + 1];
+    {
+      const C2* yr = Y + c_hoff[TJ] + mb * (TJ + 1);
+      const C2* y4 = Y + c_hoff[TJ] + (TJ / 2) * (TJ + 1);
+#pragma unroll
+      for (int x = 0; x <= TJ; ++x) {
+        const double w = half_w(TJ, mb, x), w4 = half_w(TJ, TJ / 2, x);
+        G[x] = C2{w * yr[x].re, w * yr[x].im};
+        G4[x] = C2{w4 * y4[x].re, w4 * y4[x].im};
+      }
+    }
+    C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
+    AdjR4::bwd<TJ>(G, G4, g, mb, rp, Y, hist, lane, Sa, Sb);
+    __syncwarp();
+    // fixed-order sums over the 4 row lanes of the pair
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double f = __shfl_down_sync(0xffffffffu, F, r);
+      const double ar = __shfl_down_sync(0xffffffffu, Sa.re, r), ai = __shfl_down_sync(0xffffffffu, Sa.im, r);
+      const double br = __shfl_down_sync(0xffffffffu, Sb.re, r), bi = __shfl_down_sync(0xffffffffu, Sb.im, r);
+      if (mb == 0) {
+        F += f;
+        Sa.re += ar; Sa.im += ai;
+        Sb.re += br; Sb.im += bi;
+      }
+    }
+    if (valid && mb == 0) {
+      double* o = dedr + (atom * maxn + s) * 3;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double re = pg.da[k].re * Sa.re - pg.da[k].im * Sa.im + pg.db[k].re * Sb.re - pg.db[k].im * Sb.im;
+        o[k] = pg.dfc * pg.u[k] * F + pg.fc * re;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel: gather
 __global__ void k_snap_gather(int64_t natoms, int N, Box box, const double* __restrict__ q,
                               const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt,
@@ -2284,6 +2543,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_adj4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
   // register-resident kernels are instantiated for twojmax = 8 (PL_SNAP_RR=0 selects the
@@ -2362,7 +2622,15 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     const char* e = getenv("PL_SNAP_ADJ");
     return (e && e[0] == '4') ? 1 : 0;  // 4: compact [half][pair] history (bitwise equal, measured slower)
   }();
-  if (rr && adj_env && adj_hl == 1) {
+  static const bool adj4 = [] {
+    const char* e = getenv("PL_SNAP_ADJ");
+    return !(e && (e[0] == '2' || e[0] == '4'));  // 2: 5 lanes per pair ([slot][lane] history)
+  }();
+  if (rr && adj_env && adj4 && S->tj == 8) {
+    size_t sm = rp_bytes + sizeof(C2) * ADJ4_WARPS * (D.nhalf + ADJ4_SLOTS * 32);
+    k_snap_deidrj_adj4<<<(unsigned)((na + ADJ4_WARPS - 1) / ADJ4_WARPS), ADJ4_WARPS * 32, sm, ctx->stream>>>(
+        D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
+  } else if (rr && adj_env && adj_hl == 1) {
     size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + yi5::hoff(9) * ADJ_P);
     k_snap_deidrj_adj<8, 1><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
         D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
