@@ -2155,13 +2155,7 @@ k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __res
   }
 }
 
-// ------------------------------------------------------------------ reverse-mode dE/dr, 4 lanes per pair
-// twojmax 8: lanes own half rows 0..3 of a pair (8 pairs per warp instead of 6);
-// row 4 exists only in layer 8, where it is born from row 3 of layer 7, so the
-// row-3 lane carries it (forward step, direct term, adjoint, and the adjoint of
-// the virtual row flowing back to row 3 stay inside that lane).  Balances the
-// lanes (rows 0..4 carry 45, 42, 35, 24, 9 elements; the row-3 lane now 33) and
-// stores only layers 0..7 (the backward never reads layer 8): 18.4 KB per warp.
+// layer J of row mb from layer J-1 in place, no born-row handling
 template <int TJ, int J>
 __device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb,
                                            const double (*rp)[SNAP_JMAX + 2]) {
@@ -2184,6 +2178,134 @@ __device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g
   }
 }
 
+// U_tot with 4 lanes per pair (twojmax 8; see k_snap_deidrj_adj4): lanes own
+// rows 0..3, the row-3 lane also builds row 4 of layer 8 from its own row 3 of
+// layer 7.  Each lane accumulates its rows over its pairs in registers; one
+// store per element into its pair slot, then a fixed-order sum over 8 slots.
+constexpr int UI4_WARPS = 4;
+
+template <int J>
+__device__ __forceinline__ void ui4_layers(C2 (&u)[9], C2 (&u4)[9], const RowGeom<8>& g, int mb,
+                                           const double (*rp)[SNAP_JMAX + 2], bool on, double fc,
+                                           C2 (&acc)[45], C2* row4) {
+  if constexpr (J > 0) {
+    ui4_layers<J - 1>(u, u4, g, mb, rp, on, fc, acc, row4);
+    if constexpr (J == 8) {
+#pragma unroll
+      for (int i = 0; i < J; ++i) {
+        const int x = J - 1 - i;
+        const C2 v = u[i];
+        u4[x] = ((x + J / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+      }
+      u4[J] = C2{0.0, 0.0};
+    }
+    C2 du[9];
+    row_step<8, J, false>(u, du, g, mb, rp);
+    if (on && 2 * mb <= J) {
+#pragma unroll
+      for (int ma = 0; ma <= J; ++ma) {
+        C2& a = acc[J * (J + 1) / 2 + ma];
+        a.re = fma(fc, u[ma].re, a.re);
+        a.im = fma(fc, u[ma].im, a.im);
+      }
+    }
+    if constexpr (J == 8) {
+      row_update<8, 8>(u4, g, 4, rp);
+      if (on && mb == 3) {  // row 4 accumulates in the lane's own slot (shared memory)
+#pragma unroll
+        for (int ma = 0; ma <= 8; ++ma) {
+          row4[ma].re = fma(fc, u4[ma].re, row4[ma].re);
+          row4[ma].im = fma(fc, u4[ma].im, row4[ma].im);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(UI4_WARPS * 32)
+k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn, C2* __restrict__ utot) {
+  constexpr int TJ = 8, R = 4, P = 8;
+  extern __shared__ double smem[];
+  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ps = nh + 2;  // padded pair-slot stride
+  C2* part = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * P * ps;
+  stage_rootpq(rp);
+  const int64_t atom = (int64_t)blockIdx.x * UI4_WARPS + warp;
+  __syncthreads();
+  if (atom >= natoms) return;
+  const int64_t b = atom / N;
+  const int i = (int)(atom - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const int p = lane / R, mb = lane - p * R;
+  const int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  C2 acc[45];
+#pragma unroll
+  for (int k = 0; k < 45; ++k) acc[k] = C2{0.0, 0.0};
+  C2* row4 = part + p * ps + c_hoff[TJ] + 4 * (TJ + 1);
+  if (mb == 3)
+#pragma unroll
+    for (int k = 0; k <= TJ; ++k) row4[k] = C2{0.0, 0.0};
+  for (int s0 = 0; s0 < n; s0 += P) {
+    const int s = s0 + p;
+    const bool valid = s < n;
+    RowGeom<TJ> g;
+    double fc = 0.0;
+    if (valid) {
+      double dx, dy, dz;
+      pair_vec(qb, i, nb[s], box, dx, dy, dz);
+      PairGeom pg;
+      pair_geom(D, dx, dy, dz, pg, false);
+      g.a = pg.a;
+      g.b = pg.b;
+      fc = pg.fc;
+    } else {
+      g.a = C2{1.0, 0.0};
+      g.b = C2{0.0, 0.0};
+    }
+    C2 u[TJ + 1], u4[TJ + 1];
+#pragma unroll
+    for (int k = 0; k <= TJ; ++k) u[k] = u4[k] = C2{0.0, 0.0};
+    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
+    if (valid && mb == 0) acc[0].re += fc;  // J = 0
+    ui4_layers<TJ>(u, u4, g, mb, rp, valid, fc, acc, row4);
+  }
+  {  // each lane owns its (pair slot, rows): plain stores (every element of every slot is written)
+    C2* mypart = part + p * ps;
+#pragma unroll
+    for (int J = 0; J <= TJ; ++J)
+      if (2 * mb <= J)
+#pragma unroll
+        for (int ma = 0; ma <= J; ++ma) mypart[c_hoff[J] + mb * (J + 1) + ma] = acc[J * (J + 1) / 2 + ma];
+  }
+  __syncwarp();
+  C2* out = utot + atom * nh;
+  for (int t = lane; t < nh; t += 32) {
+    C2 a{0.0, 0.0};
+#pragma unroll
+    for (int pp = 0; pp < P; ++pp) {
+      a.re += part[pp * ps + t].re;
+      a.im += part[pp * ps + t].im;
+    }
+    int J = 0;
+    while (J < TJ && t >= c_hoff[J + 1]) ++J;
+    const int e = t - c_hoff[J];
+    const int mbb = e / (J + 1), maa = e - mbb * (J + 1);
+    if (maa == mbb) a.re += D.wself;
+    out[t] = a;
+  }
+}
+
+// ------------------------------------------------------------------ reverse-mode dE/dr, 4 lanes per pair
+// twojmax 8: lanes own half rows 0..3 of a pair (8 pairs per warp instead of 6);
+// row 4 exists only in layer 8, where it is born from row 3 of layer 7, so the
+// row-3 lane carries it (forward step, direct term, adjoint, and the adjoint of
+// the virtual row flowing back to row 3 stay inside that lane).  Balances the
+// lanes (rows 0..4 carry 45, 42, 35, 24, 9 elements; the row-3 lane now 33) and
+// stores only layers 0..7 (the backward never reads layer 8): 18.4 KB per warp.
 __device__ __forceinline__ double half_w(int J, int mb, int ma) {
   return (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
 }
@@ -2544,6 +2666,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_deidrj_adj<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_ui_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
   // register-resident kernels are instantiated for twojmax = 8 (PL_SNAP_RR=0 selects the
@@ -2562,7 +2685,15 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
       const char* e = getenv("PL_SNAP_UI");
       return !(e && e[0] == '0');  // 0: accumulate through shared memory every pair
     }();
-    if (ui_reg)
+    static const bool ui4 = [] {
+      const char* e = getenv("PL_SNAP_UI");
+      return !(e && (e[0] == '0' || e[0] == '1'));  // 0/1: 5 lanes per pair (smem / register rows)
+    }();
+    if (ui4 && S->tj == 8) {
+      const size_t sm4 = rp_bytes + sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2);
+      k_snap_ui_r4<<<(unsigned)((na + UI4_WARPS - 1) / UI4_WARPS), UI4_WARPS * 32, sm4, ctx->stream>>>(
+          D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.utot);
+    } else if (ui_reg)
       k_snap_ui_rr<8, true><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
                                                                           nl.maxn, buf.utot);
     else
