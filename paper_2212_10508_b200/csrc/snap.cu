@@ -2454,6 +2454,10 @@ struct AdjR4 {
 constexpr int ADJ4_WARPS = 2;
 constexpr int ADJ4_SLOTS = 36;  // layers 0..7
 
+// APW atoms per warp: their pair lists are concatenated so the 8 pair slots of
+// a round stay filled across the atom boundary (26 pairs per atom fill 4
+// rounds of 8 only to 81 %)
+template <int APW>
 __global__ void __launch_bounds__(ADJ4_WARPS * 32)
 k_snap_deidrj_adj4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
                    const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
@@ -2463,28 +2467,43 @@ k_snap_deidrj_adj4(SnapDev D, int64_t natoms, int N, Box box, const double* __re
   double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
   const int nh = D.nhalf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  C2* Y = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * nh;
-  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + ADJ4_WARPS * nh +
+  C2* Yw = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * APW * nh;
+  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + ADJ4_WARPS * APW * nh +
              warp * ADJ4_SLOTS * 32;
   stage_rootpq(rp);
-  const int64_t atom = (int64_t)blockIdx.x * ADJ4_WARPS + warp;
-  if (atom < natoms)
-    for (int t = lane; t < nh; t += 32) Y[t] = ylist[atom * nh + t];
+  const int64_t atom0 = ((int64_t)blockIdx.x * ADJ4_WARPS + warp) * APW;
+  int nat[APW];
+  int total = 0;
+#pragma unroll
+  for (int k = 0; k < APW; ++k) {
+    const int64_t a = atom0 + k;
+    nat[k] = a < natoms ? cnt[a] : 0;
+    total += nat[k];
+    if (a < natoms)
+      for (int t = lane; t < nh; t += 32) Yw[k * nh + t] = ylist[a * nh + t];
+  }
   __syncthreads();
-  if (atom >= natoms) return;
-  const int64_t b = atom / N;
-  const int i = (int)(atom - b * N);
-  const double* qb = q + b * (int64_t)N * 3;
+  if (atom0 >= natoms) return;
   const int p = lane / R, mb = lane - p * R;
-  const int n = cnt[atom];
-  const int32_t* nb = nbr + atom * maxn;
-  for (int s0 = 0; s0 < n; s0 += P) {
-    const int s = s0 + p;
-    const bool valid = s < n;
+  for (int s0 = 0; s0 < total; s0 += P) {
+    // pair slot -> (atom of the warp, neighbour slot)
+    int k = s0 + p, w = 0;
+#pragma unroll
+    for (int a = 0; a + 1 < APW; ++a)
+      if (w == a && k >= nat[a]) {
+        k -= nat[a];
+        w = a + 1;
+      }
+    const bool valid = s0 + p < total;
+    const int64_t atom = atom0 + w;
+    const int s = k;
+    const C2* Y = Yw + w * nh;
     PairGeom pg;
     if (valid) {
+      const int64_t b = atom / N;
+      const int i = (int)(atom - b * N);
       double dx, dy, dz;
-      pair_vec(qb, i, nb[s], box, dx, dy, dz);
+      pair_vec(q + b * (int64_t)N * 3, i, nbr[atom * maxn + s], box, dx, dy, dz);
       pair_geom(D, dx, dy, dz, pg, true);
     } else {
       pair_geom(D, 1.0, 0.0, 0.0, pg, true);
@@ -2665,7 +2684,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_adj4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_adj4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_adj4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_ui_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
@@ -2758,9 +2778,18 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     return !(e && (e[0] == '2' || e[0] == '4'));  // 2: 5 lanes per pair ([slot][lane] history)
   }();
   if (rr && adj_env && adj4 && S->tj == 8) {
-    size_t sm = rp_bytes + sizeof(C2) * ADJ4_WARPS * (D.nhalf + ADJ4_SLOTS * 32);
-    k_snap_deidrj_adj4<<<(unsigned)((na + ADJ4_WARPS - 1) / ADJ4_WARPS), ADJ4_WARPS * 32, sm, ctx->stream>>>(
-        D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
+    static const int apw = [] {
+      const char* e = getenv("PL_SNAP_ADJ_APW");
+      return (e && e[0] == '1') ? 1 : 2;
+    }();
+    const size_t sm = rp_bytes + sizeof(C2) * ADJ4_WARPS * (apw * D.nhalf + ADJ4_SLOTS * 32);
+    const unsigned grid = (unsigned)((na + ADJ4_WARPS * apw - 1) / (ADJ4_WARPS * apw));
+    if (apw == 2)
+      k_snap_deidrj_adj4<2><<<grid, ADJ4_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
+                                                                        buf.y, buf.dedr);
+    else
+      k_snap_deidrj_adj4<1><<<grid, ADJ4_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
+                                                                        buf.y, buf.dedr);
   } else if (rr && adj_env && adj_hl == 1) {
     size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + yi5::hoff(9) * ADJ_P);
     k_snap_deidrj_adj<8, 1><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
