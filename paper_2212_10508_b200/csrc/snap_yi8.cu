@@ -57,9 +57,15 @@ struct Cx {
   double re, im;
 };
 
+// The middle row (2 mb = J): the terms of mb1 and X - mb1 are images of each
+// other under U[J-ma][J-mb] = (-1)^(ma+mb) conj(U[ma][mb]) (CG included), so
+// only mb1 <= X/2 is summed (the self-image X/2 with weight 1/2, exact) over the
+// whole band ma = 0..J; the kernel folds the row's upper half onto the lower
+// half once all items are in (fold_middle_rows).
 template <int X>
-__device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int SH, int jtop, int mb, int boff,
+__device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int SH, int J, bool mid, int mb, int boff,
                                       double cy, Cx* __restrict__ yrow) {
+  const int jtop = J;
   constexpr int S = X + yib::TJ;
   constexpr int FX = yib::foff(X);
   Cx d[S + 1];
@@ -67,11 +73,11 @@ __device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int SH, 
   for (int s = 0; s <= S; ++s) d[s] = Cx{0.0, 0.0};
   const double* cb = c_box + boff;  // [Y+1][X+1]: cb[b * (X + 1) + a] = C(ma = a + b - SH, ma1 = a)
   const int FY = yib::foff(Y);
-  const int lo = max(0, mb + SH - Y), hi = min(X, mb + SH);
+  const int lo = max(0, mb + SH - Y), hi = mid ? X / 2 : min(X, mb + SH);
 #pragma unroll 1
   for (int mb1 = lo; mb1 <= hi; ++mb1) {
     const int mb2 = mb + SH - mb1;
-    const double cbv = cb[mb2 * (X + 1) + mb1];  // C(mb, mb1)
+    const double cbv = (mid && 2 * mb1 == X) ? 0.5 * cb[mb2 * (X + 1) + mb1] : cb[mb2 * (X + 1) + mb1];  // C(mb, mb1)
     const Cx* px = Ul + (FX + mb1 * (X + 1)) * yib::ATOMS;
     const Cx* py = Ul + (FY + mb2 * (Y + 1)) * yib::ATOMS;
     Cx ux[X + 1];
@@ -153,21 +159,40 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
     const int code = c_box_code[tid];
     const int X = code / 100, Y = (code / 10) % 10;
     const int SH = (X + Y - J) / 2;
-    const int jtop = (2 * mb == J) ? J / 2 : J;
+    const bool mid = (2 * mb == J);
     const int boff = c_box_off[tid];
     const double cy = coef[tid];
     Cx* yrow = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + lane;
     switch (X) {
-      case 0: box_x<0>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
-      case 1: box_x<1>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
-      case 2: box_x<2>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
-      case 3: box_x<3>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
-      case 4: box_x<4>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
-      case 5: box_x<5>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
-      case 6: box_x<6>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
-      case 7: box_x<7>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
-      default: box_x<8>(Ul, Y, SH, jtop, mb, boff, cy, yrow); break;
+      case 0: box_x<0>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+      case 1: box_x<1>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+      case 2: box_x<2>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+      case 3: box_x<3>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+      case 4: box_x<4>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+      case 5: box_x<5>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+      case 6: box_x<6>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+      case 7: box_x<7>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+      default: box_x<8>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
     }
+  }
+  __syncthreads();
+  // middle rows: Y[ma] += (-1)^(J/2+ma) conj(Y[J-ma]) for ma <= J/2 (the images of
+  // the mb1 > X/2 terms), then the upper half is cleared
+  for (int t = threadIdx.x; t < 5 * yib::ATOMS; t += blockDim.x) {
+    const int J = 2 * (t >> 5), at = t & 31, mb = J / 2;
+    if (S > 1 && c_box_rowsplit[V][yib::rowoff(J) + mb] != split) continue;
+    Cx* y = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + at;
+    for (int ma = 0; ma < mb; ++ma) {
+      Cx lo = y[ma * yib::ATOMS];
+      const Cx up = y[(J - ma) * yib::ATOMS];
+      const bool neg = ((mb + ma) & 1) != 0;
+      lo.re += neg ? -up.re : up.re;
+      lo.im += neg ? up.im : -up.im;
+      y[ma * yib::ATOMS] = lo;
+      y[(J - ma) * yib::ATOMS] = Cx{0.0, 0.0};
+    }
+    Cx c = y[mb * yib::ATOMS];
+    y[mb * yib::ATOMS] = Cx{c.re + c.re, 0.0};
   }
   __syncthreads();
   // energy: E - beta0 is cubic in U and Y = dE/dU, so E = beta0 + (1/3) sum_J <U^J, Y^J>
