@@ -359,7 +359,8 @@ int snap_prepare(pl_pot* pot, const double* beta) {
           double c = 0.0;
           for (int tid : byJ[J]) {
             int x = code[tid] / 100, y = (code[tid] / 10) % 10, sh = (x + y - J) / 2;
-            for (int mb1 = 0; mb1 <= (2 * mb == J ? x / 2 : x); ++mb1)  // middle rows: half of mb1
+            const int mb1_hi = 2 * mb == J ? x / 2 : (x == y ? (mb + sh) / 2 : x);  // symmetry halvings
+            for (int mb1 = 0; mb1 <= mb1_hi; ++mb1)
               if (mb + sh - mb1 >= 0 && mb + sh - mb1 <= y) c += 7.0 * (x + 1) * (y + 1) + 2.0 * (x + y + 2) + 12.0;
             c += 60.0;
           }

@@ -73,11 +73,16 @@ __device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int SH, 
   for (int s = 0; s <= S; ++s) d[s] = Cx{0.0, 0.0};
   const double* cb = c_box + boff;  // [Y+1][X+1]: cb[b * (X + 1) + a] = C(ma = a + b - SH, ma1 = a)
   const int FY = yib::foff(Y);
-  const int lo = max(0, mb + SH - Y), hi = mid ? X / 2 : min(X, mb + SH);
+  // X = Y (other rows): the (mb1, ma1) and (mb2, ma2) factors swap roles with an
+  // unchanged CG product, so mb1 <= mb2 is summed with weight 2 off the diagonal
+  const bool swap = (Y == X) && !mid;
+  const int lo = max(0, mb + SH - Y);
+  const int hi = mid ? X / 2 : (swap ? (mb + SH) / 2 : min(X, mb + SH));
 #pragma unroll 1
   for (int mb1 = lo; mb1 <= hi; ++mb1) {
     const int mb2 = mb + SH - mb1;
-    const double cbv = (mid && 2 * mb1 == X) ? 0.5 * cb[mb2 * (X + 1) + mb1] : cb[mb2 * (X + 1) + mb1];  // C(mb, mb1)
+    const double w = mid ? (2 * mb1 == X ? 0.5 : 1.0) : (swap ? (mb1 == mb2 ? 1.0 : 2.0) : 1.0);
+    const double cbv = w * cb[mb2 * (X + 1) + mb1];  // w C(mb, mb1), w exact
     const Cx* px = Ul + (FX + mb1 * (X + 1)) * yib::ATOMS;
     const Cx* py = Ul + (FY + mb2 * (Y + 1)) * yib::ATOMS;
     Cx ux[X + 1];
