@@ -145,6 +145,38 @@ def test_snap_vs_oracle(pl, ncell, count):
         np.testing.assert_allclose(V[b], v, rtol=1e-10, atol=1e-10 * np.abs(v).max())
 
 
+_AB_SCRIPT = """
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2212_10508_b200 import tungsten as W
+q0, box = W.bcc_sia(4)
+rs = np.random.default_rng(5)
+Q = torch.from_numpy(q0[None] + 0.1 * rs.normal(size=(6, q0.shape[0]))).cuda()
+E, G, V = (x.cpu().numpy() for x in W.make_snap(q0.shape[0] // 3, box).evaluate(Q, True, True, True))
+np.savez(sys.argv[1], E=E, G=G, V=V)
+"""
+
+
+def test_snap_pair_form_matches_ordered_form(pl, tmp_path):
+    """k_snap_deidrj_pair (one adjoint sweep per unordered pair with
+    Y_i + Y_k^dagger, U(-r) = U(r)^dagger) against k_snap_deidrj_adj4 (one sweep
+    per ordered pair): same energies, forces and virials to 1e-12."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("0", "1"):
+        f = str(tmp_path / f"ab{mode}.npz")
+        env = dict(os.environ, PL_SNAP_PAIR=mode)
+        subprocess.run([sys.executable, "-c", _AB_SCRIPT, f], cwd=root, env=env, check=True)
+        out[mode] = np.load(f)
+    a, b = out["0"], out["1"]
+    np.testing.assert_array_equal(a["E"], b["E"])  # energies do not depend on the force form
+    np.testing.assert_allclose(b["G"], a["G"], rtol=1e-12, atol=1e-12 * np.abs(a["G"]).max())
+    np.testing.assert_allclose(b["V"], a["V"], rtol=1e-12, atol=1e-12 * np.abs(a["V"]).max())
+
+
 def test_snap_invariances_on_device(pl):
     """Sum F = 0, rotation invariance of E (cluster in a large box), FD gradient."""
     from paper_2212_10508_b200.potentials import SNAP
