@@ -2315,14 +2315,15 @@ __device__ __forceinline__ double half_w(int J, int mb, int ma) {
 // the pair form Y_i + Y_k^dagger (see k_snap_deidrj_pair)
 struct YSmem {
   const C2* y;
-  __device__ __forceinline__ C2 operator()(int off) const { return y[off]; }
+  __device__ __forceinline__ C2 operator()(int J, int row, int x) const { return y[c_hoff[J] + row * (J + 1) + x]; }
 };
 struct YPair {
   const C2* y;   // Y_i, shared memory
   const C2* yt;  // Y_k^dagger, global
-  __device__ __forceinline__ C2 operator()(int off) const {
-    const double2 t = __ldg(reinterpret_cast<const double2*>(yt) + off);
-    const C2 a = y[off];
+  __device__ __forceinline__ C2 operator()(int J, int row, int x) const {
+    // yt is column-interleaved: [J][x][row], so the 4 row lanes of a pair read 64 contiguous bytes
+    const double2 t = __ldg(reinterpret_cast<const double2*>(yt) + c_hoff[J] + x * (J / 2 + 1) + row);
+    const C2 a = y[c_hoff[J] + row * (J + 1) + x];
     return C2{a.re + t.x, a.im + t.y};
   }
 };
@@ -2351,22 +2352,20 @@ struct AdjR4 {
       if constexpr (J == TJ) row_update<TJ, TJ>(u4, g, TJ / 2, rp);
     }
     if (2 * mb <= J) {
-      const int yo = c_hoff[J] + mb * (J + 1);
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
         if constexpr (J < TJ) hist[(J * (J + 1) / 2 + ma) * 32 + lane] = u[ma];
         if constexpr (!LAZY) {
-          const C2 y = Y(yo + ma);
+          const C2 y = Y(J, mb, ma);
           F += half_w(J, mb, ma) * (u[ma].re * y.re + u[ma].im * y.im);
         }
       }
     }
     if constexpr (J == TJ && !LAZY) {
       if (mb == TJ / 2 - 1) {
-        const int yo = c_hoff[J] + (TJ / 2) * (J + 1);
 #pragma unroll
         for (int ma = 0; ma <= J; ++ma) {
-          const C2 y = Y(yo + ma);
+          const C2 y = Y(J, TJ / 2, ma);
           F += half_w(J, TJ / 2, ma) * (u4[ma].re * y.re + u4[ma].im * y.im);
         }
       }
@@ -2464,11 +2463,10 @@ struct AdjR4 {
         }
       }
       if (2 * mb <= J - 1) {
-        const int yo = c_hoff[J - 1] + mb * J;
 #pragma unroll
         for (int x = 0; x < J; ++x) {
           const double w = half_w(J - 1, mb, x);
-          const C2 y = Y(yo + x);
+          const C2 y = Y(J - 1, mb, x);
           if constexpr (LAZY) F += w * (up[x].re * y.re + up[x].im * y.im);
           G[x].re += w * y.re;
           G[x].im += w * y.im;
@@ -2601,7 +2599,8 @@ __device__ __forceinline__ C2 y_full(const C2* y, int J, int r, int c) {
   return y[c_hoff[J] + r * (J + 1) + c];
 }
 
-// Y^dagger in half-row form: yt[J][mb][ma] = conj(Y[J][ma][mb])
+// Y^dagger, half rows stored column-interleaved: yt[J][ma][mb] = conj(Y[J][ma][mb])
+// for mb <= J/2 (element (mb, ma) of the Y^dagger half rows)
 __global__ void k_snap_ytrans(int64_t natoms, int nh, int tj, const C2* __restrict__ y, C2* __restrict__ yt) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= natoms * nh) return;
@@ -2612,7 +2611,7 @@ __global__ void k_snap_ytrans(int64_t natoms, int nh, int tj, const C2* __restri
   const int e = h - c_hoff[J];
   const int mb = e / (J + 1), ma = e - mb * (J + 1);
   const C2 v = y_full(y + atom * nh, J, ma, mb);
-  yt[t] = C2{v.re, -v.im};
+  yt[atom * nh + c_hoff[J] + ma * (J / 2 + 1) + mb] = C2{v.re, -v.im};
 }
 
 constexpr int PAIR_WARPS = 4;  // 2 CTAs of 4 warps per SM (shared memory), neighbouring atoms share an SM
@@ -2621,9 +2620,13 @@ constexpr int PAIR_WARPS = 4;  // 2 CTAs of 4 warps per SM (shared memory), neig
 // list), the owned lists of the warp's atoms are concatenated into rounds of 8
 // pair slots.  h_ik goes to dedr[i, s] (slots k < i are not written).  Y_i is
 // staged in shared memory, Y_k^dagger read through L1/L2; F is accumulated in
-// the backward sweep (AdjR4 LAZY) so every Y element is read once.  Measured
-// (1025 atoms x 64): 1.53 ms vs 1.78 ms for adj4 at 0.6x its instructions; the
-// global Y_k^dagger loads (long-scoreboard stalls) hold the issue rate at 28 %.
+// the backward sweep (AdjR4 LAZY) so every Y element is read once; Y^dagger is
+// column-interleaved so the 4 row lanes of a pair read 64 contiguous bytes.
+// Measured (1025 atoms x 64): 1.50 ms vs 1.78 ms for adj4 at 0.6x its
+// instructions; the global Y_k^dagger loads (long-scoreboard stalls) hold the
+// issue rate at 28 %.  Staging Y_k^dagger in shared memory (cp.async during the
+// forward pass, or Y_i + Y_k^dagger per slot) costs occupancy (5 warps/SM) and
+// measured slower (1.88 / 2.16 ms), as did L1 prefetch one layer ahead (1.63 ms).
 template <int APW, int NWB>
 __global__ void __launch_bounds__(NWB * 32)
 k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
@@ -2700,11 +2703,10 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
     __syncwarp();
     C2 G[TJ + 1], G4[TJ + 1];
     {
-      const int yo = c_hoff[TJ] + mb * (TJ + 1), y4 = c_hoff[TJ] + (TJ / 2) * (TJ + 1);
 #pragma unroll
       for (int x = 0; x <= TJ; ++x) {
-        G[x] = Y(yo + x);
-        G4[x] = (mb == TJ / 2 - 1) ? Y(y4 + x) : C2{0.0, 0.0};
+        G[x] = Y(TJ, mb, x);
+        G4[x] = (mb == TJ / 2 - 1) ? Y(TJ, TJ / 2, x) : C2{0.0, 0.0};
       }
     }
 #pragma unroll
