@@ -263,7 +263,11 @@ def run_ours(args, rank, world, local_rank):
             parareal["ranks"] = world
 
     if rank == 0:
-        launches_per_step = (5 + 7 * L)  # SNAP eval = neigh + ui + yi + deidrj + gather; + open/close
+        # L+1 SNAP evaluations per window batch, each: neighbours (cell lists at >= 512
+        # atoms and >= 3 cells per axis: count, scan, fill, list; else one brute-force
+        # kernel), ui, yi, ytrans, deidrj (pair form), gather; + open/close per substep
+        cells = n >= 512 and min(inp["box"]) / 4.73 >= 3
+        launches_per_step = (L + 1) * ((4 if cells else 1) + 5) + 2 * L
         line = {
             "metric": "SNAP Langevin atom-steps/s over batched parareal slices",
             "value": value, "unit": "atom-steps/s", "n_gpus": world, "steps": args.steps,
