@@ -146,8 +146,9 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
   }
   prof_mark(st, ST_NEIGH, true);
   if (!cells_ok) {
-    dim3 grid((N + NB_THREADS - 1) / NB_THREADS, (unsigned)B);
-    k_neigh_brute<<<grid, NB_THREADS, 0, st>>>(B, N, box, rc2, maxn, q, out->nbr, out->cnt, out->overflow);
+    const int64_t warps = B * N;
+    k_neigh_brute_w<<<(unsigned)((warps * 32 + NB_THREADS - 1) / NB_THREADS), NB_THREADS, 0, st>>>(
+        B, N, box, rc2, maxn, q, out->nbr, out->cnt, out->overflow);
     PL_CHECK_LAUNCH();
   } else {
     int64_t cells = (int64_t)g.n[0] * g.n[1] * g.n[2];

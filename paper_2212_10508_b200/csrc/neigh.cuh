@@ -85,6 +85,41 @@ k_neigh_brute(int64_t B, int N, Box box, double rc2, int maxn, const double* __r
   }
 }
 
+// one warp per atom i: lanes test 32 candidates j at a time, hits are written
+// in ascending j by ballot/popc (the same list as k_neigh_brute, for small
+// systems where one thread per atom leaves the latency of N serial tests)
+static __global__ void __launch_bounds__(NB_THREADS)
+k_neigh_brute_w(int64_t B, int N, Box box, double rc2, int maxn, const double* __restrict__ q,
+                int32_t* __restrict__ nbr, int32_t* __restrict__ cnt, int* __restrict__ overflow) {
+  const int64_t t = (blockIdx.x * (int64_t)NB_THREADS + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= B * N) return;
+  const int64_t b = t / N;
+  const int i = (int)(t - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const double xi = qb[3 * i], yi = qb[3 * i + 1], zi = qb[3 * i + 2];
+  int32_t* my = nbr + t * (int64_t)maxn;
+  int c = 0;
+  for (int j0 = 0; j0 < N; j0 += 32) {
+    const int j = j0 + lane;
+    bool hit = false;
+    if (j < N && j != i) {
+      const double dx = min_image(sub(qb[3 * j], xi), box.L[0], box.inv[0]);
+      const double dy = min_image(sub(qb[3 * j + 1], yi), box.L[1], box.inv[1]);
+      const double dz = min_image(sub(qb[3 * j + 2], zi), box.L[2], box.inv[2]);
+      hit = r2_exact(dx, dy, dz) < rc2;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    const int slot = c + __popc(m & ((1u << lane) - 1u));
+    if (hit && slot < maxn) my[slot] = j;
+    c += __popc(m);
+  }
+  if (lane == 0) {
+    cnt[t] = c < maxn ? c : maxn;
+    if (c > maxn) atomicExch(overflow, 1);
+  }
+}
+
 // displacement r_j - r_i under the minimum image (same ops as the builder)
 __device__ __forceinline__ void pair_vec(const double* qb, int i, int j, const Box& box, double& dx,
                                          double& dy, double& dz) {

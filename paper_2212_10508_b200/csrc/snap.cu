@@ -2742,6 +2742,72 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
   }
 }
 
+// gather of the pair form, one warp per atom (lanes over neighbour slots, the
+// reverse-slot searches in parallel, fixed-order shuffle tree):
+// grad_i = -sum_{k>i} h_ik + sum_{k<i} h_ki; the owner books the pair virial
+__global__ void __launch_bounds__(128)
+k_snap_gather_pair_w(int64_t natoms, int N, Box box, const double* __restrict__ q,
+                     const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+                     const double* __restrict__ dedr, double* __restrict__ grad, double* __restrict__ vatom) {
+  const int64_t atom = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (atom >= natoms) return;
+  const int64_t b = atom / N;
+  const int a = (int)(atom - b * N);
+  const int n = cnt[atom];
+  const int32_t* nb = nbr + atom * maxn;
+  const double* qb = q + b * (int64_t)N * 3;
+  double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // g[3], vir[6]
+  for (int s = lane; s < n; s += 32) {
+    const int k = nb[s];
+    if (k > a) {
+      const double* h = dedr + (atom * maxn + s) * 3;
+      v[0] -= h[0];
+      v[1] -= h[1];
+      v[2] -= h[2];
+      if (vatom) {
+        double dx, dy, dz;
+        pair_vec(qb, a, k, box, dx, dy, dz);
+        v[3] -= h[0] * dx;
+        v[4] -= h[1] * dy;
+        v[5] -= h[2] * dz;
+        v[6] -= 0.5 * (h[0] * dy + h[1] * dx);
+        v[7] -= 0.5 * (h[0] * dz + h[2] * dx);
+        v[8] -= 0.5 * (h[1] * dz + h[2] * dy);
+      }
+    } else {
+      const int64_t katom = b * N + k;
+      const int32_t* kl = nbr + katom * maxn;
+      int lo = 0, hi = cnt[katom] - 1, sk = -1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const int val = kl[mid];
+        if (val == a) { sk = mid; break; }
+        if (val < a) lo = mid + 1; else hi = mid - 1;
+      }
+      if (sk >= 0) {
+        const double* h = dedr + (katom * maxn + sk) * 3;
+        v[0] += h[0];
+        v[1] += h[1];
+        v[2] += h[2];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 9; ++c)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+  if (lane == 0) {
+    if (grad) {
+      grad[3 * atom] = v[0];
+      grad[3 * atom + 1] = v[1];
+      grad[3 * atom + 2] = v[2];
+    }
+    if (vatom)
+      for (int c = 0; c < 6; ++c) vatom[6 * atom + c] = v[3 + c];
+  }
+}
+
 // gather of the pair form: grad_i = -sum_{k>i} h_ik + sum_{k<i} h_ki; the
 // owner (smaller index) books the pair's virial -h_ik (x) r_ik
 __global__ void k_snap_gather_pair(int64_t natoms, int N, Box box, const double* __restrict__ q,
@@ -3086,7 +3152,7 @@ int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double
   Box box = make_box(pot->box);
   prof_mark(ctx->stream, ST_GATHER, true);
   if (buf.pair)
-    k_snap_gather_pair<<<(unsigned)((na + 127) / 128), 128, 0, ctx->stream>>>(
+    k_snap_gather_pair_w<<<(unsigned)((na * 32 + 127) / 128), 128, 0, ctx->stream>>>(
         na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr);
   else
     k_snap_gather<<<(unsigned)((na + 127) / 128), 128, 0, ctx->stream>>>(
