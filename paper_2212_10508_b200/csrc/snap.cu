@@ -2659,9 +2659,19 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
       }
       lo[k] = below;
       nat[k] = c - below;
-      for (int t = lane; t < nh; t += 32) Yw[k * nh + t] = ylist[a * nh + t];
     }
     total += nat[k];
+  }
+  {  // the warp's Y rows are one contiguous range: all loads in flight before the stores
+    constexpr int NL = (APW * 155 + 31) / 32;  // twojmax 8: nh = 155
+    const int nel = (int)min((int64_t)APW, natoms - atom0) * nh;
+    C2 tmp[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (lane + 32 * j < nel) tmp[j] = ylist[atom0 * nh + lane + 32 * j];
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (lane + 32 * j < nel) Yw[lane + 32 * j] = tmp[j];
   }
   __syncthreads();
   if (atom0 >= natoms) return;

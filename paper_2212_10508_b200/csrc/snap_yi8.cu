@@ -134,6 +134,30 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
   const int split = (int)(blockIdx.x - blk * S);
   const int64_t a0 = blk * yib::ATOMS;
   const int na_blk = (int)min((int64_t)yib::ATOMS, natoms - a0);
+  // the block's U_tot half rows are one contiguous range: one bulk async copy
+  // (TMA engine) into the Y area, which is free until the expansion is done
+  __shared__ __align__(8) uint64_t mbar;
+  const Cx* Ust = reinterpret_cast<const Cx*>(Ys);
+  {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&mbar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned bytes = (unsigned)(sizeof(Cx) * yib::NHALF * na_blk);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              (unsigned)__cvta_generic_to_shared(Ys)),
+          "l"(utot + a0 * yib::NHALF), "r"(bytes), "r"(bar)
+          : "memory");
+    }
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra W;\n}" ::"r"(bar)
+        : "memory");
+  }
   for (int t = threadIdx.x; t < yib::NFULL * yib::ATOMS; t += blockDim.x) {
     const int at = t & (yib::ATOMS - 1), f = t >> 5;
     int J = 0;
@@ -141,7 +165,7 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
     const int e = f - yib::foff(J), mb = e / (J + 1), ma = e - mb * (J + 1);
     Cx v{0.0, 0.0};
     if (at < na_blk) {
-      const Cx* ua = utot + (a0 + at) * yib::NHALF + yib::hoff(J);
+      const Cx* ua = Ust + at * yib::NHALF + yib::hoff(J);
       if (2 * mb <= J) {
         v = ua[mb * (J + 1) + ma];
       } else {
@@ -151,6 +175,7 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
     }
     Uf[f * yib::ATOMS + at] = v;
   }
+  __syncthreads();  // staged U_tot consumed before Y is cleared
   for (int t = threadIdx.x; t < yib::NHALF * yib::ATOMS; t += blockDim.x) Ys[t] = Cx{0.0, 0.0};
   for (int t = threadIdx.x; t < BOX_ROWS * yib::ATOMS; t += blockDim.x) erow[t] = 0.0;
   __syncthreads();
@@ -285,12 +310,13 @@ int snap_box_variants(int* nw, int* ns) {
 template <int NW, int V, int S>
 static cudaError_t box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const void* utot,
                               void* ylist, double* eatom, double* erow_g) {
+  const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * BOX_ROWS * yib::ATOMS;
   static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_snap_yi_box<NW, V, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (!attr) {  // exactly the dynamic size: the static mbarrier counts against the 227 KB too
+    cudaError_t e = cudaFuncSetAttribute(k_snap_yi_box<NW, V, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
-  const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * BOX_ROWS * yib::ATOMS;
   const unsigned grid = (unsigned)(S * ((natoms + yib::ATOMS - 1) / yib::ATOMS));
   k_snap_yi_box<NW, V, S><<<grid, NW * 32, sm, st>>>(natoms, beta0, coef, (const Cx*)utot, (Cx*)ylist, eatom,
                                                      erow_g);
