@@ -2233,6 +2233,10 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ps = nh + 2;  // padded pair-slot stride
   C2* part = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * P * ps;
+  // per-pair (a, b, fc) of the whole list, one lane per pair (instead of the 4 row
+  // lanes of a slot recomputing it every round)
+  double* geo = reinterpret_cast<double*>(reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) +
+                                          UI4_WARPS * P * ps) + warp * SNAP_MAXN * 5;
   stage_rootpq(rp);
   const int64_t atom = (int64_t)blockIdx.x * UI4_WARPS + warp;
   __syncthreads();
@@ -2250,19 +2254,25 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   if (mb == 3)
 #pragma unroll
     for (int k = 0; k <= TJ; ++k) row4[k] = C2{0.0, 0.0};
+  for (int j = lane; j < n; j += 32) {
+    double dx, dy, dz;
+    pair_vec(qb, i, nb[j], box, dx, dy, dz);
+    PairGeom pg;
+    pair_geom(D, dx, dy, dz, pg, false);
+    double* o = geo + 5 * j;
+    o[0] = pg.a.re; o[1] = pg.a.im; o[2] = pg.b.re; o[3] = pg.b.im; o[4] = pg.fc;
+  }
+  __syncwarp();
   for (int s0 = 0; s0 < n; s0 += P) {
     const int s = s0 + p;
     const bool valid = s < n;
     RowGeom<TJ> g;
     double fc = 0.0;
     if (valid) {
-      double dx, dy, dz;
-      pair_vec(qb, i, nb[s], box, dx, dy, dz);
-      PairGeom pg;
-      pair_geom(D, dx, dy, dz, pg, false);
-      g.a = pg.a;
-      g.b = pg.b;
-      fc = pg.fc;
+      const double* o = geo + 5 * s;
+      g.a = C2{o[0], o[1]};
+      g.b = C2{o[2], o[3]};
+      fc = o[4];
     } else {
       g.a = C2{1.0, 0.0};
       g.b = C2{0.0, 0.0};
@@ -3038,7 +3048,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
       return !(e && (e[0] == '0' || e[0] == '1'));  // 0/1: 5 lanes per pair (smem / register rows)
     }();
     if (ui4 && S->tj == 8) {
-      const size_t sm4 = rp_bytes + sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2);
+      const size_t sm4 = rp_bytes + sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2) + sizeof(double) * UI4_WARPS * SNAP_MAXN * 5;
       k_snap_ui_r4<<<(unsigned)((na + UI4_WARPS - 1) / UI4_WARPS), UI4_WARPS * 32, sm4, ctx->stream>>>(
           D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.utot);
     } else if (ui_reg)
