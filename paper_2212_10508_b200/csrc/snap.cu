@@ -686,6 +686,18 @@ struct PairGeom {
   C2 a, b, da[3], db[3];
 };
 
+// d(a, b)/dr_k from the unit vector, sin/cos of the angle and 1/r
+__device__ __forceinline__ void pair_deriv(double kappa, const double (&u)[3], double s, double c, double inv,
+                                           C2 (&da)[3], C2 (&db)[3]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double dxk = (k == 0) - u[0] * u[k], dyk = (k == 1) - u[1] * u[k];
+    double dzk = (k == 2) - u[2] * u[k];
+    da[k] = C2{-s * kappa * u[k], -(c * kappa * u[k] * u[2] + s * dzk * inv)};
+    db[k] = C2{c * kappa * u[k] * u[1] + s * dyk * inv, -(c * kappa * u[k] * u[0] + s * dxk * inv)};
+  }
+}
+
 __device__ __forceinline__ void pair_geom(const SnapDev& D, double dx, double dy, double dz, PairGeom& g,
                                           bool with_deriv) {
   double r = sqrt(dx * dx + dy * dy + dz * dz);
@@ -706,15 +718,7 @@ __device__ __forceinline__ void pair_geom(const SnapDev& D, double dx, double dy
     g.fc = 1.0;
     g.dfc = 0.0;
   }
-  if (with_deriv) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      double dxk = (k == 0) - g.u[0] * g.u[k], dyk = (k == 1) - g.u[1] * g.u[k];
-      double dzk = (k == 2) - g.u[2] * g.u[k];
-      g.da[k] = C2{-s * kappa * g.u[k], -(c * kappa * g.u[k] * g.u[2] + s * dzk * inv)};
-      g.db[k] = C2{c * kappa * g.u[k] * g.u[1] + s * dyk * inv, -(c * kappa * g.u[k] * g.u[0] + s * dxk * inv)};
-    }
-  }
+  if (with_deriv) pair_deriv(kappa, g.u, s, c, inv, g.da, g.db);
 }
 
 // element (ma, mb) of layer Jp = J-1 from its half-row buffer (row length J);
@@ -2625,6 +2629,7 @@ __global__ void k_snap_ytrans(int64_t natoms, int nh, int tj, const C2* __restri
 }
 
 constexpr int PAIR_WARPS = 4;  // 2 CTAs of 4 warps per SM (shared memory), neighbouring atoms share an SM
+constexpr int PAIR_GEO = 12;   // doubles of geometry per pair (k_snap_deidrj_pair)
 
 // APW atoms per warp; atom i owns its neighbours k > i (a suffix of its sorted
 // list), the owned lists of the warp's atoms are concatenated into rounds of 8
@@ -2650,6 +2655,13 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
   C2* Yw = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * APW * nh;
   C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + NWB * APW * nh +
              warp * ADJ4_SLOTS * 32;
+  // geometry of 32 consecutive pairs (4 rounds), one lane per pair:
+  // a, b, fc, dfc, u[3], sin, cos, 1/r and the partner atom
+  double* gb = reinterpret_cast<double*>(reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) +
+                                         NWB * (APW * nh + ADJ4_SLOTS * 32)) + warp * 32 * PAIR_GEO;
+  int64_t* gk = reinterpret_cast<int64_t*>(reinterpret_cast<double*>(
+                    reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) +
+                    NWB * (APW * nh + ADJ4_SLOTS * 32)) + NWB * 32 * PAIR_GEO) + warp * 32;
   stage_rootpq(rp);
   const int64_t atom0 = ((int64_t)blockIdx.x * NWB + warp) * APW;
   int nat[APW], lo[APW];
@@ -2687,6 +2699,44 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
   if (atom0 >= natoms) return;
   const int p = lane / R, mb = lane - p * R;
   for (int s0 = 0; s0 < total; s0 += P) {
+    if ((s0 & 31) == 0) {  // geometry of pairs s0 .. s0 + 31
+      __syncwarp();
+      const int t = s0 + lane;
+      int kt = t, wt = 0;
+#pragma unroll
+      for (int a = 0; a + 1 < APW; ++a)
+        if (wt == a && kt >= nat[a]) {
+          kt -= nat[a];
+          wt = a + 1;
+        }
+      double* o = gb + lane * PAIR_GEO;
+      if (t < total) {
+        const int64_t at = atom0 + wt;
+        const int64_t bt = at / N;
+        const int kk = nbr[at * maxn + lo[wt] + kt];
+        double dx, dy, dz;
+        pair_vec(q + bt * (int64_t)N * 3, (int)(at - bt * N), kk, box, dx, dy, dz);
+        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+        const double inv = 1.0 / r;
+        const double u0 = dx * inv, u1 = dy * inv, u2 = dz * inv;
+        double sn, cs;
+        sincos(D.kappa * (r - D.rmin0), &sn, &cs);
+        double fc = 1.0, dfc = 0.0;
+        if (D.switchflag) {
+          double sa, ca;
+          sincos(D.pi_span * (r - D.rmin0), &sa, &ca);
+          fc = 0.5 * (ca + 1.0);
+          dfc = -D.half_pi_span * sa;
+        }
+        o[0] = cs; o[1] = -u2 * sn; o[2] = u1 * sn; o[3] = -u0 * sn;  // a, b
+        o[4] = fc; o[5] = dfc; o[6] = u0; o[7] = u1; o[8] = u2; o[9] = sn; o[10] = cs; o[11] = inv;
+        gk[lane] = bt * N + kk;
+      } else {
+        o[0] = 1.0; o[1] = 0.0; o[2] = 0.0; o[3] = 0.0;
+        gk[lane] = -1;
+      }
+      __syncwarp();
+    }
     int k = s0 + p, w = 0;
 #pragma unroll
     for (int a = 0; a + 1 < APW; ++a)
@@ -2696,24 +2746,11 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
       }
     const bool valid = s0 + p < total;
     const int64_t atom = atom0 + w;
-    const int64_t b = atom / N;
     const int s = lo[w] + k;
-    PairGeom pg;
-    int64_t katom = atom;  // invalid slots read the warp atom's own Y^dagger (weight 0)
-    if (valid) {
-      const int i = (int)(atom - b * N);
-      const int kk = nbr[atom * maxn + s];
-      katom = b * N + kk;
-      double dx, dy, dz;
-      pair_vec(q + b * (int64_t)N * 3, i, kk, box, dx, dy, dz);
-      pair_geom(D, dx, dy, dz, pg, true);
-    } else {
-      pair_geom(D, 1.0, 0.0, 0.0, pg, true);
-      pg.fc = 0.0;
-      pg.dfc = 0.0;
-    }
+    const double* go = gb + ((s0 & 31) + p) * PAIR_GEO;
+    const int64_t katom = valid ? gk[(s0 & 31) + p] : atom;  // invalid slots: own Y^dagger (weight 0)
     const YPair Y{Yw + w * nh, ytlist + katom * nh};
-    RowGeom<TJ> g{pg.a, pg.b, C2{0.0, 0.0}, C2{0.0, 0.0}};
+    RowGeom<TJ> g{C2{go[0], go[1]}, C2{go[2], go[3]}, C2{0.0, 0.0}, C2{0.0, 0.0}};
     C2 u[TJ + 1], u4[TJ + 1];
 #pragma unroll
     for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
@@ -2752,11 +2789,15 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
       }
     }
     if (valid && mb == 0) {
+      const double uu[3] = {go[6], go[7], go[8]};
+      C2 da[3], db[3];
+      pair_deriv(D.kappa, uu, go[9], go[10], go[11], da, db);
+      const double fc = go[4], dfc = go[5];
       double* o = dedr + (atom * maxn + s) * 3;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double re = pg.da[c].re * Sa.re - pg.da[c].im * Sa.im + pg.db[c].re * Sb.re - pg.db[c].im * Sb.im;
-        o[c] = pg.dfc * pg.u[c] * F + pg.fc * re;
+        const double re = da[c].re * Sa.re - da[c].im * Sa.im + db[c].re * Sb.re - db[c].im * Sb.im;
+        o[c] = dfc * uu[c] * F + fc * re;
       }
     }
   }
@@ -3123,7 +3164,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     const int64_t nel = na * D.nhalf;
     k_snap_ytrans<<<(unsigned)((nel + 255) / 256), 256, 0, ctx->stream>>>(na, D.nhalf, D.tj, buf.y, buf.yt);
     PL_CHECK_LAUNCH();
-    const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32);
+    const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
+                      (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32;
     const unsigned grid = (unsigned)((na + PAIR_WARPS * 2 - 1) / (PAIR_WARPS * 2));
     k_snap_deidrj_pair<2, PAIR_WARPS><<<grid, PAIR_WARPS * 32, sm, ctx->stream>>>(
         D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr);
