@@ -143,8 +143,8 @@ def heavy(L=1000):
     fl = bench.snap_flops_per_eval(snap, Q0)
     peak = bench.ctypes_peak()
     per_kernel = {}
-    for name, i, f in (("k_snap_ui_rr", 1, fl["ui"]), ("k_snap_yi_box", 2, fl["yi"]),
-                       ("k_snap_deidrj_adj", 3, fl["deidrj"])):
+    for name, i, f in (("k_snap_ui_r4", 1, fl["ui"]), ("k_snap_yi_box", 2, fl["yi"]),
+                       ("k_snap_deidrj_pair", 3, fl["deidrj"])):
         t_launch = ms[i] / max(cnt[i], 1) * 1e-3
         tf = f / t_launch / 1e12
         per_kernel[name] = {"ms_per_launch": round(ms[i] / max(cnt[i], 1), 4), "tflops": round(tf, 3),
