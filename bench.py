@@ -265,9 +265,12 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         # L+1 SNAP evaluations per window batch, each: neighbours (cell lists at >= 512
         # atoms and >= 3 cells per axis: count, scan, fill, list; else one brute-force
-        # kernel), ui, yi, ytrans, deidrj (pair form), gather; + open/close per substep
+        # kernel), ui, yi (+ k_box_energy when a batch has fewer 32-atom blocks than SMs
+        # and the Y rows are split over 2 CTAs), ytrans, deidrj (pair form), gather;
+        # + open/close per substep
         cells = n >= 512 and min(inp["box"]) / 4.73 >= 3
-        launches_per_step = (L + 1) * ((4 if cells else 1) + 5) + 2 * L
+        split = (slices * n + 31) // 32 < 148
+        launches_per_step = (L + 1) * ((4 if cells else 1) + 5 + (1 if split else 0)) + 2 * L
         line = {
             "metric": "SNAP Langevin atom-steps/s over batched parareal slices",
             "value": value, "unit": "atom-steps/s", "n_gpus": world, "steps": args.steps,

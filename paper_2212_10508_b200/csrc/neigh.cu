@@ -121,6 +121,86 @@ k_neigh_cell(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, const 
   if (nf > maxn) atomicExch(overflow, 1);
 }
 
+// one warp per atom: lane c < 27 owns neighbour cell c, a warp scan of the cell
+// counts flattens the ~200 candidates over the lanes (all loads of a pass in
+// flight together), hits are collected by ballot and ranked into ascending j
+// (the same list as k_neigh_cell, without one thread's serial 27-cell walk)
+constexpr int NC_WARPS = 4;
+__global__ void __launch_bounds__(NC_WARPS * 32)
+k_neigh_cell_w(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, const double* __restrict__ q,
+               const int32_t* __restrict__ cell_of_atom, const int32_t* __restrict__ cstart,
+               const int32_t* __restrict__ catoms, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
+               int* __restrict__ overflow) {
+  __shared__ int32_t s_found[NC_WARPS][CELL_MAXN];
+  __shared__ int32_t s_off[NC_WARPS][32], s_beg[NC_WARPS][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * NC_WARPS + warp;
+  if (t >= B * N) return;
+  const int64_t b = t / N;
+  const int i = (int)(t - b * N);
+  const double* qb = q + b * (int64_t)N * 3;
+  const int64_t cells = (int64_t)g.n[0] * g.n[1] * g.n[2];
+  const int c = (int)(cell_of_atom[t] - b * cells);
+  const int cx = c % g.n[0], cy = (c / g.n[0]) % g.n[1], cz = c / (g.n[0] * g.n[1]);
+  const double xi = qb[3 * i], yi = qb[3 * i + 1], zi = qb[3 * i + 2];
+  int beg = 0, num = 0;
+  if (lane < 27) {  // same cell order as k_neigh_cell (dz, dy, dx)
+    const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
+    const int ex = (cx + dx + g.n[0]) % g.n[0], ey = (cy + dy + g.n[1]) % g.n[1], ez = (cz + dz + g.n[2]) % g.n[2];
+    const int64_t cc = b * cells + (ez * g.n[1] + ey) * g.n[0] + ex;
+    beg = cstart[cc];
+    num = cstart[cc + 1] - beg;
+  }
+  int incl = num;  // inclusive warp scan of the cell counts
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  s_off[warp][lane] = incl - num;
+  s_beg[warp][lane] = beg;
+  __syncwarp();
+  int nf = 0;
+  for (int base = 0; base < total; base += 32) {
+    const int idx = base + lane;
+    bool hit = false;
+    int j = -1;
+    if (idx < total) {
+      int lo = 0, hi = 26;  // last cell with off <= idx (empty cells share offsets: take the last)
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_off[warp][mid] <= idx) lo = mid; else hi = mid - 1;
+      }
+      j = catoms[s_beg[warp][lo] + idx - s_off[warp][lo]];
+      if (j != i) {
+        const double ddx = min_image(sub(qb[3 * j], xi), box.L[0], box.inv[0]);
+        const double ddy = min_image(sub(qb[3 * j + 1], yi), box.L[1], box.inv[1]);
+        const double ddz = min_image(sub(qb[3 * j + 2], zi), box.L[2], box.inv[2]);
+        hit = r2_exact(ddx, ddy, ddz) < rc2;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    const int slot = nf + __popc(m & ((1u << lane) - 1u));
+    if (hit && slot < CELL_MAXN) s_found[warp][slot] = j;
+    nf += __popc(m);
+  }
+  __syncwarp();
+  const int keep = nf < CELL_MAXN ? nf : CELL_MAXN;
+  const int outn = keep < maxn ? keep : maxn;
+  int32_t* my = nbr + t * maxn;
+  for (int e = lane; e < keep; e += 32) {  // rank = number of smaller j (j distinct)
+    const int v = s_found[warp][e];
+    int r = 0;
+    for (int f = 0; f < keep; ++f) r += s_found[warp][f] < v;
+    if (r < outn) my[r] = v;
+  }
+  if (lane == 0) {
+    cnt[t] = outn;
+    if (nf > maxn) atomicExch(overflow, 1);
+  }
+}
+
 int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out) {
   int N = pot->n_atoms;
   size_t lists = sizeof(int32_t) * (size_t)B * N * maxn;
@@ -166,8 +246,13 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
     k_cell_count<<<ga, 256, 0, st>>>(B, N, box, g, q, cell_of_atom, ccount);
     k_cell_scan<<<1, 1024, 0, st>>>(nc, ccount, cstart, cfill);
     k_cell_fill<<<ga, 256, 0, st>>>(na, N, cell_of_atom, cfill, catoms);
-    k_neigh_cell<<<(unsigned)((na + 127) / 128), 128, 0, st>>>(B, N, box, g, rc2, maxn, q, cell_of_atom,
-                                                              cstart, catoms, out->nbr, out->cnt, out->overflow);
+    static const bool warp_cells = !getenv("PL_NEIGH_THREAD");
+    if (warp_cells)
+      k_neigh_cell_w<<<(unsigned)((na + NC_WARPS - 1) / NC_WARPS), NC_WARPS * 32, 0, st>>>(
+          B, N, box, g, rc2, maxn, q, cell_of_atom, cstart, catoms, out->nbr, out->cnt, out->overflow);
+    else
+      k_neigh_cell<<<(unsigned)((na + 127) / 128), 128, 0, st>>>(B, N, box, g, rc2, maxn, q, cell_of_atom,
+                                                                cstart, catoms, out->nbr, out->cnt, out->overflow);
     PL_CHECK_LAUNCH();
   }
   prof_mark(st, ST_NEIGH, false);
