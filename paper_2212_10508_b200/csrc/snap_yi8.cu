@@ -245,8 +245,11 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
   }
   __syncthreads();
   // rows owned by this CTA -> global (all rows when S = 1)
-  for (int t = threadIdx.x; t < na_blk * yib::NHALF; t += blockDim.x) {
-    const int at = t / yib::NHALF, h = t - at * yib::NHALF;
+  // 8 consecutive threads take 8 consecutive atoms of one element h: conflict-free
+  // shared-memory reads ([h][atom] layout), 16-byte global stores
+  for (int t = threadIdx.x; t < yib::ATOMS * yib::NHALF; t += blockDim.x) {
+    const int rest = t >> 3, h = rest % yib::NHALF, at = (rest / yib::NHALF) * 8 + (t & 7);
+    if (at >= na_blk) continue;
     if (S > 1) {
       int J = 0;
       while (J < yib::TJ && h >= yib::hoff(J + 1)) ++J;
