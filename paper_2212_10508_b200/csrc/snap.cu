@@ -2714,6 +2714,10 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
         const int64_t at = atom0 + wt;
         const int64_t bt = at / N;
         const int kk = nbr[at * maxn + lo[wt] + kt];
+        // the partner's Y^dagger (2.5 KB) towards L2 ahead of the rounds that read it
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ytlist + (bt * N + kk) * nh),
+                     "r"((unsigned)(nh * sizeof(C2)))
+                     : "memory");
         double dx, dy, dz;
         pair_vec(q + bt * (int64_t)N * 3, (int)(at - bt * N), kk, box, dx, dy, dz);
         const double r = sqrt(dx * dx + dy * dy + dz * dz);
