@@ -203,8 +203,8 @@ class DevicePropagator:
     def __call__(self, state: PhaseState, m: int) -> PhaseState:
         import torch
         dev = self.kernel.device
-        Q0 = torch.from_numpy(np.ascontiguousarray(state.q)[None]).to(dev)
-        P0 = torch.from_numpy(np.ascontiguousarray(state.p)[None]).to(dev)
+        Q0 = torch.from_numpy(np.array(state.q)[None]).to(dev)
+        P0 = torch.from_numpy(np.array(state.p)[None]).to(dev)
         Q1, P1, blow = self.kernel.run(Q0, P0, self.noise_all()[m:m + 1])
         b = int(blow.cpu()[0])
         if b:
@@ -303,8 +303,8 @@ class _DeviceRun:
         f64 = dict(dtype=torch.float64, device=dev)
         self.Q = torch.zeros((n + 1, d), **f64)
         self.P = torch.zeros((n + 1, d), **f64)
-        self.Q[0] = torch.from_numpy(np.ascontiguousarray(initial.q))
-        self.P[0] = torch.from_numpy(np.ascontiguousarray(initial.p))
+        self.Q[0] = torch.from_numpy(np.array(initial.q))
+        self.P[0] = torch.from_numpy(np.array(initial.p))
         self.prevQ = torch.zeros((n + 1, d), **f64)
         self.baseQ = torch.zeros((n, d), **f64)
         self.baseP = torch.zeros((n, d), **f64)
@@ -422,8 +422,8 @@ def sequential_propagate(initial: PhaseState, n_windows: int, pot, params: Lange
     d = initial.dim
     Q = torch.empty((n_windows + 1, d), dtype=torch.float64, device=k.device)
     P = torch.empty_like(Q)
-    Q[0] = torch.from_numpy(np.ascontiguousarray(initial.q))
-    P[0] = torch.from_numpy(np.ascontiguousarray(initial.p))
+    Q[0] = torch.from_numpy(np.array(initial.q))
+    P[0] = torch.from_numpy(np.array(initial.p))
     blows = torch.zeros(n_windows, dtype=torch.int32, device=k.device)
     for m in range(n_windows):
         _, _, b = k.run(Q[m:m + 1], P[m:m + 1], noise[m:m + 1], Q[m + 1:m + 2], P[m + 1:m + 2])
@@ -564,8 +564,8 @@ class _BatchRun:
         self.Q = torch.zeros((R, n + 1, d), **f64)
         self.P = torch.zeros((R, n + 1, d), **f64)
         for r, st in enumerate(initials):
-            self.Q[r, 0] = torch.from_numpy(np.ascontiguousarray(st.q))
-            self.P[r, 0] = torch.from_numpy(np.ascontiguousarray(st.p))
+            self.Q[r, 0] = torch.from_numpy(np.array(st.q))
+            self.P[r, 0] = torch.from_numpy(np.array(st.p))
         self.baseQ = torch.zeros((R, n, d), **f64)
         self.baseP = torch.zeros((R, n, d), **f64)
         self.jumpQ = torch.zeros((R, n, d), **f64)

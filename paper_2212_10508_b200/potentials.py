@@ -346,7 +346,7 @@ def minimize_batch(pot: Potential, starts, tol: float = 1e-8, max_iter: int = 50
     if pot.dimension is not None and d != pot.dimension:
         raise PotentialError(f"{type(pot).__name__} expects dimension {pot.dimension}, got {d}")
     ctx = _lib.context()
-    Xd = torch.from_numpy(np.ascontiguousarray(X)).to(torch.device("cuda", ctx.device))
+    Xd = torch.from_numpy(np.array(X)).to(torch.device("cuda", ctx.device))
     status = np.zeros(B, dtype=np.int32)
     iters = np.zeros(B, dtype=np.int64)
     energy = np.zeros(B, dtype=float)
