@@ -38,6 +38,25 @@ constexpr int hoff(int J) {
 }  // namespace yib
 
 __constant__ double c_box[yib::BOX_MAX];  // per triple: [Y+1][X+1]
+
+// full-matrix element f -> its source in the half-row storage: (src << 2) |
+// (mirrored << 1) | (odd ma + mb); U[ma][mb] for 2 mb > J is (-1)^(ma+mb)
+// conj(U[J-ma][J-mb]).  One warp expands one element f for its 32 atoms, so the
+// lookup is a uniform constant-bank read.
+struct BoxExpand {
+  int e[yib::NFULL];
+  constexpr BoxExpand() : e() {
+    int f = 0;
+    for (int J = 0; J <= yib::TJ; ++J)
+      for (int mb = 0; mb <= J; ++mb)
+        for (int ma = 0; ma <= J; ++ma, ++f) {
+          const bool mir = 2 * mb > J;
+          const int src = yib::hoff(J) + (mir ? (J - mb) * (J + 1) + (J - ma) : mb * (J + 1) + ma);
+          e[f] = (src << 2) | (mir ? 2 : 0) | ((ma + mb) & 1);
+        }
+  }
+};
+__constant__ BoxExpand c_box_exp = BoxExpand();
 __constant__ int c_box_off[yib::NT];
 __constant__ int c_box_code[yib::NT];         // X*100 + Y*10 + J
 constexpr int BOX_MAX_ITEMS = 400;            // (row, triple) pairs: 375 at twojmax 8
@@ -158,22 +177,14 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
         "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra W;\n}" ::"r"(bar)
         : "memory");
   }
-  for (int t = threadIdx.x; t < yib::NFULL * yib::ATOMS; t += blockDim.x) {
-    const int at = t & (yib::ATOMS - 1), f = t >> 5;
-    int J = 0;
-    while (J < yib::TJ && f >= yib::foff(J + 1)) ++J;
-    const int e = f - yib::foff(J), mb = e / (J + 1), ma = e - mb * (J + 1);
+  for (int f = warp; f < yib::NFULL; f += NW) {  // one full-matrix element per warp, lanes = atoms
+    const int code = c_box_exp.e[f];
     Cx v{0.0, 0.0};
-    if (at < na_blk) {
-      const Cx* ua = Ust + at * yib::NHALF + yib::hoff(J);
-      if (2 * mb <= J) {
-        v = ua[mb * (J + 1) + ma];
-      } else {
-        const Cx w = ua[(J - mb) * (J + 1) + (J - ma)];
-        v = ((ma + mb) & 1) ? Cx{-w.re, w.im} : Cx{w.re, -w.im};
-      }
+    if (lane < na_blk) {
+      const Cx w = Ust[lane * yib::NHALF + (code >> 2)];
+      v = !(code & 2) ? w : ((code & 1) ? Cx{-w.re, w.im} : Cx{w.re, -w.im});
     }
-    Uf[f * yib::ATOMS + at] = v;
+    Uf[f * yib::ATOMS + lane] = v;
   }
   __syncthreads();  // staged U_tot consumed before Y is cleared
   for (int t = threadIdx.x; t < yib::NHALF * yib::ATOMS; t += blockDim.x) Ys[t] = Cx{0.0, 0.0};
