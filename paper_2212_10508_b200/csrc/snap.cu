@@ -99,6 +99,25 @@ struct SnapDev {  // POD view passed to kernels
 __constant__ double c_rootpq[SNAP_JMAX + 2][SNAP_JMAX + 2];  // sqrt(p/q)
 // layer offsets depend on J only (not on twojmax): half rows and full matrices
 __constant__ int c_hoff[SNAP_JMAX + 2];
+
+// layer J and its half-storage offset of element t at twojmax 8, from
+// immediate constants (a lane-divergent c_hoff search serialises on the
+// constant cache)
+constexpr int hoff8(int J) {
+  int h = 0;
+  for (int j = 0; j < J; ++j) h += (j + 1) * (j / 2 + 1);
+  return h;
+}
+__device__ __forceinline__ void half_layer8(int t, int& J, int& base) {
+  J = 0;
+  base = 0;
+#pragma unroll
+  for (int j = 1; j <= 8; ++j)
+    if (t >= hoff8(j)) {
+      J = j;
+      base = hoff8(j);
+    }
+}
 __constant__ int c_foff[SNAP_JMAX + 2];
 // dense Clebsch-Gordan blocks C(x m1, y m2 | J M) as [M-row][m1] per (x, y, J),
 // x >= y, read with warp-uniform addresses by k_snap_yi (36.7 KB at twojmax 8)
@@ -1783,9 +1802,14 @@ struct Layers<TJ, 0> {
 
 constexpr int RR_WARPS = 4;  // warps per CTA of the register-resident kernels (one atom per warp)
 
+// sqrt(p/q) table into shared memory, computed in place (correctly rounded
+// divide and sqrt: the host table's values bit for bit) instead of 100
+// lane-divergent constant-bank reads that serialise per warp
 __device__ __forceinline__ void stage_rootpq(double (*rp)[SNAP_JMAX + 2]) {
-  for (int t = threadIdx.x; t < (SNAP_JMAX + 2) * (SNAP_JMAX + 2); t += blockDim.x)
-    rp[t / (SNAP_JMAX + 2)][t % (SNAP_JMAX + 2)] = c_rootpq[t / (SNAP_JMAX + 2)][t % (SNAP_JMAX + 2)];
+  for (int t = threadIdx.x; t < (SNAP_JMAX + 2) * (SNAP_JMAX + 2); t += blockDim.x) {
+    const int p = t / (SNAP_JMAX + 2), q = t % (SNAP_JMAX + 2);
+    rp[p][q] = q ? __dsqrt_rn(__ddiv_rn((double)p, (double)q)) : 0.0;
+  }
 }
 
 template <int TJ, bool REG>
@@ -2305,9 +2329,9 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
       a.re += part[pp * ps + t].re;
       a.im += part[pp * ps + t].im;
     }
-    int J = 0;
-    while (J < TJ && t >= c_hoff[J + 1]) ++J;
-    const int e = t - c_hoff[J];
+    int J, base;
+    half_layer8(t, J, base);
+    const int e = t - base;
     const int mbb = e / (J + 1), maa = e - mbb * (J + 1);
     if (maa == mbb) a.re += D.wself;
     out[t] = a;
@@ -2605,12 +2629,12 @@ k_snap_deidrj_adj4(SnapDev D, int64_t natoms, int N, Box box, const double* __re
 
 // element (r, c) of the full layer-J Y matrix from the stored half rows
 // (middle row valid for c <= J/2 after the box kernel's fold)
-__device__ __forceinline__ C2 y_full(const C2* y, int J, int r, int c) {
+__device__ __forceinline__ C2 y_full(const C2* y, int J, int base, int r, int c) {  // base: offset of layer J
   if (2 * r > J || (2 * r == J && 2 * c > J)) {
-    const C2 v = y[c_hoff[J] + (J - r) * (J + 1) + (J - c)];
+    const C2 v = y[base + (J - r) * (J + 1) + (J - c)];
     return ((r + c) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};  // (-1)^(r+c) conj
   }
-  return y[c_hoff[J] + r * (J + 1) + c];
+  return y[base + r * (J + 1) + c];
 }
 
 // Y^dagger, half rows stored column-interleaved: yt[J][ma][mb] = conj(Y[J][ma][mb])
@@ -2620,12 +2644,12 @@ __global__ void k_snap_ytrans(int64_t natoms, int nh, int tj, const C2* __restri
   if (t >= natoms * nh) return;
   const int64_t atom = t / nh;
   const int h = (int)(t - atom * nh);
-  int J = 0;
-  while (J < tj && h >= c_hoff[J + 1]) ++J;
-  const int e = h - c_hoff[J];
+  int J, base;
+  half_layer8(h, J, base);  // the pair form runs at twojmax 8 only
+  const int e = h - base;
   const int mb = e / (J + 1), ma = e - mb * (J + 1);
-  const C2 v = y_full(y + atom * nh, J, ma, mb);
-  yt[atom * nh + c_hoff[J] + ma * (J / 2 + 1) + mb] = C2{v.re, -v.im};
+  const C2 v = y_full(y + atom * nh, J, base, ma, mb);
+  yt[atom * nh + base + ma * (J / 2 + 1) + mb] = C2{v.re, -v.im};
 }
 
 constexpr int PAIR_WARPS = 4;  // 2 CTAs of 4 warps per SM (shared memory), neighbouring atoms share an SM
