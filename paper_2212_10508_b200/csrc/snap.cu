@@ -2652,6 +2652,12 @@ __global__ void k_snap_ytrans(int64_t natoms, int nh, int tj, const C2* __restri
   yt[atom * nh + base + ma * (J / 2 + 1) + mb] = C2{v.re, -v.im};
 }
 
+// owner of the unordered pair {i, k}: i when (i + k even and k > i) or (i + k odd
+// and k < i).  Antisymmetric, so every pair has one owner; on the BCC lattices
+// every atom owns 10-17 of its 26 neighbours (k > i alone gives 0-26, and the
+// slowest warp of a small batch waits for 7 rounds instead of 4).
+__host__ __device__ __forceinline__ bool pair_owned(int i, int k) { return ((i + k) & 1) ? (k < i) : (k > i); }
+
 constexpr int PAIR_WARPS = 4;  // 2 CTAs of 4 warps per SM (shared memory), neighbouring atoms share an SM
 constexpr int PAIR_GEO = 12;   // doubles of geometry per pair (k_snap_deidrj_pair)
 
@@ -2686,28 +2692,31 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
   int64_t* gk = reinterpret_cast<int64_t*>(reinterpret_cast<double*>(
                     reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) +
                     NWB * (APW * nh + ADJ4_SLOTS * 32)) + NWB * 32 * PAIR_GEO) + warp * 32;
+  // list slots of the owned neighbours of the warp's atoms, [APW][SNAP_MAXN]
+  int32_t* oslot = reinterpret_cast<int32_t*>(gk + (NWB - warp) * 32) + warp * APW * SNAP_MAXN;
   stage_rootpq(rp);
   const int64_t atom0 = ((int64_t)blockIdx.x * NWB + warp) * APW;
-  int nat[APW], lo[APW];
+  int nat[APW];
   int total = 0;
 #pragma unroll
   for (int k = 0; k < APW; ++k) {
     const int64_t a = atom0 + k;
     nat[k] = 0;
-    lo[k] = 0;
     if (a < natoms) {
       const int i = (int)(a % N);
       const int c = cnt[a];
-      int below = 0;
-      for (int t0 = 0; t0 < c; t0 += 32) {
-        const bool lt = t0 + lane < c && nbr[a * maxn + t0 + lane] < i;
-        below += __popc(__ballot_sync(0xffffffffu, lt));
+      int m = 0;
+      for (int t0 = 0; t0 < c; t0 += 32) {  // compaction of the owned slots, list order
+        const bool own = t0 + lane < c && pair_owned(i, nbr[a * maxn + t0 + lane]);
+        const unsigned bal = __ballot_sync(0xffffffffu, own);
+        if (own) oslot[k * SNAP_MAXN + m + __popc(bal & ((1u << lane) - 1u))] = t0 + lane;
+        m += __popc(bal);
       }
-      lo[k] = below;
-      nat[k] = c - below;
+      nat[k] = m;
     }
     total += nat[k];
   }
+  __syncwarp();
   {  // the warp's Y rows are one contiguous range: all loads in flight before the stores
     constexpr int NL = (APW * 155 + 31) / 32;  // twojmax 8: nh = 155
     const int nel = (int)min((int64_t)APW, natoms - atom0) * nh;
@@ -2737,7 +2746,7 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
       if (t < total) {
         const int64_t at = atom0 + wt;
         const int64_t bt = at / N;
-        const int kk = nbr[at * maxn + lo[wt] + kt];
+        const int kk = nbr[at * maxn + oslot[wt * SNAP_MAXN + kt]];
         // the partner's Y^dagger (2.5 KB) towards L2 ahead of the rounds that read it
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ytlist + (bt * N + kk) * nh),
                      "r"((unsigned)(nh * sizeof(C2)))
@@ -2774,7 +2783,7 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
       }
     const bool valid = s0 + p < total;
     const int64_t atom = atom0 + w;
-    const int s = lo[w] + k;
+    const int s = oslot[w * SNAP_MAXN + k];
     const double* go = gb + ((s0 & 31) + p) * PAIR_GEO;
     const int64_t katom = valid ? gk[(s0 & 31) + p] : atom;  // invalid slots: own Y^dagger (weight 0)
     const YPair Y{Yw + w * nh, ytlist + katom * nh};
@@ -2833,7 +2842,7 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
 
 // gather of the pair form, one warp per atom (lanes over neighbour slots, the
 // reverse-slot searches in parallel, fixed-order shuffle tree):
-// grad_i = -sum_{k>i} h_ik + sum_{k<i} h_ki; the owner books the pair virial
+// grad_i = -sum_{owned} h_ik + sum_{owned by k} h_ki; the owner books the pair virial
 __global__ void __launch_bounds__(128)
 k_snap_gather_pair_w(int64_t natoms, int N, Box box, const double* __restrict__ q,
                      const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
@@ -2849,7 +2858,7 @@ k_snap_gather_pair_w(int64_t natoms, int N, Box box, const double* __restrict__ 
   double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // g[3], vir[6]
   for (int s = lane; s < n; s += 32) {
     const int k = nb[s];
-    if (k > a) {
+    if (pair_owned(a, k)) {
       const double* h = dedr + (atom * maxn + s) * 3;
       v[0] -= h[0];
       v[1] -= h[1];
@@ -2895,65 +2904,6 @@ k_snap_gather_pair_w(int64_t natoms, int N, Box box, const double* __restrict__ 
     if (vatom)
       for (int c = 0; c < 6; ++c) vatom[6 * atom + c] = v[3 + c];
   }
-}
-
-// gather of the pair form: grad_i = -sum_{k>i} h_ik + sum_{k<i} h_ki; the
-// owner (smaller index) books the pair's virial -h_ik (x) r_ik
-__global__ void k_snap_gather_pair(int64_t natoms, int N, Box box, const double* __restrict__ q,
-                                   const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
-                                   const double* __restrict__ dedr, double* __restrict__ grad,
-                                   double* __restrict__ vatom) {
-  int64_t atom = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (atom >= natoms) return;
-  int64_t b = atom / N;
-  int a = (int)(atom - b * N);
-  int n = cnt[atom];
-  const int32_t* nb = nbr + atom * maxn;
-  double gx = 0.0, gy = 0.0, gz = 0.0;
-  double v[6] = {0, 0, 0, 0, 0, 0};
-  const double* qb = q + b * (int64_t)N * 3;
-  for (int s = 0; s < n; ++s) {
-    const int k = nb[s];
-    if (k > a) {
-      const double* h = dedr + (atom * maxn + s) * 3;
-      gx -= h[0];
-      gy -= h[1];
-      gz -= h[2];
-      if (vatom) {
-        double dx, dy, dz;
-        pair_vec(qb, a, k, box, dx, dy, dz);
-        v[0] -= h[0] * dx;
-        v[1] -= h[1] * dy;
-        v[2] -= h[2] * dz;
-        v[3] -= 0.5 * (h[0] * dy + h[1] * dx);
-        v[4] -= 0.5 * (h[0] * dz + h[2] * dx);
-        v[5] -= 0.5 * (h[1] * dz + h[2] * dy);
-      }
-    } else {
-      const int64_t katom = b * N + k;
-      const int32_t* kl = nbr + katom * maxn;
-      int lo = 0, hi = cnt[katom] - 1, sk = -1;
-      while (lo <= hi) {
-        const int mid = (lo + hi) >> 1;
-        const int val = kl[mid];
-        if (val == a) { sk = mid; break; }
-        if (val < a) lo = mid + 1; else hi = mid - 1;
-      }
-      if (sk >= 0) {
-        const double* h = dedr + (katom * maxn + sk) * 3;
-        gx += h[0];
-        gy += h[1];
-        gz += h[2];
-      }
-    }
-  }
-  if (grad) {
-    grad[3 * atom] = gx;
-    grad[3 * atom + 1] = gy;
-    grad[3 * atom + 2] = gz;
-  }
-  if (vatom)
-    for (int c = 0; c < 6; ++c) vatom[6 * atom + c] = v[c];
 }
 
 // ------------------------------------------------------------------ kernel: gather
@@ -3193,7 +3143,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     k_snap_ytrans<<<(unsigned)((nel + 255) / 256), 256, 0, ctx->stream>>>(na, D.nhalf, D.tj, buf.y, buf.yt);
     PL_CHECK_LAUNCH();
     const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
-                      (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32;
+                      (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
+                      sizeof(int32_t) * PAIR_WARPS * 2 * SNAP_MAXN;
     const unsigned grid = (unsigned)((na + PAIR_WARPS * 2 - 1) / (PAIR_WARPS * 2));
     k_snap_deidrj_pair<2, PAIR_WARPS><<<grid, PAIR_WARPS * 32, sm, ctx->stream>>>(
         D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr);
