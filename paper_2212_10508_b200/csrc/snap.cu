@@ -2840,6 +2840,187 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
   }
 }
 
+// Pair form, one warp walking a run of CH consecutive atoms: the owned lists of
+// the run are concatenated, a round of 8 slots spans at most 2 atoms (a round
+// that would reach a third atom stops short), and Y_i of the live atoms sit in a
+// 2-slot ring (slot = local atom parity) refilled by cp.async as soon as an
+// atom's last pair is done, behind the next round's forward pass (which reads
+// no Y).  Slot fill ~98 % instead of 85 % for 2-atom warps.
+template <int CH, int NWB>
+__global__ void __launch_bounds__(NWB * 32)
+k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+                  const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+                  const C2* __restrict__ ylist, const C2* __restrict__ ytlist, double* __restrict__ dedr) {
+  constexpr int TJ = 8, R = 4, P = 8;
+  extern __shared__ double smem[];
+  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  C2* base = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2));
+  C2* Yw = base + warp * 2 * nh;  // ring [2][nh]
+  C2* hist = base + NWB * 2 * nh + warp * ADJ4_SLOTS * 32;
+  double* gb0 = reinterpret_cast<double*>(base + NWB * (2 * nh + ADJ4_SLOTS * 32));
+  double* gb = gb0 + warp * 32 * PAIR_GEO;
+  int64_t* gk = reinterpret_cast<int64_t*>(gb0 + NWB * 32 * PAIR_GEO) + warp * 32;
+  int16_t* oslot = reinterpret_cast<int16_t*>(reinterpret_cast<int64_t*>(gb0 + NWB * 32 * PAIR_GEO) + NWB * 32) +
+                   warp * CH * SNAP_MAXN;
+  int32_t* cum = reinterpret_cast<int32_t*>(reinterpret_cast<int16_t*>(
+                     reinterpret_cast<int64_t*>(gb0 + NWB * 32 * PAIR_GEO) + NWB * 32) + NWB * CH * SNAP_MAXN) +
+                 warp * (CH + 2);
+  stage_rootpq(rp);
+  const int64_t a0 = ((int64_t)blockIdx.x * NWB + warp) * CH;
+  const int nrun = (int)max((int64_t)0, min((int64_t)CH, natoms - a0));
+  int tot = 0;
+  for (int c = 0; c < CH; ++c) {
+    if (lane == 0) cum[c] = tot;
+    const int base_c = tot;
+    if (c < nrun) {
+      const int64_t a = a0 + c;
+      const int i = (int)(a % N);
+      const int n = cnt[a];
+      for (int t0 = 0; t0 < n; t0 += 32) {
+        const bool own = t0 + lane < n && pair_owned(i, nbr[a * maxn + t0 + lane]);
+        const unsigned bal = __ballot_sync(0xffffffffu, own);
+        if (own) oslot[c * SNAP_MAXN + (tot - base_c) + __popc(bal & ((1u << lane) - 1u))] = (int16_t)(t0 + lane);
+        tot += __popc(bal);
+      }
+    }
+  }
+  if (lane == 0) {
+    cum[CH] = tot;
+    cum[CH + 1] = tot;
+  }
+  {  // Y of local atoms 0 and 1 (one contiguous range): loads in flight before the stores
+    constexpr int NL = (2 * 155 + 31) / 32;
+    const int nel = min(2, nrun) * nh;
+    C2 tmp[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (lane + 32 * j < nel) tmp[j] = ylist[a0 * nh + lane + 32 * j];
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (lane + 32 * j < nel) Yw[lane + 32 * j] = tmp[j];
+  }
+  __syncthreads();
+  if (nrun == 0) return;
+  const int p = lane / R, mb = lane - p * R;
+  int pos = 0, ca = 0, gbase = -64, next_load = 2;
+  while (pos < tot) {
+    while (cum[ca + 1] <= pos) ++ca;  // first atom of the round (skips atoms without owned pairs)
+    const int end = min(min(pos + P, tot), cum[ca + 2]);
+    // ring refill: every finished atom hands its slot to the atom two ahead (atoms
+    // already finished themselves are skipped, so a slot gets one copy at a time);
+    // the copies land behind this round's forward pass
+    while (next_load < nrun + 2 && cum[next_load - 1] <= pos) {
+      if (next_load < nrun && cum[next_load + 1] > pos) {
+        const C2* src = ylist + (a0 + next_load) * nh;
+        C2* dst = Yw + (next_load & 1) * nh;
+        for (int e = lane; e < nh; e += 32) {
+          const unsigned d = (unsigned)__cvta_generic_to_shared(dst + e);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + e) : "memory");
+        }
+      }
+      ++next_load;
+    }
+    if (pos + P > gbase + 32) {  // geometry of list positions pos .. pos + 31
+      __syncwarp();
+      gbase = pos;
+      const int t = gbase + lane;
+      double* o = gb + lane * PAIR_GEO;
+      if (t < tot) {
+        int ct = ca;
+        while (cum[ct + 1] <= t) ++ct;
+        const int64_t at = a0 + ct;
+        const int64_t bt = at / N;
+        const int kk = nbr[at * maxn + oslot[ct * SNAP_MAXN + (t - cum[ct])]];
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ytlist + (bt * N + kk) * nh),
+                     "r"((unsigned)(nh * sizeof(C2)))
+                     : "memory");
+        double dx, dy, dz;
+        pair_vec(q + bt * (int64_t)N * 3, (int)(at - bt * N), kk, box, dx, dy, dz);
+        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+        const double inv = 1.0 / r;
+        const double u0 = dx * inv, u1 = dy * inv, u2 = dz * inv;
+        double sn, cs;
+        sincos(D.kappa * (r - D.rmin0), &sn, &cs);
+        double fc = 1.0, dfc = 0.0;
+        if (D.switchflag) {
+          double sa, ca2;
+          sincos(D.pi_span * (r - D.rmin0), &sa, &ca2);
+          fc = 0.5 * (ca2 + 1.0);
+          dfc = -D.half_pi_span * sa;
+        }
+        o[0] = cs; o[1] = -u2 * sn; o[2] = u1 * sn; o[3] = -u0 * sn;  // a, b
+        o[4] = fc; o[5] = dfc; o[6] = u0; o[7] = u1; o[8] = u2; o[9] = sn; o[10] = cs; o[11] = inv;
+        gk[lane] = bt * N + kk;
+      } else {
+        o[0] = 1.0; o[1] = 0.0; o[2] = 0.0; o[3] = 0.0;
+        gk[lane] = -1;
+      }
+      __syncwarp();
+    }
+    const int pp = pos + p;
+    const bool valid = pp < end;
+    const int c = (valid && pp >= cum[ca + 1]) ? ca + 1 : ca;
+    const int64_t atom = a0 + c;
+    const int s = valid ? oslot[c * SNAP_MAXN + (pp - cum[c])] : 0;
+    const double* go = gb + (valid ? pp - gbase : 0) * PAIR_GEO;
+    const int64_t katom = valid ? gk[pp - gbase] : atom;  // invalid slots: own Y^dagger (weight 0)
+    const YPair Y{Yw + (c & 1) * nh, ytlist + katom * nh};
+    RowGeom<TJ> g{valid ? C2{go[0], go[1]} : C2{1.0, 0.0}, valid ? C2{go[2], go[3]} : C2{0.0, 0.0}, C2{0.0, 0.0},
+                  C2{0.0, 0.0}};
+    C2 u[TJ + 1], u4[TJ + 1];
+#pragma unroll
+    for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
+    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
+    double F = 0.0;
+    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, rp, Y, hist, lane, F);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");  // ring refills issued after the last round
+    __syncwarp();
+    C2 G[TJ + 1], G4[TJ + 1];
+#pragma unroll
+    for (int x = 0; x <= TJ; ++x) {
+      G[x] = Y(TJ, mb, x);
+      G4[x] = (mb == TJ / 2 - 1) ? Y(TJ, TJ / 2, x) : C2{0.0, 0.0};
+    }
+#pragma unroll
+    for (int x = 0; x <= TJ; ++x) {  // layer-8 terms of F (row mb; row 4 on the row-3 lane)
+      const double w8 = half_w(TJ, mb, x), w4 = half_w(TJ, TJ / 2, x);
+      if (2 * mb <= TJ) F += w8 * (u[x].re * G[x].re + u[x].im * G[x].im);
+      if (mb == TJ / 2 - 1) F += w4 * (u4[x].re * G4[x].re + u4[x].im * G4[x].im);
+      G[x] = C2{w8 * G[x].re, w8 * G[x].im};
+      G4[x] = C2{w4 * G4[x].re, w4 * G4[x].im};
+    }
+    C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
+    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, rp, Y, hist, lane, Sa, Sb, F);
+    __syncwarp();
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double f = __shfl_down_sync(0xffffffffu, F, r);
+      const double ar = __shfl_down_sync(0xffffffffu, Sa.re, r), ai = __shfl_down_sync(0xffffffffu, Sa.im, r);
+      const double br = __shfl_down_sync(0xffffffffu, Sb.re, r), bi = __shfl_down_sync(0xffffffffu, Sb.im, r);
+      if (mb == 0) {
+        F += f;
+        Sa.re += ar; Sa.im += ai;
+        Sb.re += br; Sb.im += bi;
+      }
+    }
+    if (valid && mb == 0) {
+      const double uu[3] = {go[6], go[7], go[8]};
+      C2 da[3], db[3];
+      pair_deriv(D.kappa, uu, go[9], go[10], go[11], da, db);
+      const double fc = go[4], dfc = go[5];
+      double* o = dedr + (atom * maxn + s) * 3;
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) {
+        const double re = da[cc].re * Sa.re - da[cc].im * Sa.im + db[cc].re * Sb.re - db[cc].im * Sb.im;
+        o[cc] = dfc * uu[cc] * F + fc * re;
+      }
+    }
+    pos = end;
+  }
+}
+
 // gather of the pair form, one warp per atom (lanes over neighbour slots, the
 // reverse-slot searches in parallel, fixed-order shuffle tree):
 // grad_i = -sum_{owned} h_ik + sum_{owned by k} h_ki; the owner books the pair virial
@@ -3043,6 +3224,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_deidrj_adj4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_adj4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_pair<2, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_run<8, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_ui_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_done = true;
   }
@@ -3142,12 +3324,26 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     const int64_t nel = na * D.nhalf;
     k_snap_ytrans<<<(unsigned)((nel + 255) / 256), 256, 0, ctx->stream>>>(na, D.nhalf, D.tj, buf.y, buf.yt);
     PL_CHECK_LAUNCH();
-    const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
-                      (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
-                      sizeof(int32_t) * PAIR_WARPS * 2 * SNAP_MAXN;
-    const unsigned grid = (unsigned)((na + PAIR_WARPS * 2 - 1) / (PAIR_WARPS * 2));
-    k_snap_deidrj_pair<2, PAIR_WARPS><<<grid, PAIR_WARPS * 32, sm, ctx->stream>>>(
-        D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr);
+    static const int prun = [] {
+      const char* e = getenv("PL_SNAP_PAIR_RUN");
+      return e ? atoi(e) : 1;  // 0: 2-atom warps only, 2: runs at every size (tests)
+    }();
+    constexpr int RUN = 8;
+    if (prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4)) {  // >= 4 waves of runs
+      const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
+                        (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
+                        sizeof(int16_t) * PAIR_WARPS * RUN * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (RUN + 2);
+      const unsigned grid = (unsigned)((na + PAIR_WARPS * RUN - 1) / (PAIR_WARPS * RUN));
+      k_snap_deidrj_run<RUN, PAIR_WARPS><<<grid, PAIR_WARPS * 32, sm, ctx->stream>>>(
+          D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr);
+    } else {
+      const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
+                        (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
+                        sizeof(int32_t) * PAIR_WARPS * 2 * SNAP_MAXN;
+      const unsigned grid = (unsigned)((na + PAIR_WARPS * 2 - 1) / (PAIR_WARPS * 2));
+      k_snap_deidrj_pair<2, PAIR_WARPS><<<grid, PAIR_WARPS * 32, sm, ctx->stream>>>(
+          D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr);
+    }
     buf.pair = true;
   } else if (rr && adj_env && adj4 && S->tj == 8) {
     static const int apw = [] {

@@ -166,15 +166,21 @@ def test_snap_pair_form_matches_ordered_form(pl, tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    for mode in ("0", "1"):
-        f = str(tmp_path / f"ab{mode}.npz")
-        env = dict(os.environ, PL_SNAP_PAIR=mode)
+    # ordered form; pair form with 2-atom warps; pair form with 8-atom runs (forced)
+    for mode, env_add in (("ord", {"PL_SNAP_PAIR": "0"}), ("pair", {"PL_SNAP_PAIR_RUN": "0"}),
+                          ("run", {"PL_SNAP_PAIR_RUN": "2"})):
+        f = str(tmp_path / f"ab_{mode}.npz")
+        env = dict(os.environ, **env_add)
         subprocess.run([sys.executable, "-c", _AB_SCRIPT, f], cwd=root, env=env, check=True)
         out[mode] = np.load(f)
-    a, b = out["0"], out["1"]
-    np.testing.assert_array_equal(a["E"], b["E"])  # energies do not depend on the force form
-    np.testing.assert_allclose(b["G"], a["G"], rtol=1e-12, atol=1e-12 * np.abs(a["G"]).max())
-    np.testing.assert_allclose(b["V"], a["V"], rtol=1e-12, atol=1e-12 * np.abs(a["V"]).max())
+    a = out["ord"]
+    for m in ("pair", "run"):
+        b = out[m]
+        np.testing.assert_array_equal(a["E"], b["E"])  # energies do not depend on the force form
+        np.testing.assert_allclose(b["G"], a["G"], rtol=1e-12, atol=1e-12 * np.abs(a["G"]).max())
+        np.testing.assert_allclose(b["V"], a["V"], rtol=1e-12, atol=1e-12 * np.abs(a["V"]).max())
+    # the pair gather sums each pair once, in list order: runs and 2-atom warps agree bit for bit
+    np.testing.assert_array_equal(out["pair"]["G"], out["run"]["G"])
 
 
 def test_snap_invariances_on_device(pl):
