@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 #include <stdlib.h>
 
+
 #include "eam.cuh"
 #include "neigh.cuh"
 #include "pl_common.cuh"
@@ -54,6 +55,7 @@ inline void cluster_layout(int n, int& C, int& tpa) {
 struct ClArgs {
   int64_t d;
   int n_atoms, L, mode, C, tpa;
+  int cache;  // table derivatives cached by the density pass: 0 none, 1 drho/dr, 2 drho/dr and dphi/dr
   double* Q;
   double* P;
   double* baseQ;
@@ -87,14 +89,16 @@ struct ClSmem {  // carve-up of the dynamic shared memory of one CTA
   double* g;       // own gradient
   double* qref;    // own positions at the last list build
   double* rr;      // own exact-pair distances [own][CL_MAXN]
+  double* drf;     // d rho/dr of the exact pairs [own][CL_MAXN] (cache >= 1)
+  double* dpf;     // d phi/dr of the exact pairs [own][CL_MAXN] (cache == 2)
   int32_t* cand;   // [own][CL_MAXC]
   int32_t* ncand;  // [own]
   int32_t* nbr;    // [own][CL_MAXN]
   int32_t* nnbr;   // [own]
 };
 
-__host__ __device__ inline size_t cl_smem_bytes(int n, int own) {
-  return sizeof(double) * (6 * (size_t)n + n + 4 * 3 * (size_t)own + (size_t)own * CL_MAXN) +
+__host__ __device__ inline size_t cl_smem_bytes(int n, int own, int cache = 0) {
+  return sizeof(double) * (6 * (size_t)n + n + 4 * 3 * (size_t)own + (size_t)(1 + cache) * own * CL_MAXN) +
          sizeof(int32_t) * ((size_t)own * CL_MAXC + own + (size_t)own * CL_MAXN + own) + 64;
 }
 
@@ -146,7 +150,9 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
   M.g = M.ph + 3 * own;
   M.qref = M.g + 3 * own;
   M.rr = M.qref + 3 * own;
-  M.cand = reinterpret_cast<int32_t*>(M.rr + (size_t)own * CL_MAXN);
+  M.drf = M.rr + (size_t)own * CL_MAXN;
+  M.dpf = M.drf + (A.cache >= 1 ? (size_t)own * CL_MAXN : 0);
+  M.cand = reinterpret_cast<int32_t*>(M.dpf + (A.cache == 2 ? (size_t)own * CL_MAXN : 0));
   M.ncand = M.cand + (size_t)own * CL_MAXC;
   M.nbr = M.ncand + own;
   M.nnbr = M.nbr + (size_t)own * CL_MAXN;
@@ -241,9 +247,18 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
       const int nl = live ? M.nnbr[ii] : 0;
       double s = 0.0;
       for (int k = sl; k < nl; k += tpa) {
+        // the force pass's table values for the same pair: d rho/dr is this
+        // lookup's derivative, d phi/dr an independent lookup issued alongside
+        const size_t ix = (size_t)ii * CL_MAXN + k;
         double f, df;
-        tab_eval(A.rho, M.rr[(size_t)ii * CL_MAXN + k], f, df);
+        tab_eval(A.rho, M.rr[ix], f, df);
         s = __dadd_rn(s, f);
+        if (A.cache >= 1) M.drf[ix] = df;
+        if (A.cache == 2) {
+          double pf, dpf;
+          tab_eval(A.phi, M.rr[ix], pf, dpf);
+          M.dpf[ix] = dpf;
+        }
       }
       s = group_sum(s, tpa);
       if (live && sl == 0) {
@@ -273,8 +288,14 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
         pair_vec(q, ai, j, A.box, dx, dy, dz);
         const double rr = M.rr[(size_t)ii * CL_MAXN + k];
         double rf, drf, pf, dpf;
-        tab_eval(A.rho, rr, rf, drf);
-        tab_eval(A.phi, rr, pf, dpf);
+        if (A.cache >= 1)
+          drf = M.drf[(size_t)ii * CL_MAXN + k];
+        else
+          tab_eval(A.rho, rr, rf, drf);
+        if (A.cache == 2)
+          dpf = M.dpf[(size_t)ii * CL_MAXN + k];
+        else
+          tab_eval(A.phi, rr, pf, dpf);
         const double sc = __ddiv_rn(fma(__dadd_rn(fpi, M.fp[j]), drf, dpf), rr);
         gx = fma(-sc, dx, gx);
         gy = fma(-sc, dy, gy);
@@ -466,10 +487,17 @@ int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N
   int C, tpa;
   cluster_layout(n, C, tpa);
   const int own = (n + C - 1) / C;
-  const size_t smem = cl_smem_bytes(n, own);
-  if (smem > 220 * 1024) return -1;
+  if (cl_smem_bytes(n, own) > 220 * 1024) return -1;
+  // cache as many table derivatives as shared memory allows (values bitwise the same)
+  static const int cache_env = [] {
+    const char* e = getenv("PL_SWEEP_CACHE");
+    return e ? atoi(e) : 2;
+  }();
+  int cache = cache_env;
+  while (cache > 0 && cl_smem_bytes(n, own, cache) > 220 * 1024) --cache;
+  const size_t smem = cl_smem_bytes(n, own, cache);
   ClArgs A{};
-  A.d = d; A.n_atoms = n; A.L = L; A.mode = mode; A.C = C; A.tpa = tpa;
+  A.d = d; A.n_atoms = n; A.L = L; A.mode = mode; A.C = C; A.tpa = tpa; A.cache = cache;
   A.Q = Q; A.P = P; A.baseQ = baseQ; A.baseP = baseP;
   A.jumpQ = mode == 0 ? jumpQ : baseQ;
   A.jumpP = mode == 0 ? jumpP : baseP;
