@@ -33,7 +33,6 @@ struct StepConsts {
   int L;
 };
 
-constexpr int MAX_L_CONST = 4096;
 struct AmpTable {
   const double* d_amp;  // L+1 scalar amplitudes (device)
 };
