@@ -174,6 +174,7 @@ __global__ void k_open(int64_t W, int64_t d, int s, bool first, StepConsts K,
                        const double* __restrict__ mass, const double* __restrict__ grad,
                        const double* __restrict__ p, double* __restrict__ ph,
                        double* __restrict__ q) {
+  griddep_wait();
   int64_t n = W * d;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -194,6 +195,7 @@ __global__ void k_close(int64_t W, int64_t d, int s, StepConsts K, const double*
                         const double* __restrict__ grad, const double* __restrict__ ph,
                         const double* __restrict__ q, double* __restrict__ p,
                         int32_t* __restrict__ blow, double* __restrict__ s1, double* __restrict__ s2) {
+  griddep_wait();
   int64_t n = W * d;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -276,12 +278,13 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
   unsigned g = grid_for((int64_t)nd);
   for (int s = 1; s <= L; ++s) {
     prof_mark(st, ST_INT, true);
-    k_open<<<g, 256, 0, st>>>(W, d, s, s == 1, K, amp, noise, mass, grad, p1, ph, q1);
+    PL_CUDA(launch_pdl(k_open, dim3(g), dim3(256), 0, st, W, d, s, s == 1, K, amp, noise, mass, grad, p1, ph, q1));
     PL_CHECK_LAUNCH();
     prof_mark(st, ST_INT, false);
     PL_TRY(compute(pot, W, d, q1, nullptr, grad, nullptr));
     prof_mark(st, ST_INT, true);
-    k_close<<<g, 256, 0, st>>>(W, d, s, K, amp, noise, mass, grad, ph, q1, p1, blow, s1, s2);
+    PL_CUDA(launch_pdl(k_close, dim3(g), dim3(256), 0, st, W, d, s, K, amp, noise, mass, grad, ph, q1, p1, blow, s1,
+                       s2));
     PL_CHECK_LAUNCH();
     prof_mark(st, ST_INT, false);
   }

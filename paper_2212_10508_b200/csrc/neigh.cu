@@ -27,6 +27,7 @@ __device__ __forceinline__ int cell_of(double x, double L, double inv, int n) {
 
 __global__ void k_cell_count(int64_t B, int N, Box box, CellGrid g, const double* __restrict__ q,
                              int32_t* __restrict__ cell_of_atom, int32_t* __restrict__ ccount) {
+  griddep_wait();
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= B * N) return;
   int64_t b = t / N;
@@ -43,6 +44,7 @@ __global__ void k_cell_count(int64_t B, int N, Box box, CellGrid g, const double
 // exclusive scan of cell counts (single CTA, chunked)
 __global__ void __launch_bounds__(1024) k_cell_scan(int64_t ncell, const int32_t* __restrict__ ccount,
                                                    int32_t* __restrict__ cstart, int32_t* __restrict__ cfill) {
+  griddep_wait();
   typedef cub::BlockScan<int32_t, 1024> S;
   __shared__ typename S::TempStorage tmp;
   __shared__ int32_t carry;
@@ -65,6 +67,7 @@ __global__ void __launch_bounds__(1024) k_cell_scan(int64_t ncell, const int32_t
 
 __global__ void k_cell_fill(int64_t natoms, int N, const int32_t* __restrict__ cell_of_atom,
                             int32_t* __restrict__ cfill, int32_t* __restrict__ catoms) {
+  griddep_wait();
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= natoms) return;
   int slot = atomicAdd(&cfill[cell_of_atom[t]], 1);
@@ -131,6 +134,7 @@ k_neigh_cell_w(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, cons
                const int32_t* __restrict__ cell_of_atom, const int32_t* __restrict__ cstart,
                const int32_t* __restrict__ catoms, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
                int* __restrict__ overflow) {
+  griddep_wait();
   __shared__ int32_t s_found[NC_WARPS][CELL_MAXN];
   __shared__ int32_t s_off[NC_WARPS][32], s_beg[NC_WARPS][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -227,8 +231,8 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
   prof_mark(st, ST_NEIGH, true);
   if (!cells_ok) {
     const int64_t warps = B * N;
-    k_neigh_brute_w<<<(unsigned)((warps * 32 + NB_THREADS - 1) / NB_THREADS), NB_THREADS, 0, st>>>(
-        B, N, box, rc2, maxn, q, out->nbr, out->cnt, out->overflow);
+    PL_CUDA(launch_pdl(k_neigh_brute_w, dim3((unsigned)((warps * 32 + NB_THREADS - 1) / NB_THREADS)), dim3(NB_THREADS),
+                       0, st, B, N, box, rc2, maxn, q, out->nbr, out->cnt, out->overflow));
     PL_CHECK_LAUNCH();
   } else {
     int64_t cells = (int64_t)g.n[0] * g.n[1] * g.n[2];
@@ -243,13 +247,14 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
     int32_t* catoms = cfill + (nc + 1);
     PL_CUDA(cudaMemsetAsync(ccount, 0, sizeof(int32_t) * nc, st));
     unsigned ga = (unsigned)((na + 255) / 256);
-    k_cell_count<<<ga, 256, 0, st>>>(B, N, box, g, q, cell_of_atom, ccount);
-    k_cell_scan<<<1, 1024, 0, st>>>(nc, ccount, cstart, cfill);
-    k_cell_fill<<<ga, 256, 0, st>>>(na, N, cell_of_atom, cfill, catoms);
+    PL_CUDA(launch_pdl(k_cell_count, dim3(ga), dim3(256), 0, st, B, N, box, g, q, cell_of_atom, ccount));
+    PL_CUDA(launch_pdl(k_cell_scan, dim3(1), dim3(1024), 0, st, nc, ccount, cstart, cfill));
+    PL_CUDA(launch_pdl(k_cell_fill, dim3(ga), dim3(256), 0, st, na, N, cell_of_atom, cfill, catoms));
     static const bool warp_cells = !getenv("PL_NEIGH_THREAD");
     if (warp_cells)
-      k_neigh_cell_w<<<(unsigned)((na + NC_WARPS - 1) / NC_WARPS), NC_WARPS * 32, 0, st>>>(
-          B, N, box, g, rc2, maxn, q, cell_of_atom, cstart, catoms, out->nbr, out->cnt, out->overflow);
+      PL_CUDA(launch_pdl(k_neigh_cell_w, dim3((unsigned)((na + NC_WARPS - 1) / NC_WARPS)), dim3(NC_WARPS * 32), 0, st,
+                         B, N, box, g, rc2, maxn, q, cell_of_atom, cstart, catoms, out->nbr, out->cnt,
+                         out->overflow));
     else
       k_neigh_cell<<<(unsigned)((na + 127) / 128), 128, 0, st>>>(B, N, box, g, rc2, maxn, q, cell_of_atom,
                                                                 cstart, catoms, out->nbr, out->cnt, out->overflow);

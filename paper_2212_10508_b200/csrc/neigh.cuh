@@ -91,6 +91,7 @@ k_neigh_brute(int64_t B, int N, Box box, double rc2, int maxn, const double* __r
 static __global__ void __launch_bounds__(NB_THREADS)
 k_neigh_brute_w(int64_t B, int N, Box box, double rc2, int maxn, const double* __restrict__ q,
                 int32_t* __restrict__ nbr, int32_t* __restrict__ cnt, int* __restrict__ overflow) {
+  griddep_wait();
   const int64_t t = (blockIdx.x * (int64_t)NB_THREADS + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= B * N) return;

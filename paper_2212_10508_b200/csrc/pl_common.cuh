@@ -30,6 +30,29 @@ int fail(int code, const std::string& msg);
     if (_rc != PL_OK) return _rc; \
   } while (0)
 
+// ---- programmatic dependent launch: the kernels of one force evaluation and
+// the integrator steps around it are launched with programmatic stream
+// serialisation, so a grid's launch is processed while its predecessor runs;
+// every such kernel waits for the predecessor's completion (griddep_wait) before
+// it touches memory, so the ordering is the stream's.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- exact-order fp64 arithmetic: no FMA contraction on the parity path.
 // numpy evaluates left to right with one rounding per operation
 // (integrator.py:174-177, rng.py:130-135); these intrinsics pin that.

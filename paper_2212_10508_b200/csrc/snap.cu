@@ -2254,6 +2254,7 @@ __device__ __forceinline__ void ui4_layers(C2 (&u)[9], C2 (&u4)[9], const RowGeo
 __global__ void __launch_bounds__(UI4_WARPS * 32)
 k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
              const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn, C2* __restrict__ utot) {
+  griddep_wait();
   constexpr int TJ = 8, R = 4, P = 8;
   extern __shared__ double smem[];
   double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
@@ -2640,6 +2641,7 @@ __device__ __forceinline__ C2 y_full(const C2* y, int J, int base, int r, int c)
 // Y^dagger, half rows stored column-interleaved: yt[J][ma][mb] = conj(Y[J][ma][mb])
 // for mb <= J/2 (element (mb, ma) of the Y^dagger half rows)
 __global__ void k_snap_ytrans(int64_t natoms, int nh, int tj, const C2* __restrict__ y, C2* __restrict__ yt) {
+  griddep_wait();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= natoms * nh) return;
   const int64_t atom = t / nh;
@@ -2677,6 +2679,7 @@ __global__ void __launch_bounds__(NWB * 32)
 k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
                    const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
                    const C2* __restrict__ ylist, const C2* __restrict__ ytlist, double* __restrict__ dedr) {
+  griddep_wait();
   constexpr int TJ = 8, R = 4, P = 8;
   extern __shared__ double smem[];
   double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
@@ -2851,6 +2854,7 @@ __global__ void __launch_bounds__(NWB * 32)
 k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
                   const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
                   const C2* __restrict__ ylist, const C2* __restrict__ ytlist, double* __restrict__ dedr) {
+  griddep_wait();
   constexpr int TJ = 8, R = 4, P = 8;
   extern __shared__ double smem[];
   double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
@@ -3028,6 +3032,7 @@ __global__ void __launch_bounds__(128)
 k_snap_gather_pair_w(int64_t natoms, int N, Box box, const double* __restrict__ q,
                      const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
                      const double* __restrict__ dedr, double* __restrict__ grad, double* __restrict__ vatom) {
+  griddep_wait();
   const int64_t atom = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (atom >= natoms) return;
@@ -3144,6 +3149,7 @@ __global__ void k_snap_gather(int64_t natoms, int N, Box box, const double* __re
 
 __global__ void k_sys_sum(int64_t B, int N, int width, const double* __restrict__ per_atom,
                           double* __restrict__ out) {
+  griddep_wait();
   __shared__ double sh[256];
   int64_t b = blockIdx.x;
   for (int c = 0; c < width; ++c) {
@@ -3250,8 +3256,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     }();
     if (ui4 && S->tj == 8) {
       const size_t sm4 = rp_bytes + sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2) + sizeof(double) * UI4_WARPS * SNAP_MAXN * 5;
-      k_snap_ui_r4<<<(unsigned)((na + UI4_WARPS - 1) / UI4_WARPS), UI4_WARPS * 32, sm4, ctx->stream>>>(
-          D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.utot);
+      PL_CUDA(launch_pdl(k_snap_ui_r4, dim3((unsigned)((na + UI4_WARPS - 1) / UI4_WARPS)), dim3(UI4_WARPS * 32), sm4,
+                         ctx->stream, D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.utot));
     } else if (ui_reg)
       k_snap_ui_rr<8, true><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
                                                                           nl.maxn, buf.utot);
@@ -3322,7 +3328,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   }();
   if (rr && adj_env && adj4 && pair_env && S->tj == 8) {
     const int64_t nel = na * D.nhalf;
-    k_snap_ytrans<<<(unsigned)((nel + 255) / 256), 256, 0, ctx->stream>>>(na, D.nhalf, D.tj, buf.y, buf.yt);
+    PL_CUDA(launch_pdl(k_snap_ytrans, dim3((unsigned)((nel + 255) / 256)), dim3(256), 0, ctx->stream, na, D.nhalf,
+                       D.tj, buf.y, buf.yt));
     PL_CHECK_LAUNCH();
     static const int prun = [] {
       const char* e = getenv("PL_SNAP_PAIR_RUN");
@@ -3334,15 +3341,15 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
                         (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
                         sizeof(int16_t) * PAIR_WARPS * RUN * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (RUN + 2);
       const unsigned grid = (unsigned)((na + PAIR_WARPS * RUN - 1) / (PAIR_WARPS * RUN));
-      k_snap_deidrj_run<RUN, PAIR_WARPS><<<grid, PAIR_WARPS * 32, sm, ctx->stream>>>(
-          D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr);
+      PL_CUDA(launch_pdl(k_snap_deidrj_run<RUN, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), sm, ctx->stream, D,
+                         na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
     } else {
       const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
                         (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
                         sizeof(int32_t) * PAIR_WARPS * 2 * SNAP_MAXN;
       const unsigned grid = (unsigned)((na + PAIR_WARPS * 2 - 1) / (PAIR_WARPS * 2));
-      k_snap_deidrj_pair<2, PAIR_WARPS><<<grid, PAIR_WARPS * 32, sm, ctx->stream>>>(
-          D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr);
+      PL_CUDA(launch_pdl(k_snap_deidrj_pair<2, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), sm, ctx->stream, D,
+                         na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
     }
     buf.pair = true;
   } else if (rr && adj_env && adj4 && S->tj == 8) {
@@ -3389,18 +3396,18 @@ int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double
   Box box = make_box(pot->box);
   prof_mark(ctx->stream, ST_GATHER, true);
   if (buf.pair)
-    k_snap_gather_pair_w<<<(unsigned)((na * 32 + 127) / 128), 128, 0, ctx->stream>>>(
-        na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr);
+    PL_CUDA(launch_pdl(k_snap_gather_pair_w, dim3((unsigned)((na * 32 + 127) / 128)), dim3(128), 0, ctx->stream, na,
+                       N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr));
   else
     k_snap_gather<<<(unsigned)((na + 127) / 128), 128, 0, ctx->stream>>>(
         na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr);
   PL_CHECK_LAUNCH();
   if (energy) {
-    k_sys_sum<<<(unsigned)B, 256, 0, ctx->stream>>>(B, N, 1, buf.eatom, energy);
+    PL_CUDA(launch_pdl(k_sys_sum, dim3((unsigned)B), dim3(256), 0, ctx->stream, B, N, 1, buf.eatom, energy));
     PL_CHECK_LAUNCH();
   }
   if (virial) {
-    k_sys_sum<<<(unsigned)B, 256, 0, ctx->stream>>>(B, N, 6, buf.vatom, virial);
+    PL_CUDA(launch_pdl(k_sys_sum, dim3((unsigned)B), dim3(256), 0, ctx->stream, B, N, 6, buf.vatom, virial));
     PL_CHECK_LAUNCH();
   }
   prof_mark(ctx->stream, ST_GATHER, false);

@@ -21,6 +21,25 @@
 
 namespace pl {
 
+__device__ __forceinline__ void griddep_wait_yi() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// programmatic dependent launch (see pl_common.cuh launch_pdl)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl_yi(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 namespace yib {
 constexpr int TJ = 8;
 constexpr int NT = 125;        // (X >= Y, J) triples at twojmax 8
@@ -144,6 +163,7 @@ template <int NW, int V, int S>
 __global__ void __maxnreg__(box_regs(NW))
 k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, const Cx* __restrict__ utot,
               Cx* __restrict__ ylist, double* __restrict__ eatom, double* __restrict__ erow_g) {
+  griddep_wait_yi();
   extern __shared__ double smem[];
   Cx* Uf = reinterpret_cast<Cx*>(smem);                 // [NFULL][32] full U matrices
   Cx* Ys = Uf + yib::NFULL * yib::ATOMS;               // [NHALF][32] Y half rows
@@ -286,6 +306,7 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
 // split mode: E_i = beta0 + sum over rows in row order (the S = 1 arithmetic)
 __global__ void k_box_energy(int64_t natoms, double beta0, const double* __restrict__ erow_g,
                              double* __restrict__ eatom) {
+  griddep_wait_yi();
   for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < natoms; a += (int64_t)gridDim.x * blockDim.x) {
     double e = beta0;
     for (int r = 0; r < BOX_ROWS; ++r) e += erow_g[(int64_t)r * natoms + a];
@@ -332,9 +353,13 @@ static cudaError_t box_launch(cudaStream_t st, int64_t natoms, double beta0, con
     attr = true;
   }
   const unsigned grid = (unsigned)(S * ((natoms + yib::ATOMS - 1) / yib::ATOMS));
-  k_snap_yi_box<NW, V, S><<<grid, NW * 32, sm, st>>>(natoms, beta0, coef, (const Cx*)utot, (Cx*)ylist, eatom,
-                                                     erow_g);
-  if (S > 1) k_box_energy<<<(unsigned)((natoms + 255) / 256), 256, 0, st>>>(natoms, beta0, erow_g, eatom);
+  cudaError_t e = launch_pdl_yi(k_snap_yi_box<NW, V, S>, dim3(grid), dim3(NW * 32), sm, st, natoms, beta0, coef,
+                                (const Cx*)utot, (Cx*)ylist, eatom, erow_g);
+  if (e != cudaSuccess) return e;
+  if (S > 1)
+    e = launch_pdl_yi(k_box_energy, dim3((unsigned)((natoms + 255) / 256)), dim3(256), 0, st, natoms, beta0,
+                      (const double*)erow_g, eatom);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
