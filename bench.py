@@ -399,14 +399,20 @@ def parareal_run():
     snap = W.make_snap(n, box)
     pair = pl.PropagatorPair(snap, eam, 100.0, 1.0)
     cfg = pl.PararealConfig(N, 1e-10, 0.35)   # delta_conv / delta_expl of configs/adaptive.json
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    try:
-        res = pl.parareal_adaptive(init, pair, params, sched, plan, cfg)
-    except Exception as exc:  # report, do not fail the bench
-        return {"error": f"{type(exc).__name__}: {exc}"}
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t
+    # the first run pays the one-time setup (SNAP index tables and Y-row schedules,
+    # buffer allocations); wall_s is a second, warm run (every engine run starts
+    # from an empty fine-window cache, so nothing carries over but the setup)
+    walls = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        try:
+            res = pl.parareal_adaptive(init, pair, params, sched, plan, cfg)
+        except Exception as exc:  # report, do not fail the bench
+            return {"error": f"{type(exc).__name__}: {exc}"}
+        torch.cuda.synchronize()
+        walls.append(time.perf_counter() - t)
+    wall = walls[1]
     # measured per-window costs C_f / C_c (one window, device-resident, CUDA events)
     # and the reference cost model's gain Gamma (accounting.py:141-159)
     from paper_2212_10508_b200 import accounting
@@ -429,7 +435,7 @@ def parareal_run():
     cf, cc = window_ms(snap), window_ms(eam)
     g = accounting.adaptive_gain(res.slabs, N, cf, cc)
     return {"config": "PR1: 129 atoms, 16 slices x 100, SNAP fine / EAM coarse, delta_conv 1e-10, "
-                      "delta_expl 0.35", "wall_s": wall, "n_slab": res.n_slab,
+                      "delta_expl 0.35", "wall_s": wall, "wall_s_cold": walls[0], "n_slab": res.n_slab,
             "sum_k": res.total_iterations, "converged": res.converged,
             "cf_ms": cf, "cc_ms": cc, "gain_model": g.gain, "gain_ideal": g.ideal_gain,
             "sequential_fine_s": N * cf / 1e3, "speedup_vs_sequential_fine": (N * cf / 1e3) / wall}
