@@ -2669,11 +2669,12 @@ constexpr int PAIR_GEO = 12;   // doubles of geometry per pair (k_snap_deidrj_pa
 // staged in shared memory, Y_k^dagger read through L1/L2; F is accumulated in
 // the backward sweep (AdjR4 LAZY) so every Y element is read once; Y^dagger is
 // column-interleaved so the 4 row lanes of a pair read 64 contiguous bytes.
-// Measured (1025 atoms x 64): 1.50 ms vs 1.78 ms for adj4 at 0.6x its
-// instructions; the global Y_k^dagger loads (long-scoreboard stalls) hold the
-// issue rate at 28 %.  Staging Y_k^dagger in shared memory (cp.async during the
-// forward pass, or Y_i + Y_k^dagger per slot) costs occupancy (5 warps/SM) and
-// measured slower (1.88 / 2.16 ms), as did L1 prefetch one layer ahead (1.63 ms).
+// Used for batches under 4 waves of runs (k_snap_deidrj_run otherwise).  At the
+// larger config (1025 atoms x 64) this form took 1.30 ms against 1.78 ms for
+// adj4 (0.6x its instructions); the global Y_k^dagger loads (long-scoreboard
+// stalls) hold the issue rate near 30 %.  Staging Y_k^dagger in shared memory
+// (cp.async during the forward pass, Y_i + Y_k^dagger per slot, or through the
+// dead history slots) cost occupancy or barriers and measured slower.
 template <int APW, int NWB>
 __global__ void __launch_bounds__(NWB * 32)
 k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
