@@ -166,6 +166,7 @@ k_neigh_cell_w(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, cons
   s_beg[warp][lane] = beg;
   __syncwarp();
   int nf = 0;
+#pragma unroll 4
   for (int base = 0; base < total; base += 32) {
     const int idx = base + lane;
     bool hit = false;
