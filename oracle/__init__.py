@@ -23,8 +23,12 @@ Parity pins: ``rng``/``integrator``/``parareal``/``toy`` are checked bit for
 bit against golden vectors produced by the reference itself in the build
 container (``scripts/make_golden.py`` -> ``tests/golden/``).  SNAP/EAM/neighbour
 lists have no reference implementation ("parity unpinned" w.r.t. the
-reference); they are pinned by finite differences, rotation/translation/
-permutation invariance, Sum F = 0, an independent slow bispectrum built from
-explicit polynomial representations, and the index counts of SURVEY.md
-Appendix B.
+reference); the C SNAP oracle is pinned externally by
+``tests/test_snap_oracle_pin.py``: its Clebsch-Gordan coefficients against
+``sympy.physics.wigner.clebsch_gordan`` (all 4,451 with 2j <= 8), its U
+recursion against the spin-J/2 representation built from explicit polynomials
+(itself checked against sympy's ``wigner_d``), its per-atom bispectrum against
+a slow numpy/sympy evaluation on open clusters, its forces against central
+differences and rotation covariance.  Neighbour lists are checked by counts on
+the perfect lattice and EAM by the FS-W cohesive energy.
 """

@@ -53,26 +53,53 @@ def _bounded(q, p):
     return bool((np.abs(q) <= BLOWUP_LIMIT).all() and (np.abs(p) <= BLOWUP_LIMIT).all())
 
 
+class WindowStepper:
+    """One window advanced in chunks of substeps (the bench's bounded CPU samples).
+
+    Exactly the arithmetic of ``propagate_window`` (integrator.py:259-289):
+    ``open()`` evaluates grad(q0); ``advance(k)`` runs the next k substeps.
+    propagate_window below is open() + advance(L), so the goldens pin both.
+    """
+
+    def __init__(self, q, p, grad_fn, gamma, inv_beta, dt, substeps, schedule, seed,
+                 mass=None, noise=None):
+        self.q = np.asarray(q, dtype=float)
+        self.p = np.asarray(p, dtype=float)
+        d = self.q.shape[0]
+        self.mass = np.ones(d) if mass is None else np.asarray(mass, dtype=float)
+        sqrt_m = np.sqrt(self.mass)
+        self.amps = [amplitude(gamma, inv_beta, dt, c) * sqrt_m for c in schedule]
+        if noise is None:
+            noise = rng.gaussian_stream(seed, (substeps + 1) * d)
+        self.g = np.asarray(noise, dtype=float).reshape(substeps + 1, d)
+        self.grad_fn, self.gamma, self.dt, self.L = grad_fn, gamma, dt, substeps
+        self.l = 0
+        self.grad = None
+        self.p_ref = self.p
+
+    def open(self):
+        self.grad = self.grad_fn(self.q)
+
+    def advance(self, k):
+        q, p, grad, p_ref = self.q, self.p, self.grad, self.p_ref
+        dt, gamma, mass, amps, g = self.dt, self.gamma, self.mass, self.amps, self.g
+        for l in range(self.l, min(self.L, self.l + k)):
+            p_half = p - 0.5 * dt * grad - 0.5 * dt * gamma * p_ref + amps[l] * g[l]
+            q = q + dt * (p_half / mass)
+            grad = self.grad_fn(q)
+            p = p_half - 0.5 * dt * grad - 0.5 * dt * gamma * p_half + amps[l + 1] * g[l + 1]
+            if not _bounded(q, p):
+                raise OracleBlowUp(l + 1)
+            p_ref = p_half
+            self.l = l + 1
+        self.q, self.p, self.grad, self.p_ref = q, p, grad, p_ref
+        return self.l == self.L
+
+
 def propagate_window(q, p, grad_fn, gamma, inv_beta, dt, substeps, schedule, seed,
                      mass=None, noise=None):
     """One window; returns (q, p).  ``noise`` ((L+1)*d) may be injected."""
-    q = np.asarray(q, dtype=float)
-    p = np.asarray(p, dtype=float)
-    d = q.shape[0]
-    mass = np.ones(d) if mass is None else np.asarray(mass, dtype=float)
-    sqrt_m = np.sqrt(mass)
-    amps = [amplitude(gamma, inv_beta, dt, c) * sqrt_m for c in schedule]
-    if noise is None:
-        noise = rng.gaussian_stream(seed, (substeps + 1) * d)
-    g = np.asarray(noise, dtype=float).reshape(substeps + 1, d)
-    grad = grad_fn(q)
-    p_ref = p
-    for l in range(substeps):
-        p_half = p - 0.5 * dt * grad - 0.5 * dt * gamma * p_ref + amps[l] * g[l]
-        q = q + dt * (p_half / mass)
-        grad = grad_fn(q)
-        p = p_half - 0.5 * dt * grad - 0.5 * dt * gamma * p_half + amps[l + 1] * g[l + 1]
-        if not _bounded(q, p):
-            raise OracleBlowUp(l + 1)
-        p_ref = p_half
-    return q, p
+    w = WindowStepper(q, p, grad_fn, gamma, inv_beta, dt, substeps, schedule, seed, mass=mass, noise=noise)
+    w.open()
+    w.advance(substeps)
+    return w.q, w.p

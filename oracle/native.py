@@ -43,6 +43,11 @@ def load():
             _lib.orc_snap.restype = C.c_int
             _lib.orc_snap.argtypes = [C.c_int, pd, C.c_int, C.c_double, C.c_double, C.c_double,
                                       C.c_int, C.c_double, pd, C.c_int, pd, pd, pd, pd, pd]
+        if hasattr(_lib, "orc_ulist"):
+            _lib.orc_ulist.restype = C.c_int
+            _lib.orc_ulist.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, pd, pd]
+        _lib.orc_cg.restype = C.c_double
+        _lib.orc_cg.argtypes = [C.c_int] * 6
     return _lib
 
 
@@ -102,6 +107,28 @@ def snap(q, box, pot, want_bispectrum=False):
     if rcode < 0:
         raise RuntimeError(f"oracle SNAP failed ({rcode})")
     return (e[0], g, v, bs) if want_bispectrum else (e[0], g, v)
+
+
+def ulist(twojmax, rfac0, rmin0, rcut, rv):
+    """U^J of one neighbour vector as a list of full (J+1)x(J+1) complex matrices
+    indexed [ma][mb] (the oracle's recursion, snap_oracle.c u_and_du)."""
+    lib = load()
+    size = sum((J + 1) ** 2 for J in range(twojmax + 1))
+    out = np.zeros(2 * size)
+    lib.orc_ulist(int(twojmax), float(rfac0), float(rmin0), float(rcut), _d(np.asarray(rv, float)),
+                  out.ctypes.data_as(pd))
+    u = out[0::2] + 1j * out[1::2]
+    mats, o = [], 0
+    for J in range(twojmax + 1):
+        m = u[o:o + (J + 1) ** 2].reshape(J + 1, J + 1)  # stored [mb][ma]
+        mats.append(m.T.copy())
+        o += (J + 1) ** 2
+    return mats
+
+
+def cg(j1, m1, j2, m2, J, M):
+    """Clebsch-Gordan <j1 m1 j2 m2 | J M> of the oracle (arguments are 2j / 2m)."""
+    return load().orc_cg(j1, m1, j2, m2, J, M)
 
 
 def snap_fn(pot):

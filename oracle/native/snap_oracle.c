@@ -357,3 +357,13 @@ int orc_snap(int n, const double* box, int twojmax, double rcut, double rfac0, d
   free(nbr); free(cnt); free(Ut); free(Y); free(U); free(dU); free(Z); free(dEdr);
   return nb;
 }
+
+/* U^J (full layers J = 0..twojmax, [J][mb][ma] order, interleaved re/im) of one
+ * neighbour vector rv, for the external pins of the recursion (tests only). */
+int orc_ulist(int twojmax, double rfac0, double rmin0, double rcut, const double* rv, double* out) {
+  if (twojmax > JMAX) return -1;
+  init_offsets(twojmax);
+  int size = moff[twojmax + 1];
+  u_and_du(twojmax, rfac0, rmin0, rcut, rv, (cplx*)out, NULL, size);
+  return size;
+}

@@ -16,7 +16,7 @@
 //   * Lennard-Jones clusters: one CTA owns one window, positions in shared
 //     memory, all L substeps in one launch;
 //   * periodic many-body (EAM/SNAP/mixtures): per substep, the batched force
-//     pipeline over all W windows, then one fused close+open kernel.
+//     pipeline over all W windows, then one fused close(s)+open(s+1) kernel.
 #include <climits>
 
 #include "pl_common.cuh"
@@ -211,6 +211,38 @@ __global__ void k_close(int64_t W, int64_t d, int s, StepConsts K, const double*
   }
 }
 
+// close substep s and open substep s+1 in one pass: both read noise block s
+// (block s closes s and reopens s+1, integrator.py:281-288) and the same grad
+// and p_half, so one kernel moves 56 B per component instead of 96 B for
+// k_close + k_open.  Same operations in the same order as the two kernels.
+__global__ void k_close_open(int64_t W, int64_t d, int s, StepConsts K, const double* __restrict__ amp,
+                             const double* __restrict__ noise, const double* __restrict__ mass,
+                             const double* __restrict__ grad, double* __restrict__ ph,
+                             double* __restrict__ q, double* __restrict__ p, int32_t* __restrict__ blow,
+                             double* __restrict__ s1, double* __restrict__ s2) {
+  griddep_wait();
+  int64_t n = W * d;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t w = t / d, i = t - w * d;
+    const double m = mass ? mass[i] : 1.0;
+    const double smm = mass ? __dsqrt_rn(m) : 1.0;
+    const double al = mul(amp[s], smm);
+    const double gl = noise[(w * (K.L + 1) + s) * d + i];
+    const double g = grad[t];
+    const double h = ph[t];
+    const double qv = q[t];
+    const double pn = add(sub(sub(h, mul(K.h, g)), mul(K.hg, h)), mul(al, gl));
+    p[t] = pn;
+    if (!(bounded(qv) && bounded(pn))) record_blowup(blow, w, s);
+    if (s1) moment(s1, s2, (w * K.L + (s - 1)) * d + i, pn);
+    // open s + 1: p_ref = p_half of substep s
+    const double hn = add(sub(sub(pn, mul(K.h, g)), mul(K.hg, h)), mul(al, gl));
+    ph[t] = hn;
+    q[t] = add(qv, mul(K.dt, dvd(hn, m)));
+  }
+}
+
 static unsigned grid_for(int64_t n, int threads = 256) {
   int64_t b = (n + threads - 1) / threads;
   if (b > 148 * 32) b = 148 * 32;
@@ -276,15 +308,19 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
   if (p1 != p0) PL_CUDA(cudaMemcpyAsync(p1, p0, sizeof(double) * nd, cudaMemcpyDeviceToDevice, st));
   PL_TRY(compute(pot, W, d, q1, nullptr, grad, nullptr));
   unsigned g = grid_for((int64_t)nd);
+  prof_mark(st, ST_INT, true);
+  PL_CUDA(launch_pdl(k_open, dim3(g), dim3(256), 0, st, W, d, 1, true, K, amp, noise, mass, grad, p1, ph, q1));
+  PL_CHECK_LAUNCH();
+  prof_mark(st, ST_INT, false);
   for (int s = 1; s <= L; ++s) {
-    prof_mark(st, ST_INT, true);
-    PL_CUDA(launch_pdl(k_open, dim3(g), dim3(256), 0, st, W, d, s, s == 1, K, amp, noise, mass, grad, p1, ph, q1));
-    PL_CHECK_LAUNCH();
-    prof_mark(st, ST_INT, false);
     PL_TRY(compute(pot, W, d, q1, nullptr, grad, nullptr));
     prof_mark(st, ST_INT, true);
-    PL_CUDA(launch_pdl(k_close, dim3(g), dim3(256), 0, st, W, d, s, K, amp, noise, mass, grad, ph, q1, p1, blow, s1,
-                       s2));
+    if (s < L)
+      PL_CUDA(launch_pdl(k_close_open, dim3(g), dim3(256), 0, st, W, d, s, K, amp, noise, mass, grad, ph, q1, p1,
+                         blow, s1, s2));
+    else
+      PL_CUDA(launch_pdl(k_close, dim3(g), dim3(256), 0, st, W, d, s, K, amp, noise, mass, grad, ph, q1, p1, blow,
+                         s1, s2));
     PL_CHECK_LAUNCH();
     prof_mark(st, ST_INT, false);
   }

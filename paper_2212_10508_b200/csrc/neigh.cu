@@ -121,7 +121,7 @@ k_neigh_cell(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, const 
   int32_t* my = nbr + t * maxn;
   for (int a = 0; a < outn; ++a) my[a] = found[a];
   cnt[t] = outn;
-  if (nf > maxn) atomicExch(overflow, 1);
+  if (nf > outn) atomicExch(overflow, 1);  // also when nf exceeds the CELL_MAXN buffer
 }
 
 // one warp per atom: lane c < 27 owns neighbour cell c, a warp scan of the cell
@@ -202,7 +202,7 @@ k_neigh_cell_w(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, cons
   }
   if (lane == 0) {
     cnt[t] = outn;
-    if (nf > maxn) atomicExch(overflow, 1);
+    if (nf > outn) atomicExch(overflow, 1);  // also when nf exceeds the CELL_MAXN buffer
   }
 }
 

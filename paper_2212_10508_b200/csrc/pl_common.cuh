@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -51,6 +52,16 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// ---- once-per-device setup (function attributes, __constant__ tables): true
+// the first time it is called on the current device for this mask.  Device
+// state is per device, so a process-wide flag would skip a second GPU.
+inline bool first_on_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const uint64_t bit = 1ull << dev;
+  return (mask.fetch_or(bit) & bit) == 0;
 }
 
 // ---- exact-order fp64 arithmetic: no FMA contraction on the parity path.

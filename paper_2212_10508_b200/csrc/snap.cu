@@ -45,14 +45,12 @@ constexpr int DE_WARPS = 4;
 constexpr int YI_THREADS = 256;
 constexpr int YI_ATOMS = 32;                 // lanes = atoms in k_snap_yi
 constexpr int YI_WARPS = YI_THREADS / 32;
-constexpr int YI3_WARPS = 16;                // k_snap_yi_full: 512 threads, one CTA per SM
 
 struct SnapItem {      // one half-row element of one Z^{xy}_J
   int16_t x, y, J, ma, mb;
   int16_t ma1lo, na, mb1lo, nb;
   int16_t bidx;        // canonical B index or -1
   int32_t cga, cgb;    // offsets into the CG pool (na, nb values)
-  int32_t cgblk;       // offset of the (x,y,J) block [(J+1) x (x+1)] in c_cgt (dense table)
   double coefY;        // weight of this Z element in Y^J (0 if none)
   double coefE;        // beta_b * w(ma,mb) if canonical, else 0
   double w;            // half-row weight
@@ -75,8 +73,7 @@ struct SnapIndex {
   double beta0 = 0.0;
   double flops_ui_pair = 0, flops_yi_atom = 0, flops_de_pair = 0;
   double flops_de_pair_adj = 0, flops_yi_atom_reg = 0;
-  bool cgt_fits = false;
-  bool yi_reg = false;  // k_snap_yi_reg usable (twojmax = 8, CG table in constant memory)
+  bool yi_reg = false;  // box-form Y tables set up (twojmax = 8)
   double* d_yi5 = nullptr;  // [2][NT]: coefY(X,Y,J), beta_b of canonical triples (else 0)
 };
 
@@ -119,54 +116,11 @@ __device__ __forceinline__ void half_layer8(int t, int& J, int& base) {
     }
 }
 __constant__ int c_foff[SNAP_JMAX + 2];
-// dense Clebsch-Gordan blocks C(x m1, y m2 | J M) as [M-row][m1] per (x, y, J),
-// x >= y, read with warp-uniform addresses by k_snap_yi (36.7 KB at twojmax 8)
-constexpr int CGT_MAX = 5000;  // doubles (40 KB; twojmax = 8 needs 4698)
-__constant__ double c_cgt[CGT_MAX];
-
-namespace yi5 {
-constexpr int TJ = 8;
-constexpr int foff(int J) { return J * (J + 1) * (2 * J + 1) / 6; }
-constexpr int hoff(int J) {
-  int h = 0;
-  for (int j = 0; j < J; ++j) h += (j + 1) * (j / 2 + 1);
-  return h;
-}
-constexpr int cgoff(int X, int Y, int J) {  // offset of block (X, Y, J) in c_cgt
-  int o = 0;
-  for (int x = 0; x <= TJ; ++x)
-    for (int y = 0; y <= x; ++y)
-      for (int j = x - y; j <= (TJ < x + y ? TJ : x + y); j += 2) {
-        if (x == X && y == Y && j == J) return o;
-        o += (j + 1) * (x + 1);
-      }
-  return -1;
-}
-constexpr int ntriples() {
-  int n = 0;
-  for (int x = 0; x <= TJ; ++x)
-    for (int y = 0; y <= x; ++y)
-      for (int j = x - y; j <= (TJ < x + y ? TJ : x + y); j += 2) ++n;
-  return n;
-}
-constexpr int NT = ntriples();
-}  // namespace yi5
-
-constexpr int YI5_WARPS = 8;
-__constant__ int c_yi5_code[130];     // triple id -> X*100 + Y*10 + J
-__constant__ int c_yi5_jstart[yi5::TJ + 2];  // triples of row-layer J: [jstart[J], jstart[J+1]) in tlist
-__constant__ int c_yi5_tlist[130];    // triple ids sorted by J
-__constant__ int c_yi5_gseg[YI5_WARPS + 1];  // groups of warp w
-__constant__ int c_yi5_groups[32];    // (J << 8) | mb
-__constant__ int c_yi5_cgoff[130];    // triple id -> offset of its block in c_cgt
-constexpr int YI6_WARPS = 16;
-__constant__ int c_yi6_gseg[YI6_WARPS + 1];
-__constant__ int c_yi6_groups[32];
 // box-form Z/Y kernel (snap_yi8.cu, own constant bank)
 cudaError_t snap_box_setup(const double* box, int nbox, const int* off, const int* code, const int* iseg,
                            const int* items, int nitems, const int* rowsplit);
 int snap_box_variants(int* nw, int* ns);
-cudaError_t snap_box_launch(int nw, cudaStream_t st, int64_t natoms, double beta0, const double* coef,
+cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef,
                             const void* utot, void* ylist, double* eatom, double* erow_g);
 
 // ------------------------------------------------------------------ host setup
@@ -243,31 +197,10 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     coefY[{J, j2, j1}] += bb * (double)(J + 1) / (double)(j1 + 1);   // slot j1
     coefY[{J, j1, j2}] += bb * (double)(J + 1) / (double)(j2 + 1);   // slot j2
   }
-  // dense CG blocks per (x, y, J)
-  std::map<std::tuple<int, int, int>, int> cgblk;
-  std::vector<double> cgt;
-  for (int x = 0; x <= tj; ++x)
-    for (int y = 0; y <= x; ++y)
-      for (int J = x - y; J <= std::min(tj, x + y); J += 2) {
-        cgblk[{x, y, J}] = (int)cgt.size();
-        for (int ma = 0; ma <= J; ++ma)
-          for (int m1 = 0; m1 <= x; ++m1) {
-            int M = 2 * ma - J, mm1 = 2 * m1 - x, m2 = M - mm1;
-            cgt.push_back(std::abs(m2) <= y ? clebsch(x, mm1, y, m2, J, M) : 0.0);
-          }
-      }
-  // the constant table's layout depends on twojmax: the first SNAP potential of
-  // the process owns it; potentials with another twojmax use the global CG pool
-  static int g_cgt_tj = -1;
-  S->cgt_fits = cgt.size() <= (size_t)CGT_MAX && (g_cgt_tj < 0 || g_cgt_tj == tj);
-  if (S->cgt_fits && g_cgt_tj < 0) {
-    PL_CUDA(cudaMemcpyToSymbol(c_cgt, cgt.data(), sizeof(double) * cgt.size()));
-    g_cgt_tj = tj;
-  }
-  // register-tiled Y (k_snap_yi_reg, twojmax = 8): per-triple coefficients, rows by J,
-  // LPT schedule of the (J, mb) rows over the CTA's warps
+  // box-form Y (snap_yi8.cu, twojmax = 8): per-triple coefficients, rows by J,
+  // schedule of the (J, mb) rows over the CTA's warps
   S->yi_reg = false;
-  if (tj == 8 && S->cgt_fits) {
+  if (tj == 8) {
     std::vector<double> cy, be;
     std::vector<int> code;
     std::vector<std::vector<int>> byJ(tj + 1);
@@ -283,26 +216,7 @@ int snap_prepare(pl_pot* pot, const double* beta) {
           code.push_back(x * 100 + y * 10 + J);
           byJ[J].push_back(tid);
         }
-    std::vector<int> tlist, jstart(tj + 2, 0);
-    for (int J = 0; J <= tj; ++J) {
-      jstart[J] = (int)tlist.size();
-      tlist.insert(tlist.end(), byJ[J].begin(), byJ[J].end());
-    }
-    jstart[tj + 1] = (int)tlist.size();
-    // row costs: sum over the row's triples of nb * (J+1) * (X+1)
-    std::vector<std::pair<double, int>> rows;
-    for (int J = 0; J <= tj; ++J)
-      for (int mb = 0; 2 * mb <= J; ++mb) {
-        double c = 0.0;
-        for (int tid : byJ[J]) {
-          int x = code[tid] / 100, y = (code[tid] / 10) % 10, sh = (x + y - J) / 2;
-          int nb = 0;
-          for (int mb1 = 0; mb1 <= x; ++mb1) nb += (mb + sh - mb1 >= 0 && mb + sh - mb1 <= y);
-          c += (double)nb * (J + 1) * (x + 1) + 20.0;
-        }
-        rows.push_back({c, (J << 8) | mb});
-      }
-    std::sort(rows.begin(), rows.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    std::vector<std::pair<double, int>> rows;  // (cost, J << 8 | mb) of the (J, mb) half rows
     // rows -> NW warps: LPT, then deterministic local search (single moves and
     // pairwise swaps) that lowers the makespan, ties broken by the sum of
     // squared loads.  For 25 rows on 12 warps LPT reaches ~83 % balance, the
@@ -367,12 +281,7 @@ int snap_prepare(pl_pot* pot, const double* beta) {
       }
       gseg[NW] = (int)groups.size();
     };
-    std::vector<int> groups, gseg, groups16, gseg16;
-    lpt(8, groups, gseg);
-    lpt(YI6_WARPS, groups16, gseg16);
     {  // box kernel (snap_yi8.cu): every (X+1)(Y+1) product of each admissible mb1
-      auto rows6 = rows;
-      rows.clear();
       for (int J = 0; J <= tj; ++J)
         for (int mb = 0; 2 * mb <= J; ++mb) {
           double c = 0.0;
@@ -428,9 +337,8 @@ int snap_prepare(pl_pot* pot, const double* beta) {
         items_all.insert(items_all.end(), it.begin(), it.end());
       }
       const int n_items = (int)items_all.size() / box_nv;
-      rows = rows6;
-      static bool box_done = false;
-      if (!box_done) {
+      static std::atomic<uint64_t> box_devs{0};  // __constant__ tables are per device
+      if (first_on_device(box_devs)) {
         std::vector<double> box;
         std::vector<int> boff;
         for (int c : code) {
@@ -442,28 +350,15 @@ int snap_prepare(pl_pot* pot, const double* beta) {
               box.push_back(ma >= 0 && ma <= J ? clebsch(x, 2 * a - x, y, 2 * b - y, J, 2 * ma - J) : 0.0);
             }
         }
-        if ((int)code.size() != yi5::NT) return fail(PL_EARG, "SNAP box tables: unexpected triple count");
+        if ((int)code.size() != 125) return fail(PL_EARG, "SNAP box tables: unexpected triple count");
         PL_CUDA(snap_box_setup(box.data(), (int)box.size(), boff.data(), code.data(), iseg_all.data(),
                                items_all.data(), n_items, rowsplit_all.data()));
-        box_done = true;
       }
     }
-    PL_CUDA(cudaMemcpyToSymbol(c_yi6_gseg, gseg16.data(), sizeof(int) * gseg16.size()));
-    PL_CUDA(cudaMemcpyToSymbol(c_yi6_groups, groups16.data(), sizeof(int) * groups16.size()));
     std::vector<double> cb2(cy);
     cb2.insert(cb2.end(), be.begin(), be.end());
     PL_CUDA(cudaMalloc(&S->d_yi5, sizeof(double) * cb2.size()));
     PL_CUDA(cudaMemcpy(S->d_yi5, cb2.data(), sizeof(double) * cb2.size(), cudaMemcpyHostToDevice));
-    PL_CUDA(cudaMemcpyToSymbol(c_yi5_code, code.data(), sizeof(int) * code.size()));
-    {
-      std::vector<int> offs;
-      for (int c : code) offs.push_back(cgblk[{c / 100, (c / 10) % 10, c % 10}]);
-      PL_CUDA(cudaMemcpyToSymbol(c_yi5_cgoff, offs.data(), sizeof(int) * offs.size()));
-    }
-    PL_CUDA(cudaMemcpyToSymbol(c_yi5_tlist, tlist.data(), sizeof(int) * tlist.size()));
-    PL_CUDA(cudaMemcpyToSymbol(c_yi5_jstart, jstart.data(), sizeof(int) * jstart.size()));
-    PL_CUDA(cudaMemcpyToSymbol(c_yi5_gseg, gseg.data(), sizeof(int) * gseg.size()));
-    PL_CUDA(cudaMemcpyToSymbol(c_yi5_groups, groups.data(), sizeof(int) * groups.size()));
     S->yi_reg = true;
   }
   // items grouped by target half index
@@ -506,7 +401,6 @@ int snap_prepare(pl_pot* pot, const double* beta) {
             it.cgb = (int32_t)pool.size();
             pool.insert(pool.end(), cb.begin(), cb.end());
             it.w = half_weight(J, ma, mb);
-            it.cgblk = cgblk[{x, y, J}];
             it.coefY = cy;
             it.bidx = (int16_t)bidx;
             it.coefE = bidx >= 0 ? beta[bidx + 1] * it.w : 0.0;
@@ -555,13 +449,7 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     tseg[S->nhalf] = pos;
   }
   // targets -> warps of k_snap_yi by longest-processing-time greedy on cost
-  // (the CG table must be known to fit constant memory to pick the kernel)
-  size_t cg_doubles = 0;
-  for (int x = 0; x <= tj; ++x)
-    for (int y = 0; y <= x; ++y)
-      for (int J = x - y; J <= std::min(tj, x + y); J += 2) cg_doubles += (size_t)(J + 1) * (x + 1);
-  const int nwarps = S->cgt_fits ? YI3_WARPS : YI_WARPS;
-  (void)cg_doubles;
+  const int nwarps = YI_WARPS;
   std::vector<std::pair<double, int>> tc;
   for (int t = 0; t < S->nhalf; ++t) {
     double c = 0.0;
@@ -901,616 +789,6 @@ k_snap_yi(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict
     eatom[atom] = e;
   }
 }
-
-// v3: full matrices in shared memory ([285][32 atoms], no symmetry branch in
-// the inner loop), CG from constant memory, strided inner walk.
-__global__ void __launch_bounds__(YI3_WARPS * 32)
-k_snap_yi_full(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
-               double* __restrict__ eatom) {
-  extern __shared__ double smem[];
-  C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
-  double* epart = reinterpret_cast<double*>(Uf + D.nfull * YI_ATOMS);  // [warps][32]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
-  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
-  // stage: half rows -> full matrices, transposed to [element][atom]
-  for (int t = threadIdx.x; t < D.nfull * YI_ATOMS; t += blockDim.x) {
-    const int at = t & (YI_ATOMS - 1), f = t >> 5;
-    int J = 0;
-    while (J < D.tj && f >= c_foff[J + 1]) ++J;
-    const int e = f - c_foff[J], mb = e / (J + 1), ma = e - mb * (J + 1);
-    C2 v{0.0, 0.0};
-    if (at < na_blk) {
-      if (2 * mb <= J) {
-        v = utot[(a0 + at) * D.nhalf + c_hoff[J] + mb * (J + 1) + ma];
-      } else {
-        C2 w = utot[(a0 + at) * D.nhalf + c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
-        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
-      }
-    }
-    Uf[f * YI_ATOMS + at] = v;
-  }
-  __syncthreads();
-  double esum = 0.0;
-  const int64_t atom = a0 + lane;
-  for (int wt = D.wseg[warp]; wt < D.wseg[warp + 1]; ++wt) {
-    const int target = D.wtarget[wt];
-    C2 ysum{0.0, 0.0};
-    for (int k = D.tseg[target]; k < D.tseg[target + 1]; ++k) {
-      const SnapItem it = D.items[k];
-      const int x = it.x, y = it.y, J = it.J, sh = (x + y - J) / 2;
-      const double* cga = c_cgt + it.cgblk + it.ma * (x + 1) + it.ma1lo;
-      const double* cgb = c_cgt + it.cgblk + it.mb * (x + 1) + it.mb1lo;
-      C2 z{0.0, 0.0};
-      for (int jb = 0; jb < it.nb; ++jb) {
-        const int mb1 = it.mb1lo + jb, mb2 = it.mb - mb1 + sh;
-        // U^x[ma1][mb1] walks +1 in ma1, U^y[ma2][mb2] walks -1 (ma2 = ma - ma1 + sh)
-        const C2* px = Uf + (c_foff[x] + mb1 * (x + 1) + it.ma1lo) * YI_ATOMS + lane;
-        const C2* py = Uf + (c_foff[y] + mb2 * (y + 1) + (it.ma - it.ma1lo + sh)) * YI_ATOMS + lane;
-        // two independent accumulator chains (ILP); fixed pairing => deterministic
-        double s0r = 0.0, s0i = 0.0, s1r = 0.0, s1i = 0.0;
-        int ja = 0;
-        for (; ja + 1 < it.na; ja += 2) {
-          const C2 ux0 = px[ja * YI_ATOMS], ux1 = px[(ja + 1) * YI_ATOMS];
-          const C2 uy0 = py[-ja * YI_ATOMS], uy1 = py[-(ja + 1) * YI_ATOMS];
-          const double c0 = cga[ja], c1 = cga[ja + 1];
-          s0r += c0 * (ux0.re * uy0.re - ux0.im * uy0.im);
-          s0i += c0 * (ux0.re * uy0.im + ux0.im * uy0.re);
-          s1r += c1 * (ux1.re * uy1.re - ux1.im * uy1.im);
-          s1i += c1 * (ux1.re * uy1.im + ux1.im * uy1.re);
-        }
-        if (ja < it.na) {
-          const C2 ux0 = px[ja * YI_ATOMS], uy0 = py[-ja * YI_ATOMS];
-          const double c0 = cga[ja];
-          s0r += c0 * (ux0.re * uy0.re - ux0.im * uy0.im);
-          s0i += c0 * (ux0.re * uy0.im + ux0.im * uy0.re);
-        }
-        const C2 sacc{s0r + s1r, s0i + s1i};
-        const double c = cgb[jb];
-        z.re += c * sacc.re;
-        z.im += c * sacc.im;
-      }
-      ysum.re += it.coefY * z.re;
-      ysum.im += it.coefY * z.im;
-      if (it.bidx >= 0) {
-        const C2 uJ = Uf[(c_foff[J] + it.mb * (J + 1) + it.ma) * YI_ATOMS + lane];
-        esum += it.coefE * (uJ.re * z.re + uJ.im * z.im);  // Re(conj(U) z)
-      }
-    }
-    if (lane < na_blk) ylist[atom * D.nhalf + target] = ysum;
-  }
-  epart[warp * YI_ATOMS + lane] = esum;
-  __syncthreads();
-  if (warp == 0 && lane < na_blk) {
-    double e = D.beta0;
-    for (int w = 0; w < YI3_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
-    eatom[atom] = e;
-  }
-}
-
-// v4: half rows in shared memory ([155][32 atoms] = 79 KB -> 2 CTAs per SM).
-// A column mb1 > x/2 of U^x is read through U[ma][mb] = (-1)^(ma+mb)
-// conj(U[x-ma][x-mb]): per jb the two columns are direct or mirrored (warp-
-// uniform), the conjugations select one of four compiled inner loops, and the
-// alternating signs fold into the even/odd accumulator chains.
-template <bool CX, bool CY>
-__device__ __forceinline__ void yi_inner(const C2* px, int sx, const C2* py, int sy, const double* cga, int na,
-                                         double& e_re, double& e_im, double& o_re, double& o_im) {
-  // px/py: first element, sx/sy: element stride (+-YI_ATOMS); conj applied when CX/CY
-  int ja = 0;
-  for (; ja + 1 < na; ja += 2) {
-    const C2 ux0 = px[ja * sx], ux1 = px[(ja + 1) * sx];
-    const C2 uy0 = py[ja * sy], uy1 = py[(ja + 1) * sy];
-    const double c0 = cga[ja], c1 = cga[ja + 1];
-    const double x0i = CX ? -ux0.im : ux0.im, x1i = CX ? -ux1.im : ux1.im;
-    const double y0i = CY ? -uy0.im : uy0.im, y1i = CY ? -uy1.im : uy1.im;
-    e_re += c0 * (ux0.re * uy0.re - x0i * y0i);
-    e_im += c0 * (ux0.re * y0i + x0i * uy0.re);
-    o_re += c1 * (ux1.re * uy1.re - x1i * y1i);
-    o_im += c1 * (ux1.re * y1i + x1i * uy1.re);
-  }
-  if (ja < na) {
-    const C2 ux0 = px[ja * sx], uy0 = py[ja * sy];
-    const double c0 = cga[ja];
-    const double x0i = CX ? -ux0.im : ux0.im, y0i = CY ? -uy0.im : uy0.im;
-    e_re += c0 * (ux0.re * uy0.re - x0i * y0i);
-    e_im += c0 * (ux0.re * y0i + x0i * uy0.re);
-  }
-}
-
-__global__ void __launch_bounds__(YI3_WARPS * 32, 2)
-k_snap_yi_half(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
-               double* __restrict__ eatom) {
-  extern __shared__ double smem[];
-  C2* Us = reinterpret_cast<C2*>(smem);                                // [nhalf][32]
-  double* epart = reinterpret_cast<double*>(Us + D.nhalf * YI_ATOMS);  // [warps][32]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
-  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
-  for (int t = threadIdx.x; t < D.nhalf * YI_ATOMS; t += blockDim.x) {
-    const int at = t / D.nhalf, e = t - at * D.nhalf;
-    Us[e * YI_ATOMS + at] = at < na_blk ? utot[(a0 + at) * D.nhalf + e] : C2{0.0, 0.0};
-  }
-  __syncthreads();
-  double esum = 0.0;
-  const int64_t atom = a0 + lane;
-  const C2* Ul = Us + lane;
-  for (int wt = D.wseg[warp]; wt < D.wseg[warp + 1]; ++wt) {
-    const int target = D.wtarget[wt];
-    C2 ysum{0.0, 0.0};
-    for (int k = D.tseg[target]; k < D.tseg[target + 1]; ++k) {
-      const SnapItem it = D.items[k];
-      const int x = it.x, y = it.y, J = it.J, sh = (x + y - J) / 2;
-      const double* cga = c_cgt + it.cgblk + it.ma * (x + 1) + it.ma1lo;
-      const double* cgb = c_cgt + it.cgblk + it.mb * (x + 1) + it.mb1lo;
-      const int ma2s = it.ma - it.ma1lo + sh;  // ma2 of ja = 0 (then -1 per ja)
-      C2 z{0.0, 0.0};
-      for (int jb = 0; jb < it.nb; ++jb) {
-        const int mb1 = it.mb1lo + jb, mb2 = it.mb - mb1 + sh;
-        const bool mx = 2 * mb1 > x, my = 2 * mb2 > y;
-        // first element addresses and strides ([element][atom] layout)
-        const C2* px;
-        int sx;
-        int sgx = 1;
-        if (!mx) {
-          px = Ul + (c_hoff[x] + mb1 * (x + 1) + it.ma1lo) * YI_ATOMS;
-          sx = YI_ATOMS;
-        } else {
-          px = Ul + (c_hoff[x] + (x - mb1) * (x + 1) + (x - it.ma1lo)) * YI_ATOMS;
-          sx = -YI_ATOMS;
-          sgx = ((it.ma1lo + mb1) & 1) ? -1 : 1;
-        }
-        const C2* py;
-        int sy;
-        int sgy = 1;
-        if (!my) {
-          py = Ul + (c_hoff[y] + mb2 * (y + 1) + ma2s) * YI_ATOMS;
-          sy = -YI_ATOMS;
-        } else {
-          py = Ul + (c_hoff[y] + (y - mb2) * (y + 1) + (y - ma2s)) * YI_ATOMS;
-          sy = YI_ATOMS;
-          sgy = ((ma2s + mb2) & 1) ? -1 : 1;
-        }
-        double e_re = 0.0, e_im = 0.0, o_re = 0.0, o_im = 0.0;
-        switch ((mx ? 2 : 0) | (my ? 1 : 0)) {
-          case 0: yi_inner<false, false>(px, sx, py, sy, cga, it.na, e_re, e_im, o_re, o_im); break;
-          case 1: yi_inner<false, true>(px, sx, py, sy, cga, it.na, e_re, e_im, o_re, o_im); break;
-          case 2: yi_inner<true, false>(px, sx, py, sy, cga, it.na, e_re, e_im, o_re, o_im); break;
-          default: yi_inner<true, true>(px, sx, py, sy, cga, it.na, e_re, e_im, o_re, o_im); break;
-        }
-        // signs: mirrored columns alternate with ja (x: +1 per step, y: -1 per step)
-        const int s0 = sgx * sgy;
-        const int s1 = s0 * (mx ? -1 : 1) * (my ? -1 : 1);
-        const double sr = s0 > 0 ? e_re : -e_re, si = s0 > 0 ? e_im : -e_im;
-        const double tr = s1 > 0 ? o_re : -o_re, ti = s1 > 0 ? o_im : -o_im;
-        const double c = cgb[jb];
-        z.re += c * (sr + tr);
-        z.im += c * (si + ti);
-      }
-      ysum.re += it.coefY * z.re;
-      ysum.im += it.coefY * z.im;
-      if (it.bidx >= 0) {
-        const C2 uJ = Ul[(c_hoff[J] + it.mb * (J + 1) + it.ma) * YI_ATOMS];
-        esum += it.coefE * (uJ.re * z.re + uJ.im * z.im);  // Re(conj(U) z)
-      }
-    }
-    if (lane < na_blk) ylist[atom * D.nhalf + target] = ysum;
-  }
-  epart[warp * YI_ATOMS + lane] = esum;
-  __syncthreads();
-  if (warp == 0 && lane < na_blk) {
-    double e = D.beta0;
-    for (int w = 0; w < YI3_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
-    eatom[atom] = e;
-  }
-}
-
-// v5: register-tiled Z/Y for twojmax = 8.  Work = whole Y rows (J, mb) per warp
-// (LPT schedule).  For every contributing (X, Y) pair one instantiation of
-// yi_xyj<X,Y,J> loads the U^X column mb1 and the U^Y column mb2 into registers
-// once per mb1 and produces all J+1 outputs of the row; all ma / ma1 indices
-// are compile-time, CG coefficients are constant-bank operands at compile-time
-// offsets (c_cgt layout = host enumeration, reproduced by constexpr below).
-
-
-
-template <int X, int Y, int J>
-__device__ __forceinline__ void yi_xyj(const C2* __restrict__ Ul, int mb, double cy, double be,
-                                       C2 (&yacc)[yi5::TJ + 1], double& esum) {
-  constexpr int SH = (X + Y - J) / 2;
-  constexpr int OFF = yi5::cgoff(X, Y, J);
-  constexpr int FX = yi5::foff(X), FY = yi5::foff(Y);
-  C2 z[J + 1];
-#pragma unroll
-  for (int m = 0; m <= J; ++m) z[m] = C2{0.0, 0.0};
-  const bool mid = (2 * mb == J);
-  const int lo = max(0, mb + SH - Y), hi = min(X, mb + SH);
-  for (int mb1 = lo; mb1 <= hi; ++mb1) {
-    const int mb2 = mb + SH - mb1;
-    C2 ux[X + 1], uy[Y + 1];
-    const C2* px = Ul + (FX + mb1 * (X + 1)) * YI_ATOMS;
-    const C2* py = Ul + (FY + mb2 * (Y + 1)) * YI_ATOMS;
-#pragma unroll
-    for (int a = 0; a <= X; ++a) ux[a] = px[a * YI_ATOMS];
-#pragma unroll
-    for (int a = 0; a <= Y; ++a) uy[a] = py[a * YI_ATOMS];
-    const double cb = c_cgt[OFF + mb * (X + 1) + mb1];
-#pragma unroll
-    for (int ma = 0; ma <= J; ++ma) {
-      if (mid && 2 * ma > J) continue;  // zero weight on the middle row's upper half
-      double sr = 0.0, si = 0.0;
-#pragma unroll
-      for (int ma1 = 0; ma1 <= X; ++ma1) {
-        const int ma2 = ma + SH - ma1;
-        if (ma2 < 0 || ma2 > Y) continue;  // folded after unrolling
-        const double c = c_cgt[OFF + ma * (X + 1) + ma1];
-        sr += c * (ux[ma1].re * uy[ma2].re - ux[ma1].im * uy[ma2].im);
-        si += c * (ux[ma1].re * uy[ma2].im + ux[ma1].im * uy[ma2].re);
-      }
-      z[ma].re += cb * sr;
-      z[ma].im += cb * si;
-    }
-  }
-  const C2* pj = Ul + (yi5::foff(J) + mb * (J + 1)) * YI_ATOMS;
-#pragma unroll
-  for (int ma = 0; ma <= J; ++ma) {
-    yacc[ma].re += cy * z[ma].re;
-    yacc[ma].im += cy * z[ma].im;
-    if (be != 0.0) {
-      const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
-      const C2 u = pj[ma * YI_ATOMS];
-      esum += be * w * (u.re * z[ma].re + u.im * z[ma].im);
-    }
-  }
-}
-
-// flat switch (faster than the recursive compare chain): generated per triple id
-#define YI5_CASES(F) \
-  F(0,0,0) F(1,0,1) F(1,1,0) F(1,1,2) F(2,0,2) F(2,1,1) F(2,1,3) F(2,2,0) F(2,2,2) F(2,2,4) \
-  F(3,0,3) F(3,1,2) F(3,1,4) F(3,2,1) F(3,2,3) F(3,2,5) F(3,3,0) F(3,3,2) F(3,3,4) F(3,3,6) \
-  F(4,0,4) F(4,1,3) F(4,1,5) F(4,2,2) F(4,2,4) F(4,2,6) F(4,3,1) F(4,3,3) F(4,3,5) F(4,3,7) \
-  F(4,4,0) F(4,4,2) F(4,4,4) F(4,4,6) F(4,4,8) F(5,0,5) F(5,1,4) F(5,1,6) F(5,2,3) F(5,2,5) \
-  F(5,2,7) F(5,3,2) F(5,3,4) F(5,3,6) F(5,3,8) F(5,4,1) F(5,4,3) F(5,4,5) F(5,4,7) F(5,5,0) \
-  F(5,5,2) F(5,5,4) F(5,5,6) F(5,5,8) F(6,0,6) F(6,1,5) F(6,1,7) F(6,2,4) F(6,2,6) F(6,2,8) \
-  F(6,3,3) F(6,3,5) F(6,3,7) F(6,4,2) F(6,4,4) F(6,4,6) F(6,4,8) F(6,5,1) F(6,5,3) F(6,5,5) \
-  F(6,5,7) F(6,6,0) F(6,6,2) F(6,6,4) F(6,6,6) F(6,6,8) F(7,0,7) F(7,1,6) F(7,1,8) F(7,2,5) \
-  F(7,2,7) F(7,3,4) F(7,3,6) F(7,3,8) F(7,4,3) F(7,4,5) F(7,4,7) F(7,5,2) F(7,5,4) F(7,5,6) \
-  F(7,5,8) F(7,6,1) F(7,6,3) F(7,6,5) F(7,6,7) F(7,7,0) F(7,7,2) F(7,7,4) F(7,7,6) F(7,7,8) \
-  F(8,0,8) F(8,1,7) F(8,2,6) F(8,2,8) F(8,3,5) F(8,3,7) F(8,4,4) F(8,4,6) F(8,4,8) F(8,5,3) \
-  F(8,5,5) F(8,5,7) F(8,6,2) F(8,6,4) F(8,6,6) F(8,6,8) F(8,7,1) F(8,7,3) F(8,7,5) F(8,7,7) \
-  F(8,8,0) F(8,8,2) F(8,8,4) F(8,8,6) F(8,8,8)
-
-__device__ __forceinline__ void yi5_call(int code, double cy, double be, const C2* Ul, int mb,
-                                         C2 (&yacc)[yi5::TJ + 1], double& esum) {
-  // code = X*100 + Y*10 + J
-  switch (code) {
-#define YI5_CASE(X, Y, J) \
-  case X * 100 + Y * 10 + J: yi_xyj<X, Y, J>(Ul, mb, cy, be, yacc, esum); break;
-    YI5_CASES(YI5_CASE)
-#undef YI5_CASE
-    default: break;
-  }
-}
-
-
-
-__global__ void __launch_bounds__(YI5_WARPS * 32, 1)
-k_snap_yi_reg(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
-              double* __restrict__ eatom) {
-  extern __shared__ double smem[];
-  C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
-  double* epart = reinterpret_cast<double*>(Uf + D.nfull * YI_ATOMS);  // [warps][32]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
-  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
-  for (int t = threadIdx.x; t < D.nfull * YI_ATOMS; t += blockDim.x) {
-    const int at = t & (YI_ATOMS - 1), f = t >> 5;
-    int J = 0;
-    while (J < D.tj && f >= c_foff[J + 1]) ++J;
-    const int e = f - c_foff[J], mb = e / (J + 1), ma = e - mb * (J + 1);
-    C2 v{0.0, 0.0};
-    if (at < na_blk) {
-      if (2 * mb <= J) {
-        v = utot[(a0 + at) * D.nhalf + c_hoff[J] + mb * (J + 1) + ma];
-      } else {
-        C2 w = utot[(a0 + at) * D.nhalf + c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
-        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
-      }
-    }
-    Uf[f * YI_ATOMS + at] = v;
-  }
-  __syncthreads();
-  const C2* Ul = Uf + lane;
-  const int64_t atom = a0 + lane;
-  double esum = 0.0;
-  for (int gi = c_yi5_gseg[warp]; gi < c_yi5_gseg[warp + 1]; ++gi) {
-    const int J = c_yi5_groups[gi] >> 8, mb = c_yi5_groups[gi] & 0xff;
-    C2 yacc[yi5::TJ + 1];
-#pragma unroll
-    for (int m = 0; m <= yi5::TJ; ++m) yacc[m] = C2{0.0, 0.0};
-    for (int k = c_yi5_jstart[J]; k < c_yi5_jstart[J + 1]; ++k) {
-      const int tid = c_yi5_tlist[k];
-      yi5_call(c_yi5_code[tid], D.yi5[tid], D.yi5[yi5::NT + tid], Ul, mb, yacc, esum);
-    }
-    if (lane < na_blk) {
-      C2* yo = ylist + atom * D.nhalf + c_hoff[J] + mb * (J + 1);
-#pragma unroll
-      for (int m = 0; m <= yi5::TJ; ++m)
-        if (m <= J) yo[m] = yacc[m];
-    }
-  }
-  epart[warp * YI_ATOMS + lane] = esum;
-  __syncthreads();
-  if (warp == 0 && lane < na_blk) {
-    double e = D.beta0;
-    for (int w = 0; w < YI5_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
-    eatom[atom] = e;
-  }
-}
-
-// v6: small code.  Row work (J, mb) per warp as in v5, but one instantiation per X
-// only: the U^X column sits in registers (compile-time ma1), U^Y is read from
-// shared memory (one load per product), the z row accumulates in a per-lane
-// shared strip, CG rows come from constant memory with warp-uniform offsets.
-template <int X>
-__device__ __forceinline__ void yi6_xyj(const C2* __restrict__ Ul, int Y, int J, int mb, int off, double cy,
-                                        double be, C2* __restrict__ zs, C2 (&yacc)[yi5::TJ + 1], double& esum) {
-  const int SH = (X + Y - J) / 2;
-  const bool mid = (2 * mb == J);
-  const int jtop = mid ? J / 2 : J;  // middle row: upper half has zero weight
-  for (int ma = 0; ma <= jtop; ++ma) zs[ma * 32] = C2{0.0, 0.0};
-  const int lo = max(0, mb + SH - Y), hi = min(X, mb + SH);
-  const int FX = c_foff[X], FY = c_foff[Y];
-  for (int mb1 = lo; mb1 <= hi; ++mb1) {
-    const int mb2 = mb + SH - mb1;
-    C2 ux[X + 1];
-    const C2* px = Ul + (FX + mb1 * (X + 1)) * YI_ATOMS;
-#pragma unroll
-    for (int a = 0; a <= X; ++a) ux[a] = px[a * YI_ATOMS];
-    const C2* py = Ul + (FY + mb2 * (Y + 1)) * YI_ATOMS;
-    const double cb = c_cgt[off + mb * (X + 1) + mb1];
-    for (int ma = 0; ma <= jtop; ++ma) {
-      const double* cga = c_cgt + off + ma * (X + 1);
-      const int base2 = ma + SH;  // ma2 = base2 - ma1
-      // two accumulator pairs (even / odd ma1): shorter dependent FMA chains
-      double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
-#pragma unroll
-      for (int ma1 = 0; ma1 <= X; ++ma1) {
-        const int ma2 = base2 - ma1;
-        if (ma2 >= 0 && ma2 <= Y) {
-          const C2 uy = py[ma2 * YI_ATOMS];
-          const double c = cga[ma1];
-          const double tr = ux[ma1].re * uy.re - ux[ma1].im * uy.im;
-          const double ti = ux[ma1].re * uy.im + ux[ma1].im * uy.re;
-          if (ma1 & 1) {
-            sr1 += c * tr;
-            si1 += c * ti;
-          } else {
-            sr0 += c * tr;
-            si0 += c * ti;
-          }
-        }
-      }
-      C2 zz = zs[ma * 32];
-      zz.re += cb * (sr0 + sr1);
-      zz.im += cb * (si0 + si1);
-      zs[ma * 32] = zz;
-    }
-  }
-  const C2* pj = Ul + (c_foff[J] + mb * (J + 1)) * YI_ATOMS;
-#pragma unroll
-  for (int ma = 0; ma <= yi5::TJ; ++ma) {
-    if (ma > jtop) break;
-    const C2 z = zs[ma * 32];
-    yacc[ma].re += cy * z.re;
-    yacc[ma].im += cy * z.im;
-    if (be != 0.0) {
-      const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
-      const C2 u = pj[ma * YI_ATOMS];
-      esum += be * w * (u.re * z.re + u.im * z.im);
-    }
-  }
-}
-
-template <int Y>
-__device__ __forceinline__ void yi7_xyj(const C2* __restrict__ Ul, int X, int J, int mb, int off, double cy,
-                                        double be, C2* __restrict__ zs, C2 (&yacc)[yi5::TJ + 1], double& esum) {
-  const int SH = (X + Y - J) / 2;
-  const bool mid = (2 * mb == J);
-  const int jtop = mid ? J / 2 : J;  // middle row: upper half has zero weight
-  for (int ma = 0; ma <= jtop; ++ma) zs[ma * 32] = C2{0.0, 0.0};
-  const int lo = max(0, mb + SH - Y), hi = min(X, mb + SH);
-  const int FX = c_foff[X], FY = c_foff[Y];
-  for (int mb1 = lo; mb1 <= hi; ++mb1) {
-    const int mb2 = mb + SH - mb1;
-    C2 uy[Y + 1];
-    const C2* py = Ul + (FY + mb2 * (Y + 1)) * YI_ATOMS;
-#pragma unroll
-    for (int a = 0; a <= Y; ++a) uy[a] = py[a * YI_ATOMS];
-    const C2* px = Ul + (FX + mb1 * (X + 1)) * YI_ATOMS;
-    const double cb = c_cgt[off + mb * (X + 1) + mb1];
-    for (int ma = 0; ma <= jtop; ++ma) {
-      const double* cga = c_cgt + off + ma * (X + 1);
-      const int base1 = ma + SH;  // ma1 = base1 - ma2
-      double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
-#pragma unroll
-      for (int ma2 = 0; ma2 <= Y; ++ma2) {
-        const int ma1 = base1 - ma2;
-        if (ma1 >= 0 && ma1 <= X) {
-          const C2 ux = px[ma1 * YI_ATOMS];
-          const double c = cga[ma1];
-          const double tr = ux.re * uy[ma2].re - ux.im * uy[ma2].im;
-          const double ti = ux.re * uy[ma2].im + ux.im * uy[ma2].re;
-          if (ma2 & 1) {
-            sr1 += c * tr;
-            si1 += c * ti;
-          } else {
-            sr0 += c * tr;
-            si0 += c * ti;
-          }
-        }
-      }
-      C2 zz = zs[ma * 32];
-      zz.re += cb * (sr0 + sr1);
-      zz.im += cb * (si0 + si1);
-      zs[ma * 32] = zz;
-    }
-  }
-  const C2* pj = Ul + (c_foff[J] + mb * (J + 1)) * YI_ATOMS;
-#pragma unroll
-  for (int ma = 0; ma <= yi5::TJ; ++ma) {
-    if (ma > jtop) break;
-    const C2 z = zs[ma * 32];
-    yacc[ma].re += cy * z.re;
-    yacc[ma].im += cy * z.im;
-    if (be != 0.0) {
-      const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
-      const C2 u = pj[ma * YI_ATOMS];
-      esum += be * w * (u.re * z.re + u.im * z.im);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(YI6_WARPS * 32)
-k_snap_yi_six(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
-              double* __restrict__ eatom) {
-  extern __shared__ double smem[];
-  C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
-  C2* zsm = Uf + D.nfull * YI_ATOMS;                                   // [warps][9][32]
-  double* epart = reinterpret_cast<double*>(zsm + YI6_WARPS * (yi5::TJ + 1) * YI_ATOMS);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
-  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
-  for (int t = threadIdx.x; t < D.nfull * YI_ATOMS; t += blockDim.x) {
-    const int at = t & (YI_ATOMS - 1), f = t >> 5;
-    int J = 0;
-    while (J < D.tj && f >= c_foff[J + 1]) ++J;
-    const int e = f - c_foff[J], mb = e / (J + 1), ma = e - mb * (J + 1);
-    C2 v{0.0, 0.0};
-    if (at < na_blk) {
-      if (2 * mb <= J) {
-        v = utot[(a0 + at) * D.nhalf + c_hoff[J] + mb * (J + 1) + ma];
-      } else {
-        C2 w = utot[(a0 + at) * D.nhalf + c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
-        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
-      }
-    }
-    Uf[f * YI_ATOMS + at] = v;
-  }
-  __syncthreads();
-  const C2* Ul = Uf + lane;
-  C2* zs = zsm + warp * (yi5::TJ + 1) * YI_ATOMS + lane;
-  const int64_t atom = a0 + lane;
-  double esum = 0.0;
-  for (int gi = c_yi6_gseg[warp]; gi < c_yi6_gseg[warp + 1]; ++gi) {
-    const int J = c_yi6_groups[gi] >> 8, mb = c_yi6_groups[gi] & 0xff;
-    C2 yacc[yi5::TJ + 1];
-#pragma unroll
-    for (int m = 0; m <= yi5::TJ; ++m) yacc[m] = C2{0.0, 0.0};
-    for (int k = c_yi5_jstart[J]; k < c_yi5_jstart[J + 1]; ++k) {
-      const int tid = c_yi5_tlist[k];
-      const int code = c_yi5_code[tid];
-      const int X = code / 100, Y = (code / 10) % 10;
-      const int off = c_yi5_cgoff[tid];
-      const double cy = D.yi5[tid], be = D.yi5[yi5::NT + tid];
-      switch (X) {
-        case 0: yi6_xyj<0>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 1: yi6_xyj<1>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 2: yi6_xyj<2>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 3: yi6_xyj<3>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 4: yi6_xyj<4>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 5: yi6_xyj<5>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 6: yi6_xyj<6>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 7: yi6_xyj<7>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-        default: yi6_xyj<8>(Ul, Y, J, mb, off, cy, be, zs, yacc, esum); break;
-      }
-    }
-    if (lane < na_blk) {
-      C2* yo = ylist + atom * D.nhalf + c_hoff[J] + mb * (J + 1);
-#pragma unroll
-      for (int m = 0; m <= yi5::TJ; ++m)
-        if (m <= J) yo[m] = yacc[m];
-    }
-  }
-  epart[warp * YI_ATOMS + lane] = esum;
-  __syncthreads();
-  if (warp == 0 && lane < na_blk) {
-    double e = D.beta0;
-    for (int w = 0; w < YI6_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
-    eatom[atom] = e;
-  }
-}
-
-__global__ void __launch_bounds__(YI6_WARPS * 32)
-k_snap_yi_seven(SnapDev D, int64_t natoms, const C2* __restrict__ utot, C2* __restrict__ ylist,
-              double* __restrict__ eatom) {
-  extern __shared__ double smem[];
-  C2* Uf = reinterpret_cast<C2*>(smem);                                // [nfull][32]
-  C2* zsm = Uf + D.nfull * YI_ATOMS;                                   // [warps][9][32]
-  double* epart = reinterpret_cast<double*>(zsm + YI6_WARPS * (yi5::TJ + 1) * YI_ATOMS);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t a0 = (int64_t)blockIdx.x * YI_ATOMS;
-  const int na_blk = (int)min((int64_t)YI_ATOMS, natoms - a0);
-  for (int t = threadIdx.x; t < D.nfull * YI_ATOMS; t += blockDim.x) {
-    const int at = t & (YI_ATOMS - 1), f = t >> 5;
-    int J = 0;
-    while (J < D.tj && f >= c_foff[J + 1]) ++J;
-    const int e = f - c_foff[J], mb = e / (J + 1), ma = e - mb * (J + 1);
-    C2 v{0.0, 0.0};
-    if (at < na_blk) {
-      if (2 * mb <= J) {
-        v = utot[(a0 + at) * D.nhalf + c_hoff[J] + mb * (J + 1) + ma];
-      } else {
-        C2 w = utot[(a0 + at) * D.nhalf + c_hoff[J] + (J - mb) * (J + 1) + (J - ma)];
-        v = ((ma + mb) & 1) ? C2{-w.re, w.im} : C2{w.re, -w.im};
-      }
-    }
-    Uf[f * YI_ATOMS + at] = v;
-  }
-  __syncthreads();
-  const C2* Ul = Uf + lane;
-  C2* zs = zsm + warp * (yi5::TJ + 1) * YI_ATOMS + lane;
-  const int64_t atom = a0 + lane;
-  double esum = 0.0;
-  for (int gi = c_yi6_gseg[warp]; gi < c_yi6_gseg[warp + 1]; ++gi) {
-    const int J = c_yi6_groups[gi] >> 8, mb = c_yi6_groups[gi] & 0xff;
-    C2 yacc[yi5::TJ + 1];
-#pragma unroll
-    for (int m = 0; m <= yi5::TJ; ++m) yacc[m] = C2{0.0, 0.0};
-    for (int k = c_yi5_jstart[J]; k < c_yi5_jstart[J + 1]; ++k) {
-      const int tid = c_yi5_tlist[k];
-      const int code = c_yi5_code[tid];
-      const int X = code / 100, Y = (code / 10) % 10;
-      const int off = c_yi5_cgoff[tid];
-      const double cy = D.yi5[tid], be = D.yi5[yi5::NT + tid];
-      switch (Y) {
-        case 0: yi7_xyj<0>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 1: yi7_xyj<1>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 2: yi7_xyj<2>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 3: yi7_xyj<3>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 4: yi7_xyj<4>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 5: yi7_xyj<5>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 6: yi7_xyj<6>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-        case 7: yi7_xyj<7>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-        default: yi7_xyj<8>(Ul, X, J, mb, off, cy, be, zs, yacc, esum); break;
-      }
-    }
-    if (lane < na_blk) {
-      C2* yo = ylist + atom * D.nhalf + c_hoff[J] + mb * (J + 1);
-#pragma unroll
-      for (int m = 0; m <= yi5::TJ; ++m)
-        if (m <= J) yo[m] = yacc[m];
-    }
-  }
-  epart[warp * YI_ATOMS + lane] = esum;
-  __syncthreads();
-  if (warp == 0 && lane < na_blk) {
-    double e = D.beta0;
-    for (int w = 0; w < YI6_WARPS; ++w) e += epart[w * YI_ATOMS + lane];
-    eatom[atom] = e;
-  }
-}
-
 // per-atom bispectrum (debug / parity path; per item, deterministic)
 __global__ void k_snap_bispectrum(SnapDev D, const C2* __restrict__ utot, double* __restrict__ bout,
                                   int nitems) {
@@ -1734,74 +1012,6 @@ __device__ __forceinline__ void row_step(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], cons
   }
 }
 
-// contraction of layer J's row with Y (full-matrix weights) for one component
-template <int TJ, int J>
-__device__ __forceinline__ double row_contract(const C2 (&u)[TJ + 1], const C2 (&du)[TJ + 1], const C2* Y,
-                                               int mb, double fc, double dfc_uk) {
-  if (2 * mb > J) return 0.0;
-  double acc = 0.0;
-  const C2* yr = Y + c_hoff[J] + mb * (J + 1);
-#pragma unroll
-  for (int ma = 0; ma <= J; ++ma) {
-    const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
-    const C2 y = yr[ma];
-    acc += w * (fc * (du[ma].re * y.re + du[ma].im * y.im) + dfc_uk * (u[ma].re * y.re + u[ma].im * y.im));
-  }
-  return acc;
-}
-
-template <int TJ, int J>
-struct Layers {
-  __device__ __forceinline__ static void de(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                            const double (*rp)[SNAP_JMAX + 2], const C2* Y, double fc,
-                                            double dfc_uk, double& acc) {
-    Layers<TJ, J - 1>::de(u, du, g, mb, rp, Y, fc, dfc_uk, acc);
-    row_step<TJ, J, true>(u, du, g, mb, rp);
-    acc += row_contract<TJ, J>(u, du, Y, mb, fc, dfc_uk);
-  }
-  __device__ __forceinline__ static void ui(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                            const double (*rp)[SNAP_JMAX + 2], C2* part, double fc) {
-    Layers<TJ, J - 1>::ui(u, du, g, mb, rp, part, fc);
-    row_step<TJ, J, false>(u, du, g, mb, rp);
-    if (part && 2 * mb <= J) {
-      C2* pr = part + c_hoff[J] + mb * (J + 1);
-#pragma unroll
-      for (int ma = 0; ma <= J; ++ma) {
-        pr[ma].re = fma(fc, u[ma].re, pr[ma].re);
-        pr[ma].im = fma(fc, u[ma].im, pr[ma].im);
-      }
-    }
-  }
-  // same recursion, the lane's row accumulated in registers over its pairs
-  // (acc[J(J+1)/2 + ma]); one shared-memory write per element at the end
-  __device__ __forceinline__ static void ui_reg(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                                const double (*rp)[SNAP_JMAX + 2], bool on, double fc,
-                                                C2 (&acc)[(TJ + 1) * (TJ + 2) / 2]) {
-    Layers<TJ, J - 1>::ui_reg(u, du, g, mb, rp, on, fc, acc);
-    row_step<TJ, J, false>(u, du, g, mb, rp);
-    if (on && 2 * mb <= J) {
-#pragma unroll
-      for (int ma = 0; ma <= J; ++ma) {
-        C2& a = acc[J * (J + 1) / 2 + ma];
-        a.re = fma(fc, u[ma].re, a.re);
-        a.im = fma(fc, u[ma].im, a.im);
-      }
-    }
-  }
-};
-template <int TJ>
-struct Layers<TJ, 0> {
-  __device__ __forceinline__ static void de(C2 (&)[TJ + 1], C2 (&)[TJ + 1], const RowGeom<TJ>&, int,
-                                            const double (*)[SNAP_JMAX + 2], const C2*, double, double, double&) {}
-  __device__ __forceinline__ static void ui(C2 (&)[TJ + 1], C2 (&)[TJ + 1], const RowGeom<TJ>&, int,
-                                            const double (*)[SNAP_JMAX + 2], C2*, double) {}
-  __device__ __forceinline__ static void ui_reg(C2 (&)[TJ + 1], C2 (&)[TJ + 1], const RowGeom<TJ>&, int,
-                                                const double (*)[SNAP_JMAX + 2], bool, double,
-                                                C2 (&)[(TJ + 1) * (TJ + 2) / 2]) {}
-};
-
-constexpr int RR_WARPS = 4;  // warps per CTA of the register-resident kernels (one atom per warp)
-
 // sqrt(p/q) table into shared memory, computed in place (correctly rounded
 // divide and sqrt: the host table's values bit for bit) instead of 100
 // lane-divergent constant-bank reads that serialise per warp
@@ -1809,162 +1019,6 @@ __device__ __forceinline__ void stage_rootpq(double (*rp)[SNAP_JMAX + 2]) {
   for (int t = threadIdx.x; t < (SNAP_JMAX + 2) * (SNAP_JMAX + 2); t += blockDim.x) {
     const int p = t / (SNAP_JMAX + 2), q = t % (SNAP_JMAX + 2);
     rp[p][q] = q ? __dsqrt_rn(__ddiv_rn((double)p, (double)q)) : 0.0;
-  }
-}
-
-template <int TJ, bool REG>
-__global__ void __launch_bounds__(RR_WARPS * 32)
-k_snap_ui_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
-             const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
-             C2* __restrict__ utot) {
-  constexpr int R = TJ / 2 + 1, P = 32 / R;
-  extern __shared__ double smem[];
-  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
-  const int nh = D.nhalf;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // pair-slot stride nh + 2 (= 5 mod 8 complex at twojmax 8): the 8 lanes of a
-  // 128-bit shared-memory phase hit distinct bank groups in the top layer
-  const int ps = nh + 2;
-  C2* part = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * P * ps;
-  stage_rootpq(rp);
-  const int64_t atom = (int64_t)blockIdx.x * RR_WARPS + warp;
-  for (int t = lane; t < P * ps; t += 32) part[t] = C2{0.0, 0.0};
-  __syncthreads();
-  if (atom >= natoms) return;
-  const int64_t b = atom / N;
-  const int i = (int)(atom - b * N);
-  const double* qb = q + b * (int64_t)N * 3;
-  const int p = lane / R, mb = lane - p * R;
-  const bool lane_ok = lane < P * R;
-  const int n = cnt[atom];
-  const int32_t* nb = nbr + atom * maxn;
-  C2 acc[(TJ + 1) * (TJ + 2) / 2];
-  if (REG) {
-#pragma unroll
-    for (int k = 0; k < (TJ + 1) * (TJ + 2) / 2; ++k) acc[k] = C2{0.0, 0.0};
-  }
-  for (int s0 = 0; s0 < n; s0 += P) {
-    const int s = s0 + p;
-    const bool valid = lane_ok && s < n;
-    RowGeom<TJ> g;
-    double fc = 0.0;
-    if (valid) {
-      double dx, dy, dz;
-      pair_vec(qb, i, nb[s], box, dx, dy, dz);
-      PairGeom pg;
-      pair_geom(D, dx, dy, dz, pg, false);
-      g.a = pg.a;
-      g.b = pg.b;
-      fc = pg.fc;
-    } else {
-      g.a = C2{1.0, 0.0};
-      g.b = C2{0.0, 0.0};
-    }
-    C2 u[TJ + 1], du[TJ + 1];
-#pragma unroll
-    for (int k = 0; k <= TJ; ++k) u[k] = du[k] = C2{0.0, 0.0};
-    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
-    if (REG) {
-      if (valid && mb == 0) acc[0].re += fc;  // J = 0
-      Layers<TJ, TJ>::ui_reg(u, du, g, mb, rp, valid, fc, acc);
-    } else {
-      C2* mypart = part + p * ps;
-      if (valid && mb == 0) mypart[0].re += fc;  // J = 0
-      // every lane runs the recursion (shuffles need the full warp); only valid
-      // lanes accumulate, each into its own pair slot
-      Layers<TJ, TJ>::ui(u, du, g, mb, rp, valid ? mypart : nullptr, fc);
-    }
-  }
-  if (REG && lane_ok) {  // each lane owns its (pair slot, row): plain stores
-    C2* mypart = part + p * ps;
-#pragma unroll
-    for (int J = 0; J <= TJ; ++J)
-      if (2 * mb <= J)
-#pragma unroll
-        for (int ma = 0; ma <= J; ++ma) mypart[c_hoff[J] + mb * (J + 1) + ma] = acc[J * (J + 1) / 2 + ma];
-  }
-  __syncwarp();
-  // fixed-order sum over the P pair slots + self term
-  C2* out = utot + atom * nh;
-  for (int t = lane; t < nh; t += 32) {
-    C2 acc{0.0, 0.0};
-#pragma unroll
-    for (int pp = 0; pp < P; ++pp) {
-      acc.re += part[pp * ps + t].re;
-      acc.im += part[pp * ps + t].im;
-    }
-    int J = 0;
-    while (J < TJ && t >= c_hoff[J + 1]) ++J;
-    const int e = t - c_hoff[J];
-    const int mbb = e / (J + 1), maa = e - mbb * (J + 1);
-    if (maa == mbb) acc.re += D.wself;
-    out[t] = acc;
-  }
-}
-
-template <int TJ>
-__global__ void __launch_bounds__(RR_WARPS * 32)
-k_snap_deidrj_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
-                 const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
-                 const C2* __restrict__ ylist, double* __restrict__ dedr) {
-  constexpr int R = TJ / 2 + 1, P = 32 / R;
-  extern __shared__ double smem[];
-  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
-  const int nh = D.nhalf;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  C2* Y = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * nh;
-  stage_rootpq(rp);
-  const int64_t atom = (int64_t)blockIdx.x * RR_WARPS + warp;
-  if (atom < natoms)
-    for (int t = lane; t < nh; t += 32) Y[t] = ylist[atom * nh + t];
-  __syncthreads();
-  if (atom >= natoms) return;
-  const int64_t b = atom / N;
-  const int i = (int)(atom - b * N);
-  const double* qb = q + b * (int64_t)N * 3;
-  const int p = lane / R, mb = lane - p * R;
-  const bool lane_ok = lane < P * R;
-  const int n = cnt[atom];
-  const int32_t* nb = nbr + atom * maxn;
-  const double y0 = Y[0].re;
-  for (int s0 = 0; s0 < n; s0 += P) {
-    const int s = s0 + p;
-    const bool valid = lane_ok && s < n;
-    PairGeom pg;
-    if (valid) {
-      double dx, dy, dz;
-      pair_vec(qb, i, nb[s], box, dx, dy, dz);
-      pair_geom(D, dx, dy, dz, pg, true);
-    } else {
-      pair_geom(D, 1.0, 0.0, 0.0, pg, true);
-      pg.fc = 0.0;
-      pg.dfc = 0.0;
-    }
-    double res0 = 0.0, res1 = 0.0, res2 = 0.0;
-#pragma unroll 1
-    for (int k = 0; k < 3; ++k) {
-      RowGeom<TJ> g{pg.a, pg.b, pg.da[k], pg.db[k]};
-      C2 u[TJ + 1], du[TJ + 1];
-#pragma unroll
-      for (int e = 0; e <= TJ; ++e) u[e] = du[e] = C2{0.0, 0.0};
-      u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
-      const double dfc_uk = pg.dfc * pg.u[k];
-      double acc = (mb == 0) ? dfc_uk * y0 : 0.0;  // J = 0: U = 1, dU = 0, weight 1
-      Layers<TJ, TJ>::de(u, du, g, mb, rp, Y, pg.fc, dfc_uk, acc);
-      // fixed-order sum over the R row lanes of this pair
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        double v = __shfl_down_sync(0xffffffffu, acc, r);
-        if (mb == 0) acc += v;  // acc(mb=0) + acc(1) + ... in row order
-      }
-      if (k == 0) res0 = acc; else if (k == 1) res1 = acc; else res2 = acc;
-    }
-    if (valid && mb == 0) {
-      double* o = dedr + (atom * maxn + s) * 3;
-      o[0] = res0;
-      o[1] = res1;
-      o[2] = res2;
-    }
   }
 }
 
@@ -1978,212 +1032,6 @@ k_snap_deidrj_rr(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
 // born at even J from row J/2-1 by symmetry passes its adjoint back the same
 // way (G_{mb-1}[J-1-x] += (-1)^(x+mb) conj(G_mb[x])).  ~3x fewer FP64
 // operations than propagating the three dU/dr_k.
-constexpr int ADJ_WARPS = 2;
-
-// Forward-row history layouts: HL = 0 [slot (J, x)][lane] (23 KB per warp);
-// HL = 1 [half index (J, row, x)][pair slot] (155 x 7 complex, 17.4 KB per warp:
-// only the rows that exist are stored; slot 6 is the scratch of the two lanes
-// without a pair), which leaves room for more warps per SM.
-constexpr int ADJ_P = 7;  // pair slots per warp (32 / 5 rows = 6, + 1)
-
-template <int HL, int J>
-__device__ __forceinline__ int hpos(int x, int row, int mb, int lane, int p) {
-  if constexpr (HL == 0) {
-    return (J * (J + 1) / 2 + x) * 32 + lane + (row - mb);  // row mb - 1 is the lane below
-  } else {
-    return (yi5::hoff(J) + row * (J + 1) + x) * ADJ_P + p;
-  }
-}
-
-template <int TJ, int HL>
-struct AdjLayers {
-  // forward: layer J from J-1 (in place), store the row, accumulate F
-  template <int J>
-  __device__ __forceinline__ static void fwd(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                             const double (*rp)[SNAP_JMAX + 2], const C2* Y, C2* hist,
-                                             int lane, int p, double& F) {
-    if constexpr (J > 0) {
-      fwd<J - 1>(u, g, mb, rp, Y, hist, lane, p, F);
-      C2 du[TJ + 1];
-      row_step<TJ, J, false>(u, du, g, mb, rp);
-    }
-    if (2 * mb <= J) {
-      const C2* yr = Y + c_hoff[J] + mb * (J + 1);
-#pragma unroll
-      for (int ma = 0; ma <= J; ++ma) {
-        hist[hpos<HL, J>(ma, mb, mb, lane, p)] = u[ma];
-        const double w = (2 * mb < J || 2 * ma < J) ? 2.0 : (2 * ma == J ? 1.0 : 0.0);
-        F += w * (u[ma].re * yr[ma].re + u[ma].im * yr[ma].im);
-      }
-    }
-  }
-
-  // backward from layer J to J-1 (G holds the adjoint of layer J on entry)
-  template <int J>
-  __device__ __forceinline__ static void bwd(C2 (&G)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                             const double (*rp)[SNAP_JMAX + 2], const C2* Y, const C2* hist,
-                                             int lane, int p, C2& Sa, C2& Sb) {
-    if constexpr (J > 0) {
-      const bool active = 2 * mb <= J;
-      const bool born = (J % 2 == 0) && (2 * mb == J);  // row mb of layer J-1 is virtual
-      // U^{J-1} row mb (stored, or the symmetric image of row mb-1 of the same pair)
-      C2 up[TJ + 1];
-      if (active) {
-#pragma unroll
-        for (int x = 0; x < J; ++x) {
-          if (!born) {
-            up[x] = hist[hpos<HL, J - 1>(x, mb, mb, lane, p)];
-          } else {
-            const C2 v = hist[hpos<HL, J - 1>(J - 1 - x, mb - 1, mb, lane, p)];
-            up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
-          }
-        }
-      }
-      if (active) {
-#pragma unroll
-        for (int ma = 0; ma <= J; ++ma) {
-          if (ma < J) {
-            const double A = rp[J - ma][J - mb];
-            const C2 t = cmulc(up[ma], G[ma]);  // conj(U') G
-            Sa.re += A * t.re;
-            Sa.im += A * t.im;
-          }
-          if (ma > 0) {
-            const double Bc = rp[ma][J - mb];
-            const C2 t = cmulc(up[ma - 1], G[ma]);
-            Sb.re -= Bc * t.re;
-            Sb.im -= Bc * t.im;
-          }
-        }
-        // G^{J-1}[x] = A(J,x) a G[x] - B(J,x+1) b G[x+1]  (ascending x, in place)
-#pragma unroll
-        for (int x = 0; x < J; ++x) {
-          const double A = rp[J - x][J - mb];
-          const double Bc = rp[x + 1][J - mb];
-          const C2 t1 = cmul(g.a, G[x]);
-          const C2 t2 = cmul(g.b, G[x + 1]);
-          G[x] = C2{A * t1.re - Bc * t2.re, A * t1.im - Bc * t2.im};
-        }
-        G[J] = C2{0.0, 0.0};
-      }
-      // adjoint of the virtual row flows to the lane below (row mb-1), all lanes shuffle
-      if (J % 2 == 0) {
-#pragma unroll
-        for (int x = 0; x < J; ++x) {
-          const C2 v = C2{__shfl_down_sync(0xffffffffu, G[x].re, 1), __shfl_down_sync(0xffffffffu, G[x].im, 1)};
-          if (2 * (mb + 1) == J) {  // this lane is row J/2-1; the lane above was born at J
-            const int xs = J - 1 - x;
-            const bool neg = ((x + mb + 1) & 1) != 0;
-            G[xs].re += neg ? -v.re : v.re;
-            G[xs].im += neg ? v.im : -v.im;
-          }
-        }
-        if (born) {
-#pragma unroll
-          for (int x = 0; x <= J; ++x) G[x] = C2{0.0, 0.0};
-        }
-      }
-      // direct term of layer J-1 on stored rows
-      if (2 * mb <= J - 1) {
-        const C2* yr = Y + c_hoff[J - 1] + mb * J;
-#pragma unroll
-        for (int x = 0; x < J; ++x) {
-          const double w = (2 * mb < J - 1 || 2 * x < J - 1) ? 2.0 : (2 * x == J - 1 ? 1.0 : 0.0);
-          G[x].re += w * yr[x].re;
-          G[x].im += w * yr[x].im;
-        }
-      }
-      bwd<J - 1>(G, g, mb, rp, Y, hist, lane, p, Sa, Sb);
-    }
-  }
-};
-
-template <int TJ, int HL>
-__global__ void __launch_bounds__(ADJ_WARPS * 32)
-k_snap_deidrj_adj(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
-                  const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
-                  const C2* __restrict__ ylist, double* __restrict__ dedr) {
-  constexpr int R = TJ / 2 + 1, P = 32 / R;
-  constexpr int HIST = HL == 0 ? (TJ + 1) * (TJ + 2) / 2 * 32 : yi5::hoff(TJ + 1) * ADJ_P;  // complex per warp
-  extern __shared__ double smem[];
-  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
-  const int nh = D.nhalf;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  C2* Y = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * nh;
-  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + ADJ_WARPS * nh + warp * HIST;
-  stage_rootpq(rp);
-  const int64_t atom = (int64_t)blockIdx.x * ADJ_WARPS + warp;
-  if (atom < natoms)
-    for (int t = lane; t < nh; t += 32) Y[t] = ylist[atom * nh + t];
-  __syncthreads();
-  if (atom >= natoms) return;
-  const int64_t b = atom / N;
-  const int i = (int)(atom - b * N);
-  const double* qb = q + b * (int64_t)N * 3;
-  const int p = lane / R, mb = lane - p * R;
-  const int pc = p;  // lanes 30, 31 (no pair) write their own scratch slot 6
-  const bool lane_ok = lane < P * R;
-  const int n = cnt[atom];
-  const int32_t* nb = nbr + atom * maxn;
-  for (int s0 = 0; s0 < n; s0 += P) {
-    const int s = s0 + p;
-    const bool valid = lane_ok && s < n;
-    PairGeom pg;
-    if (valid) {
-      double dx, dy, dz;
-      pair_vec(qb, i, nb[s], box, dx, dy, dz);
-      pair_geom(D, dx, dy, dz, pg, true);
-    } else {
-      pair_geom(D, 1.0, 0.0, 0.0, pg, true);
-      pg.fc = 0.0;
-      pg.dfc = 0.0;
-    }
-    RowGeom<TJ> g{pg.a, pg.b, C2{0.0, 0.0}, C2{0.0, 0.0}};
-    C2 u[TJ + 1];
-#pragma unroll
-    for (int e = 0; e <= TJ; ++e) u[e] = C2{0.0, 0.0};
-    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
-    double F = 0.0;
-    AdjLayers<TJ, HL>::template fwd<TJ>(u, g, mb, rp, Y, hist, lane, pc, F);
-    __syncwarp();
-    // adjoint of the top layer: its direct term
-    C2 G[TJ + 1];
-#pragma unroll
-    for (int e = 0; e <= TJ; ++e) G[e] = C2{0.0, 0.0};
-    if (2 * mb <= TJ) {
-      const C2* yr = Y + c_hoff[TJ] + mb * (TJ + 1);
-#pragma unroll
-      for (int x = 0; x <= TJ; ++x) {
-        const double w = (2 * mb < TJ || 2 * x < TJ) ? 2.0 : (2 * x == TJ ? 1.0 : 0.0);
-        G[x] = C2{w * yr[x].re, w * yr[x].im};
-      }
-    }
-    C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
-    AdjLayers<TJ, HL>::template bwd<TJ>(G, g, mb, rp, Y, hist, lane, pc, Sa, Sb);
-    __syncwarp();
-    // fixed-order sums over the R row lanes of the pair
-#pragma unroll
-    for (int r = 1; r < R; ++r) {
-      const double f = __shfl_down_sync(0xffffffffu, F, r);
-      const double ar = __shfl_down_sync(0xffffffffu, Sa.re, r), ai = __shfl_down_sync(0xffffffffu, Sa.im, r);
-      const double br = __shfl_down_sync(0xffffffffu, Sb.re, r), bi = __shfl_down_sync(0xffffffffu, Sb.im, r);
-      if (mb == 0) {
-        F += f;
-        Sa.re += ar; Sa.im += ai;
-        Sb.re += br; Sb.im += bi;
-      }
-    }
-    if (valid && mb == 0) {
-      double* o = dedr + (atom * maxn + s) * 3;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const double re = pg.da[k].re * Sa.re - pg.da[k].im * Sa.im + pg.db[k].re * Sb.re - pg.db[k].im * Sb.im;
-        o[k] = pg.dfc * pg.u[k] * F + pg.fc * re;
-      }
-    }
-  }
-}
-
 // layer J of row mb from layer J-1 in place, no born-row handling
 template <int TJ, int J>
 __device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb,
@@ -2516,110 +1364,7 @@ struct AdjR4 {
   }
 };
 
-constexpr int ADJ4_WARPS = 2;
 constexpr int ADJ4_SLOTS = 36;  // layers 0..7
-
-// APW atoms per warp: their pair lists are concatenated so the 8 pair slots of
-// a round stay filled across the atom boundary (26 pairs per atom fill 4
-// rounds of 8 only to 81 %)
-template <int APW>
-__global__ void __launch_bounds__(ADJ4_WARPS * 32)
-k_snap_deidrj_adj4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
-                   const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
-                   const C2* __restrict__ ylist, double* __restrict__ dedr) {
-  constexpr int TJ = 8, R = 4, P = 8;
-  extern __shared__ double smem[];
-  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
-  const int nh = D.nhalf;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  C2* Yw = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * APW * nh;
-  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + ADJ4_WARPS * APW * nh +
-             warp * ADJ4_SLOTS * 32;
-  stage_rootpq(rp);
-  const int64_t atom0 = ((int64_t)blockIdx.x * ADJ4_WARPS + warp) * APW;
-  int nat[APW];
-  int total = 0;
-#pragma unroll
-  for (int k = 0; k < APW; ++k) {
-    const int64_t a = atom0 + k;
-    nat[k] = a < natoms ? cnt[a] : 0;
-    total += nat[k];
-    if (a < natoms)
-      for (int t = lane; t < nh; t += 32) Yw[k * nh + t] = ylist[a * nh + t];
-  }
-  __syncthreads();
-  if (atom0 >= natoms) return;
-  const int p = lane / R, mb = lane - p * R;
-  for (int s0 = 0; s0 < total; s0 += P) {
-    // pair slot -> (atom of the warp, neighbour slot)
-    int k = s0 + p, w = 0;
-#pragma unroll
-    for (int a = 0; a + 1 < APW; ++a)
-      if (w == a && k >= nat[a]) {
-        k -= nat[a];
-        w = a + 1;
-      }
-    const bool valid = s0 + p < total;
-    const int64_t atom = atom0 + w;
-    const int s = k;
-    const C2* Y = Yw + w * nh;
-    PairGeom pg;
-    if (valid) {
-      const int64_t b = atom / N;
-      const int i = (int)(atom - b * N);
-      double dx, dy, dz;
-      pair_vec(q + b * (int64_t)N * 3, i, nbr[atom * maxn + s], box, dx, dy, dz);
-      pair_geom(D, dx, dy, dz, pg, true);
-    } else {
-      pair_geom(D, 1.0, 0.0, 0.0, pg, true);
-      pg.fc = 0.0;
-      pg.dfc = 0.0;
-    }
-    RowGeom<TJ> g{pg.a, pg.b, C2{0.0, 0.0}, C2{0.0, 0.0}};
-    C2 u[TJ + 1], u4[TJ + 1];
-#pragma unroll
-    for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
-    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
-    double F = 0.0;
-    AdjR4::fwd<TJ>(u, u4, g, mb, rp, YSmem{Y}, hist, lane, F);
-    __syncwarp();
-    C2 G[TJ + 1], G4[TJ + 1];
-    {
-      const C2* yr = Y + c_hoff[TJ] + mb * (TJ + 1);
-      const C2* y4 = Y + c_hoff[TJ] + (TJ / 2) * (TJ + 1);
-#pragma unroll
-      for (int x = 0; x <= TJ; ++x) {
-        const double w = half_w(TJ, mb, x), w4 = half_w(TJ, TJ / 2, x);
-        G[x] = C2{w * yr[x].re, w * yr[x].im};
-        G4[x] = C2{w4 * y4[x].re, w4 * y4[x].im};
-      }
-    }
-    C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
-    AdjR4::bwd<TJ>(G, G4, g, mb, rp, YSmem{Y}, hist, lane, Sa, Sb, F);
-    __syncwarp();
-    // fixed-order sums over the 4 row lanes of the pair
-#pragma unroll
-    for (int r = 1; r < R; ++r) {
-      const double f = __shfl_down_sync(0xffffffffu, F, r);
-      const double ar = __shfl_down_sync(0xffffffffu, Sa.re, r), ai = __shfl_down_sync(0xffffffffu, Sa.im, r);
-      const double br = __shfl_down_sync(0xffffffffu, Sb.re, r), bi = __shfl_down_sync(0xffffffffu, Sb.im, r);
-      if (mb == 0) {
-        F += f;
-        Sa.re += ar; Sa.im += ai;
-        Sb.re += br; Sb.im += bi;
-      }
-    }
-    if (valid && mb == 0) {
-      double* o = dedr + (atom * maxn + s) * 3;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const double re = pg.da[k].re * Sa.re - pg.da[k].im * Sa.im + pg.db[k].re * Sb.re - pg.db[k].im * Sb.im;
-        o[k] = pg.dfc * pg.u[k] * F + pg.fc * re;
-      }
-    }
-  }
-}
-
 // ------------------------------------------------------------------ pair-symmetric reverse-mode dE/dr
 // U(-r) = U(r)^dagger (the Cayley-Klein parameters of -r are (conj a, -b), the
 // inverse SU(2) element), and the adjoint sweep is linear in Y.  So for the
@@ -3190,6 +1935,21 @@ static size_t de_smem(const SnapDev& D) {
   return sizeof(C2) * (D.nhalf + DE_WARPS * 2 * 4 * layer_max);
 }
 
+// Kernel selection.  twojmax = 8 (the BASELINE potential) runs the specialised
+// kernels: k_snap_ui_r4, the box-form Y kernel (snap_yi8.cu) and the
+// pair-symmetric force kernels.  Every other twojmax runs the general kernels
+// k_snap_ui / k_snap_yi / k_snap_deidrj, which PL_SNAP_GENERIC=1 also forces at
+// twojmax = 8 so the two families can be checked against each other.
+// PL_SNAP_PAIR_RUN = 0 / 2 forces 2-atom warps / 8-atom runs of the pair kernel
+// at every batch size (both give bitwise-identical forces; tests).
+static bool snap_generic_forced() {
+  static const bool g = [] {
+    const char* e = getenv("PL_SNAP_GENERIC");
+    return e && e[0] == '1';
+  }();
+  return g;
+}
+
 static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf, NeighList& nl) {
   pl_ctx* ctx = pot->ctx;
   SnapIndex* S = pot->snap;
@@ -3211,123 +1971,40 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   buf.yt = reinterpret_cast<C2*>(erow + na * 25);
   buf.pair = false;
   Box box = make_box(pot->box);
-  size_t s1 = ui_smem(D), s2 = yi_smem(D), s3 = de_smem(D);
-  static thread_local bool attr_done = false;
-  if (!attr_done) {
+  static std::atomic<uint64_t> attr_devs{0};
+  if (first_on_device(attr_devs)) {
     cudaFuncSetAttribute(k_snap_ui, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_yi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_bispectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_ui_rr<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_ui_rr<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_yi_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_snap_yi_half, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-    cudaFuncSetAttribute(k_snap_yi_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_snap_yi_six, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
-    cudaFuncSetAttribute(k_snap_yi_seven, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_rr<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_adj<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_adj<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_adj4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_snap_deidrj_adj4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_pair<2, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_run<8, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_ui_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_done = true;
   }
-  // register-resident kernels are instantiated for twojmax = 8 (PL_SNAP_RR=0 selects the
-  // shared-memory layer kernels, kept as the general-twojmax path and for A/B checks)
-  static const bool rr_env = [] {
-    const char* e = getenv("PL_SNAP_RR");
-    return !(e && e[0] == '0');
-  }();
-  const bool rr = rr_env && (D.tj == 8);
+  const bool special = S->tj == 8 && S->yi_reg && !snap_generic_forced();
   const size_t rp_bytes = sizeof(double) * (SNAP_JMAX + 2) * (SNAP_JMAX + 2);
-  const unsigned rr_grid = (unsigned)((na + RR_WARPS - 1) / RR_WARPS);
   prof_mark(ctx->stream, ST_UI, true);
-  if (rr) {
-    size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * (32 / 5) * (D.nhalf + 2);
-    static const bool ui_reg = [] {
-      const char* e = getenv("PL_SNAP_UI");
-      return !(e && e[0] == '0');  // 0: accumulate through shared memory every pair
-    }();
-    static const bool ui4 = [] {
-      const char* e = getenv("PL_SNAP_UI");
-      return !(e && (e[0] == '0' || e[0] == '1'));  // 0/1: 5 lanes per pair (smem / register rows)
-    }();
-    if (ui4 && S->tj == 8) {
-      const size_t sm4 = rp_bytes + sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2) + sizeof(double) * UI4_WARPS * SNAP_MAXN * 5;
-      PL_CUDA(launch_pdl(k_snap_ui_r4, dim3((unsigned)((na + UI4_WARPS - 1) / UI4_WARPS)), dim3(UI4_WARPS * 32), sm4,
-                         ctx->stream, D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.utot));
-    } else if (ui_reg)
-      k_snap_ui_rr<8, true><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
-                                                                          nl.maxn, buf.utot);
-    else
-      k_snap_ui_rr<8, false><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
-                                                                           nl.maxn, buf.utot);
+  if (special) {
+    const size_t sm4 = rp_bytes + sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2) + sizeof(double) * UI4_WARPS * SNAP_MAXN * 5;
+    PL_CUDA(launch_pdl(k_snap_ui_r4, dim3((unsigned)((na + UI4_WARPS - 1) / UI4_WARPS)), dim3(UI4_WARPS * 32), sm4,
+                       ctx->stream, D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.utot));
   } else {
-    k_snap_ui<<<(unsigned)na, UI_WARPS * 32, s1, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
-                                                                 buf.utot);
+    k_snap_ui<<<(unsigned)na, UI_WARPS * 32, ui_smem(D), ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
+                                                                       buf.utot);
   }
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_UI, false);
   prof_mark(ctx->stream, ST_YI, true);
-  static const int yi_var = [] {
-    const char* e = getenv("PL_SNAP_YI");
-    return e ? atoi(e) : 8;
-  }();
-  static const int box_nw = [] {
-    const char* e = getenv("PL_SNAP_BOXW");
-    return e ? atoi(e) : 12;
-  }();
-  if (S->yi_reg && yi_var == 8) {
-    PL_CUDA(snap_box_launch(box_nw, ctx->stream, na, D.beta0, D.yi5, buf.utot, buf.y, buf.eatom, erow));
-  } else if (S->yi_reg && yi_var == 7) {
-    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI6_WARPS * 9 * YI_ATOMS +
-                sizeof(double) * YI6_WARPS * YI_ATOMS;
-    k_snap_yi_seven<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI6_WARPS * 32, sm, ctx->stream>>>(
-        D, na, buf.utot, buf.y, buf.eatom);
-  } else if (S->yi_reg && yi_var == 6) {
-    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(C2) * YI6_WARPS * 9 * YI_ATOMS +
-                sizeof(double) * YI6_WARPS * YI_ATOMS;
-    k_snap_yi_six<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI6_WARPS * 32, sm, ctx->stream>>>(
-        D, na, buf.utot, buf.y, buf.eatom);
-  } else if (S->yi_reg && yi_var >= 5) {
-    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(double) * YI5_WARPS * YI_ATOMS;
-    k_snap_yi_reg<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI5_WARPS * 32, sm, ctx->stream>>>(
-        D, na, buf.utot, buf.y, buf.eatom);
-  } else if (S->cgt_fits && yi_var == 4) {
-    size_t sm = sizeof(C2) * D.nhalf * YI_ATOMS + sizeof(double) * YI3_WARPS * YI_ATOMS;
-    k_snap_yi_half<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI3_WARPS * 32, sm, ctx->stream>>>(
-        D, na, buf.utot, buf.y, buf.eatom);
-  } else if (S->cgt_fits) {
-    size_t sm = sizeof(C2) * D.nfull * YI_ATOMS + sizeof(double) * YI3_WARPS * YI_ATOMS;
-    k_snap_yi_full<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI3_WARPS * 32, sm, ctx->stream>>>(
-        D, na, buf.utot, buf.y, buf.eatom);
+  if (special) {
+    PL_CUDA(snap_box_launch(ctx->stream, na, D.beta0, D.yi5, buf.utot, buf.y, buf.eatom, erow));
   } else {
-    k_snap_yi<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI_THREADS, s2, ctx->stream>>>(D, na, buf.utot,
-                                                                                          buf.y, buf.eatom);
+    k_snap_yi<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI_THREADS, yi_smem(D), ctx->stream>>>(D, na, buf.utot,
+                                                                                                 buf.y, buf.eatom);
   }
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_YI, false);
   prof_mark(ctx->stream, ST_DE, true);
-  static const bool adj_env = [] {
-    const char* e = getenv("PL_SNAP_ADJ");
-    return !(e && e[0] == '0');
-  }();
-  static const int adj_hl = [] {
-    const char* e = getenv("PL_SNAP_ADJ");
-    return (e && e[0] == '4') ? 1 : 0;  // 4: compact [half][pair] history (bitwise equal, measured slower)
-  }();
-  static const bool adj4 = [] {
-    const char* e = getenv("PL_SNAP_ADJ");
-    return !(e && (e[0] == '2' || e[0] == '4'));  // 2: 5 lanes per pair ([slot][lane] history)
-  }();
-  static const bool pair_env = [] {
-    const char* e = getenv("PL_SNAP_PAIR");
-    return !(e && e[0] == '0');  // 0: one adjoint sweep per ordered pair (k_snap_deidrj_adj4)
-  }();
-  if (rr && adj_env && adj4 && pair_env && S->tj == 8) {
+  if (special) {
     const int64_t nel = na * D.nhalf;
     PL_CUDA(launch_pdl(k_snap_ytrans, dim3((unsigned)((nel + 255) / 256)), dim3(256), 0, ctx->stream, na, D.nhalf,
                        D.tj, buf.y, buf.yt));
@@ -3353,34 +2030,9 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
                          na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
     }
     buf.pair = true;
-  } else if (rr && adj_env && adj4 && S->tj == 8) {
-    static const int apw = [] {
-      const char* e = getenv("PL_SNAP_ADJ_APW");
-      return (e && e[0] == '1') ? 1 : 2;
-    }();
-    const size_t sm = rp_bytes + sizeof(C2) * ADJ4_WARPS * (apw * D.nhalf + ADJ4_SLOTS * 32);
-    const unsigned grid = (unsigned)((na + ADJ4_WARPS * apw - 1) / (ADJ4_WARPS * apw));
-    if (apw == 2)
-      k_snap_deidrj_adj4<2><<<grid, ADJ4_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
-                                                                        buf.y, buf.dedr);
-    else
-      k_snap_deidrj_adj4<1><<<grid, ADJ4_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn,
-                                                                        buf.y, buf.dedr);
-  } else if (rr && adj_env && adj_hl == 1) {
-    size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + yi5::hoff(9) * ADJ_P);
-    k_snap_deidrj_adj<8, 1><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
-        D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
-  } else if (rr && adj_env) {
-    size_t sm = rp_bytes + sizeof(C2) * ADJ_WARPS * (D.nhalf + 45 * 32);
-    k_snap_deidrj_adj<8, 0><<<(unsigned)((na + ADJ_WARPS - 1) / ADJ_WARPS), ADJ_WARPS * 32, sm, ctx->stream>>>(
-        D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.dedr);
-  } else if (rr) {
-    size_t sm = rp_bytes + sizeof(C2) * RR_WARPS * D.nhalf;
-    k_snap_deidrj_rr<8><<<rr_grid, RR_WARPS * 32, sm, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
-                                                                      nl.maxn, buf.y, buf.dedr);
   } else {
-    k_snap_deidrj<<<(unsigned)na, DE_WARPS * 32, s3, ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
-                                                                     nl.maxn, buf.y, buf.dedr);
+    k_snap_deidrj<<<(unsigned)na, DE_WARPS * 32, de_smem(D), ctx->stream>>>(D, na, N, box, q, nl.nbr, nl.cnt,
+                                                                           nl.maxn, buf.y, buf.dedr);
   }
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_DE, false);
@@ -3447,18 +2099,11 @@ extern "C" int pl_snap_info(pl_pot* pot, int32_t* h_counts, double* h_flops) {
   h_counts[0] = S->nhalf; h_counts[1] = S->nfull; h_counts[2] = S->nB; h_counts[3] = S->nitems;
   h_counts[4] = S->nunits;
   // FLOPs of the kernel variants that compute_snap actually launches
-  const char* ey = getenv("PL_SNAP_YI");
-  const int yv = ey ? atoi(ey) : 8;
-  const char* ea = getenv("PL_SNAP_ADJ");
-  const char* er = getenv("PL_SNAP_RR");
-  const bool rr = !(er && er[0] == '0') && S->tj == 8;
-  const bool adj = rr && !(ea && ea[0] == '0');
-  const char* ep = getenv("PL_SNAP_PAIR");
-  const bool pair = adj && !(ea && (ea[0] == '2' || ea[0] == '4')) && !(ep && ep[0] == '0');
+  const bool special = S->tj == 8 && S->yi_reg && !pl::snap_generic_forced();
   h_flops[0] = S->flops_ui_pair;
-  h_flops[1] = (S->yi_reg && yv >= 5) ? S->flops_yi_atom_reg : S->flops_yi_atom;
+  h_flops[1] = special ? S->flops_yi_atom_reg : S->flops_yi_atom;
   // pair form: one sweep (+ the Y_i + Y_k^dagger adds, one read of every half element) per
   // unordered pair, quoted per ordered pair like the other stages
-  h_flops[2] = pair ? 0.5 * (S->flops_de_pair_adj + 2.0 * S->nhalf) : adj ? S->flops_de_pair_adj : S->flops_de_pair;
+  h_flops[2] = special ? 0.5 * (S->flops_de_pair_adj + 2.0 * S->nhalf) : S->flops_de_pair;
   return PL_OK;
 }

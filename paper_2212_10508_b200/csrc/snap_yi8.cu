@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace pl {
 
 __device__ __forceinline__ void griddep_wait_yi() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -346,11 +348,14 @@ template <int NW, int V, int S>
 static cudaError_t box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const void* utot,
                               void* ylist, double* eatom, double* erow_g) {
   const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * BOX_ROWS * yib::ATOMS;
-  static bool attr = false;
-  if (!attr) {  // exactly the dynamic size: the static mbarrier counts against the 227 KB too
+  static std::atomic<uint64_t> attr_devs{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_devs.load() & bit)) {  // exactly the dynamic size: the static mbarrier counts against the 227 KB too
     cudaError_t e = cudaFuncSetAttribute(k_snap_yi_box<NW, V, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_devs.fetch_or(bit);
   }
   const unsigned grid = (unsigned)(S * ((natoms + yib::ATOMS - 1) / yib::ATOMS));
   cudaError_t e = launch_pdl_yi(k_snap_yi_box<NW, V, S>, dim3(grid), dim3(NW * 32), sm, st, natoms, beta0, coef,
@@ -363,12 +368,11 @@ static cudaError_t box_launch(cudaStream_t st, int64_t natoms, double beta0, con
   return cudaGetLastError();
 }
 
-// nw: warps per CTA (12 or 8); split rows over 2 CTAs per block when the
-// batch has fewer blocks than SMs (erow_g: 25 x natoms doubles of scratch)
-cudaError_t snap_box_launch(int nw, cudaStream_t st, int64_t natoms, double beta0, const double* coef,
+// split rows over 2 CTAs per block when the batch has fewer blocks than SMs
+// (erow_g: 25 x natoms doubles of scratch)
+cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef,
                             const void* utot, void* ylist, double* eatom, double* erow_g) {
   const int64_t blocks = (natoms + yib::ATOMS - 1) / yib::ATOMS;
-  if (nw == 8) return box_launch<8, 1, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
   if (blocks < 148 && erow_g) return box_launch<12, 2, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
   return box_launch<12, 0, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
 }

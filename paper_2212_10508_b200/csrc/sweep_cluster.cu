@@ -534,11 +534,10 @@ int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N
   PL_CUDA(cudaMemcpyAsync(m1, h_m1, sizeof(int64_t) * R_act, cudaMemcpyHostToDevice, st));
   PL_CUDA(cudaMemcpyAsync(ridx, h_ridx, sizeof(int32_t) * R_act, cudaMemcpyHostToDevice, st));
   PL_CUDA(cudaMemcpyAsync(inc, h_inc, sizeof(int32_t) * R_act, cudaMemcpyHostToDevice, st));
-  static thread_local bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_devs{0};
+  if (first_on_device(attr_devs)) {
     cudaFuncSetAttribute(k_sweep_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_sweep_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(C * R_act));

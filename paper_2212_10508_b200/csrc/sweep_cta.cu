@@ -450,10 +450,9 @@ int sweep_cta(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t
   double init[2] = {h_state[0], h_state[1]};
   PL_CUDA(cudaMemcpyAsync(amp, h_amp, sizeof(double) * (L + 1), cudaMemcpyHostToDevice, st));
   PL_CUDA(cudaMemcpyAsync(acc, init, sizeof(init), cudaMemcpyHostToDevice, st));
-  static thread_local bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_devs{0};
+  if (first_on_device(attr_devs)) {
     cudaFuncSetAttribute(k_sweep_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   k_sweep_cta<<<1, SW_THREADS, smem, st>>>(A);
   PL_CHECK_LAUNCH();
@@ -543,10 +542,9 @@ int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, in
   PL_CUDA(cudaMemcpyAsync(m1, h_m1, sizeof(int64_t) * R_act, cudaMemcpyHostToDevice, st));
   PL_CUDA(cudaMemcpyAsync(ridx, h_ridx, sizeof(int32_t) * R_act, cudaMemcpyHostToDevice, st));
   PL_CUDA(cudaMemcpyAsync(inc, h_inc, sizeof(int32_t) * R_act, cudaMemcpyHostToDevice, st));
-  static thread_local bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_devs{0};
+  if (first_on_device(attr_devs)) {
     cudaFuncSetAttribute(k_sweep_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
   }
   k_sweep_cta<<<R_act, SW_THREADS, smem, st>>>(A);
   PL_CHECK_LAUNCH();

@@ -525,10 +525,8 @@ def _adaptive_machine(n, conv, expl, cap):
     return slabs, history, converged
 
 
-def _adaptive_device(initial, fine, coarse, config):
-    n = config.n_windows
-    run = _DeviceRun(initial, fine, coarse, n)
-    machine = _adaptive_machine(n, config.delta_conv, config.delta_expl, config.iteration_cap)
+def _drive_adaptive(machine, run):
+    """Answer the machine's actions with ``run.bootstrap`` / ``run.iterate``."""
     reply = None
     try:
         while True:
@@ -537,12 +535,27 @@ def _adaptive_device(initial, fine, coarse, config):
                 run.bootstrap(act[1])
                 reply = None
             else:
-                _, n_init, n_final, inc, it = act
-                run.jumps(n_init, n_final, it)
-                run.snapshot_prev(n_init, n_final)
-                reply = run.sweep(n_init, n_final, inc, config.delta_expl, it)
+                reply = run.iterate(*act[1:])
     except StopIteration as stop:
-        slabs, history, converged = stop.value
+        return stop.value
+
+
+def _adaptive_device(initial, fine, coarse, config):
+    n = config.n_windows
+    run = _DeviceRun(initial, fine, coarse, n)
+    expl = config.delta_expl
+
+    class _Dev:
+        bootstrap = staticmethod(run.bootstrap)
+
+        @staticmethod
+        def iterate(n_init, n_final, inc, it):
+            run.jumps(n_init, n_final, it)
+            run.snapshot_prev(n_init, n_final)
+            return run.sweep(n_init, n_final, inc, expl, it)
+
+    machine = _adaptive_machine(n, config.delta_conv, expl, config.iteration_cap)
+    slabs, history, converged = _drive_adaptive(machine, _Dev)
     return PararealResult(trajectory=run.trajectory(), slabs=tuple(slabs),
                           error_history=tuple(history), converged=converged)
 
@@ -726,6 +739,40 @@ def _corrected(coarse, state, m, iteration, jump):
                           window=m + 1, iteration=iteration) from err
 
 
+class _HostRun:
+    """The adaptive machine's actions for arbitrary callables (parareal.py:399-445):
+    bootstrap by coarse windows, jump stage, corrected sweep truncated at the
+    first node whose running error exceeds delta_expl."""
+
+    def __init__(self, initial, fine, coarse, n, expl):
+        self.fine, self.coarse, self.expl = fine, coarse, expl
+        self.cur = [initial] + [None] * n
+
+    def bootstrap(self, n_init):
+        cur = self.cur
+        for m in range(n_init, len(cur) - 1):
+            cur[m + 1] = _call(self.coarse, cur[m], m, 0)
+
+    def iterate(self, n_init, n_final, include_m0, iteration):
+        cur = self.cur
+        prev = list(cur)
+        jumps = _compute_jumps(self.fine, self.coarse, prev, range(n_init, n_final), iteration)
+        num = den = 0.0
+        if include_m0:
+            num, den = _accumulate(num, den, prev[n_init], cur[n_init])
+        deltas = []
+        for m in range(n_init, n_final):
+            cur[m + 1] = _corrected(self.coarse, cur[m], m, iteration, jumps[m - n_init])
+            num, den = _accumulate(num, den, prev[m + 1], cur[m + 1])
+            if den == 0.0:  # the machine raises for nodes max(n_init, 1)..m+1
+                deltas.append(float("nan"))
+                return deltas, den
+            deltas.append(num / den)
+            if deltas[-1] > self.expl:
+                break
+        return deltas, den
+
+
 def parareal_classic_engine(initial: PhaseState, fine: WindowPropagator, coarse: WindowPropagator,
                             config: PararealConfig, workers: int | None = None,
                             record_iterates: bool = False) -> PararealResult:
@@ -771,65 +818,10 @@ def parareal_adaptive_engine(initial: PhaseState, fine: WindowPropagator, coarse
         raise ValueError("adaptive mode needs delta_expl in the configuration")
     if _is_device(fine, coarse):
         return _adaptive_device(initial, fine, coarse, config)
-    n = config.n_windows
-    conv, expl = config.delta_conv, config.delta_expl
-    mid = 0.5 * (conv + expl)
-    cur = [initial] + [None] * n
-    n_init = n_final = 0
-    delta = mid
-    n_slab = 0
-    slabs, history, attempts = [], [], []
-    k_in_slab = 0
-    converged = True
-    while n_final < n:
-        if delta < expl:
-            n_init, n_final = n_final, n
-            for m in range(n_init, n):
-                cur[m + 1] = _call(coarse, cur[m], m, 0)
-            n_slab += 1
-            attempts = []
-            k_in_slab = 0
-        delta = mid
-        k_attempt = 0
-        aborted = False
-        while conv <= delta <= expl:
-            if k_attempt >= config.iteration_cap:
-                aborted = True
-                break
-            prev = list(cur)
-            jumps = _compute_jumps(fine, coarse, prev, range(n_init, n_final), k_in_slab + 1)
-            k_attempt += 1
-            k_in_slab += 1
-            num = den = 0.0
-            if n_init >= 1:
-                num, den = _accumulate(num, den, prev[n_init], cur[n_init])
-            for m in range(n_init, n_final):
-                cur[m + 1] = _corrected(coarse, cur[m], m, k_in_slab, jumps[m - n_init])
-                num, den = _accumulate(num, den, prev[m + 1], cur[m + 1])
-                if den == 0.0:
-                    raise DegenerateNormalizationError(
-                        f"all reference positions on nodes {max(n_init, 1)}..{m + 1} are zero")
-                delta = num / den
-                history.append((n_slab, k_in_slab, delta))
-                if delta > expl:
-                    if m == n_init:
-                        raise SlabCollapseError(
-                            f"slab {n_slab} exploded at its first window {n_init + 1}; "
-                            f"no shorter slab exists", slab_index=n_slab, n_init=n_init)
-                    _close_attempt(attempts, n_init, n_final, k_attempt)
-                    n_final = m
-                    break
-        if aborted:
-            _close_attempt(attempts, n_init, n_final, k_attempt)
-            slabs.append(SlabRecord(n_slab, n_init, tuple(attempts), n_final,
-                                    sum(a.iterations for a in attempts)))
-            converged = False
-            break
-        if delta < conv:
-            _close_attempt(attempts, n_init, n_final, k_attempt)
-            slabs.append(SlabRecord(n_slab, n_init, tuple(attempts), n_final,
-                                    sum(a.iterations for a in attempts)))
-    return PararealResult(trajectory=NodeTrajectory(tuple(cur)), slabs=tuple(slabs),
+    run = _HostRun(initial, fine, coarse, config.n_windows, config.delta_expl)
+    machine = _adaptive_machine(config.n_windows, config.delta_conv, config.delta_expl, config.iteration_cap)
+    slabs, history, converged = _drive_adaptive(machine, run)
+    return PararealResult(trajectory=NodeTrajectory(tuple(run.cur)), slabs=tuple(slabs),
                           error_history=tuple(history), converged=converged)
 
 

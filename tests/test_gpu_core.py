@@ -112,12 +112,96 @@ def test_batched_windows_match_single(pl):
         assert one.q.tobytes() == b.q.tobytes() and one.p.tobytes() == b.p.tobytes()
 
 
-def test_blowup_reports_substep(pl):
+# ------------------------------------------------------------------ blow-up parity
+# The reference's own failure tests (test_integrator.py:602-627,
+# test_parareal.py:238-244, 397-422), run through the device path.
+def _st(q, p=None):
+    q = np.asarray(q, dtype=float)
+    return q, (np.zeros_like(q) if p is None else np.asarray(p, dtype=float))
+
+
+def test_blow_up_raises_with_substep(pl):
+    """omega*dt = 100: the splitting is unstable; first bad substep is 2, no window context."""
     params = pl.LangevinParams(0.0, 0.0, 0.1, 20)
+    sched = pl.TemperatureSchedule.identity(20)
+    q, p = _st([1.0])
+    with pytest.raises(pl.BlowUpError, match="substep") as ei:
+        pl.propagate_window(pl.PhaseState(q=q, p=p), pl.Harmonic(k=1e6), params, sched, 1)
+    assert ei.value.substep == 2
+    assert ei.value.window is None
+
+
+def test_blow_up_on_out_of_range_start(pl):
+    params = pl.LangevinParams(0.0, 0.0, 0.1, 2)
+    q, p = _st([10.0 * 1e12])
     with pytest.raises(pl.BlowUpError) as ei:
-        pl.propagate_window(pl.PhaseState(q=[1e6], p=[0.0]), pl.DoubleWell(1.0, 1.0), params,
-                            pl.TemperatureSchedule.identity(20), 5)
-    assert ei.value.substep >= 1
+        pl.propagate_window(pl.PhaseState(q=q, p=p), pl.Free(), params, pl.TemperatureSchedule.identity(2), 1)
+    assert ei.value.substep == 1
+
+
+def test_blow_up_on_non_finite(pl):
+    """A gradient that overflows to inf at the first substep: 'non-finite', substep 1."""
+    params = pl.LangevinParams(0.0, 0.0, 0.1, 2)
+    q, p = _st([1.0])
+    with pytest.raises(pl.BlowUpError, match="non-finite") as ei:
+        pl.propagate_window(pl.PhaseState(q=q, p=p), pl.Harmonic(k=1e308), params,
+                            pl.TemperatureSchedule.identity(2), 1)
+    assert ei.value.substep == 1
+
+
+def test_blow_up_in_batch_reports_first_window(pl):
+    """Batched windows: the first blown-up row raises, with its own substep."""
+    params = pl.LangevinParams(0.0, 0.0, 0.1, 20)
+    sched = pl.TemperatureSchedule.identity(20)
+    states = [pl.PhaseState(q=[1e-9], p=[0.0]), pl.PhaseState(q=[1.0], p=[0.0])]
+    with pytest.raises(pl.BlowUpError) as ei:
+        pl.propagate_windows(states, pl.Harmonic(k=1e6), params, sched, [1, 2])
+    assert ei.value.substep >= 2
+
+
+def test_blow_up_sequential_reports_window(pl):
+    params = pl.LangevinParams(0.0, 0.0, 0.1, 20)
+    sched = pl.TemperatureSchedule.identity(20)
+    plan = pl.NoisePlan.for_windows(3, 4)
+    q, p = _st([1.0])
+    with pytest.raises(pl.BlowUpError) as ei:
+        pl.sequential_propagate(pl.PhaseState(q=q, p=p), 4, pl.Harmonic(k=1e6), params, sched, plan)
+    assert ei.value.window == 1
+    assert ei.value.substep == 2
+
+
+def test_blow_up_during_jump_reports_context(pl):
+    params = pl.LangevinParams(0.0, 0.0, 0.1, 20)
+    sched = pl.TemperatureSchedule.identity(20)
+    plan = pl.NoisePlan.for_windows(3, 3)
+    pair = pl.PropagatorPair(fine=pl.Harmonic(k=1e6), coarse=pl.Harmonic(k=1.0), cost_fine=2.0,
+                             cost_coarse=1.0)
+    q, p = _st([1.0])
+    cfg = pl.PararealConfig(n_windows=3, delta_conv=1e-8)
+    with pytest.raises(pl.BlowUpError) as ei:
+        pl.parareal_classic(pl.PhaseState(q=q, p=p), pair, params, sched, plan, cfg)
+    assert ei.value.window == 1
+    assert ei.value.iteration == 1
+    assert ei.value.substep is not None
+    with pytest.raises(pl.BlowUpError) as ei:
+        pl.parareal_adaptive(pl.PhaseState(q=q, p=p), pair, params, sched, plan, cfg)
+    assert ei.value.window == 1
+    assert ei.value.iteration == 1
+
+
+def test_blow_up_during_bootstrap_is_iteration_zero(pl):
+    params = pl.LangevinParams(0.0, 0.0, 0.1, 20)
+    sched = pl.TemperatureSchedule.identity(20)
+    plan = pl.NoisePlan.for_windows(3, 3)
+    pair = pl.PropagatorPair(fine=pl.Harmonic(k=1.0), coarse=pl.Harmonic(k=1e6), cost_fine=2.0,
+                             cost_coarse=1.0)
+    q, p = _st([1.0])
+    cfg = pl.PararealConfig(n_windows=3, delta_conv=1e-8)
+    for engine in (pl.parareal_classic, pl.parareal_adaptive):
+        with pytest.raises(pl.BlowUpError) as ei:
+            engine(pl.PhaseState(q=q, p=p), pair, params, sched, plan, cfg)
+        assert ei.value.window == 1
+        assert ei.value.iteration == 0
 
 
 # ------------------------------------------------------------------ engines

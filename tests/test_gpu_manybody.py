@@ -145,6 +145,49 @@ def test_snap_vs_oracle(pl, ncell, count):
         np.testing.assert_allclose(V[b], v, rtol=1e-10, atol=1e-10 * np.abs(v).max())
 
 
+def _snap_oracle_check(native, Q, box, pot, E, G, V, systems):
+    for b in systems:
+        e, g, v = native.snap(Q[b], box, pot)
+        assert E[b] == pytest.approx(e, rel=1e-10)
+        np.testing.assert_allclose(G[b], g, rtol=1e-10, atol=1e-10 * np.abs(g).max())
+        np.testing.assert_allclose(V[b], v, rtol=1e-10, atol=1e-10 * np.abs(v).max())
+
+
+def test_snap_production_batch_vs_oracle(pl):
+    """150 x 129 atoms = 19,350 atoms (605 blocks of 32 atoms, > 148 SMs, >= 4 waves of
+    8-atom runs): the batch sizes of the bench, force sweep and ensemble, which dispatch
+    the non-split Y kernel k_snap_yi_box<12,0,1> and the run force kernel
+    k_snap_deidrj_run<8,4> naturally.  Sampled systems vs the oracle (<= 1e-10), and
+    each sampled system bitwise equal to its single-system evaluation (split Y
+    kernel <12,2,2> + 2-atom pair kernel): the batch never changes the arithmetic."""
+    from oracle import native
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(4, 150, seed=11)
+    n = Q.shape[1] // 3
+    pot = W.make_snap(n, box)
+    E, G, V = (x.cpu().numpy() for x in pot.evaluate(Q, True, True, True))
+    sample = (0, 1, 74, 75, 148, 149)
+    _snap_oracle_check(native, Q, box, pot, E, G, V, sample)
+    for b in sample:
+        e1, g1, v1 = (x.cpu().numpy() for x in pot.evaluate(Q[b:b + 1], True, True, True))
+        assert e1[0].tobytes() == E[b].tobytes()
+        assert g1[0].tobytes() == G[b].tobytes()
+        assert v1[0].tobytes() == V[b].tobytes()
+
+
+def test_snap_heavy_system_vs_oracle(pl):
+    """Two 16,001-atom systems (BASELINE configs[4] cell; cell-list neighbours,
+    32,002 atoms dispatch the run force kernel): system 0 vs the oracle <= 1e-10."""
+    from oracle import native
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(20, 2, sigma=0.08, seed=13)
+    n = Q.shape[1] // 3
+    assert n == 16001
+    pot = W.make_snap(n, box)
+    E, G, V = (x.cpu().numpy() for x in pot.evaluate(Q, True, True, True))
+    _snap_oracle_check(native, Q, box, pot, E, G, V, (0,))
+
+
 _AB_SCRIPT = """
 import sys, numpy as np, torch
 sys.path.insert(0, '.')
@@ -157,30 +200,46 @@ np.savez(sys.argv[1], E=E, G=G, V=V)
 """
 
 
-def test_snap_pair_form_matches_ordered_form(pl, tmp_path):
-    """k_snap_deidrj_pair (one adjoint sweep per unordered pair with
-    Y_i + Y_k^dagger, U(-r) = U(r)^dagger) against k_snap_deidrj_adj4 (one sweep
-    per ordered pair): same energies, forces and virials to 1e-12."""
+def test_snap_specialised_matches_general_kernels(pl, tmp_path):
+    """twojmax-8 kernels (k_snap_ui_r4, box-form Y, pair-symmetric reverse-mode forces
+    with 2-atom warps or 8-atom runs) against the general-twojmax kernels (k_snap_ui,
+    k_snap_yi, forward-mode k_snap_deidrj; PL_SNAP_GENERIC=1): energies, forces and
+    virials to 1e-12; the two pair-kernel forms agree bit for bit."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    # ordered form; pair form with 2-atom warps; pair form with 8-atom runs (forced)
-    for mode, env_add in (("ord", {"PL_SNAP_PAIR": "0"}), ("pair", {"PL_SNAP_PAIR_RUN": "0"}),
+    for mode, env_add in (("gen", {"PL_SNAP_GENERIC": "1"}), ("pair", {"PL_SNAP_PAIR_RUN": "0"}),
                           ("run", {"PL_SNAP_PAIR_RUN": "2"})):
         f = str(tmp_path / f"ab_{mode}.npz")
         env = dict(os.environ, **env_add)
         subprocess.run([sys.executable, "-c", _AB_SCRIPT, f], cwd=root, env=env, check=True)
         out[mode] = np.load(f)
-    a = out["ord"]
+    a = out["gen"]
     for m in ("pair", "run"):
         b = out[m]
-        np.testing.assert_array_equal(a["E"], b["E"])  # energies do not depend on the force form
+        np.testing.assert_allclose(b["E"], a["E"], rtol=1e-12)
         np.testing.assert_allclose(b["G"], a["G"], rtol=1e-12, atol=1e-12 * np.abs(a["G"]).max())
         np.testing.assert_allclose(b["V"], a["V"], rtol=1e-12, atol=1e-12 * np.abs(a["V"]).max())
     # the pair gather sums each pair once, in list order: runs and 2-atom warps agree bit for bit
     np.testing.assert_array_equal(out["pair"]["G"], out["run"]["G"])
+    np.testing.assert_array_equal(out["pair"]["E"], out["run"]["E"])
+
+
+@pytest.mark.parametrize("twojmax", [2, 4, 6])
+def test_snap_other_twojmax_vs_oracle(pl, twojmax):
+    """General-twojmax kernels (paper Strategy I coarse SNAP-6 is twojmax 2) vs the oracle."""
+    from oracle import native
+    from paper_2212_10508_b200.potentials import SNAP
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(4, 3, seed=21)
+    n = Q.shape[1] // 3
+    nb = {2: 5, 4: 14, 6: 30}[twojmax]
+    beta = np.concatenate([[0.1], 0.05 * np.random.default_rng(twojmax).normal(size=nb)])
+    pot = SNAP(n_atoms=n, box=box, beta=beta, twojmax=twojmax)
+    E, G, V = (x.cpu().numpy() for x in pot.evaluate(Q, True, True, True))
+    _snap_oracle_check(native, Q, box, pot, E, G, V, range(3))
 
 
 def test_snap_invariances_on_device(pl):
