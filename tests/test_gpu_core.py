@@ -184,7 +184,8 @@ def test_blow_up_during_jump_reports_context(pl):
     assert ei.value.iteration == 1
     assert ei.value.substep is not None
     with pytest.raises(pl.BlowUpError) as ei:
-        pl.parareal_adaptive(pl.PhaseState(q=q, p=p), pair, params, sched, plan, cfg)
+        pl.parareal_adaptive(pl.PhaseState(q=q, p=p), pair, params, sched, plan,
+                             pl.PararealConfig(n_windows=3, delta_conv=1e-8, delta_expl=0.35))
     assert ei.value.window == 1
     assert ei.value.iteration == 1
 
@@ -196,7 +197,7 @@ def test_blow_up_during_bootstrap_is_iteration_zero(pl):
     pair = pl.PropagatorPair(fine=pl.Harmonic(k=1.0), coarse=pl.Harmonic(k=1e6), cost_fine=2.0,
                              cost_coarse=1.0)
     q, p = _st([1.0])
-    cfg = pl.PararealConfig(n_windows=3, delta_conv=1e-8)
+    cfg = pl.PararealConfig(n_windows=3, delta_conv=1e-8, delta_expl=0.35)
     for engine in (pl.parareal_classic, pl.parareal_adaptive):
         with pytest.raises(pl.BlowUpError) as ei:
             engine(pl.PhaseState(q=q, p=p), pair, params, sched, plan, cfg)
