@@ -117,9 +117,7 @@ __device__ __forceinline__ void half_layer8(int t, int& J, int& base) {
 }
 __constant__ int c_foff[SNAP_JMAX + 2];
 // box-form Z/Y kernel (snap_yi8.cu, own constant bank)
-cudaError_t snap_box_setup(const double* box, int nbox, const int* off, const int* code, const int* iseg,
-                           const int* items, int nitems, const int* rowsplit);
-int snap_box_variants(int* nw, int* ns);
+cudaError_t snap_yi8_setup(double* balance_out);
 cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef,
                             const void* utot, void* ylist, double* eatom, double* erow_g);
 
@@ -131,7 +129,7 @@ static double fact(int n) {
 }
 
 // Condon-Shortley <j1 m1 j2 m2 | J M> (Racah formula), arguments are 2j / 2m
-static double clebsch(int j1, int m1, int j2, int m2, int J, int M) {
+double snap_clebsch(int j1, int m1, int j2, int m2, int J, int M) {
   if (m1 + m2 != M || std::abs(m1) > j1 || std::abs(m2) > j2 || std::abs(M) > J) return 0.0;
   if (J < std::abs(j1 - j2) || J > j1 + j2 || ((j1 + j2 + J) & 1)) return 0.0;
   double pre = std::sqrt((J + 1) * fact((j1 + j2 - J) / 2) * fact((j1 - j2 + J) / 2) *
@@ -204,7 +202,6 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     std::vector<double> cy, be;
     std::vector<int> code;
     std::vector<std::vector<int>> byJ(tj + 1);
-    std::vector<double> rowcost(64, 0.0);
     for (int x = 0; x <= tj; ++x)
       for (int y = 0; y <= x; ++y)
         for (int J = x - y; J <= std::min(tj, x + y); J += 2) {
@@ -216,144 +213,10 @@ int snap_prepare(pl_pot* pot, const double* beta) {
           code.push_back(x * 100 + y * 10 + J);
           byJ[J].push_back(tid);
         }
-    std::vector<std::pair<double, int>> rows;  // (cost, J << 8 | mb) of the (J, mb) half rows
-    // rows -> NW warps: LPT, then deterministic local search (single moves and
-    // pairwise swaps) that lowers the makespan, ties broken by the sum of
-    // squared loads.  For 25 rows on 12 warps LPT reaches ~83 % balance, the
-    // search ~96 % (cost model).
-    auto lpt = [&](int NW, std::vector<int>& groups, std::vector<int>& gseg) {
-      const int nr = (int)rows.size();
-      std::vector<int> asg(nr);
-      std::vector<double> wl(NW, 0.0);
-      for (int i = 0; i < nr; ++i) {
-        int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
-        asg[i] = w;
-        wl[w] += rows[i].first;
-      }
-      auto score = [&](const std::vector<double>& l) {
-        double mx = 0.0, sq = 0.0;
-        for (double v : l) {
-          mx = std::max(mx, v);
-          sq += v * v;
-        }
-        return std::make_pair(mx, sq);
-      };
-      for (bool improved = true; improved;) {
-        improved = false;
-        auto cur = score(wl);
-        for (int i = 0; i < nr; ++i)
-          for (int w = 0; w < NW; ++w) {
-            if (w == asg[i]) continue;
-            std::vector<double> nl(wl);
-            nl[asg[i]] -= rows[i].first;
-            nl[w] += rows[i].first;
-            auto sc = score(nl);
-            if (sc < cur) {
-              wl = nl;
-              asg[i] = w;
-              cur = sc;
-              improved = true;
-            }
-          }
-        for (int i = 0; i < nr; ++i)
-          for (int j = i + 1; j < nr; ++j) {
-            const int a = asg[i], b = asg[j];
-            if (a == b) continue;
-            std::vector<double> nl(wl);
-            nl[a] += rows[j].first - rows[i].first;
-            nl[b] += rows[i].first - rows[j].first;
-            auto sc = score(nl);
-            if (sc < cur) {
-              wl = nl;
-              std::swap(asg[i], asg[j]);
-              cur = sc;
-              improved = true;
-            }
-          }
-      }
-      std::vector<std::vector<int>> wr(NW);
-      for (int i = 0; i < nr; ++i) wr[asg[i]].push_back(rows[i].second);
-      gseg.assign(NW + 1, 0);
-      groups.clear();
-      for (int w = 0; w < NW; ++w) {
-        gseg[w] = (int)groups.size();
-        groups.insert(groups.end(), wr[w].begin(), wr[w].end());
-      }
-      gseg[NW] = (int)groups.size();
-    };
-    {  // box kernel (snap_yi8.cu): every (X+1)(Y+1) product of each admissible mb1
-      for (int J = 0; J <= tj; ++J)
-        for (int mb = 0; 2 * mb <= J; ++mb) {
-          double c = 0.0;
-          for (int tid : byJ[J]) {
-            int x = code[tid] / 100, y = (code[tid] / 10) % 10, sh = (x + y - J) / 2;
-            const int mb1_hi = 2 * mb == J ? x / 2 : (x == y ? (mb + sh) / 2 : x);  // symmetry halvings
-            for (int mb1 = 0; mb1 <= mb1_hi; ++mb1)
-              if (mb + sh - mb1 >= 0 && mb + sh - mb1 <= y) c += 7.0 * (x + 1) * (y + 1) + 2.0 * (x + y + 2) + 12.0;
-            c += 60.0;
-          }
-          rows.push_back({c, (J << 8) | mb});
-        }
-      std::sort(rows.begin(), rows.end(), [](auto& a, auto& b) { return a.first > b.first; });
-      // rows -> NW*S virtual warps (LPT; virtual warp w runs on CTA w / NW of the
-      // block), then each warp's (row, triple) items in ascending X
-      auto row_index = [](int J, int mb) {
-        int r = 0;
-        for (int j = 0; j < J; ++j) r += j / 2 + 1;
-        return r + mb;
-      };
-      auto itemize = [&](int NW, int NS, std::vector<int>& iseg, std::vector<int>& items,
-                         std::vector<int>& rowsplit) {
-        std::vector<int> g, sg;
-        const int NV = NW * NS;
-        lpt(NV, g, sg);
-        iseg.assign(26, 0);
-        rowsplit.assign(25, 0);
-        items.clear();
-        for (int w = 0; w < NV; ++w) {
-          iseg[w] = (int)items.size();
-          std::vector<std::pair<int, int>> mine;  // (sort key, item)
-          for (int gi = sg[w]; gi < sg[w + 1]; ++gi) {
-            const int J = g[gi] >> 8, mb = g[gi] & 0xff;
-            rowsplit[row_index(J, mb)] = w / NW;
-            for (int tid : byJ[J]) {
-              const int x = code[tid] / 100, y = (code[tid] / 10) % 10;
-              mine.push_back({x * 10000 + y * 100 + J * 10 + mb, (tid << 16) | (J << 8) | mb});
-            }
-          }
-          std::sort(mine.begin(), mine.end());
-          for (auto& m : mine) items.push_back(m.second);
-        }
-        for (int w = NV; w < 26; ++w) iseg[w] = (int)items.size();
-      };
-      int box_nw[8], box_ns[8];
-      const int box_nv = snap_box_variants(box_nw, box_ns);
-      std::vector<int> iseg_all(box_nv * 26, 0), items_all, rowsplit_all(box_nv * 25, 0);
-      for (int v = 0; v < box_nv; ++v) {
-        std::vector<int> is, it, rs;
-        itemize(box_nw[v], box_ns[v], is, it, rs);
-        std::copy(is.begin(), is.end(), iseg_all.begin() + v * 26);
-        std::copy(rs.begin(), rs.end(), rowsplit_all.begin() + v * 25);
-        items_all.insert(items_all.end(), it.begin(), it.end());
-      }
-      const int n_items = (int)items_all.size() / box_nv;
-      static std::atomic<uint64_t> box_devs{0};  // __constant__ tables are per device
-      if (first_on_device(box_devs)) {
-        std::vector<double> box;
-        std::vector<int> boff;
-        for (int c : code) {
-          const int x = c / 100, y = (c / 10) % 10, J = c % 10, sh = (x + y - J) / 2;
-          boff.push_back((int)box.size());
-          for (int b = 0; b <= y; ++b)
-            for (int a = 0; a <= x; ++a) {
-              const int ma = a + b - sh;
-              box.push_back(ma >= 0 && ma <= J ? clebsch(x, 2 * a - x, y, 2 * b - y, J, 2 * ma - J) : 0.0);
-            }
-        }
-        if ((int)code.size() != 125) return fail(PL_EARG, "SNAP box tables: unexpected triple count");
-        PL_CUDA(snap_box_setup(box.data(), (int)box.size(), boff.data(), code.data(), iseg_all.data(),
-                               items_all.data(), n_items, rowsplit_all.data()));
-      }
+    static std::atomic<uint64_t> yi_devs{0};  // __constant__ tables are per device
+    if (first_on_device(yi_devs)) {
+      double bal = 0.0;
+      PL_CUDA(snap_yi8_setup(&bal));
     }
     std::vector<double> cb2(cy);
     cb2.insert(cb2.end(), be.begin(), be.end());
@@ -383,7 +246,7 @@ int snap_prepare(pl_pot* pot, const double* beta) {
               int m2 = M - (2 * ma1 - x);
               if (std::abs(m2) > y) continue;
               if (lo < 0) lo = ma1;
-              ca.push_back(clebsch(x, 2 * ma1 - x, y, m2, J, M));
+              ca.push_back(snap_clebsch(x, 2 * ma1 - x, y, m2, J, M));
             }
             it.ma1lo = (int16_t)lo;
             it.na = (int16_t)ca.size();
@@ -392,7 +255,7 @@ int snap_prepare(pl_pot* pot, const double* beta) {
               int m2 = Mp - (2 * mb1 - x);
               if (std::abs(m2) > y) continue;
               if (lo < 0) lo = mb1;
-              cb.push_back(clebsch(x, 2 * mb1 - x, y, m2, J, Mp));
+              cb.push_back(snap_clebsch(x, 2 * mb1 - x, y, m2, J, Mp));
             }
             it.mb1lo = (int16_t)lo;
             it.nb = (int16_t)cb.size();

@@ -1,31 +1,46 @@
-// SNAP Z/Y contraction, twojmax = 8, "box" form (k_snap_yi_box).
+// SNAP Z/Y contraction at twojmax = 8: k_snap_yi_p ("P form").
 //
-// Lanes = atoms (32 per CTA, U^J of all layers expanded to full matrices in
-// shared memory, as k_snap_yi_six); warps own (J, mb) half rows by an LPT
-// schedule.  For every triple (X, Y, J) of a row and every admissible mb1,
-// both U columns U^X[.][mb1] and U^Y[.][mb2] are loaded into registers (the
-// b-side CG factor C(mb, mb1) folded into U^Y) and ALL (X+1)(Y+1) products are
-// accumulated on their anti-diagonal s = ma1 + ma2 (compile-time register
-// index), weighted by the box table C(ma = s - SH, ma1) that is zero outside
-// the CG band.  The code per (X, Y) is one branch-free block of independent
-// FMA chains with constant-bank coefficients at compile-time offsets; the
-// corner products it spends on zeros (~40%) are cheaper than the per-product
-// index arithmetic and predication of the banded loops (k_snap_yi_six).  The
-// diagonals are mapped to the z row (runtime shift SH) through the warp's
-// shared strip once per (triple, row).
+// For a triple (X, Y, J) (X >= Y) and a half row mb of layer J,
+//   Z[ma][mb] = sum_{a, mb1} C(ma; a) C(mb; mb1) U^X[a][mb1] U^Y[b][mb2],
+//   b = ma + SH - a,  mb2 = mb + SH - mb1,  SH = (X + Y - J) / 2.
+// The kernel sums over mb1 FIRST, per cell (a, b) of the CG band
+// (SH <= a + b <= SH + J):
+//   P[a][b] = sum_mb1 U^X[a][mb1] (C(mb; mb1) U^Y[b][mb2])          4 DFMA / product
+//   Z[ma]   = sum_a C(ma; a) P[a][ma + SH - a]                      once per cell
+// so the a-side CG weight leaves the inner loop (the previous "box" kernel
+// applied it per product: 2 DMUL + 4 DFMA, and spent ~40 % of its products on
+// the zero corners of the (X+1)(Y+1) box; this form issues only band products,
+// 1.83x fewer FP64 instructions per atom).  The band is compile-time, so P
+// lives in registers: one body per triple, ptri<X, Y, J> (125 bodies).
 //
-// Separate translation unit: the box table (32.8 KB) has its own constant
-// bank next to snap.cu's CG blocks.
+// Lanes = atoms (32 per CTA; U^J of all layers expanded to full matrices in
+// shared memory, [element][atom], conflict-free), warps own (J, mb) half rows.
+// Code size: 125 bodies are ~4x the box kernel's, more than the instruction
+// cache holds.  The CTA therefore walks the triples in PHASES of X (X <= 4,
+// 5, 6, 7, 8) separated by __syncthreads(): only one phase's bodies are live
+// at a time, and the rows are re-assigned to warps per phase (host LPT +
+// local search on a cost model), which also balances each phase.  A row's
+// items are summed in (X, Y) order whatever warp or phase takes them, so Y
+// does not depend on the schedule or on the batch (bitwise).
+//
+// Symmetries (as in the box kernel): middle rows (2 mb = J) sum mb1 <= X/2 and
+// are folded once at the end (U[J-ma][J-mb] = (-1)^(ma+mb) conj U[ma][mb]);
+// for X = Y the other rows sum mb1 <= mb2 with weight 2 off the diagonal.
+// Energy by Euler's identity E = beta0 + (1/3) sum_J <U^J, Y^J>.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
+#include <utility>
+#include <vector>
 
 namespace pl {
 
+double snap_clebsch(int j1, int m1, int j2, int m2, int J, int M);  // snap.cu
+
 __device__ __forceinline__ void griddep_wait_yi() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// programmatic dependent launch (see pl_common.cuh launch_pdl)
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl_yi(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                                  Args&&... args) {
@@ -49,6 +64,8 @@ constexpr int NFULL = 285;     // sum (J+1)^2
 constexpr int NHALF = 155;     // sum (J+1)(J/2+1)
 constexpr int ATOMS = 32;
 constexpr int BOX_MAX = 4098;  // sum over triples of (X+1)(Y+1)
+constexpr int ROWS = 25;       // (J, mb <= J/2) half rows
+constexpr int NPH = 5;         // phases: X <= 4, 5, 6, 7, 8
 constexpr int foff(int J) { return J * (J + 1) * (2 * J + 1) / 6; }
 constexpr int rowoff(int J) { return (J / 2 + 1) * (J / 2 + 1) - (J % 2 == 0 ? J / 2 + 1 : 0); }  // rows of layers < J
 constexpr int hoff(int J) {
@@ -56,9 +73,21 @@ constexpr int hoff(int J) {
   for (int j = 0; j < J; ++j) h += (j + 1) * (j / 2 + 1);
   return h;
 }
+constexpr int phase(int X) { return X <= 4 ? 0 : X - 4; }
+// offset of triple (X, Y, J) in the box table, triples in (x, y <= x, J) order
+constexpr int box_off(int X, int Y, int J) {
+  int o = 0;
+  for (int x = 0; x <= TJ; ++x)
+    for (int y = 0; y <= x; ++y)
+      for (int j = x - y; j <= (TJ < x + y ? TJ : x + y); j += 2) {
+        if (x == X && y == Y && j == J) return o;
+        o += (x + 1) * (y + 1);
+      }
+  return -1;
+}
 }  // namespace yib
 
-__constant__ double c_box[yib::BOX_MAX];  // per triple: [Y+1][X+1]
+__constant__ double c_box[yib::BOX_MAX];  // per triple: [Y+1][X+1], C(ma = a + b - SH; X a, Y b)
 
 // full-matrix element f -> its source in the half-row storage: (src << 2) |
 // (mirrored << 1) | (odd ma + mb); U[ma][mb] for 2 mb > J is (-1)^(ma+mb)
@@ -78,93 +107,101 @@ struct BoxExpand {
   }
 };
 __constant__ BoxExpand c_box_exp = BoxExpand();
-__constant__ int c_box_off[yib::NT];
-__constant__ int c_box_code[yib::NT];         // X*100 + Y*10 + J
-constexpr int BOX_MAX_ITEMS = 400;            // (row, triple) pairs: 375 at twojmax 8
-// compiled variants: (warps per CTA, CTAs per 32-atom block).  A block's
-// (J, mb) rows are split over S CTAs when the batch has fewer blocks than SMs
-// (latency of small systems); each row stays with one warp.  (3 warps per SM
-// sub-partition leave 168 registers per thread; 4 would force 128 and spill.)
-constexpr int BOX_NV = 3;
-constexpr int BOX_NW[BOX_NV] = {12, 8, 12};
-constexpr int BOX_NS[BOX_NV] = {1, 1, 2};
-constexpr int BOX_ROWS = 25;                              // (J, mb <= J/2) half rows at twojmax 8
-__constant__ int c_box_iseg[BOX_NV][BOX_ROWS + 1];        // items of virtual warp w: [iseg[w], iseg[w+1])
-__constant__ int c_box_items[BOX_NV][BOX_MAX_ITEMS];     // tid << 16 | J << 8 | mb
-__constant__ int c_box_rowsplit[BOX_NV][BOX_ROWS];       // CTA of the block that owns row r
+__constant__ int c_box_code[yib::NT];  // X*100 + Y*10 + J
+// compiled variants: (warps per CTA, CTAs per 32-atom block).  A block's rows
+// are split over S CTAs when the batch has fewer blocks than SMs (latency of
+// small systems); a row stays with one CTA for the whole kernel.
+constexpr int P_NV = 2;
+constexpr int P_NW[P_NV] = {8, 8};
+constexpr int P_NS[P_NV] = {1, 2};
+constexpr int P_MAX_VW = 24;
+constexpr int P_MAX_ITEMS = 400;  // (row, triple) items: 375 at twojmax 8
+__constant__ int c_p_iseg[P_NV][yib::NPH][P_MAX_VW + 1];  // items of virtual warp w in phase p
+__constant__ int c_p_items[P_NV][P_MAX_ITEMS];           // tid << 16 | J << 8 | mb
+__constant__ int c_p_rowsplit[P_NV][yib::ROWS];          // CTA of the block that owns row r
 
 struct Cx {
   double re, im;
 };
 
-// The middle row (2 mb = J): the terms of mb1 and X - mb1 are images of each
-// other under U[J-ma][J-mb] = (-1)^(ma+mb) conj(U[ma][mb]) (CG included), so
-// only mb1 <= X/2 is summed (the self-image X/2 with weight 1/2, exact) over the
-// whole band ma = 0..J; the kernel folds the row's upper half onto the lower
-// half once all items are in (fold_middle_rows).
-template <int X>
-__device__ __forceinline__ void box_x(const Cx* __restrict__ Ul, int Y, int SH, int J, bool mid, int mb, int boff,
-                                      double cy, Cx* __restrict__ yrow) {
-  const int jtop = J;
-  constexpr int S = X + yib::TJ;
-  constexpr int FX = yib::foff(X);
-  Cx d[S + 1];
+struct PItem {
+  const Cx* Ul;  // full U matrices, this lane's atom
+  Cx* yrow;      // Y half row (J, mb), this lane's atom
+  double cy;     // coefficient of Z^{XY}_J in Y^J
+  int mb, lo, hi;
+  bool mid, swap;
+};
+
+// rows a in [A0, A1] of the band (the whole band except for (8, 8, 8), whose 61
+// cells do not fit 255 registers and run as two halves)
+template <int X, int Y, int J, int A0 = 0, int A1 = X>
+__device__ __forceinline__ void ptri(const PItem& A) {
+  constexpr int SH = (X + Y - J) / 2;
+  constexpr int OFF = yib::box_off(X, Y, J);
+  constexpr int FX = yib::foff(X), FY = yib::foff(Y);
+  constexpr int AT = yib::ATOMS;
+  Cx P[X + 1][Y + 1];
 #pragma unroll
-  for (int s = 0; s <= S; ++s) d[s] = Cx{0.0, 0.0};
-  const double* cb = c_box + boff;  // [Y+1][X+1]: cb[b * (X + 1) + a] = C(ma = a + b - SH, ma1 = a)
-  const int FY = yib::foff(Y);
-  // X = Y (other rows): the (mb1, ma1) and (mb2, ma2) factors swap roles with an
-  // unchanged CG product, so mb1 <= mb2 is summed with weight 2 off the diagonal
-  const bool swap = (Y == X) && !mid;
-  const int lo = max(0, mb + SH - Y);
-  const int hi = mid ? X / 2 : (swap ? (mb + SH) / 2 : min(X, mb + SH));
+  for (int a = 0; a <= X; ++a)
+#pragma unroll
+    for (int b = 0; b <= Y; ++b) P[a][b] = Cx{0.0, 0.0};  // corners are never read: no registers
+  const Cx* __restrict__ Ul = A.Ul;
 #pragma unroll 1
-  for (int mb1 = lo; mb1 <= hi; ++mb1) {
-    const int mb2 = mb + SH - mb1;
-    const double w = mid ? (2 * mb1 == X ? 0.5 : 1.0) : (swap ? (mb1 == mb2 ? 1.0 : 2.0) : 1.0);
-    const double cbv = w * cb[mb2 * (X + 1) + mb1];  // w C(mb, mb1), w exact
-    const Cx* px = Ul + (FX + mb1 * (X + 1)) * yib::ATOMS;
-    const Cx* py = Ul + (FY + mb2 * (Y + 1)) * yib::ATOMS;
+  for (int mb1 = A.lo; mb1 <= A.hi; ++mb1) {
+    const int mb2 = A.mb + SH - mb1;
+    const double w = A.mid ? (2 * mb1 == X ? 0.5 : 1.0) : (A.swap ? (mb1 == mb2 ? 1.0 : 2.0) : 1.0);
+    const double cbv = w * c_box[OFF + mb2 * (X + 1) + mb1];  // w C(mb; mb1), w exact
+    const Cx* px = Ul + (FX + mb1 * (X + 1)) * AT;
+    const Cx* py = Ul + (FY + mb2 * (Y + 1)) * AT;
     Cx ux[X + 1];
 #pragma unroll
-    for (int a = 0; a <= X; ++a) ux[a] = px[a * yib::ATOMS];
-    // element b of the U^Y column times row block b of the box: X+1 independent
-    // diagonals (skipping the zero corners per product costs more than it saves)
+    for (int a = A0; a <= A1; ++a) ux[a] = px[a * AT];
 #pragma unroll
-    for (int b = 0; b <= yib::TJ; ++b) {
-      if (b > Y) break;
-      const Cx v = py[b * yib::ATOMS];
+    for (int b = 0; b <= Y; ++b) {
+      const Cx v = py[b * AT];
       const Cx uy{cbv * v.re, cbv * v.im};
 #pragma unroll
-      for (int a = 0; a <= X; ++a) {
-        const double c = cb[b * (X + 1) + a];
-        const double tr = c * ux[a].re, ti = c * ux[a].im;
-        d[a + b].re = fma(tr, uy.re, d[a + b].re);
-        d[a + b].im = fma(tr, uy.im, d[a + b].im);
-        d[a + b].re = fma(-ti, uy.im, d[a + b].re);
-        d[a + b].im = fma(ti, uy.re, d[a + b].im);
+      for (int a = A0; a <= A1; ++a) {
+        if (a + b < SH || a + b > SH + J) continue;  // outside the CG band (compile time)
+        P[a][b].re = fma(ux[a].re, uy.re, P[a][b].re);
+        P[a][b].im = fma(ux[a].re, uy.im, P[a][b].im);
+        P[a][b].re = fma(-ux[a].im, uy.im, P[a][b].re);
+        P[a][b].im = fma(ux[a].im, uy.re, P[a][b].im);
       }
     }
   }
-  // diagonal s -> element ma = s - SH of the Y row (the warp owns the row)
-  Cx* yo = yrow - SH * yib::ATOMS;
+  // Z[ma] = sum_a C(ma; a) P[a][ma + SH - a], then Y[ma] += cy Z[ma] (the warp owns the row)
+  Cx* yo = A.yrow;
 #pragma unroll
-  for (int s = 0; s <= S; ++s) {
-    if (s >= SH && s <= SH + jtop) {
-      Cx y = yo[s * yib::ATOMS];
-      y.re = fma(cy, d[s].re, y.re);
-      y.im = fma(cy, d[s].im, y.im);
-      yo[s * yib::ATOMS] = y;
+  for (int ma = 0; ma <= J; ++ma) {
+    Cx z{0.0, 0.0};
+#pragma unroll
+    for (int a = A0; a <= A1; ++a) {
+      const int b = ma + SH - a;
+      if (b < 0 || b > Y) continue;
+      const double c = c_box[OFF + b * (X + 1) + a];
+      z.re = fma(c, P[a][b].re, z.re);
+      z.im = fma(c, P[a][b].im, z.im);
     }
+    Cx y = yo[ma * AT];
+    y.re = fma(A.cy, z.re, y.re);
+    y.im = fma(A.cy, z.im, y.im);
+    yo[ma * AT] = y;
   }
 }
 
-constexpr int box_regs(int nw) { return nw <= 8 ? 255 : 168; }
+__device__ __forceinline__ void ptri_dispatch(int tid, const PItem& A) {
+  switch (tid) {
+    // one case per triple, in (x, y <= x, J) order (generated)
+#include "snap_yi8_cases.inc"
+    default: break;
+  }
+}
 
 template <int NW, int V, int S>
-__global__ void __maxnreg__(box_regs(NW))
-k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, const Cx* __restrict__ utot,
-              Cx* __restrict__ ylist, double* __restrict__ eatom, double* __restrict__ erow_g) {
+__global__ void __launch_bounds__(NW * 32, 1)
+k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const Cx* __restrict__ utot,
+            Cx* __restrict__ ylist, double* __restrict__ eatom, double* __restrict__ erow_g) {
   griddep_wait_yi();
   extern __shared__ double smem[];
   Cx* Uf = reinterpret_cast<Cx*>(smem);                 // [NFULL][32] full U matrices
@@ -210,40 +247,34 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
   }
   __syncthreads();  // staged U_tot consumed before Y is cleared
   for (int t = threadIdx.x; t < yib::NHALF * yib::ATOMS; t += blockDim.x) Ys[t] = Cx{0.0, 0.0};
-  for (int t = threadIdx.x; t < BOX_ROWS * yib::ATOMS; t += blockDim.x) erow[t] = 0.0;
+  for (int t = threadIdx.x; t < yib::ROWS * yib::ATOMS; t += blockDim.x) erow[t] = 0.0;
   __syncthreads();
-  const Cx* Ul = Uf + lane;
   const int vw = split * NW + warp;  // virtual warp of the block's schedule
-  // the warp's (row, triple) items in ascending X: all warps sweep the X
-  // instantiations in the same order, so the live code stays small
-  for (int it = c_box_iseg[V][vw]; it < c_box_iseg[V][vw + 1]; ++it) {
-    const int item = c_box_items[V][it];
-    const int tid = item >> 16, J = (item >> 8) & 0xff, mb = item & 0xff;
-    const int code = c_box_code[tid];
-    const int X = code / 100, Y = (code / 10) % 10;
-    const int SH = (X + Y - J) / 2;
-    const bool mid = (2 * mb == J);
-    const int boff = c_box_off[tid];
-    const double cy = coef[tid];
-    Cx* yrow = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + lane;
-    switch (X) {
-      case 0: box_x<0>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
-      case 1: box_x<1>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
-      case 2: box_x<2>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
-      case 3: box_x<3>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
-      case 4: box_x<4>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
-      case 5: box_x<5>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
-      case 6: box_x<6>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
-      case 7: box_x<7>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
-      default: box_x<8>(Ul, Y, SH, J, mid, mb, boff, cy, yrow); break;
+  for (int ph = 0; ph < yib::NPH; ++ph) {
+    for (int it = c_p_iseg[V][ph][vw]; it < c_p_iseg[V][ph][vw + 1]; ++it) {
+      const int item = c_p_items[V][it];
+      const int tid = item >> 16, J = (item >> 8) & 0xff, mb = item & 0xff;
+      const int code = c_box_code[tid];
+      const int X = code / 100, Y = (code / 10) % 10;
+      const int SH = (X + Y - J) / 2;
+      PItem A;
+      A.Ul = Uf + lane;
+      A.yrow = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + lane;
+      A.cy = coef[tid];
+      A.mb = mb;
+      A.mid = (2 * mb == J);
+      A.swap = (Y == X) && !A.mid;
+      A.lo = max(0, mb + SH - Y);
+      A.hi = A.mid ? X / 2 : (A.swap ? (mb + SH) / 2 : min(X, mb + SH));
+      ptri_dispatch(tid, A);
     }
+    __syncthreads();  // next phase: rows change owners
   }
-  __syncthreads();
   // middle rows: Y[ma] += (-1)^(J/2+ma) conj(Y[J-ma]) for ma <= J/2 (the images of
   // the mb1 > X/2 terms), then the upper half is cleared
   for (int t = threadIdx.x; t < 5 * yib::ATOMS; t += blockDim.x) {
     const int J = 2 * (t >> 5), at = t & 31, mb = J / 2;
-    if (S > 1 && c_box_rowsplit[V][yib::rowoff(J) + mb] != split) continue;
+    if (S > 1 && c_p_rowsplit[V][yib::rowoff(J) + mb] != split) continue;
     Cx* y = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + at;
     for (int ma = 0; ma < mb; ++ma) {
       Cx lo = y[ma * yib::ATOMS];
@@ -260,9 +291,9 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
   __syncthreads();
   // energy: E - beta0 is cubic in U and Y = dE/dU, so E = beta0 + (1/3) sum_J <U^J, Y^J>
   // (half rows with the full-matrix weights); per row, rows summed in row order
-  for (int t = threadIdx.x; t < BOX_ROWS * yib::ATOMS; t += blockDim.x) {
+  for (int t = threadIdx.x; t < yib::ROWS * yib::ATOMS; t += blockDim.x) {
     const int r = t >> 5, at = t & 31;
-    if (S > 1 && c_box_rowsplit[V][r] != split) continue;
+    if (S > 1 && c_p_rowsplit[V][r] != split) continue;
     int J = 0;
     while (J < yib::TJ && r >= yib::rowoff(J + 1)) ++J;
     const int mb = r - yib::rowoff(J);
@@ -287,20 +318,20 @@ k_snap_yi_box(int64_t natoms, double beta0, const double* __restrict__ coef, con
       int J = 0;
       while (J < yib::TJ && h >= yib::hoff(J + 1)) ++J;
       const int r = yib::rowoff(J) + (h - yib::hoff(J)) / (J + 1);
-      if (c_box_rowsplit[V][r] != split) continue;
+      if (c_p_rowsplit[V][r] != split) continue;
     }
     ylist[(a0 + at) * yib::NHALF + h] = Ys[h * yib::ATOMS + at];
   }
   if (S == 1) {
     if (warp == 0 && lane < na_blk) {
       double e = beta0;
-      for (int r = 0; r < BOX_ROWS; ++r) e += erow[r * yib::ATOMS + lane];
+      for (int r = 0; r < yib::ROWS; ++r) e += erow[r * yib::ATOMS + lane];
       eatom[a0 + lane] = e;
     }
   } else {
-    for (int t = threadIdx.x; t < BOX_ROWS * na_blk; t += blockDim.x) {
+    for (int t = threadIdx.x; t < yib::ROWS * na_blk; t += blockDim.x) {
       const int r = t / na_blk, at = t - r * na_blk;
-      if (c_box_rowsplit[V][r] == split) erow_g[(int64_t)r * natoms + a0 + at] = erow[r * yib::ATOMS + at];
+      if (c_p_rowsplit[V][r] == split) erow_g[(int64_t)r * natoms + a0 + at] = erow[r * yib::ATOMS + at];
     }
   }
 }
@@ -311,54 +342,222 @@ __global__ void k_box_energy(int64_t natoms, double beta0, const double* __restr
   griddep_wait_yi();
   for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < natoms; a += (int64_t)gridDim.x * blockDim.x) {
     double e = beta0;
-    for (int r = 0; r < BOX_ROWS; ++r) e += erow_g[(int64_t)r * natoms + a];
+    for (int r = 0; r < yib::ROWS; ++r) e += erow_g[(int64_t)r * natoms + a];
     eatom[a] = e;
   }
 }
 
-// Upload the box table, the per-virtual-warp item lists and the row owners
-// (process-wide; twojmax 8 only).  iseg: [BOX_NV][ROWS+1], items: [BOX_NV][nitems],
-// rowsplit: [BOX_NV][ROWS].
-cudaError_t snap_box_setup(const double* box, int nbox, const int* off, const int* code, const int* iseg,
-                           const int* items, int nitems, const int* rowsplit) {
-  if (nbox > yib::BOX_MAX || nitems > BOX_MAX_ITEMS) return cudaErrorInvalidValue;
+// ------------------------------------------------------------------ host schedule
+namespace {
+
+struct Triple {
+  int X, Y, J;
+};
+
+std::vector<Triple> triples8() {
+  std::vector<Triple> t;
+  for (int x = 0; x <= yib::TJ; ++x)
+    for (int y = 0; y <= x; ++y)
+      for (int J = x - y; J <= std::min(yib::TJ, x + y); J += 2) t.push_back({x, y, J});
+  return t;
+}
+
+int row_index(int J, int mb) { return yib::rowoff(J) + mb; }
+
+// cost of item (triple, mb) for the k_snap_yi_p body: per summed mb1, band
+// products (4 DFMA) + the C(mb; mb1) scaling + the column loads; epilogue per
+// band cell and per Y element
+double item_cost(const Triple& t, int mb) {
+  const int SH = (t.X + t.Y - t.J) / 2;
+  const bool mid = 2 * mb == t.J, swap = (t.X == t.Y) && !mid;
+  const int lo = std::max(0, mb + SH - t.Y);
+  const int hi = mid ? t.X / 2 : (swap ? (mb + SH) / 2 : std::min(t.X, mb + SH));
+  int K = 0;
+  for (int mb1 = lo; mb1 <= hi; ++mb1) K += (mb + SH - mb1 >= 0 && mb + SH - mb1 <= t.Y);
+  int band = 0;
+  for (int a = 0; a <= t.X; ++a)
+    for (int b = 0; b <= t.Y; ++b) band += (a + b >= SH && a + b <= SH + t.J);
+  return K * (4.0 * band + 2.0 * (t.Y + 1) + 3.0 * (t.X + t.Y + 2) + 12.0) + 2.0 * band + 5.0 * (t.J + 1) + 40.0;
+}
+
+// jobs (cost, id) -> NB bins: LPT, then deterministic local search (single moves
+// and pairwise swaps) that lowers the makespan, ties broken by the sum of squares.
+// Returns bin[id] (ids < max id + 1; unused ids map to -1).
+std::vector<int> balance(const std::vector<std::pair<double, int>>& jobs_in, int NB) {
+  std::vector<std::pair<double, int>> jobs(jobs_in);
+  std::stable_sort(jobs.begin(), jobs.end(), [](auto& a, auto& b) { return a.first > b.first; });
+  const int nj = (int)jobs.size();
+  std::vector<int> asg(nj);
+  std::vector<double> wl(NB, 0.0);
+  for (int i = 0; i < nj; ++i) {
+    const int w = (int)(std::min_element(wl.begin(), wl.end()) - wl.begin());
+    asg[i] = w;
+    wl[w] += jobs[i].first;
+  }
+  auto score = [](const std::vector<double>& l) {
+    double mx = 0.0, sq = 0.0;
+    for (double v : l) {
+      mx = std::max(mx, v);
+      sq += v * v;
+    }
+    return std::make_pair(mx, sq);
+  };
+  for (bool improved = true; improved;) {
+    improved = false;
+    auto cur = score(wl);
+    for (int i = 0; i < nj; ++i)
+      for (int w = 0; w < NB; ++w) {
+        if (w == asg[i]) continue;
+        std::vector<double> nl(wl);
+        nl[asg[i]] -= jobs[i].first;
+        nl[w] += jobs[i].first;
+        auto sc = score(nl);
+        if (sc < cur) {
+          wl = nl;
+          asg[i] = w;
+          cur = sc;
+          improved = true;
+        }
+      }
+    for (int i = 0; i < nj; ++i)
+      for (int j = i + 1; j < nj; ++j) {
+        const int a = asg[i], b = asg[j];
+        if (a == b) continue;
+        std::vector<double> nl(wl);
+        nl[a] += jobs[j].first - jobs[i].first;
+        nl[b] += jobs[i].first - jobs[j].first;
+        auto sc = score(nl);
+        if (sc < cur) {
+          wl = nl;
+          std::swap(asg[i], asg[j]);
+          cur = sc;
+          improved = true;
+        }
+      }
+  }
+  int maxid = -1;
+  for (auto& j : jobs_in) maxid = std::max(maxid, j.second);
+  std::vector<int> out(maxid + 1, -1);
+  for (int i = 0; i < nj; ++i) out[jobs[i].second] = asg[i];
+  return out;
+}
+
+}  // namespace
+
+// Upload the CG box table, the triple codes and the per-variant phase schedules
+// (twojmax 8; call once per device).  *balance_out: work-weighted mean / max warp
+// load of the S = 1 schedule over the phases (cost model).
+cudaError_t snap_yi8_setup(double* balance_out) {
+  const auto T = triples8();
+  if ((int)T.size() != yib::NT) return cudaErrorInvalidValue;
+  std::vector<double> box;
+  std::vector<int> code;
+  for (const auto& t : T) {
+    const int sh = (t.X + t.Y - t.J) / 2;
+    if ((int)box.size() != yib::box_off(t.X, t.Y, t.J)) return cudaErrorInvalidValue;
+    for (int b = 0; b <= t.Y; ++b)
+      for (int a = 0; a <= t.X; ++a) {
+        const int ma = a + b - sh;
+        box.push_back(ma >= 0 && ma <= t.J ? snap_clebsch(t.X, 2 * a - t.X, t.Y, 2 * b - t.Y, t.J, 2 * ma - t.J) : 0.0);
+      }
+    code.push_back(t.X * 100 + t.Y * 10 + t.J);
+  }
+  // items per (row, phase)
+  std::vector<std::vector<std::vector<int>>> ritems(yib::ROWS, std::vector<std::vector<int>>(yib::NPH));
+  std::vector<std::vector<double>> rcost(yib::ROWS, std::vector<double>(yib::NPH, 0.0));
+  for (int tid = 0; tid < yib::NT; ++tid) {
+    const Triple& t = T[tid];
+    for (int mb = 0; 2 * mb <= t.J; ++mb) {
+      const int r = row_index(t.J, mb), ph = yib::phase(t.X);
+      ritems[r][ph].push_back((tid << 16) | (t.J << 8) | mb);
+      rcost[r][ph] += item_cost(t, mb);
+    }
+  }
+  std::vector<int> iseg(P_NV * yib::NPH * (P_MAX_VW + 1), 0), items(P_NV * P_MAX_ITEMS, 0),
+      rowsplit(P_NV * yib::ROWS, 0);
+  double bal_num = 0.0, bal_den = 0.0;
+  for (int v = 0; v < P_NV; ++v) {
+    const int NW = P_NW[v], NS = P_NS[v];
+    // rows -> CTAs of the block (fixed for the whole kernel)
+    std::vector<int> cta(yib::ROWS, 0);
+    if (NS > 1) {
+      std::vector<std::pair<double, int>> jobs;
+      for (int r = 0; r < yib::ROWS; ++r) {
+        double c = 0.0;
+        for (int ph = 0; ph < yib::NPH; ++ph) c += rcost[r][ph];
+        jobs.push_back({c, r});
+      }
+      cta = balance(jobs, NS);
+    }
+    for (int r = 0; r < yib::ROWS; ++r) rowsplit[v * yib::ROWS + r] = cta[r];
+    int n = 0;
+    for (int ph = 0; ph < yib::NPH; ++ph) {
+      std::vector<int> vwarp(yib::ROWS, -1);
+      for (int s = 0; s < NS; ++s) {
+        std::vector<std::pair<double, int>> jobs;
+        for (int r = 0; r < yib::ROWS; ++r)
+          if (cta[r] == s && rcost[r][ph] > 0.0) jobs.push_back({rcost[r][ph], r});
+        if (jobs.empty()) continue;
+        const auto bin = balance(jobs, NW);
+        std::vector<double> load(NW, 0.0);
+        for (auto& j : jobs) {
+          vwarp[j.second] = s * NW + bin[j.second];
+          load[bin[j.second]] += j.first;
+        }
+        if (v == 0) {
+          double sum = 0.0, mx = 0.0;
+          for (double l : load) {
+            sum += l;
+            mx = std::max(mx, l);
+          }
+          bal_num += sum / NW;
+          bal_den += mx;
+        }
+      }
+      for (int w = 0; w <= P_MAX_VW; ++w) {
+        iseg[(v * yib::NPH + ph) * (P_MAX_VW + 1) + w] = n;
+        if (w == P_MAX_VW) break;
+        std::vector<std::pair<int, int>> mine;  // ((X, Y, J, mb) key, item)
+        for (int r = 0; r < yib::ROWS; ++r)
+          if (vwarp[r] == w)
+            for (int it : ritems[r][ph]) {
+              const Triple& t = T[it >> 16];
+              mine.push_back({((t.X * 10 + t.Y) * 10 + t.J) * 10 + (it & 0xff), it});
+            }
+        std::sort(mine.begin(), mine.end());
+        for (auto& m : mine) {
+          if (n >= P_MAX_ITEMS) return cudaErrorInvalidValue;
+          items[v * P_MAX_ITEMS + n++] = m.second;
+        }
+      }
+    }
+  }
+  if (balance_out) *balance_out = bal_den > 0.0 ? bal_num / bal_den : 1.0;
   cudaError_t e;
-  if ((e = cudaMemcpyToSymbol(c_box, box, sizeof(double) * nbox)) != cudaSuccess) return e;
-  if ((e = cudaMemcpyToSymbol(c_box_off, off, sizeof(int) * yib::NT)) != cudaSuccess) return e;
-  if ((e = cudaMemcpyToSymbol(c_box_code, code, sizeof(int) * yib::NT)) != cudaSuccess) return e;
-  if ((e = cudaMemcpyToSymbol(c_box_iseg, iseg, sizeof(int) * BOX_NV * (BOX_ROWS + 1))) != cudaSuccess) return e;
-  if ((e = cudaMemcpyToSymbol(c_box_rowsplit, rowsplit, sizeof(int) * BOX_NV * BOX_ROWS)) != cudaSuccess) return e;
-  for (int v = 0; v < BOX_NV; ++v)
-    if ((e = cudaMemcpyToSymbol(c_box_items, items + (size_t)v * nitems, sizeof(int) * nitems,
-                                sizeof(int) * BOX_MAX_ITEMS * v)) != cudaSuccess)
-      return e;
+  if ((e = cudaMemcpyToSymbol(c_box, box.data(), sizeof(double) * box.size())) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_box_code, code.data(), sizeof(int) * code.size())) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_p_iseg, iseg.data(), sizeof(int) * iseg.size())) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_p_items, items.data(), sizeof(int) * items.size())) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_p_rowsplit, rowsplit.data(), sizeof(int) * rowsplit.size())) != cudaSuccess)
+    return e;
   return cudaSuccess;
 }
 
-// (warps, splits) of every variant; returns the count
-int snap_box_variants(int* nw, int* ns) {
-  for (int v = 0; v < BOX_NV; ++v) {
-    nw[v] = BOX_NW[v];
-    ns[v] = BOX_NS[v];
-  }
-  return BOX_NV;
-}
-
 template <int NW, int V, int S>
-static cudaError_t box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const void* utot,
-                              void* ylist, double* eatom, double* erow_g) {
-  const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * BOX_ROWS * yib::ATOMS;
+static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const void* utot,
+                            void* ylist, double* eatom, double* erow_g) {
+  const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * yib::ROWS * yib::ATOMS;
   static std::atomic<uint64_t> attr_devs{0};
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_devs.load() & bit)) {  // exactly the dynamic size: the static mbarrier counts against the 227 KB too
-    cudaError_t e = cudaFuncSetAttribute(k_snap_yi_box<NW, V, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(k_snap_yi_p<NW, V, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     attr_devs.fetch_or(bit);
   }
   const unsigned grid = (unsigned)(S * ((natoms + yib::ATOMS - 1) / yib::ATOMS));
-  cudaError_t e = launch_pdl_yi(k_snap_yi_box<NW, V, S>, dim3(grid), dim3(NW * 32), sm, st, natoms, beta0, coef,
+  cudaError_t e = launch_pdl_yi(k_snap_yi_p<NW, V, S>, dim3(grid), dim3(NW * 32), sm, st, natoms, beta0, coef,
                                 (const Cx*)utot, (Cx*)ylist, eatom, erow_g);
   if (e != cudaSuccess) return e;
   if (S > 1)
@@ -373,8 +572,8 @@ static cudaError_t box_launch(cudaStream_t st, int64_t natoms, double beta0, con
 cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef,
                             const void* utot, void* ylist, double* eatom, double* erow_g) {
   const int64_t blocks = (natoms + yib::ATOMS - 1) / yib::ATOMS;
-  if (blocks < 148 && erow_g) return box_launch<12, 2, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
-  return box_launch<12, 0, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
+  if (blocks < 148 && erow_g) return p_launch<8, 1, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
+  return p_launch<8, 0, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
 }
 
 }  // namespace pl
