@@ -15,10 +15,10 @@
 //
 // Lanes = atoms (32 per CTA; U^J of all layers expanded to full matrices in
 // shared memory, [element][atom], conflict-free), warps own (J, mb) half rows.
-// Code size: 125 bodies are ~4x the box kernel's, more than the instruction
-// cache holds.  The CTA therefore walks the triples in PHASES of X (X <= 4,
-// 5, 6, 7, 8) separated by __syncthreads(): only one phase's bodies are live
-// at a time, and the rows are re-assigned to warps per phase (host LPT +
+// Code size: 125 bodies are ~5x the box kernel's, more than the instruction
+// cache holds.  The CTA therefore walks the triples in PHASES (consecutive
+// triples in (X, Y, J) order within a code budget) separated by
+// __syncthreads(): only one phase's bodies are live at a time, and the rows are re-assigned to warps per phase (host LPT +
 // local search on a cost model), which also balances each phase.  A row's
 // items are summed in (X, Y) order whatever warp or phase takes them, so Y
 // does not depend on the schedule or on the batch (bitwise).
@@ -31,6 +31,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <utility>
 #include <vector>
@@ -65,7 +66,7 @@ constexpr int NHALF = 155;     // sum (J+1)(J/2+1)
 constexpr int ATOMS = 32;
 constexpr int BOX_MAX = 4098;  // sum over triples of (X+1)(Y+1)
 constexpr int ROWS = 25;       // (J, mb <= J/2) half rows
-constexpr int NPH = 5;         // phases: X <= 4, 5, 6, 7, 8
+constexpr int NPH = 24;        // max phases (host: consecutive triples, code budget per phase)
 constexpr int foff(int J) { return J * (J + 1) * (2 * J + 1) / 6; }
 constexpr int rowoff(int J) { return (J / 2 + 1) * (J / 2 + 1) - (J % 2 == 0 ? J / 2 + 1 : 0); }  // rows of layers < J
 constexpr int hoff(int J) {
@@ -73,7 +74,6 @@ constexpr int hoff(int J) {
   for (int j = 0; j < J; ++j) h += (j + 1) * (j / 2 + 1);
   return h;
 }
-constexpr int phase(int X) { return X <= 4 ? 0 : X - 4; }
 // offset of triple (X, Y, J) in the box table, triples in (x, y <= x, J) order
 constexpr int box_off(int X, int Y, int J) {
   int o = 0;
@@ -119,6 +119,7 @@ constexpr int P_MAX_ITEMS = 400;  // (row, triple) items: 375 at twojmax 8
 __constant__ int c_p_iseg[P_NV][yib::NPH][P_MAX_VW + 1];  // items of virtual warp w in phase p
 __constant__ int c_p_items[P_NV][P_MAX_ITEMS];           // tid << 16 | J << 8 | mb
 __constant__ int c_p_rowsplit[P_NV][yib::ROWS];          // CTA of the block that owns row r
+__constant__ int c_p_nph;                                // phases in use
 
 struct Cx {
   double re, im;
@@ -250,7 +251,8 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
   for (int t = threadIdx.x; t < yib::ROWS * yib::ATOMS; t += blockDim.x) erow[t] = 0.0;
   __syncthreads();
   const int vw = split * NW + warp;  // virtual warp of the block's schedule
-  for (int ph = 0; ph < yib::NPH; ++ph) {
+  const int nph = c_p_nph;
+  for (int ph = 0; ph < nph; ++ph) {
     for (int it = c_p_iseg[V][ph][vw]; it < c_p_iseg[V][ph][vw + 1]; ++it) {
       const int item = c_p_items[V][it];
       const int tid = item >> 16, J = (item >> 8) & 0xff, mb = item & 0xff;
@@ -462,13 +464,37 @@ cudaError_t snap_yi8_setup(double* balance_out) {
       }
     code.push_back(t.X * 100 + t.Y * 10 + t.J);
   }
+  // phases: consecutive triples (code order, ascending X) whose bodies fit the
+  // budget (estimated SASS bytes; PL_YI_PHASE_KB, default 60 KB)
+  double budget = 60.0 * 1024.0;
+  if (const char* e = getenv("PL_YI_PHASE_KB")) budget = atof(e) * 1024.0;
+  std::vector<int> tphase(yib::NT, 0);
+  int nph = 1;
+  {
+    double acc = 0.0;
+    for (int tid = 0; tid < yib::NT; ++tid) {
+      const Triple& t = T[tid];
+      const int SH = (t.X + t.Y - t.J) / 2;
+      int band = 0;
+      for (int a = 0; a <= t.X; ++a)
+        for (int b = 0; b <= t.Y; ++b) band += (a + b >= SH && a + b <= SH + t.J);
+      const double bytes = 21.3 * (6.0 * band + 3.0 * (t.Y + 1) + (t.X + 1) + 5.0 * (t.J + 1) + 30.0);
+      if (acc > 0.0 && acc + bytes > budget) {
+        if (nph == yib::NPH) return cudaErrorInvalidValue;
+        ++nph;
+        acc = 0.0;
+      }
+      acc += bytes;
+      tphase[tid] = nph - 1;
+    }
+  }
   // items per (row, phase)
   std::vector<std::vector<std::vector<int>>> ritems(yib::ROWS, std::vector<std::vector<int>>(yib::NPH));
   std::vector<std::vector<double>> rcost(yib::ROWS, std::vector<double>(yib::NPH, 0.0));
   for (int tid = 0; tid < yib::NT; ++tid) {
     const Triple& t = T[tid];
     for (int mb = 0; 2 * mb <= t.J; ++mb) {
-      const int r = row_index(t.J, mb), ph = yib::phase(t.X);
+      const int r = row_index(t.J, mb), ph = tphase[tid];
       ritems[r][ph].push_back((tid << 16) | (t.J << 8) | mb);
       rcost[r][ph] += item_cost(t, mb);
     }
@@ -493,6 +519,10 @@ cudaError_t snap_yi8_setup(double* balance_out) {
     int n = 0;
     for (int ph = 0; ph < yib::NPH; ++ph) {
       std::vector<int> vwarp(yib::ROWS, -1);
+      if (ph >= nph) {
+        for (int w = 0; w <= P_MAX_VW; ++w) iseg[(v * yib::NPH + ph) * (P_MAX_VW + 1) + w] = n;
+        continue;
+      }
       for (int s = 0; s < NS; ++s) {
         std::vector<std::pair<double, int>> jobs;
         for (int r = 0; r < yib::ROWS; ++r)
@@ -536,6 +566,7 @@ cudaError_t snap_yi8_setup(double* balance_out) {
   cudaError_t e;
   if ((e = cudaMemcpyToSymbol(c_box, box.data(), sizeof(double) * box.size())) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_box_code, code.data(), sizeof(int) * code.size())) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_p_nph, &nph, sizeof(int))) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_p_iseg, iseg.data(), sizeof(int) * iseg.size())) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_p_items, items.data(), sizeof(int) * items.size())) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_p_rowsplit, rowsplit.data(), sizeof(int) * rowsplit.size())) != cudaSuccess)
