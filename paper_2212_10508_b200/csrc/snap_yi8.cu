@@ -111,9 +111,9 @@ __constant__ int c_box_code[yib::NT];  // X*100 + Y*10 + J
 // compiled variants: (warps per CTA, CTAs per 32-atom block).  A block's rows
 // are split over S CTAs when the batch has fewer blocks than SMs (latency of
 // small systems); a row stays with one CTA for the whole kernel.
-constexpr int P_NV = 2;
-constexpr int P_NW[P_NV] = {8, 8};
-constexpr int P_NS[P_NV] = {1, 2};
+constexpr int P_NV = 4;
+constexpr int P_NW[P_NV] = {8, 8, 12, 12};
+constexpr int P_NS[P_NV] = {1, 2, 1, 2};
 constexpr int P_MAX_VW = 24;
 constexpr int P_MAX_ITEMS = 400;  // (row, triple) items: 375 at twojmax 8
 __constant__ int c_p_iseg[P_NV][yib::NPH][P_MAX_VW + 1];  // items of virtual warp w in phase p
@@ -191,6 +191,7 @@ __device__ __forceinline__ void ptri(const PItem& A) {
   }
 }
 
+template <int NW>
 __device__ __forceinline__ void ptri_dispatch(int tid, const PItem& A) {
   switch (tid) {
     // one case per triple, in (x, y <= x, J) order (generated)
@@ -268,7 +269,7 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
       A.swap = (Y == X) && !A.mid;
       A.lo = max(0, mb + SH - Y);
       A.hi = A.mid ? X / 2 : (A.swap ? (mb + SH) / 2 : min(X, mb + SH));
-      ptri_dispatch(tid, A);
+      ptri_dispatch<NW>(tid, A);
     }
     __syncthreads();  // next phase: rows change owners
   }
@@ -603,8 +604,16 @@ static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const
 cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef,
                             const void* utot, void* ylist, double* eatom, double* erow_g) {
   const int64_t blocks = (natoms + yib::ATOMS - 1) / yib::ATOMS;
-  if (blocks < 148 && erow_g) return p_launch<8, 1, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
-  return p_launch<8, 0, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
+  static const int nw = [] {
+    const char* e = getenv("PL_YI_NW");
+    return e ? atoi(e) : 8;
+  }();
+  const bool split = blocks < 148 && erow_g;
+  if (nw == 12)
+    return split ? p_launch<12, 3, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g)
+                 : p_launch<12, 2, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
+  return split ? p_launch<8, 1, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g)
+               : p_launch<8, 0, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
 }
 
 }  // namespace pl
