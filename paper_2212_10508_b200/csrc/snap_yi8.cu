@@ -111,9 +111,9 @@ __constant__ int c_box_code[yib::NT];  // X*100 + Y*10 + J
 // compiled variants: (warps per CTA, CTAs per 32-atom block).  A block's rows
 // are split over S CTAs when the batch has fewer blocks than SMs (latency of
 // small systems); a row stays with one CTA for the whole kernel.
-constexpr int P_NV = 4;
-constexpr int P_NW[P_NV] = {8, 8, 12, 12};
-constexpr int P_NS[P_NV] = {1, 2, 1, 2};
+constexpr int P_NV = 2;
+constexpr int P_NW[P_NV] = {8, 8};   // 2 warps per SMSP, 255 registers (12 warps: 168, measured slower)
+constexpr int P_NS[P_NV] = {1, 2};
 constexpr int P_MAX_VW = 24;
 constexpr int P_MAX_ITEMS = 400;  // (row, triple) items: 375 at twojmax 8
 __constant__ int c_p_iseg[P_NV][yib::NPH][P_MAX_VW + 1];  // items of virtual warp w in phase p
@@ -142,11 +142,13 @@ __device__ __forceinline__ void ptri(const PItem& A) {
   constexpr int FX = yib::foff(X), FY = yib::foff(Y);
   constexpr int AT = yib::ATOMS;
   Cx P[X + 1][Y + 1];
+#pragma unroll
+  for (int a = 0; a <= X; ++a)
+#pragma unroll
+    for (int b = 0; b <= Y; ++b) P[a][b] = Cx{0.0, 0.0};  // corners are never read: no registers
   const Cx* __restrict__ Ul = A.Ul;
-  if (A.lo > A.hi) return;  // no admissible mb1: no contribution
-  // one mb1 step; the first one initialises P (no zero fill: P = ux uy exactly as
-  // fma(ux, uy, 0) would round)
-  auto step = [&](const int mb1, const bool first) {
+#pragma unroll 1
+  for (int mb1 = A.lo; mb1 <= A.hi; ++mb1) {
     const int mb2 = A.mb + SH - mb1;
     const double w = A.mid ? (2 * mb1 == X ? 0.5 : 1.0) : (A.swap ? (mb1 == mb2 ? 1.0 : 2.0) : 1.0);
     const double cbv = w * c_box[OFF + mb2 * (X + 1) + mb1];  // w C(mb; mb1), w exact
@@ -162,21 +164,13 @@ __device__ __forceinline__ void ptri(const PItem& A) {
 #pragma unroll
       for (int a = A0; a <= A1; ++a) {
         if (a + b < SH || a + b > SH + J) continue;  // outside the CG band (compile time)
-        if (first) {
-          P[a][b].re = ux[a].re * uy.re;
-          P[a][b].im = ux[a].re * uy.im;
-        } else {
-          P[a][b].re = fma(ux[a].re, uy.re, P[a][b].re);
-          P[a][b].im = fma(ux[a].re, uy.im, P[a][b].im);
-        }
+        P[a][b].re = fma(ux[a].re, uy.re, P[a][b].re);
+        P[a][b].im = fma(ux[a].re, uy.im, P[a][b].im);
         P[a][b].re = fma(-ux[a].im, uy.im, P[a][b].re);
         P[a][b].im = fma(ux[a].im, uy.re, P[a][b].im);
       }
     }
-  };
-  step(A.lo, true);
-#pragma unroll 1
-  for (int mb1 = A.lo + 1; mb1 <= A.hi; ++mb1) step(mb1, false);
+  }
   // Z[ma] = sum_a C(ma; a) P[a][ma + SH - a], then Y[ma] += cy Z[ma] (the warp owns the row)
   Cx* yo = A.yrow;
 #pragma unroll
@@ -472,8 +466,9 @@ cudaError_t snap_yi8_setup(double* balance_out) {
     code.push_back(t.X * 100 + t.Y * 10 + t.J);
   }
   // phases: consecutive triples (code order, ascending X) whose bodies fit the
-  // budget (estimated SASS bytes; PL_YI_PHASE_KB, default 60 KB)
-  double budget = 60.0 * 1024.0;
+  // budget (estimated SASS bytes; PL_YI_PHASE_KB, default 100 KB: measured
+  // 1.70 ms at 100-140 KB vs 1.79 at 60 and 2.5-2.6 at 170 KB-1 phase, larger config)
+  double budget = 100.0 * 1024.0;
   if (const char* e = getenv("PL_YI_PHASE_KB")) budget = atof(e) * 1024.0;
   std::vector<int> tphase(yib::NT, 0);
   int nph = 1;
@@ -610,14 +605,7 @@ static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const
 cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef,
                             const void* utot, void* ylist, double* eatom, double* erow_g) {
   const int64_t blocks = (natoms + yib::ATOMS - 1) / yib::ATOMS;
-  static const int nw = [] {
-    const char* e = getenv("PL_YI_NW");
-    return e ? atoi(e) : 8;
-  }();
   const bool split = blocks < 148 && erow_g;
-  if (nw == 12)
-    return split ? p_launch<12, 3, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g)
-                 : p_launch<12, 2, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
   return split ? p_launch<8, 1, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g)
                : p_launch<8, 0, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
 }
