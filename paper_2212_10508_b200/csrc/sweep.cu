@@ -44,15 +44,17 @@ k_combine(int64_t d, const double* __restrict__ base_q, const double* __restrict
   double s1 = 0.0, s2 = 0.0;
   int bad = 0;
   for (int64_t i = threadIdx.x; i < d; i += CT) {
-    // corrected value: coarse + jump, jump formed first (parareal.py:293)
+    // corrected value: coarse + jump, jump formed first (parareal.py:293); prev is
+    // read before cur is written, so prev_q may alias cur_q (replica batches)
+    const double pq = prev_q[i];
     double q = add(base_q[i], jump_q[i]);
     double p = add(base_p[i], jump_p[i]);
     cur_q[i] = q;
     cur_p[i] = p;
     if (!isfinite(q) || !isfinite(p)) bad = 1;
-    double e = sub(q, prev_q[i]);
+    double e = sub(q, pq);
     s1 += e * e;
-    s2 += prev_q[i] * prev_q[i];
+    s2 += pq * pq;
   }
   bad = __syncthreads_or(bad);
   double n1 = sqrt(block_sumsq(s1, sh));
@@ -242,6 +244,45 @@ int sweep(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t m0, int64_t m1,
     h_out[0] = m - m0 + 1;
     if (hacc[1] == 0.0) return PL_OK;  // caller raises DegenerateNormalizationError
     if (expl > 0.0 && hacc[2] > expl) return PL_OK;
+  }
+  return PL_OK;
+}
+
+// Replica batch through the per-window generic path (systems too large for the
+// persistent sweeps, e.g. the 16,001-atom heavy config): slot by slot, with the
+// pl_sweep_batch conventions (arrays with a leading replica dimension, out4 =
+// {nodes done, window, substep, status 1 blow-up / 2 non-finite}).
+int sweep_generic_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, int R_act, const int32_t* h_ridx,
+                        const int64_t* h_m0, const int64_t* h_m1, const int32_t* h_inc, int mode, double* Q,
+                        double* P, double* baseQ, double* baseP, const double* jumpQ, const double* jumpP,
+                        const double* noise, const double* h_amp, const double* mass, double dt, double h, double hg,
+                        double expl, double* h_state, int64_t* h_out4, double* d_hist) {
+  for (int s = 0; s < R_act; ++s) {
+    const int64_t r = h_ridx[s];
+    double* q = Q + r * (N + 1) * d;
+    double* p = P + r * (N + 1) * d;
+    double* bq = baseQ + r * N * d;
+    double* bp = baseP + r * N * d;
+    const double* nz = noise + r * N * (int64_t)(L + 1) * d;
+    int64_t* o4 = h_out4 + 4 * s;
+    int64_t out = 0;
+    int32_t blow = 0;
+    int rc;
+    if (mode == 1) {
+      rc = bootstrap(ctx, coarse, d, L, h_m0[s], h_m1[s], q, p, bq, bp, nz, h_amp, mass, dt, h, hg, &out, &blow);
+    } else {
+      rc = sweep(ctx, coarse, d, L, h_m0[s], h_m1[s], h_inc[s], q, p, q, bq, bp, jumpQ + r * N * d,
+                 jumpP + r * N * d, nz, h_amp, mass, dt, h, hg, expl, h_state + 2 * s, d_hist + r * N, &out, &blow);
+    }
+    o4[0] = o4[1] = o4[2] = o4[3] = 0;
+    if (rc == PL_EBLOWUP) {
+      o4[1] = out;
+      o4[2] = blow;
+      o4[3] = blow ? 1 : 2;
+      continue;
+    }
+    PL_TRY(rc);
+    o4[0] = out;
   }
   return PL_OK;
 }

@@ -474,6 +474,12 @@ int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N
                         const double* noise, const double* h_amp, const double* mass, double dt, double h,
                         double hg, double expl, double* h_state, int64_t* h_out4, double* d_hist);
 
+int sweep_generic_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, int R_act, const int32_t* h_ridx,
+                        const int64_t* h_m0, const int64_t* h_m1, const int32_t* h_inc, int mode, double* Q,
+                        double* P, double* baseQ, double* baseP, const double* jumpQ, const double* jumpP,
+                        const double* noise, const double* h_amp, const double* mass, double dt, double h, double hg,
+                        double expl, double* h_state, int64_t* h_out4, double* d_hist);
+
 // R_act replica slots in one launch (grid = R_act CTAs); arrays carry a leading
 // replica dimension: Q/P (R, N+1, d), base/jump (R, N, d), noise (R, N, L+1, d),
 // d_hist (R, N).  h_state (2 R_act) and h_out4 (4 R_act) per slot.
@@ -494,7 +500,9 @@ int sweep_cta_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N, in
   if (!ew && coarse->kind != POT_EAM) return fail(PL_EARG, "batched sweep needs an EAM or elementwise coarse potential");
   const int n = ew ? 0 : coarse->n_atoms;
   const size_t smem = sizeof(double) * (4 * (size_t)d + (ew ? 0 : (size_t)n + 3 * (size_t)n));
-  if (smem > 200 * 1024) return fail(PL_EARG, "system too large for the persistent sweep");
+  if (smem > 200 * 1024)  // positions do not fit one CTA: per-window generic path, replica by replica
+    return sweep_generic_batch(ctx, coarse, d, L, N, R_act, h_ridx, h_m0, h_m1, h_inc, mode, Q, P, baseQ, baseP,
+                               jumpQ, jumpP, noise, h_amp, mass, dt, h, hg, expl, h_state, h_out4, d_hist);
   A.d = d; A.n_atoms = n; A.L = L; A.mode = mode; A.use_ew = ew ? 1 : 0;
   A.Q = Q; A.P = P; A.prevQ = Q; A.baseQ = baseQ; A.baseP = baseP; A.jumpQ = jumpQ; A.jumpP = jumpP;
   A.noise = noise; A.mass = mass; A.dt = dt; A.h = h; A.hg = hg; A.expl = expl;

@@ -86,3 +86,36 @@ def mean_ci(durations):
     mean = float(np.mean(values))
     half = 1.96 * float(np.std(values, ddof=1)) / math.sqrt(values.size)
     return mean, mean - half, mean + half
+
+
+class ResidenceStats(NamedTuple):
+    """Residence-time summary of a pooled ensemble (analysis.py:177-226)."""
+
+    mean: float
+    ci_low: float
+    ci_high: float
+    n_events: int
+    censored: int
+
+    def as_dict(self) -> dict:
+        return {"mean": self.mean, "ci_low": self.ci_low, "ci_high": self.ci_high,
+                "n_events": self.n_events, "censored": self.censored}
+
+
+class EnsembleComparison(NamedTuple):
+    overlap: bool
+    intervals: tuple
+
+
+def residence_stats(events) -> ResidenceStats:
+    """Censored events are counted but never enter the mean (analysis.py:213-229)."""
+    complete = [e.duration for e in events if not e.censored]
+    censored = sum(1 for e in events if e.censored)
+    mean, lo, hi = mean_ci(complete)
+    return ResidenceStats(mean, lo, hi, len(complete), censored)
+
+
+def compare_ensembles(a: ResidenceStats, b: ResidenceStats) -> EnsembleComparison:
+    """Do the two 95 % intervals intersect? (analysis.py:232-238)"""
+    return EnsembleComparison(bool(a.ci_low <= b.ci_high and b.ci_low <= a.ci_high),
+                              ((a.ci_low, a.ci_high), (b.ci_low, b.ci_high)))

@@ -434,3 +434,31 @@ def test_sia_site_labels(pl):
     i2 = ((lab // n ** 2 % n) + 1) % n if lab < n ** 3 else None
     assert labs[0] == labs[1] == lab
     assert labs[2] != lab
+
+
+def test_heavy_system_sweeps_batch_equals_single(pl):
+    """16,001 atoms (BASELINE configs[4] cell): too large for the persistent sweeps, the
+    coarse sweep runs the per-window device path; replica batches (pl_sweep_batch) equal
+    single runs bit for bit, and a degenerate EAM/EAM pair converges in one iteration
+    with exactly zero jumps."""
+    from paper_2212_10508_b200 import tungsten as W
+    q0, box = W.bcc_sia(20)
+    n = q0.shape[0] // 3
+    L, N = 2, 3
+    params = pl.LangevinParams(1.0, W.KB * 1000.0, 0.001, L, mass=np.full(3 * n, W.MASS_W))
+    sched = pl.TemperatureSchedule.robust(L)
+    eam = W.make_eam(n, box)
+    inits = [pl.PhaseState(q=q0, p=W.maxwell_boltzmann(n, 1000.0, s)) for s in (1, 2)]
+    plans = [pl.NoisePlan.for_windows(pl.derive_seed(9, i), N) for i in range(2)]
+    cfg = pl.PararealConfig(N, 1e-10, 0.35)
+    deg = pl.parareal_adaptive_batch(inits, pl.PropagatorPair(eam, eam, 1.0, 1.0), params, sched, plans, cfg)
+    for r in deg:
+        assert r.converged and r.total_iterations == 1
+        assert all(e == 0.0 for _, _, e in r.error_history)
+    pair = pl.PropagatorPair(W.make_snap(n, box), eam, 100.0, 1.0)
+    batch = pl.parareal_adaptive_batch(inits, pair, params, sched, plans, cfg)
+    for i in range(2):
+        one = pl.parareal_adaptive(inits[i], pair, params, sched, plans[i], cfg)
+        assert one.slabs == batch[i].slabs
+        assert one.error_history == batch[i].error_history
+        assert one.trajectory.positions().tobytes() == batch[i].trajectory.positions().tobytes()
