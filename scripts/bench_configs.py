@@ -1,6 +1,6 @@
 """One-off measurements of the other BASELINE configs (bench.py covers configs[2]).
 
-    python scripts/bench_configs.py [sweep] [pr1] [ensemble] [heavy] [larger_parareal]
+    python scripts/bench_configs.py [sweep] [pr1] [ensemble] [heavy] [larger_parareal] [heavy_parareal]
 
 Prints one JSON line per config.  Synthetic inputs; timing by
 CUDA-synchronised wall clock around the measured call.
@@ -67,49 +67,52 @@ def pr1_parareal():
 
 
 def ensemble(R=256, N=32, L=100, T=1200.0, segments=None):
-    """configs[3]: R replicas x N slices x L steps at 1200 K, chained 3.2 ps segments.
-
-    20 ps / 3.2 ps = 6.25: the full config is 7 segments (the 7th overruns to
-    22.4 ps).  ``segments`` (env PL_ENSEMBLE_SEGMENTS, default 1) segments are
-    run, each from the previous segment's final states with fresh window seeds;
-    the wall-clock of the full config is extrapolated linearly from them and
-    labelled as such.  SIA site labels of every node feed the residence times.
-    """
-    segments = int(os.environ.get("PL_ENSEMBLE_SEGMENTS", "1")) if segments is None else segments
+    """configs[3]: the reference ensemble protocol (cli.py:986-1050, paper_2212_10508_b200.ensemble)
+    with R replicas of the 129-atom W + SIA system at 1200 K: minimise on the fine (SNAP) surface,
+    thermalise 10 windows, then per member a sequential fine chain and adaptive parareal (32 slices
+    x 100 steps = 3.2 ps per segment, delta from configs/ensemble.json) over the same plans,
+    chained for ``segments`` segments (20 ps / 3.2 ps = 6.25: 7 segments = 22.4 ps), SIA site
+    labels of quenched nodes, min_run 2, compare_ensembles of the two pooled CIs."""
+    from paper_2212_10508_b200.ensemble import run_ensemble
+    segments = int(os.environ.get("PL_ENSEMBLE_SEGMENTS", "7")) if segments is None else segments
+    R = int(os.environ.get("PL_ENSEMBLE_SIZE", R))
     q0, box, n, params, sched = _pr1(T=T, N=N, L=L)
     pair = pl.PropagatorPair(W.make_snap(n, box), W.make_eam(n, box), 100.0, 1.0)
-    cfg = pl.PararealConfig(N, 1e-5, 0.35)  # delta_conv of configs/ensemble.json
-    rs = np.random.default_rng(7)
-    states = [pl.PhaseState(q=q0 + 0.03 * rs.normal(size=q0.shape),
-                            p=math.sqrt(W.MASS_W * W.KB * T) * rs.normal(size=q0.shape)) for _ in range(R)]
-    walls, conv, sumk, fine_windows = [], 0, [], 0
-    label_chunks = []
-    for seg in range(segments):
-        plans = [pl.NoisePlan.for_windows(pl.derive_seed(77, 10 ** 9 + seg * R + i), N) for i in range(R)]
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        res = pl.parareal_adaptive_batch(states, pair, params, sched, plans, cfg)
-        torch.cuda.synchronize()
-        walls.append(time.perf_counter() - t0)
-        conv += int(sum(r.converged for r in res))
-        sumk += [r.total_iterations for r in res]
-        fine_windows += sum(sum(a.iterations * (a.n_final - s.n_init) for a in s.attempts)
-                            for r in res for s in r.slabs)
-        pos = np.stack([r.trajectory.positions() for r in res])  # (R, N+1, d)
-        label_chunks.append(sia.sia_site_labels(pos if seg == 0 else pos[:, 1:], 4, W.A0))
-        states = [r.trajectory[r.trajectory.n_windows] for r in res]
-    labels = np.concatenate(label_chunks, axis=1)
-    hops = int(sum(np.count_nonzero(np.diff(lab)) for lab in labels))
-    events = [e for lab in labels for e in sia.residence_times(lab)]
-    done = [e.duration for e in events if not e.censored]
-    mean, lo, hi = sia.mean_ci(done) if len(done) >= 2 else (float("nan"),) * 3
-    wall = float(sum(walls))
-    return {"config": f"ensemble: {R} replicas x {N} slices x {L} steps per 3.2 ps segment, T = {T:g} K, SNAP/EAM",
-            "segments_run": segments, "segment_wall_s": walls, "wall_s": wall,
-            "full_config_wall_s_extrapolated": wall / segments * 7,
-            "converged": conv, "mean_sum_k": float(np.mean(sumk)),
-            "fine_atom_steps_per_s": fine_windows * n * L / wall, "sia_hops": hops,
-            "residence_windows_mean_ci": [mean, lo, hi], "residence_events": len(done)}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = run_ensemble(pair, params, sched, pl.PhaseState(q=q0, p=np.zeros_like(q0)),
+                       pl.PararealConfig(N, 1e-5, 0.35), size=R, master_seed=77, n_cells=4, a=W.A0,
+                       segments=segments, thermalization_windows=10, min_run=2, quench=True)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    out = {"config": f"ensemble: {R} replicas x {segments} segments x {N} slices x {L} steps, T = {T:g} K, "
+                     "SNAP fine / EAM coarse, quenched SIA site labels, min_run 2", "wall_s": wall}
+    out.update(res.as_dict())
+    return out
+
+
+def heavy_parareal(N=8, L=1000):
+    """configs[4] end to end on one GPU: adaptive parareal, 16,001 atoms, 8 slices x 1000 steps,
+    SNAP fine (8 windows batched, cell lists) / EAM coarse sweep on the device (per-window path)."""
+    q0, box = W.bcc_sia(20)
+    n = q0.shape[0] // 3
+    params = pl.LangevinParams(1.0, W.KB * 1000.0, 0.001, L, mass=np.full(3 * n, W.MASS_W))
+    sched = pl.TemperatureSchedule.robust(L)
+    init = pl.PhaseState(q=q0, p=W.maxwell_boltzmann(n, 1000.0, 11))
+    pair = pl.PropagatorPair(W.make_snap(n, box), W.make_eam(n, box), 100.0, 1.0)
+    plan = pl.NoisePlan.for_windows(11, N)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    res = pl.parareal_adaptive(init, pair, params, sched, plan, pl.PararealConfig(N, 1e-10, 0.35))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t
+    t = time.perf_counter()
+    pl.sequential_propagate(init, N, pair.fine, params, sched, plan)
+    torch.cuda.synchronize()
+    seq = time.perf_counter() - t
+    return {"config": f"heavy adaptive parareal: {n} atoms, {N} x {L}, SNAP/EAM", "wall_s": wall,
+            "n_slab": res.n_slab, "sum_k": res.total_iterations, "converged": res.converged,
+            "sequential_fine_s": seq}
 
 
 def heavy(L=1000):
@@ -143,7 +146,7 @@ def heavy(L=1000):
     fl = bench.snap_flops_per_eval(snap, Q0)
     peak = bench.ctypes_peak()
     per_kernel = {}
-    for name, i, f in (("k_snap_ui_r4", 1, fl["ui"]), ("k_snap_yi_box", 2, fl["yi"]),
+    for name, i, f in (("k_snap_ui_r4", 1, fl["ui"]), ("k_snap_yi_p", 2, fl["yi"]),
                        ("k_snap_deidrj_pair", 3, fl["deidrj"])):
         t_launch = ms[i] / max(cnt[i], 1) * 1e-3
         tf = f / t_launch / 1e12
@@ -172,7 +175,7 @@ def larger_parareal(N=64, L=200):
 def main():
     which = sys.argv[1:] or ["sweep", "pr1", "heavy"]
     fns = {"sweep": force_sweep, "pr1": pr1_parareal, "ensemble": ensemble, "heavy": heavy,
-           "larger_parareal": larger_parareal}
+           "larger_parareal": larger_parareal, "heavy_parareal": heavy_parareal}
     for w in which:
         try:
             print(json.dumps(fns[w]()), flush=True)
