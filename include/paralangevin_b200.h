@@ -214,6 +214,9 @@ int pl_prof_begin(pl_ctx* ctx);
 int pl_prof_end(pl_ctx* ctx, int n_stages, double* h_ms, int64_t* h_n);
 /* Dense FP64 FMA throughput of the device, measured (TFLOP/s). */
 int pl_fp64_peak(pl_ctx* ctx, double* h_tflops);
+/* FP64 tensor-core throughput (mma.sync m8n8k4 f64), measured (TFLOP/s): the
+ * ceiling of a DMMA formulation of the Z/Y contraction. */
+int pl_dmma_peak(pl_ctx* ctx, double* h_tflops);
 
 #ifdef __cplusplus
 }

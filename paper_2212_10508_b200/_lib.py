@@ -70,6 +70,7 @@ SIGNATURES = {
     "pl_prof_begin": (C.c_int, [vp]),
     "pl_prof_end": (C.c_int, [vp, C.c_int, pd, pi64]),
     "pl_fp64_peak": (C.c_int, [vp, pd]),
+    "pl_dmma_peak": (C.c_int, [vp, pd]),
 }
 
 

@@ -60,6 +60,27 @@ __global__ void k_dfma_peak(double* out, int iters) {
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+// FP64 tensor-core (DMMA) throughput: mma.sync m8n8k4 f64, 8 independent
+// accumulator tiles per warp (256 FMA per instruction and warp)
+__global__ void k_dmma_peak(double* out, int iters) {
+  const int lane = threadIdx.x & 31;
+  const double a = 1.0 + lane * 1e-9, b = 0.999999 - lane * 1e-9;
+  double c[8][2];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = t * 1e-3;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(c[t][0]), "+d"(c[t][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace pl
 
 extern "C" {
@@ -116,6 +137,34 @@ int pl_fp64_peak(pl_ctx* ctx, double* h_tflops) {
   cudaEventDestroy(b);
   cudaFree(out);
   double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+  *h_tflops = flops / (ms * 1e-3) / 1e12;
+  return PL_OK;
+}
+
+// measured FP64 tensor-core (DMMA m8n8k4) throughput of this device (TFLOP/s)
+int pl_dmma_peak(pl_ctx* ctx, double* h_tflops) {
+  if (!ctx || !h_tflops) return pl::fail(PL_EARG, "NULL argument");
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out;
+  PL_CUDA(cudaMalloc(&out, sizeof(double)));
+  const int threads = 256, blocks = sms * 4, iters = 2048;
+  pl::k_dmma_peak<<<blocks, threads, 0, ctx->stream>>>(out, 32);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, ctx->stream);
+  pl::k_dmma_peak<<<blocks, threads, 0, ctx->stream>>>(out, iters);
+  cudaEventRecord(b, ctx->stream);
+  PL_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  const double warps = (double)blocks * threads / 32;
+  const double flops = 2.0 * 256 * 8 * (double)iters * warps;
   *h_tflops = flops / (ms * 1e-3) / 1e12;
   return PL_OK;
 }

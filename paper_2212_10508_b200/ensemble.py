@@ -98,12 +98,20 @@ def run_ensemble(pair: PropagatorPair, params: LangevinParams, schedule: Tempera
                  initial: PhaseState, config: PararealConfig, *, size: int, master_seed: int,
                  n_cells: int, a: float, segments: int = 1, thermalization_windows: int = 0,
                  min_run: int = 1, quench: bool = False, quench_tol: float = 1e-3, quench_iters: int = 300,
-                 minimize_start: bool = True, keep_labels: bool = False) -> EnsembleResult:
-    """The ensemble protocol above; returns pooled fine / adaptive residence statistics."""
+                 minimize_start: bool = True, minimize_tol: float = 1e-4,
+                 keep_labels: bool = False) -> EnsembleResult:
+    """The ensemble protocol above; returns pooled fine / adaptive residence statistics.
+
+    ``minimize_tol`` (eV/A, |grad| of the start): the reference minimises with
+    its default 1e-8 (cli.py:991), which steepest descent on the synthetic
+    random-beta SNAP surface does not reach (|grad| 1e-4 after 5 iterations,
+    then ~2e-6 after 20,000: scripts/probe_minimize.py); the start only has to
+    be a relaxed lattice, so 1e-4 is the default here.
+    """
     n = config.n_windows
     q0 = np.asarray(initial.q, dtype=float)
     if minimize_start:
-        q0 = local_minima(pair.fine, [q0], tol=1e-6)[0]
+        q0 = local_minima(pair.fine, [q0], tol=minimize_tol)[0]
     start = PhaseState(q=q0, p=np.zeros_like(q0))
     member_seeds = [derive_seed(master_seed, MEMBER_SEED_OFFSET + i) for i in range(size)]
     states = [start] * size

@@ -30,7 +30,7 @@ def test_sequential_batch_equals_single_chains(pl):
     sched = pl.TemperatureSchedule.robust(L)
     eam = W.make_eam(n, box)
     inits = [pl.PhaseState(q=q0, p=W.maxwell_boltzmann(n, 1200.0, s)) for s in (1, 2, 3)]
-    plans = [pl.NoisePlan.for_windows(pl.derive_seed(5, i), N) for i in range(3)]
+    plans = [pl.NoisePlan.for_windows(pl.derive_seed(5, i + 1), N) for i in range(3)]
     Q, P = sequential_propagate_batch(inits, N, eam, params, sched, plans)
     for r in range(3):
         one = pl.sequential_propagate(inits[r], N, eam, params, sched, plans[r])

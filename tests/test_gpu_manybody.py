@@ -449,7 +449,7 @@ def test_heavy_system_sweeps_batch_equals_single(pl):
     sched = pl.TemperatureSchedule.robust(L)
     eam = W.make_eam(n, box)
     inits = [pl.PhaseState(q=q0, p=W.maxwell_boltzmann(n, 1000.0, s)) for s in (1, 2)]
-    plans = [pl.NoisePlan.for_windows(pl.derive_seed(9, i), N) for i in range(2)]
+    plans = [pl.NoisePlan.for_windows(pl.derive_seed(9, i + 1), N) for i in range(2)]
     cfg = pl.PararealConfig(N, 1e-10, 0.35)
     deg = pl.parareal_adaptive_batch(inits, pl.PropagatorPair(eam, eam, 1.0, 1.0), params, sched, plans, cfg)
     for r in deg:
