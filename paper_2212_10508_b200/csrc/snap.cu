@@ -72,7 +72,7 @@ struct SnapIndex {
   double* d_cg = nullptr;
   double beta0 = 0.0;
   double flops_ui_pair = 0, flops_yi_atom = 0, flops_de_pair = 0;
-  double flops_de_pair_adj = 0, flops_yi_atom_reg = 0;
+  double flops_de_pair_adj = 0, flops_yi_atom_reg = 0, flops_ui_pair_v = 0;
   bool yi_reg = false;  // box-form Y tables set up (twojmax = 8)
   double* d_yi5 = nullptr;  // [2][NT]: coefY(X,Y,J), beta_b of canonical triples (else 0)
 };
@@ -87,6 +87,7 @@ struct SnapDev {  // POD view passed to kernels
   const int32_t* wtarget;
   const int32_t* wseg;
   const double* yi5;  // [2][NT]
+  const double* vs;   // twojmax 8: [2][nhalf] S^J[ma][mb] = N(J, ma) / N(J, mb) and its square (V recursion)
   const double* cg;
   double beta0, rcut, rfac0, rmin0, wself;
   double kappa, pi_span, half_pi_span;  // rfac0*pi/(rcut-rmin0), pi/(rcut-rmin0), 0.5*pi/(rcut-rmin0)
@@ -118,7 +119,7 @@ __device__ __forceinline__ void half_layer8(int t, int& J, int& base) {
 __constant__ int c_foff[SNAP_JMAX + 2];
 // box-form Z/Y kernel (snap_yi8.cu, own constant bank)
 cudaError_t snap_yi8_setup(double* balance_out);
-cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef,
+cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const double* vs,
                             const void* utot, void* ylist, double* eatom, double* erow_g);
 
 // ------------------------------------------------------------------ host setup
@@ -220,6 +221,22 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     }
     std::vector<double> cb2(cy);
     cb2.insert(cb2.end(), be.begin(), be.end());
+    // scale of the V recursion per half element (J, mb, ma): S = N(J, ma) / N(J, mb),
+    // N(J, x) = sqrt(x! (J - x)!); then S^2 (exact ratio of integers, rounded once)
+    std::vector<double> vs, vs2;
+    for (int J = 0; J <= tj; ++J)
+      for (int mb = 0; 2 * mb <= J; ++mb)
+        for (int ma = 0; ma <= J; ++ma) {
+          const double r = (fact(ma) * fact(J - ma)) / (fact(mb) * fact(J - mb));
+          vs.push_back(std::sqrt(r));
+          vs2.push_back(r);
+        }
+    if ((int)vs.size() != S->nhalf || (int)code.size() != 125) {
+      delete S;
+      return fail(PL_EARG, "twojmax-8 index sizes");
+    }
+    cb2.insert(cb2.end(), vs.begin(), vs.end());
+    cb2.insert(cb2.end(), vs2.begin(), vs2.end());
     PL_CUDA(cudaMalloc(&S->d_yi5, sizeof(double) * cb2.size()));
     PL_CUDA(cudaMemcpy(S->d_yi5, cb2.data(), sizeof(double) * cb2.size(), cudaMemcpyHostToDevice));
     S->yi_reg = true;
@@ -343,14 +360,16 @@ int snap_prepare(pl_pot* pot, const double* beta) {
   for (int J = 1; J <= tj; ++J) {
     int nel = (J + 1) * (J / 2 + 1);
     S->flops_ui_pair += nel * 24.0;   // 2 x (complex product + scaled accumulate) + fc accumulate
+    S->flops_ui_pair_v += nel * 18.0; // V form (k_snap_ui_r4): 2 complex products + difference + fc accumulate
     S->flops_de_pair += nel * 160.0;  // U (20) + 3 dU (108) + 3 weighted contractions (~32)
   }
   S->flops_ui_pair += 40.0;
+  S->flops_ui_pair_v += 40.0;
   S->flops_de_pair += 80.0;
-  // reverse-mode pair kernel: forward U + F contraction (25/element), adjoint
-  // (S_a, S_b, G update, direct Y term: 42/element), geometry + final (150)
+  // reverse-mode pair kernel in the V form: forward V + F contraction (19/element),
+  // adjoint (S_a, S_b, G update, direct Y term: 34/element), geometry + final (150)
   S->flops_de_pair_adj = 150.0;
-  for (int J = 1; J <= tj; ++J) S->flops_de_pair_adj += (J + 1) * (J / 2 + 1) * 67.0;
+  for (int J = 1; J <= tj; ++J) S->flops_de_pair_adj += (J + 1) * (J / 2 + 1) * 53.0;
   // register-tiled Z/Y: the middle row's upper half (zero weight) is skipped
   S->flops_yi_atom_reg = 0.0;
   for (int x = 0; x <= tj; ++x)
@@ -432,6 +451,7 @@ static SnapDev snap_dev(const pl_pot* pot) {
   D.items = S->d_items; D.units = S->d_units; D.useg = S->d_useg; D.cg = S->d_cg;
   D.tseg = S->d_tseg; D.wtarget = S->d_wtarget; D.wseg = S->d_wseg;
   D.yi5 = S->d_yi5;
+  D.vs = S->yi_reg ? S->d_yi5 + 2 * 125 : nullptr;
   D.beta0 = S->beta0; D.rcut = pot->rcut; D.rfac0 = pot->rfac0; D.rmin0 = pot->rmin0;
   D.wself = pot->wself; D.switchflag = pot->switchflag;
   D.kappa = pot->rfac0 * M_PI / (pot->rcut - pot->rmin0);
@@ -826,63 +846,51 @@ __device__ __forceinline__ C2 shfl_up_c2(C2 v, int delta) {
   return C2{__shfl_up_sync(0xffffffffu, v.re, delta), __shfl_up_sync(0xffffffffu, v.im, delta)};
 }
 
-// advance row mb of (u, du) from layer J-1 to layer J (WITH_D: also du)
-template <int TJ, int J, bool WITH_D>
-__device__ __forceinline__ void row_step(C2 (&u)[TJ + 1], C2 (&du)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                         const double (*rp)[SNAP_JMAX + 2]) {
+// Coefficient-free recursion.  With N(J, x) = sqrt(x! (J - x)!) and
+//   U^J[ma][mb] = (N(J, ma) / N(J, mb)) V^J[ma][mb],
+// the sqrt((J-ma)/(J-mb)) and sqrt(ma/(J-mb)) factors of the U recursion cancel:
+//   V^J[ma][mb] = conj(a) V^{J-1}[ma][mb] - conj(b) V^{J-1}[ma-1][mb],
+// and V keeps the inversion symmetry of U (the scale is invariant under
+// (ma, mb) -> (J - ma, J - mb)).  The twojmax-8 kernels propagate V (8 FP64
+// instructions per element instead of 12, no coefficient loads) and fold the
+// scale S^J[ma][mb] = N(J, ma) / N(J, mb) into what they produce or consume once
+// per atom: U_tot = S (.) sum_k fc_k V_k (k_snap_ui_r4), and the force sweep
+// reads S (.) Y (written by the Y kernel), because Re<U, Y> = Re<V, S (.) Y>.
+__device__ __forceinline__ C2 vstep(const C2& a, const C2& b, const C2& u, const C2& v, bool has_u, bool has_v) {
+  // conj(a) u - conj(b) v
+  C2 r{0.0, 0.0};
+  if (has_u && has_v) {
+    r.re = fma(a.re, u.re, fma(a.im, u.im, fma(-b.re, v.re, -b.im * v.im)));
+    r.im = fma(a.re, u.im, fma(-a.im, u.re, fma(-b.re, v.im, b.im * v.re)));
+  } else if (has_u) {
+    r.re = fma(a.re, u.re, a.im * u.im);
+    r.im = fma(a.re, u.im, -a.im * u.re);
+  } else if (has_v) {
+    r.re = fma(-b.re, v.re, -b.im * v.im);
+    r.im = fma(-b.re, v.im, b.im * v.re);
+  }
+  return r;
+}
+
+// advance row mb of V from layer J-1 to layer J (in place, descending ma); at
+// even J the middle row mb = J/2 is born from row J/2-1 of layer J-1 (lane - 1)
+template <int TJ, int J>
+__device__ __forceinline__ void row_step(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb) {
   if (J % 2 == 0) {
     // lane mb = J/2 receives row J/2-1 of layer J-1 from lane-1 (all lanes shuffle)
 #pragma unroll
     for (int i = 0; i < J; ++i) {
       C2 v = shfl_up_c2(u[i], 1);
-      C2 dv = WITH_D ? shfl_up_c2(du[i], 1) : C2{0.0, 0.0};
       if (2 * mb == J) {
         const int x = J - 1 - i;  // destination index in row J/2 of layer J-1
         const bool neg = ((x + J / 2) & 1) != 0;
         u[x] = neg ? C2{-v.re, v.im} : C2{v.re, -v.im};
-        if (WITH_D) du[x] = neg ? C2{-dv.re, dv.im} : C2{dv.re, -dv.im};
       }
     }
   }
   if (2 * mb > J) return;
 #pragma unroll
-  for (int ma = J; ma >= 0; --ma) {
-    C2 nu{0.0, 0.0}, nd{0.0, 0.0};
-    if (ma < J) {
-      const double A = rp[J - ma][J - mb];
-      C2 t = cmulc(g.a, u[ma]);
-      nu.re += A * t.re;
-      nu.im += A * t.im;
-      if (WITH_D) {
-        C2 t1 = cmulc(g.da, u[ma]), t2 = cmulc(g.a, du[ma]);
-        nd.re += A * (t1.re + t2.re);
-        nd.im += A * (t1.im + t2.im);
-      }
-    }
-    if (ma > 0) {
-      const double Bc = rp[ma][J - mb];
-      C2 t = cmulc(g.b, u[ma - 1]);
-      nu.re -= Bc * t.re;
-      nu.im -= Bc * t.im;
-      if (WITH_D) {
-        C2 t1 = cmulc(g.db, u[ma - 1]), t2 = cmulc(g.b, du[ma - 1]);
-        nd.re -= Bc * (t1.re + t2.re);
-        nd.im -= Bc * (t1.im + t2.im);
-      }
-    }
-    u[ma] = nu;
-    if (WITH_D) du[ma] = nd;
-  }
-}
-
-// sqrt(p/q) table into shared memory, computed in place (correctly rounded
-// divide and sqrt: the host table's values bit for bit) instead of 100
-// lane-divergent constant-bank reads that serialise per warp
-__device__ __forceinline__ void stage_rootpq(double (*rp)[SNAP_JMAX + 2]) {
-  for (int t = threadIdx.x; t < (SNAP_JMAX + 2) * (SNAP_JMAX + 2); t += blockDim.x) {
-    const int p = t / (SNAP_JMAX + 2), q = t % (SNAP_JMAX + 2);
-    rp[p][q] = q ? __dsqrt_rn(__ddiv_rn((double)p, (double)q)) : 0.0;
-  }
+  for (int ma = J; ma >= 0; --ma) u[ma] = vstep(g.a, g.b, u[ma], u[ma > 0 ? ma - 1 : 0], ma < J, ma > 0);
 }
 
 // ------------------------------------------------------------------ reverse-mode dE/dr
@@ -895,27 +903,11 @@ __device__ __forceinline__ void stage_rootpq(double (*rp)[SNAP_JMAX + 2]) {
 // born at even J from row J/2-1 by symmetry passes its adjoint back the same
 // way (G_{mb-1}[J-1-x] += (-1)^(x+mb) conj(G_mb[x])).  ~3x fewer FP64
 // operations than propagating the three dU/dr_k.
-// layer J of row mb from layer J-1 in place, no born-row handling
+// layer J of row mb from layer J-1 in place (V recursion), no born-row handling
 template <int TJ, int J>
-__device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                           const double (*rp)[SNAP_JMAX + 2]) {
+__device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g) {
 #pragma unroll
-  for (int ma = J; ma >= 0; --ma) {
-    C2 nu{0.0, 0.0};
-    if (ma < J) {
-      const double A = rp[J - ma][J - mb];
-      const C2 t = cmulc(g.a, u[ma]);
-      nu.re += A * t.re;
-      nu.im += A * t.im;
-    }
-    if (ma > 0) {
-      const double Bc = rp[ma][J - mb];
-      const C2 t = cmulc(g.b, u[ma - 1]);
-      nu.re -= Bc * t.re;
-      nu.im -= Bc * t.im;
-    }
-    u[ma] = nu;
-  }
+  for (int ma = J; ma >= 0; --ma) u[ma] = vstep(g.a, g.b, u[ma], u[ma > 0 ? ma - 1 : 0], ma < J, ma > 0);
 }
 
 // U_tot with 4 lanes per pair (twojmax 8; see k_snap_deidrj_adj4): lanes own
@@ -925,11 +917,10 @@ __device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g
 constexpr int UI4_WARPS = 4;
 
 template <int J>
-__device__ __forceinline__ void ui4_layers(C2 (&u)[9], C2 (&u4)[9], const RowGeom<8>& g, int mb,
-                                           const double (*rp)[SNAP_JMAX + 2], bool on, double fc,
-                                           C2 (&acc)[45], C2* row4) {
+__device__ __forceinline__ void ui4_layers(C2 (&u)[9], C2 (&u4)[9], const RowGeom<8>& g, int mb, bool on,
+                                           double fc, C2 (&acc)[45], C2* row4) {
   if constexpr (J > 0) {
-    ui4_layers<J - 1>(u, u4, g, mb, rp, on, fc, acc, row4);
+    ui4_layers<J - 1>(u, u4, g, mb, on, fc, acc, row4);
     if constexpr (J == 8) {
 #pragma unroll
       for (int i = 0; i < J; ++i) {
@@ -939,8 +930,7 @@ __device__ __forceinline__ void ui4_layers(C2 (&u)[9], C2 (&u4)[9], const RowGeo
       }
       u4[J] = C2{0.0, 0.0};
     }
-    C2 du[9];
-    row_step<8, J, false>(u, du, g, mb, rp);
+    row_step<8, J>(u, g, mb);
     if (on && 2 * mb <= J) {
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
@@ -950,7 +940,7 @@ __device__ __forceinline__ void ui4_layers(C2 (&u)[9], C2 (&u4)[9], const RowGeo
       }
     }
     if constexpr (J == 8) {
-      row_update<8, 8>(u4, g, 4, rp);
+      row_update<8, 8>(u4, g);
       if (on && mb == 3) {  // row 4 accumulates in the lane's own slot (shared memory)
 #pragma unroll
         for (int ma = 0; ma <= 8; ++ma) {
@@ -968,18 +958,14 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   griddep_wait();
   constexpr int TJ = 8, R = 4, P = 8;
   extern __shared__ double smem[];
-  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
   const int nh = D.nhalf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ps = nh + 2;  // padded pair-slot stride
-  C2* part = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * P * ps;
+  C2* part = reinterpret_cast<C2*>(smem) + warp * P * ps;
   // per-pair (a, b, fc) of the whole list, one lane per pair (instead of the 4 row
   // lanes of a slot recomputing it every round)
-  double* geo = reinterpret_cast<double*>(reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) +
-                                          UI4_WARPS * P * ps) + warp * SNAP_MAXN * 5;
-  stage_rootpq(rp);
+  double* geo = reinterpret_cast<double*>(reinterpret_cast<C2*>(smem) + UI4_WARPS * P * ps) + warp * SNAP_MAXN * 5;
   const int64_t atom = (int64_t)blockIdx.x * UI4_WARPS + warp;
-  __syncthreads();
   if (atom >= natoms) return;
   const int64_t b = atom / N;
   const int i = (int)(atom - b * N);
@@ -1022,7 +1008,7 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
     for (int k = 0; k <= TJ; ++k) u[k] = u4[k] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
     if (valid && mb == 0) acc[0].re += fc;  // J = 0
-    ui4_layers<TJ>(u, u4, g, mb, rp, valid, fc, acc, row4);
+    ui4_layers<TJ>(u, u4, g, mb, valid, fc, acc, row4);
   }
   {  // each lane owns its (pair slot, rows): plain stores (every element of every slot is written)
     C2* mypart = part + p * ps;
@@ -1045,6 +1031,8 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
     half_layer8(t, J, base);
     const int e = t - base;
     const int mbb = e / (J + 1), maa = e - mbb * (J + 1);
+    const double sc = __ldg(D.vs + t);  // U = S (.) V (1 on the diagonal)
+    a = C2{a.re * sc, a.im * sc};
     if (maa == mbb) a.re += D.wself;
     out[t] = a;
   }
@@ -1083,10 +1071,9 @@ struct AdjR4 {
   // forward: layer J from J-1 (in place), store rows of layers <= 7, accumulate F
   template <int J, class YS, bool LAZY = false>
   __device__ __forceinline__ static void fwd(C2 (&u)[TJ + 1], C2 (&u4)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                             const double (*rp)[SNAP_JMAX + 2], const YS& Y, C2* hist, int lane,
-                                             double& F) {
+                                             const YS& Y, C2* hist, int lane, double& F) {
     if constexpr (J > 0) {
-      fwd<J - 1, YS, LAZY>(u, u4, g, mb, rp, Y, hist, lane, F);
+      fwd<J - 1, YS, LAZY>(u, u4, g, mb, Y, hist, lane, F);
       if constexpr (J == TJ) {
         // virtual row 4 of layer 7 = born image of this lane's row 3 of layer 7
 #pragma unroll
@@ -1097,9 +1084,8 @@ struct AdjR4 {
         }
         u4[J] = C2{0.0, 0.0};
       }
-      C2 du[TJ + 1];
-      row_step<TJ, J, false>(u, du, g, mb, rp);  // rows 1..3 are born at J = 2, 4, 6 from the lane below
-      if constexpr (J == TJ) row_update<TJ, TJ>(u4, g, TJ / 2, rp);
+      row_step<TJ, J>(u, g, mb);  // rows 1..3 are born at J = 2, 4, 6 from the lane below
+      if constexpr (J == TJ) row_update<TJ, TJ>(u4, g);
     }
     if (2 * mb <= J) {
 #pragma unroll
@@ -1122,32 +1108,29 @@ struct AdjR4 {
     }
   }
 
-  // Sa/Sb of one row at layer J, then its adjoint to layer J-1 (in place)
+  // Sa/Sb of one row at layer J, then its adjoint to layer J-1 (in place), for
+  // the V recursion V^J[ma] = conj(a) V^{J-1}[ma] - conj(b) V^{J-1}[ma-1]:
+  //   S_a += conj(V^{J-1}[ma]) G^J[ma],  S_b -= conj(V^{J-1}[ma-1]) G^J[ma],
+  //   G^{J-1}[x] (+)= a G^J[x] - b G^J[x+1]
   template <int J>
   __device__ __forceinline__ static void row_adj(C2 (&G)[TJ + 1], const C2 (&up)[TJ + 1], const RowGeom<TJ>& g,
-                                                 int mb, const double (*rp)[SNAP_JMAX + 2], C2& Sa, C2& Sb) {
+                                                 C2& Sa, C2& Sb) {
 #pragma unroll
     for (int ma = 0; ma <= J; ++ma) {
-      if (ma < J) {
-        const double A = rp[J - ma][J - mb];
-        const C2 t = cmulc(up[ma], G[ma]);
-        Sa.re += A * t.re;
-        Sa.im += A * t.im;
+      if (ma < J) {  // Sa += conj(up) G
+        Sa.re = fma(up[ma].re, G[ma].re, fma(up[ma].im, G[ma].im, Sa.re));
+        Sa.im = fma(up[ma].re, G[ma].im, fma(-up[ma].im, G[ma].re, Sa.im));
       }
-      if (ma > 0) {
-        const double Bc = rp[ma][J - mb];
-        const C2 t = cmulc(up[ma - 1], G[ma]);
-        Sb.re -= Bc * t.re;
-        Sb.im -= Bc * t.im;
+      if (ma > 0) {  // Sb -= conj(up) G
+        Sb.re = fma(-up[ma - 1].re, G[ma].re, fma(-up[ma - 1].im, G[ma].im, Sb.re));
+        Sb.im = fma(-up[ma - 1].re, G[ma].im, fma(up[ma - 1].im, G[ma].re, Sb.im));
       }
     }
 #pragma unroll
-    for (int x = 0; x < J; ++x) {
-      const double A = rp[J - x][J - mb];
-      const double Bc = rp[x + 1][J - mb];
-      const C2 t1 = cmul(g.a, G[x]);
-      const C2 t2 = cmul(g.b, G[x + 1]);
-      G[x] = C2{A * t1.re - Bc * t2.re, A * t1.im - Bc * t2.im};
+    for (int x = 0; x < J; ++x) {  // a G[x] - b G[x+1]
+      const C2 p = G[x], q = G[x + 1];
+      G[x] = C2{fma(g.a.re, p.re, fma(-g.a.im, p.im, fma(-g.b.re, q.re, g.b.im * q.im))),
+                fma(g.a.re, p.im, fma(g.a.im, p.re, fma(-g.b.re, q.im, -g.b.im * q.re)))};
     }
     G[J] = C2{0.0, 0.0};
   }
@@ -1156,8 +1139,7 @@ struct AdjR4 {
   // the Y elements loaded for G (each Y element read once)
   template <int J, class YS, bool LAZY = false>
   __device__ __forceinline__ static void bwd(C2 (&G)[TJ + 1], C2 (&G4)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                             const double (*rp)[SNAP_JMAX + 2], const YS& Y, const C2* hist, int lane,
-                                             C2& Sa, C2& Sb, double& F) {
+                                             const YS& Y, const C2* hist, int lane, C2& Sa, C2& Sb, double& F) {
     if constexpr (J > 0) {
 
       const bool active = 2 * mb <= J;
@@ -1173,7 +1155,7 @@ struct AdjR4 {
             up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
           }
         }
-        row_adj<J>(G, up, g, mb, rp, Sa, Sb);
+        row_adj<J>(G, up, g, Sa, Sb);
       }
       if constexpr (J == TJ) {
         // row 4 (row-3 lane): its layer-7 image comes from this lane's own row 3
@@ -1184,7 +1166,7 @@ struct AdjR4 {
             const C2 v = hist[((J - 1) * J / 2 + (J - 1 - x)) * 32 + lane];
             up4[x] = ((x + TJ / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
           }
-          row_adj<J>(G4, up4, g, TJ / 2, rp, Sa, Sb);
+          row_adj<J>(G4, up4, g, Sa, Sb);
           // adjoint of the virtual row 4 of layer 7 flows to row 3
 #pragma unroll
           for (int x = 0; x < J; ++x) {
@@ -1222,7 +1204,7 @@ struct AdjR4 {
           G[x].im += w * y.im;
         }
       }
-      bwd<J - 1, YS, LAZY>(G, G4, g, mb, rp, Y, hist, lane, Sa, Sb, F);
+      bwd<J - 1, YS, LAZY>(G, G4, g, mb, Y, hist, lane, Sa, Sb, F);
     }
   }
 };
@@ -1247,8 +1229,11 @@ __device__ __forceinline__ C2 y_full(const C2* y, int J, int base, int r, int c)
 }
 
 // Y^dagger, half rows stored column-interleaved: yt[J][ma][mb] = conj(Y[J][ma][mb])
-// for mb <= J/2 (element (mb, ma) of the Y^dagger half rows)
-__global__ void k_snap_ytrans(int64_t natoms, int nh, int tj, const C2* __restrict__ y, C2* __restrict__ yt) {
+// for mb <= J/2 (element (mb, ma) of the Y^dagger half rows).  In the V form
+// (see vstep) y holds S (.) Y and yt must hold S (.) Y^dagger:
+//   S[ma][mb] conj(Y[ma][mb]) = S[ma][mb]^2 conj((S (.) Y)[ma][mb])   (S[mb][ma] = 1 / S[ma][mb])
+__global__ void k_snap_ytrans(int64_t natoms, int nh, const double* __restrict__ vs2, const C2* __restrict__ y,
+                              C2* __restrict__ yt) {
   griddep_wait();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= natoms * nh) return;
@@ -1259,7 +1244,8 @@ __global__ void k_snap_ytrans(int64_t natoms, int nh, int tj, const C2* __restri
   const int e = h - base;
   const int mb = e / (J + 1), ma = e - mb * (J + 1);
   const C2 v = y_full(y + atom * nh, J, base, ma, mb);
-  yt[atom * nh + base + ma * (J / 2 + 1) + mb] = C2{v.re, -v.im};
+  const double f = __ldg(vs2 + h);
+  yt[atom * nh + base + ma * (J / 2 + 1) + mb] = C2{f * v.re, -(f * v.im)};
 }
 
 // owner of the unordered pair {i, k}: i when (i + k even and k > i) or (i + k odd
@@ -1291,22 +1277,19 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
   griddep_wait();
   constexpr int TJ = 8, R = 4, P = 8;
   extern __shared__ double smem[];
-  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
   const int nh = D.nhalf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  C2* Yw = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + warp * APW * nh;
-  C2* hist = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) + NWB * APW * nh +
-             warp * ADJ4_SLOTS * 32;
+  C2* Yw = reinterpret_cast<C2*>(smem) + warp * APW * nh;
+  C2* hist = reinterpret_cast<C2*>(smem) + NWB * APW * nh + warp * ADJ4_SLOTS * 32;
   // geometry of 32 consecutive pairs (4 rounds), one lane per pair:
   // a, b, fc, dfc, u[3], sin, cos, 1/r and the partner atom
-  double* gb = reinterpret_cast<double*>(reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) +
-                                         NWB * (APW * nh + ADJ4_SLOTS * 32)) + warp * 32 * PAIR_GEO;
-  int64_t* gk = reinterpret_cast<int64_t*>(reinterpret_cast<double*>(
-                    reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2)) +
-                    NWB * (APW * nh + ADJ4_SLOTS * 32)) + NWB * 32 * PAIR_GEO) + warp * 32;
+  double* gb = reinterpret_cast<double*>(reinterpret_cast<C2*>(smem) + NWB * (APW * nh + ADJ4_SLOTS * 32)) +
+               warp * 32 * PAIR_GEO;
+  int64_t* gk = reinterpret_cast<int64_t*>(reinterpret_cast<double*>(reinterpret_cast<C2*>(smem) +
+                                                                     NWB * (APW * nh + ADJ4_SLOTS * 32)) +
+                                           NWB * 32 * PAIR_GEO) + warp * 32;
   // list slots of the owned neighbours of the warp's atoms, [APW][SNAP_MAXN]
   int32_t* oslot = reinterpret_cast<int32_t*>(gk + (NWB - warp) * 32) + warp * APW * SNAP_MAXN;
-  stage_rootpq(rp);
   const int64_t atom0 = ((int64_t)blockIdx.x * NWB + warp) * APW;
   int nat[APW];
   int total = 0;
@@ -1405,7 +1388,7 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
     for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
     double F = 0.0;
-    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, rp, Y, hist, lane, F);
+    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, Y, hist, lane, F);
     __syncwarp();
     C2 G[TJ + 1], G4[TJ + 1];
     {
@@ -1424,7 +1407,7 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
       G4[x] = C2{w4 * G4[x].re, w4 * G4[x].im};
     }
     C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
-    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, rp, Y, hist, lane, Sa, Sb, F);
+    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, Y, hist, lane, Sa, Sb, F);
     __syncwarp();
 #pragma unroll
     for (int r = 1; r < R; ++r) {
@@ -1466,10 +1449,9 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
   griddep_wait();
   constexpr int TJ = 8, R = 4, P = 8;
   extern __shared__ double smem[];
-  double (*rp)[SNAP_JMAX + 2] = reinterpret_cast<double (*)[SNAP_JMAX + 2]>(smem);
   const int nh = D.nhalf;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  C2* base = reinterpret_cast<C2*>(smem + (SNAP_JMAX + 2) * (SNAP_JMAX + 2));
+  C2* base = reinterpret_cast<C2*>(smem);
   C2* Yw = base + warp * 2 * nh;  // ring [2][nh]
   C2* hist = base + NWB * 2 * nh + warp * ADJ4_SLOTS * 32;
   double* gb0 = reinterpret_cast<double*>(base + NWB * (2 * nh + ADJ4_SLOTS * 32));
@@ -1480,7 +1462,6 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
   int32_t* cum = reinterpret_cast<int32_t*>(reinterpret_cast<int16_t*>(
                      reinterpret_cast<int64_t*>(gb0 + NWB * 32 * PAIR_GEO) + NWB * 32) + NWB * CH * SNAP_MAXN) +
                  warp * (CH + 2);
-  stage_rootpq(rp);
   const int64_t a0 = ((int64_t)blockIdx.x * NWB + warp) * CH;
   const int nrun = (int)max((int64_t)0, min((int64_t)CH, natoms - a0));
   int tot = 0;
@@ -1587,7 +1568,7 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
     for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
     double F = 0.0;
-    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, rp, Y, hist, lane, F);
+    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, Y, hist, lane, F);
     asm volatile("cp.async.wait_all;\n" ::: "memory");  // ring refills issued after the last round
     __syncwarp();
     C2 G[TJ + 1], G4[TJ + 1];
@@ -1605,7 +1586,7 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
       G4[x] = C2{w4 * G4[x].re, w4 * G4[x].im};
     }
     C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
-    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, rp, Y, hist, lane, Sa, Sb, F);
+    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, Y, hist, lane, Sa, Sb, F);
     __syncwarp();
 #pragma unroll
     for (int r = 1; r < R; ++r) {
@@ -1845,10 +1826,9 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_ui_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
   const bool special = S->tj == 8 && S->yi_reg && !snap_generic_forced();
-  const size_t rp_bytes = sizeof(double) * (SNAP_JMAX + 2) * (SNAP_JMAX + 2);
   prof_mark(ctx->stream, ST_UI, true);
   if (special) {
-    const size_t sm4 = rp_bytes + sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2) + sizeof(double) * UI4_WARPS * SNAP_MAXN * 5;
+    const size_t sm4 = sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2) + sizeof(double) * UI4_WARPS * SNAP_MAXN * 5;
     PL_CUDA(launch_pdl(k_snap_ui_r4, dim3((unsigned)((na + UI4_WARPS - 1) / UI4_WARPS)), dim3(UI4_WARPS * 32), sm4,
                        ctx->stream, D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.utot));
   } else {
@@ -1859,7 +1839,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   prof_mark(ctx->stream, ST_UI, false);
   prof_mark(ctx->stream, ST_YI, true);
   if (special) {
-    PL_CUDA(snap_box_launch(ctx->stream, na, D.beta0, D.yi5, buf.utot, buf.y, buf.eatom, erow));
+    PL_CUDA(snap_box_launch(ctx->stream, na, D.beta0, D.yi5, D.vs, buf.utot, buf.y, buf.eatom, erow));
   } else {
     k_snap_yi<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI_THREADS, yi_smem(D), ctx->stream>>>(D, na, buf.utot,
                                                                                                  buf.y, buf.eatom);
@@ -1870,7 +1850,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   if (special) {
     const int64_t nel = na * D.nhalf;
     PL_CUDA(launch_pdl(k_snap_ytrans, dim3((unsigned)((nel + 255) / 256)), dim3(256), 0, ctx->stream, na, D.nhalf,
-                       D.tj, buf.y, buf.yt));
+                       D.vs + D.nhalf, buf.y, buf.yt));
     PL_CHECK_LAUNCH();
     static const int prun = [] {
       const char* e = getenv("PL_SNAP_PAIR_RUN");
@@ -1878,14 +1858,14 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     }();
     constexpr int RUN = 8;
     if (prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4)) {  // >= 4 waves of runs
-      const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
+      const size_t sm = sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
                         (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
                         sizeof(int16_t) * PAIR_WARPS * RUN * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (RUN + 2);
       const unsigned grid = (unsigned)((na + PAIR_WARPS * RUN - 1) / (PAIR_WARPS * RUN));
       PL_CUDA(launch_pdl(k_snap_deidrj_run<RUN, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), sm, ctx->stream, D,
                          na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
     } else {
-      const size_t sm = rp_bytes + sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
+      const size_t sm = sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
                         (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
                         sizeof(int32_t) * PAIR_WARPS * 2 * SNAP_MAXN;
       const unsigned grid = (unsigned)((na + PAIR_WARPS * 2 - 1) / (PAIR_WARPS * 2));
@@ -1963,7 +1943,7 @@ extern "C" int pl_snap_info(pl_pot* pot, int32_t* h_counts, double* h_flops) {
   h_counts[4] = S->nunits;
   // FLOPs of the kernel variants that compute_snap actually launches
   const bool special = S->tj == 8 && S->yi_reg && !pl::snap_generic_forced();
-  h_flops[0] = S->flops_ui_pair;
+  h_flops[0] = special ? S->flops_ui_pair_v : S->flops_ui_pair;
   h_flops[1] = special ? S->flops_yi_atom_reg : S->flops_yi_atom;
   // pair form: one sweep (+ the Y_i + Y_k^dagger adds, one read of every half element) per
   // unordered pair, quoted per ordered pair like the other stages

@@ -202,8 +202,9 @@ __device__ __forceinline__ void ptri_dispatch(int tid, const PItem& A) {
 
 template <int NW, int V, int S>
 __global__ void __launch_bounds__(NW * 32, 1)
-k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const Cx* __restrict__ utot,
-            Cx* __restrict__ ylist, double* __restrict__ eatom, double* __restrict__ erow_g) {
+k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const double* __restrict__ vs,
+            const Cx* __restrict__ utot, Cx* __restrict__ ylist, double* __restrict__ eatom,
+            double* __restrict__ erow_g) {
   griddep_wait_yi();
   extern __shared__ double smem[];
   Cx* Uf = reinterpret_cast<Cx*>(smem);                 // [NFULL][32] full U matrices
@@ -311,7 +312,9 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
     erow[t] = e * (1.0 / 3.0);
   }
   __syncthreads();
-  // rows owned by this CTA -> global (all rows when S = 1)
+  // rows owned by this CTA -> global (all rows when S = 1), as S (.) Y: the force
+  // kernels propagate the coefficient-free V = U / S (snap.cu, vstep), and
+  // Re<U, Y> = Re<V, S (.) Y>
   // 8 consecutive threads take 8 consecutive atoms of one element h: conflict-free
   // shared-memory reads ([h][atom] layout), 16-byte global stores
   for (int t = threadIdx.x; t < yib::ATOMS * yib::NHALF; t += blockDim.x) {
@@ -323,7 +326,9 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
       const int r = yib::rowoff(J) + (h - yib::hoff(J)) / (J + 1);
       if (c_p_rowsplit[V][r] != split) continue;
     }
-    ylist[(a0 + at) * yib::NHALF + h] = Ys[h * yib::ATOMS + at];
+    const Cx y = Ys[h * yib::ATOMS + at];
+    const double sc = __ldg(vs + h);
+    ylist[(a0 + at) * yib::NHALF + h] = Cx{y.re * sc, y.im * sc};
   }
   if (S == 1) {
     if (warp == 0 && lane < na_blk) {
@@ -577,8 +582,8 @@ cudaError_t snap_yi8_setup(double* balance_out) {
 }
 
 template <int NW, int V, int S>
-static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const void* utot,
-                            void* ylist, double* eatom, double* erow_g) {
+static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const double* vs,
+                            const void* utot, void* ylist, double* eatom, double* erow_g) {
   const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * yib::ROWS * yib::ATOMS;
   static std::atomic<uint64_t> attr_devs{0};
   int dev = 0;
@@ -591,7 +596,7 @@ static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const
   }
   const unsigned grid = (unsigned)(S * ((natoms + yib::ATOMS - 1) / yib::ATOMS));
   cudaError_t e = launch_pdl_yi(k_snap_yi_p<NW, V, S>, dim3(grid), dim3(NW * 32), sm, st, natoms, beta0, coef,
-                                (const Cx*)utot, (Cx*)ylist, eatom, erow_g);
+                                vs, (const Cx*)utot, (Cx*)ylist, eatom, erow_g);
   if (e != cudaSuccess) return e;
   if (S > 1)
     e = launch_pdl_yi(k_box_energy, dim3((unsigned)((natoms + 255) / 256)), dim3(256), 0, st, natoms, beta0,
@@ -602,12 +607,12 @@ static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const
 
 // split rows over 2 CTAs per block when the batch has fewer blocks than SMs
 // (erow_g: 25 x natoms doubles of scratch)
-cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef,
+cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const double* vs,
                             const void* utot, void* ylist, double* eatom, double* erow_g) {
   const int64_t blocks = (natoms + yib::ATOMS - 1) / yib::ATOMS;
   const bool split = blocks < 148 && erow_g;
-  return split ? p_launch<8, 1, 2>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g)
-               : p_launch<8, 0, 1>(st, natoms, beta0, coef, utot, ylist, eatom, erow_g);
+  return split ? p_launch<8, 1, 2>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g)
+               : p_launch<8, 0, 1>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g);
 }
 
 }  // namespace pl

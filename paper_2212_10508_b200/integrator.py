@@ -253,8 +253,8 @@ def measure_kinetic_temperature_batch(pot: Potential, params: LangevinParams, sc
     if initial is not None:
         if initial.dim != d:
             raise ValueError(f"initial state has dimension {initial.dim}, expected {d}")
-        Q[0].copy_(torch.from_numpy(np.asarray(initial.q, dtype=float))[None].expand(R, d))
-        P[0].copy_(torch.from_numpy(np.asarray(initial.p, dtype=float))[None].expand(R, d))
+        Q[0].copy_(torch.from_numpy(np.array(initial.q, dtype=float))[None].expand(R, d))
+        P[0].copy_(torch.from_numpy(np.array(initial.p, dtype=float))[None].expand(R, d))
     S1 = torch.zeros((R, L, d), dtype=torch.float64, device=k.device)
     S2 = torch.zeros_like(S1)
     blows = torch.zeros((n_windows, R), dtype=torch.int32, device=k.device)
