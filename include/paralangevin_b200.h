@@ -50,6 +50,19 @@ const char* pl_last_error(void);
 /* Context: device + stream (cudaStream_t passed as void*; NULL = legacy). */
 int pl_ctx_create(int device, void* stream, pl_ctx** out);
 int pl_ctx_set_stream(pl_ctx* ctx, void* stream);
+/* Speculative mode (on != 0): window propagation does not synchronise the host
+ * for its neighbour-capacity check (read it later with pl_pot_overflow_async)
+ * and uses its own scratch, so speculative fine windows can be launched on a
+ * second stream while a corrected sweep runs on the first (parareal.py
+ * pipelining; no reference counterpart). */
+int pl_ctx_set_spec(pl_ctx* ctx, int on);
+/* Host-mapped progress counter of this context: single-replica cluster sweeps
+ * store the number of windows finished after each window (read it while the
+ * blocking pl_sweep runs in another host thread).  *h_progress = its address. */
+int pl_ctx_enable_progress(pl_ctx* ctx, int64_t** h_progress);
+/* 2 if a single-replica sweep with this coarse potential runs as the persistent
+ * cluster kernel (the one that reports progress), 0 otherwise; < 0 on error. */
+int pl_sweep_path(pl_pot* coarse);
 int pl_ctx_synchronize(pl_ctx* ctx);
 int pl_ctx_destroy(pl_ctx* ctx);
 
@@ -204,6 +217,10 @@ int pl_sub(pl_ctx* ctx, int64_t n, const double* d_a, const double* d_b, double*
  * configuration b (B x 3*n_atoms, unwrapped positions, cubic box n_cells*a). */
 int pl_sia_sites(pl_ctx* ctx, int64_t B, int n_atoms, int n_cells, double a, const double* d_q,
                  int32_t* d_label);
+
+/* Stream-ordered: *d_out (device int32) = 1 if any neighbour build of pot
+ * exceeded its capacity since the last check, else 0; re-arms the flag. */
+int pl_pot_overflow_async(pl_ctx* ctx, pl_pot* pot, int32_t* d_out);
 
 /* ---- measurement --------------------------------------------------------- */
 /* Record CUDA events around every kernel stage launched by this host thread

@@ -70,6 +70,10 @@ SIGNATURES = {
     "pl_prof_begin": (C.c_int, [vp]),
     "pl_prof_end": (C.c_int, [vp, C.c_int, pd, pi64]),
     "pl_fp64_peak": (C.c_int, [vp, pd]),
+    "pl_ctx_set_spec": (C.c_int, [vp, C.c_int]),
+    "pl_ctx_enable_progress": (C.c_int, [vp, C.POINTER(C.c_void_p)]),
+    "pl_sweep_path": (C.c_int, [vp]),
+    "pl_pot_overflow_async": (C.c_int, [vp, vp, vp]),
     "pl_dmma_peak": (C.c_int, [vp, pd]),
 }
 

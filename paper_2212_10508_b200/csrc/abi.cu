@@ -87,6 +87,27 @@ int pl_ctx_set_stream(pl_ctx* ctx, void* stream) {
   return PL_OK;
 }
 
+int pl_ctx_enable_progress(pl_ctx* ctx, int64_t** h_progress) {
+  if (!ctx || !h_progress) return fail(PL_EARG, "NULL argument");
+  if (!ctx->progress) {
+    void* p = nullptr;
+    PL_CUDA(cudaHostAlloc(&p, 64, cudaHostAllocMapped));
+    void* dp = nullptr;
+    PL_CUDA(cudaHostGetDevicePointer(&dp, p, 0));
+    ctx->progress = (int64_t*)p;
+    ctx->progress_dev = (int64_t*)dp;
+    *(volatile int64_t*)ctx->progress = 0;
+  }
+  *h_progress = ctx->progress;
+  return PL_OK;
+}
+
+int pl_ctx_set_spec(pl_ctx* ctx, int on) {
+  if (!ctx) return fail(PL_EARG, "ctx is NULL");
+  ctx->spec = on ? 1 : 0;
+  return PL_OK;
+}
+
 int pl_ctx_synchronize(pl_ctx* ctx) {
   if (!ctx) return fail(PL_EARG, "ctx is NULL");
   PL_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -97,6 +118,7 @@ int pl_ctx_destroy(pl_ctx* ctx) {
   if (!ctx) return PL_OK;
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->progress) cudaFreeHost(ctx->progress);
   delete ctx;
   return PL_OK;
 }

@@ -260,8 +260,11 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
   if (W == 0) return PL_OK;
   cudaStream_t st = ctx->stream;
   // amplitudes -> device (pinned-free small copy through the context scratch)
-  PL_TRY(ctx->work[1].reserve(sizeof(double) * (L + 1)));
-  double* amp = (double*)ctx->work[1].ptr;
+  // speculative windows (ctx->spec, second stream) use their own scratch slots
+  pl::Scratch& w_amp = ctx->work[ctx->spec ? 8 : 1];
+  pl::Scratch& w_grad = ctx->work[ctx->spec ? 9 : 2];
+  PL_TRY(w_amp.reserve(sizeof(double) * (L + 1)));
+  double* amp = (double*)w_amp.ptr;
   PL_CUDA(cudaMemcpyAsync(amp, h_amp, sizeof(double) * (L + 1), cudaMemcpyHostToDevice, st));
   PL_CUDA(cudaMemsetAsync(blow, 0, sizeof(int32_t) * W, st));
   StepConsts K{dt, h, hg, L};
@@ -301,8 +304,8 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
 
   // generic: batched force pipeline per substep
   size_t nd = (size_t)W * d;
-  PL_TRY(ctx->work[2].reserve(sizeof(double) * 2 * nd));
-  double* grad = (double*)ctx->work[2].ptr;
+  PL_TRY(w_grad.reserve(sizeof(double) * 2 * nd));
+  double* grad = (double*)w_grad.ptr;
   double* ph = grad + nd;
   if (q1 != q0) PL_CUDA(cudaMemcpyAsync(q1, q0, sizeof(double) * nd, cudaMemcpyDeviceToDevice, st));
   if (p1 != p0) PL_CUDA(cudaMemcpyAsync(p1, p0, sizeof(double) * nd, cudaMemcpyDeviceToDevice, st));

@@ -206,11 +206,14 @@ k_neigh_cell_w(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, cons
   }
 }
 
+__global__ void k_or_flag(const int* __restrict__ src, int32_t* __restrict__ dst) { *dst |= *src; }
+
 int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out) {
   int N = pot->n_atoms;
   size_t lists = sizeof(int32_t) * (size_t)B * N * maxn;
   size_t counts = sizeof(int32_t) * (size_t)B * N;
   PL_TRY(pot->work[0].reserve(lists));
+  void* const cnt_before = pot->work[1].ptr;
   PL_TRY(pot->work[1].reserve(counts + 64));
   out->nbr = (int32_t*)pot->work[0].ptr;
   out->cnt = (int32_t*)pot->work[1].ptr;
@@ -221,7 +224,10 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
   Box box = make_box(pot->box);
   double rc2 = rcut * rcut;
   cudaStream_t st = pot->ctx->stream;
-  PL_CUDA(cudaMemsetAsync(out->overflow, 0, sizeof(int), st));
+  // the flag is sticky between checks: every build of a window (one per substep)
+  // can raise it, and neigh_check at the end of the call sees any of them
+  if (pot->nb_armed || pot->work[1].ptr != cnt_before) PL_CUDA(cudaMemsetAsync(out->overflow, 0, sizeof(int), st));
+  pot->nb_armed = false;
   CellGrid g;
   bool cells_ok = N >= CELL_MIN_ATOMS && !getenv("PL_NEIGH_BRUTE");
   for (int c = 0; c < 3; ++c) {
@@ -277,12 +283,42 @@ int neigh_check(pl_pot* pot) {
       return PL_OK;
   }
   if (!pot->nb_overflow) return PL_OK;
+  if (pot->ctx->spec) return PL_OK;  // deferred: pl_pot_overflow_async
   int h = 0;
   PL_CUDA(cudaMemcpyAsync(&h, pot->nb_overflow, sizeof(int), cudaMemcpyDeviceToHost, pot->ctx->stream));
   PL_CUDA(cudaStreamSynchronize(pot->ctx->stream));
+  pot->nb_armed = true;
   if (h) return fail(PL_EPOT, "neighbour capacity exceeded (atoms too close / dense)");
+  return PL_OK;
+}
+
+// stream-ordered copy of the overflow flag (accumulated since the last check)
+// into d_out, OR-ed over the parts of a perturbed potential; re-arms the flag
+int overflow_async(pl_pot* pot, int32_t* d_out, bool first) {
+  cudaStream_t st = pot->ctx->stream;
+  if (pot->kind == POT_PERTURBED) {
+    PL_TRY(overflow_async(pot->base, d_out, first));
+    return pot->lam != 0.0 ? overflow_async(pot->delta, d_out, false) : PL_OK;
+  }
+  if ((pot->kind != POT_EAM && pot->kind != POT_SNAP) || !pot->nb_overflow) {
+    if (first) PL_CUDA(cudaMemsetAsync(d_out, 0, sizeof(int32_t), st));
+    return PL_OK;
+  }
+  if (first) {
+    PL_CUDA(cudaMemcpyAsync(d_out, pot->nb_overflow, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  } else {
+    k_or_flag<<<1, 1, 0, st>>>(pot->nb_overflow, d_out);
+    PL_CHECK_LAUNCH();
+  }
+  pot->nb_armed = true;
   return PL_OK;
 }
 
 
 }  // namespace pl
+
+extern "C" int pl_pot_overflow_async(pl_ctx* ctx, pl_pot* pot, int32_t* d_out) {
+  if (!ctx || !pot || !d_out) return pl::fail(PL_EARG, "NULL argument");
+  if (pot->ctx != ctx) return pl::fail(PL_EARG, "potential belongs to another context");
+  return pl::overflow_async(pot, d_out, true);
+}

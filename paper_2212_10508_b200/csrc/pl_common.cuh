@@ -107,7 +107,16 @@ namespace pl { struct SnapIndex; }  // snap.cu
 struct pl_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  pl::Scratch work[8];  // named slots, see pl_ctx slot enum in each .cu
+  pl::Scratch work[10];  // named slots, see pl_ctx slot enum in each .cu (8, 9: speculative windows)
+  // speculative mode (pl_ctx_set_spec): window propagation defers its neighbour-
+  // capacity check (no host synchronisation; pl_pot_overflow_async reads the flag
+  // on the stream) and uses its own integrator scratch slots, so it can run on a
+  // second stream next to a sweep on the first
+  int spec = 0;
+  // host-mapped progress counter (pl_ctx_enable_progress): the single-replica
+  // cluster sweep stores the number of windows it has finished after each one
+  int64_t* progress = nullptr;      // host pointer
+  int64_t* progress_dev = nullptr;  // its device alias
   // pinned host staging for small scalars read back by sync calls
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
@@ -144,7 +153,8 @@ struct pl_pot {
   int nbeta = 0;
   pl::SnapIndex* snap = nullptr;
   double flops = 0.0;
-  int* nb_overflow = nullptr;  // device flag of the last neighbour build
+  int* nb_overflow = nullptr;  // device flag: neighbour capacity exceeded since the last check (sticky)
+  bool nb_armed = true;        // the next neighbour build clears the flag (set by every check)
   // per-potential scratch (neighbour lists, per-atom buffers)
   pl::Scratch work[8];
 };

@@ -78,6 +78,7 @@ struct ClArgs {
   const int32_t* b_inc;
   int64_t s_traj, s_win, s_noise, s_hist;
   int* overflow;
+  int64_t* progress;  // host-mapped: windows finished (single-slot sweeps), or null
 };
 
 struct ClSmem {  // carve-up of the dynamic shared memory of one CTA
@@ -453,7 +454,13 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
     num = num + sqrt(t1);
     den = den + sqrt(t2);
     ++done;
-    if (rank == 0 && threadIdx.x == 0) hist[m - m0] = num / den;
+    if (rank == 0 && threadIdx.x == 0) {
+      hist[m - m0] = num / den;
+      if (A.progress) {  // node m+1 of every CTA is stored (cluster barrier above): publish it
+        __threadfence_system();
+        *(volatile int64_t*)A.progress = done;
+      }
+    }
     if (nf > 0.0) {
       fail_m = m;
       fail_kind = 2;
@@ -527,6 +534,8 @@ int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N
   int* ovf = (int*)(inc + R_act);
   A.amp = amp; A.acc = acc; A.out = out; A.hist = d_hist;
   A.b_ridx = ridx; A.b_m0 = m0; A.b_m1 = m1; A.b_inc = inc; A.overflow = ovf;
+  A.progress = (R_act == 1 && mode == 0) ? ctx->progress_dev : nullptr;
+  if (A.progress) *(volatile int64_t*)ctx->progress = 0;
   PL_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), st));
   PL_CUDA(cudaMemcpyAsync(amp, h_amp, sizeof(double) * (L + 1), cudaMemcpyHostToDevice, st));
   PL_CUDA(cudaMemcpyAsync(acc, h_state, sizeof(double) * 2 * R_act, cudaMemcpyHostToDevice, st));
@@ -561,6 +570,16 @@ int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N
   return PL_OK;
 }
 
+// 2 when a single-replica sweep of this coarse potential runs as the persistent
+// cluster kernel (the path that publishes progress), else 0
+int sweep_path(const pl_pot* coarse) {
+  if (!coarse || coarse->kind != POT_EAM || getenv("PL_SWEEP_NOCLUSTER") || getenv("PL_SWEEP_GENERIC")) return 0;
+  int C, tpa;
+  cluster_layout(coarse->n_atoms, C, tpa);
+  const int own = (coarse->n_atoms + C - 1) / C;
+  return cl_smem_bytes(coarse->n_atoms, own) > 220 * 1024 ? 0 : 2;
+}
+
 int eam_tpa_for(int n) {
   int C, tpa;
   cluster_layout(n, C, tpa);
@@ -568,3 +587,8 @@ int eam_tpa_for(int n) {
 }
 
 }  // namespace pl
+
+extern "C" int pl_sweep_path(pl_pot* coarse) {
+  if (!coarse) return pl::fail(PL_EARG, "NULL argument");
+  return pl::sweep_path(coarse);
+}

@@ -106,7 +106,15 @@ class WindowKernel:
         import torch
         self.pot, self.params, self.schedule, self.d = pot, params, schedule, d
         self.L = params.substeps
-        self.amp = np.array([amplitude(params, c) for c in schedule.coefficients], dtype=float)
+        amp = np.array([amplitude(params, c) for c in schedule.coefficients], dtype=float)
+        # pinned host copy: the library uploads it with cudaMemcpyAsync, which from
+        # pageable memory may synchronise with the stream (speculative launches
+        # on a second stream must not block the host)
+        try:
+            self._amp_pinned = torch.from_numpy(amp).pin_memory()
+            self.amp = self._amp_pinned.numpy()
+        except RuntimeError:  # no CUDA: plain host memory (the library refuses to run anyway)
+            self.amp = amp
         self.dt = float(params.dt)
         self.h = 0.5 * params.dt                      # `0.5 * dt * grad` (integrator.py:174)
         self.hg = 0.5 * params.dt * params.gamma      # `0.5 * dt * gamma * p`

@@ -32,7 +32,7 @@ from typing import Callable, NamedTuple
 import numpy as np
 
 from . import _lib
-from .distributed import sharded_fine
+from .distributed import sharded_fine, world
 from .integrator import BlowUpError, TemperatureSchedule, WindowKernel
 from .model import LangevinParams, NodeTrajectory, PhaseState
 from .potentials import PropagatorPair
@@ -286,6 +286,72 @@ class _FineCache:
             self.propagated += int(pos.numel())
         return self.outQ.index_select(0, rows), self.outP.index_select(0, rows), blow, pos
 
+    def fill(self, rows, q0, p0, FQ, FP, ok):
+        """Store results computed elsewhere (speculative windows): ``ok`` (bool,
+        per row) marks the rows whose propagation can be trusted."""
+        self.inQ.index_copy_(0, rows, q0)
+        self.inP.index_copy_(0, rows, p0)
+        self.outQ.index_copy_(0, rows, FQ)
+        self.outP.index_copy_(0, rows, FP)
+        self.valid.index_copy_(0, rows, ok)
+
+
+LAST_RUN_STATS: dict = {}  # diagnostics of the last single-run device engine (bench, tests)
+_SWEEP_POOL = None           # one worker thread for blocking sweep calls (speculation)
+
+
+def _spec_parts() -> int:
+    """Speculative batches per sweep (PL_PARAREAL_SPEC_PARTS, default 2)."""
+    import os
+    try:
+        return max(1, int(os.environ.get("PL_PARAREAL_SPEC_PARTS", "2")))
+    except ValueError:
+        return 2
+
+
+def _sweep_pool():
+    global _SWEEP_POOL
+    if _SWEEP_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _SWEEP_POOL = ThreadPoolExecutor(max_workers=1, thread_name_prefix="pl-sweep")
+    return _SWEEP_POOL
+
+
+def _spec_mode(fine, coarse, n: int, d: int) -> bool:
+    """Speculative pipelining of the fine stage behind the sweep: PL_PARAREAL_SPEC=1
+    turns it on (one rank, fine-window cache on, EAM coarse sweep on the cluster
+    kernel, which publishes its progress).  Off by default: measured on one B200
+    at the larger config it does not shorten the run (20.5 s plain; 20.9 s with 2
+    speculative batches per sweep, 21.7 s with 4, 21.9 s with 8): the speculative
+    batches run at lower efficiency than the full slab batch, the cluster sweep
+    slows down next to them, and a batch of ~2000 launches fills the launch queue,
+    so the host returns from it only near its end."""
+    import os
+    mode = os.environ.get("PL_PARAREAL_SPEC", "0")
+    if mode != "1" or os.environ.get("PL_PARAREAL_NOCACHE", "0") not in ("", "0"):
+        return False
+    if world()[1] > 1 or getattr(fine.pot, "n_atoms", None) is None:
+        return False
+    ctx = _lib.context()
+    return _lib.load().pl_sweep_path(coarse.pot.handle(ctx)) == 2  # progress comes from the cluster sweep
+
+
+def _timed(key):
+    """Accumulate the host wall time of a _DeviceRun method into self.t[key]."""
+    import functools
+    import time
+
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrap(self, *a, **kw):
+            t0 = time.perf_counter()
+            try:
+                return fn(self, *a, **kw)
+            finally:
+                self.t[key] += time.perf_counter() - t0
+        return wrap
+    return deco
+
 
 class _DeviceRun:
     """Device-resident trajectory + cached coarse outputs for one engine run."""
@@ -314,9 +380,16 @@ class _DeviceRun:
         self.noise_f = fine.noise_all()
         self.noise_c = coarse.noise_all()
         self.fcache = _FineCache(n, d, dev)
+        self.spec = torch.cuda.Stream(device=dev) if _spec_mode(fine, coarse, n, d) else None
+        self.spec_windows = 0  # speculative windows launched (diagnostics)
+        self.t = {"bootstrap": 0.0, "jumps": 0.0, "sweep": 0.0, "speculate": 0.0}  # host wall seconds
 
+    @_timed("bootstrap")
     def bootstrap(self, n_init: int) -> None:
         """cur[m+1] = C(cur[m]) for m = n_init..N-1 (parareal.py:404-405); caches base."""
+        if self.spec is not None:  # speculative copies of the old nodes must be taken first
+            import torch
+            torch.cuda.current_stream(self.Q.device).wait_stream(self.spec)
         k = self.coarse.kernel
         lib, ctx = _lib.load(), _lib.context()
         out = np.zeros(1, dtype=np.int64)
@@ -332,6 +405,7 @@ class _DeviceRun:
                               substep=int(blow[0]), window=m + 1, iteration=0)
         _lib.check(rc)
 
+    @_timed("jumps")
     def jumps(self, n_init: int, n_final: int, iteration: int) -> None:
         """jump[m] = F(prev[m]) - C(prev[m]) for all slab windows.
 
@@ -342,6 +416,8 @@ class _DeviceRun:
         """
         import torch
         W = n_final - n_init
+        if self.spec is not None:  # speculative windows of the last sweep must have landed in the cache
+            torch.cuda.current_stream(self.Q.device).wait_stream(self.spec)
 
         def run_fn(q0, p0, nz):
             def run_block(lo, hi):
@@ -369,21 +445,98 @@ class _DeviceRun:
     def snapshot_prev(self, n_init: int, n_final: int) -> None:
         self.prevQ[n_init:n_final + 1].copy_(self.Q[n_init:n_final + 1])
 
-    def sweep(self, n_init: int, n_final: int, include_m0: bool, expl: float, iteration: int):
-        """Corrected sweep on the device; returns (deltas, den) for the nodes updated."""
+    @_timed("speculate")
+    def _speculate(self, lo: int, hi: int) -> None:
+        """Fine windows lo..hi-1 of the NEXT iteration from nodes the running sweep
+        has finalised, launched on the second stream (the sweep kernel keeps its
+        SMs; these windows fill the others).  Results go to the fine-window cache
+        keyed by their exact start state, so the next jumps() uses them only if
+        it asks for the same start bit for bit: no result changes (wasted work if
+        the slab converges or shrinks instead)."""
+        import torch
+        if hi <= lo:
+            return
+        lib = _lib.load()
+        with torch.cuda.stream(self.spec):
+            ctx = _lib.context()
+            q0 = self.Q[lo:hi].clone()   # later sweeps may overwrite the nodes
+            p0 = self.P[lo:hi].clone()
+            _lib.check(lib.pl_ctx_set_spec(ctx.handle, 1))
+            try:
+                FQ, FP, blow = self.fine.kernel.run(q0, p0, self.noise_f[lo:hi])
+                over = torch.zeros(1, dtype=torch.int32, device=self.Q.device)
+                _lib.check(lib.pl_pot_overflow_async(ctx.handle, self.fine.pot.handle(ctx), _lib.ptr(over)))
+            finally:
+                _lib.check(lib.pl_ctx_set_spec(ctx.handle, 0))
+            rows = torch.arange(lo, hi, device=self.Q.device)
+            self.fcache.fill(rows, q0, p0, FQ, FP, (blow == 0) & (over == 0))
+        _lib.context()  # rebind the library stream to the main stream
+        self.spec_windows += hi - lo
+
+    def _sweep_call(self, main_stream, n_init, n_final, include_m0, expl, state, out, blow, progress):
+        """pl_sweep on the main stream; in the worker thread when speculating (own
+        library context, so the main thread can launch on the second stream)."""
         import ctypes as C
+
+        import torch
         k = self.coarse.kernel
-        lib, ctx = _lib.load(), _lib.context()
+        lib = _lib.load()
+        with torch.cuda.stream(main_stream):
+            ctx = _lib.context()
+            if progress is not None:
+                ptr = C.c_void_p()
+                _lib.check(lib.pl_ctx_enable_progress(ctx.handle, C.byref(ptr)))
+                cnt = C.c_int64.from_address(ptr.value)
+                cnt.value = 0  # (the launch resets it too) never expose the last sweep's count
+                progress.append(cnt)
+            rc = lib.pl_sweep(
+                ctx.handle, self.coarse.pot.handle(ctx), self.d, k.L, n_init, n_final,
+                1 if include_m0 else 0, _lib.ptr(self.Q), _lib.ptr(self.P), _lib.ptr(self.prevQ),
+                _lib.ptr(self.baseQ), _lib.ptr(self.baseP), _lib.ptr(self.jumpQ), _lib.ptr(self.jumpP),
+                _lib.ptr(self.noise_c), _lib.dptr(k.amp), _lib.ptr(k.mass), k.dt, k.h, k.hg,
+                float(expl), _lib.dptr(state), _lib.ptr(self.hist),
+                out.ctypes.data_as(_lib.pi64), blow.ctypes.data_as(_lib.pi32))
+            # the error text is per host thread: take it here
+            return rc, (lib.pl_last_error().decode(errors="replace") if rc != _lib.PL_OK else "")
+
+    @_timed("sweep")
+    def sweep(self, n_init: int, n_final: int, include_m0: bool, expl: float, iteration: int,
+              front: int | None = None):
+        """Corrected sweep on the device; returns (deltas, den) for the nodes updated.
+
+        With speculation on, the (blocking) sweep call runs in a worker thread and
+        this thread follows the kernel's host-mapped progress counter: as windows
+        finish, the next iteration's fine windows starting on their nodes are
+        launched on the second stream (windows below ``front``, whose start nodes
+        are frozen behind the exactness front, are cache hits and skipped).
+        """
+        import time
+
+        import torch
         state = np.zeros(2)
         out = np.zeros(1, dtype=np.int64)
         blow = np.zeros(1, dtype=np.int32)
-        rc = lib.pl_sweep(
-            ctx.handle, self.coarse.pot.handle(ctx), self.d, k.L, n_init, n_final,
-            1 if include_m0 else 0, _lib.ptr(self.Q), _lib.ptr(self.P), _lib.ptr(self.prevQ),
-            _lib.ptr(self.baseQ), _lib.ptr(self.baseP), _lib.ptr(self.jumpQ), _lib.ptr(self.jumpP),
-            _lib.ptr(self.noise_c), _lib.dptr(k.amp), _lib.ptr(k.mass), k.dt, k.h, k.hg,
-            float(expl), _lib.dptr(state), _lib.ptr(self.hist),
-            out.ctypes.data_as(_lib.pi64), blow.ctypes.data_as(_lib.pi32))
+        main = torch.cuda.current_stream(self.Q.device)
+        if self.spec is None:
+            rc, msg = self._sweep_call(main, n_init, n_final, include_m0, expl, state, out, blow, None)
+        else:
+            progress = []
+            fut = _sweep_pool().submit(self._sweep_call, main, n_init, n_final, include_m0, expl, state, out,
+                                    blow, progress)
+            lo = max(n_init + 1, front if front is not None else n_init + 1)
+            batch = max(1, -(-(n_final - n_init) // _spec_parts()))
+            while True:
+                finished = fut.done()
+                done = int(progress[0].value) if progress else 0
+                # windows whose start node n_init + done is final: n_init+1 .. n_init+done
+                hi = min(n_init + done + 1, n_final)
+                if hi - lo >= batch:
+                    self._speculate(lo, hi)
+                    lo = hi
+                if finished:
+                    break
+                time.sleep(0.0002)
+            rc, msg = fut.result()
         if rc == _lib.PL_EBLOWUP:
             m = int(out[0])
             if blow[0]:
@@ -391,7 +544,8 @@ class _DeviceRun:
                                   substep=int(blow[0]), window=m + 1, iteration=iteration)
             raise BlowUpError(f"corrected state is not finite at window {m + 1} "
                               f"(iteration {iteration})", window=m + 1, iteration=iteration)
-        _lib.check(rc)
+        if rc != _lib.PL_OK:
+            raise _lib.CallError(rc, msg)
         n_done = int(out[0])
         deltas = self.hist[:n_done].cpu().numpy()
         return deltas, state[1]
@@ -552,10 +706,14 @@ def _adaptive_device(initial, fine, coarse, config):
         def iterate(n_init, n_final, inc, it):
             run.jumps(n_init, n_final, it)
             run.snapshot_prev(n_init, n_final)
-            return run.sweep(n_init, n_final, inc, expl, it)
+            # node n_init + j is bitwise frozen from iteration j of the slab on, so after
+            # iteration `it` the windows starting below n_init + it are cache hits
+            return run.sweep(n_init, n_final, inc, expl, it, front=n_init + it)
 
     machine = _adaptive_machine(n, config.delta_conv, expl, config.iteration_cap)
     slabs, history, converged = _drive_adaptive(machine, _Dev)
+    LAST_RUN_STATS.update(fine_windows_propagated=run.fcache.propagated, speculative_windows=run.spec_windows,
+                          speculation=run.spec is not None, host_s=dict(run.t))
     return PararealResult(trajectory=run.trajectory(), slabs=tuple(slabs),
                           error_history=tuple(history), converged=converged)
 

@@ -168,8 +168,9 @@ def larger_parareal(N=64, L=200):
     plan = pl.NoisePlan.for_windows(11, N)
     t, res = timed(lambda: pl.parareal_adaptive(init, pair, params, sched, plan,
                                                 pl.PararealConfig(N, 1e-10, 0.35)))
+    from paper_2212_10508_b200 import parareal as par
     return {"config": f"larger adaptive parareal: {n} atoms, {N} x {L}, SNAP/EAM", "wall_s": t,
-            "n_slab": res.n_slab, "sum_k": res.total_iterations}
+            "n_slab": res.n_slab, "sum_k": res.total_iterations, **par.LAST_RUN_STATS}
 
 
 def main():

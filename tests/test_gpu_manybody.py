@@ -359,6 +359,31 @@ def test_persistent_sweep_matches_generic(pl, monkeypatch):
     np.testing.assert_allclose(a.trajectory.positions(), b.trajectory.positions(), rtol=0, atol=1e-9)
 
 
+def test_speculative_pipeline_is_bitwise_neutral(pl, monkeypatch):
+    """Chunked sweep + speculative fine windows on a second stream (PL_PARAREAL_SPEC=1)
+    give bit-for-bit the records and trajectory of the plain engine, and the
+    speculative windows are actually used (fewer windows propagated in jumps)."""
+    from paper_2212_10508_b200 import parareal as par, tungsten as W
+    L, N = 10, 12
+    q0, box, n, mass, params, sched, p0 = _w_pr1_setup(pl, L, N)
+    pair = pl.PropagatorPair(W.make_snap(n, box), W.make_eam(n, box), 100.0, 1.0)
+    plan = pl.NoisePlan.for_windows(13, N)
+    cfg = pl.PararealConfig(N, 1e-10, 0.35)
+    init = pl.PhaseState(q=q0, p=p0)
+    monkeypatch.setenv("PL_PARAREAL_SPEC", "0")
+    a = pl.parareal_adaptive(init, pair, params, sched, plan, cfg)
+    plain = dict(par.LAST_RUN_STATS)
+    monkeypatch.setenv("PL_PARAREAL_SPEC", "1")
+    b = pl.parareal_adaptive(init, pair, params, sched, plan, cfg)
+    spec = dict(par.LAST_RUN_STATS)
+    assert a.slabs == b.slabs
+    assert a.error_history == b.error_history
+    assert a.trajectory.positions().tobytes() == b.trajectory.positions().tobytes()
+    assert a.trajectory.momenta().tobytes() == b.trajectory.momenta().tobytes()
+    assert not plain["speculation"] and spec["speculation"] and spec["speculative_windows"] > 0
+    assert spec["fine_windows_propagated"] < plain["fine_windows_propagated"]
+
+
 def test_degenerate_pair_converges_in_one_iteration(pl):
     """coarse == fine: jumps are exactly zero, k_conv = 1 (acceptance criterion 5)."""
     from paper_2212_10508_b200 import tungsten as W
