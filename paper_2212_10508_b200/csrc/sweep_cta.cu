@@ -105,22 +105,33 @@ struct Slot {  // per-CTA (replica slot) view of the arrays, kept in registers
 // Verlet candidate lists (ascending j, rc + skin) of the current positions
 __device__ void sw_build(const SweepArgs& A, const Slot& S, const double* q, double* qref) {
   const int n = A.n_atoms;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  // one warp per atom, lanes over j, ballot compaction in ascending j (the
+  // lists of a serial scan, with a 32x shorter dependent chain)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int i = warp; i < n; i += nwarps) {
     const double xi = q[3 * i], yi = q[3 * i + 1], zi = q[3 * i + 2];
     int c = 0;
     int32_t* my = S.cand + (int64_t)i * SW_MAXN;
-    for (int j = 0; j < n; ++j) {
-      if (j == i) continue;
-      const double dx = min_image(sub(q[3 * j], xi), A.box.L[0], A.box.inv[0]);
-      const double dy = min_image(sub(q[3 * j + 1], yi), A.box.L[1], A.box.inv[1]);
-      const double dz = min_image(sub(q[3 * j + 2], zi), A.box.L[2], A.box.inv[2]);
-      if (r2_exact(dx, dy, dz) < A.rl2) {
-        if (c < SW_MAXN) my[c] = j;
-        ++c;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      bool hit = false;
+      if (j < n && j != i) {
+        const double dx = min_image(sub(q[3 * j], xi), A.box.L[0], A.box.inv[0]);
+        const double dy = min_image(sub(q[3 * j + 1], yi), A.box.L[1], A.box.inv[1]);
+        const double dz = min_image(sub(q[3 * j + 2], zi), A.box.L[2], A.box.inv[2]);
+        hit = r2_exact(dx, dy, dz) < A.rl2;
       }
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        const int pos = c + __popc(bal & ((1u << lane) - 1u));
+        if (pos < SW_MAXN) my[pos] = j;
+      }
+      c += __popc(bal);
     }
-    S.ncand[i] = c < SW_MAXN ? c : SW_MAXN;
-    if (c > SW_MAXN) *A.overflow = 1;
+    if (lane == 0) {
+      S.ncand[i] = c < SW_MAXN ? c : SW_MAXN;
+      if (c > SW_MAXN) *A.overflow = 1;
+    }
   }
   for (int t = threadIdx.x; t < 3 * n; t += blockDim.x) qref[t] = q[t];
 }
