@@ -117,7 +117,8 @@ constexpr int P_NS[P_NV] = {1, 2};
 constexpr int P_MAX_VW = 24;
 constexpr int P_MAX_ITEMS = 400;  // (row, triple) items: 375 at twojmax 8
 __constant__ int c_p_iseg[P_NV][yib::NPH][P_MAX_VW + 1];  // items of virtual warp w in phase p
-__constant__ int c_p_items[P_NV][P_MAX_ITEMS];           // tid << 16 | J << 8 | mb
+// per item, decoded on the host: {tid, Y-row offset (elements), lo | hi << 8 | mb << 16 | mid << 24 | swap << 25, 0}
+__constant__ int4 c_p_items[P_NV][P_MAX_ITEMS];
 __constant__ int c_p_rowsplit[P_NV][yib::ROWS];          // CTA of the block that owns row r
 __constant__ int c_p_nph;                                // phases in use
 
@@ -256,20 +257,17 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
   const int nph = c_p_nph;
   for (int ph = 0; ph < nph; ++ph) {
     for (int it = c_p_iseg[V][ph][vw]; it < c_p_iseg[V][ph][vw + 1]; ++it) {
-      const int item = c_p_items[V][it];
-      const int tid = item >> 16, J = (item >> 8) & 0xff, mb = item & 0xff;
-      const int code = c_box_code[tid];
-      const int X = code / 100, Y = (code / 10) % 10;
-      const int SH = (X + Y - J) / 2;
+      const int4 item = c_p_items[V][it];  // one constant load per item (host-decoded)
+      const int tid = item.x;
       PItem A;
       A.Ul = Uf + lane;
-      A.yrow = Ys + (yib::hoff(J) + mb * (J + 1)) * yib::ATOMS + lane;
+      A.yrow = Ys + item.y * yib::ATOMS + lane;
       A.cy = coef[tid];
-      A.mb = mb;
-      A.mid = (2 * mb == J);
-      A.swap = (Y == X) && !A.mid;
-      A.lo = max(0, mb + SH - Y);
-      A.hi = A.mid ? X / 2 : (A.swap ? (mb + SH) / 2 : min(X, mb + SH));
+      A.lo = item.z & 0xff;
+      A.hi = (item.z >> 8) & 0xff;
+      A.mb = (item.z >> 16) & 0xff;
+      A.mid = (item.z >> 24) & 1;
+      A.swap = (item.z >> 25) & 1;
       ptri_dispatch<NW>(tid, A);
     }
     __syncthreads();  // next phase: rows change owners
@@ -575,7 +573,18 @@ cudaError_t snap_yi8_setup(double* balance_out) {
   if ((e = cudaMemcpyToSymbol(c_box_code, code.data(), sizeof(int) * code.size())) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_p_nph, &nph, sizeof(int))) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_p_iseg, iseg.data(), sizeof(int) * iseg.size())) != cudaSuccess) return e;
-  if ((e = cudaMemcpyToSymbol(c_p_items, items.data(), sizeof(int) * items.size())) != cudaSuccess) return e;
+  std::vector<int4> items4(items.size());
+  for (size_t i = 0; i < items.size(); ++i) {
+    const int it = items[i], tid = it >> 16, J = (it >> 8) & 0xff, mb = it & 0xff;
+    const Triple& t = T[tid];
+    const int SH = (t.X + t.Y - J) / 2;
+    const bool mid = 2 * mb == J, swap = (t.X == t.Y) && !mid;
+    const int lo = std::max(0, mb + SH - t.Y);
+    const int hi = mid ? t.X / 2 : (swap ? (mb + SH) / 2 : std::min(t.X, mb + SH));
+    items4[i] = make_int4(tid, yib::hoff(J) + mb * (J + 1),
+                          lo | (hi << 8) | (mb << 16) | ((mid ? 1 : 0) << 24) | ((swap ? 1 : 0) << 25), 0);
+  }
+  if ((e = cudaMemcpyToSymbol(c_p_items, items4.data(), sizeof(int4) * items4.size())) != cudaSuccess) return e;
   if ((e = cudaMemcpyToSymbol(c_p_rowsplit, rowsplit.data(), sizeof(int) * rowsplit.size())) != cudaSuccess)
     return e;
   return cudaSuccess;
