@@ -97,13 +97,17 @@ def load():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH) or os.environ.get("PL_REBUILD"):
+        path = LIB_PATH
+        variant = os.environ.get("PL_LIB_VARIANT")  # A/B builds (build.py --variant), never built here
+        if variant:
+            path = os.path.join(HERE, f"libparalangevin_b200_{variant}.so")
+        elif not os.path.exists(LIB_PATH) or os.environ.get("PL_REBUILD"):
             from . import build as _build
             _build.build()
         try:
-            lib = C.CDLL(LIB_PATH)
+            lib = C.CDLL(path)
         except OSError as exc:  # no silent fallback
-            raise LibraryError(f"cannot load {LIB_PATH}: {exc}") from exc
+            raise LibraryError(f"cannot load {path}: {exc}") from exc
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -49,15 +49,19 @@ def up_to_date() -> bool:
     return os.path.getmtime(LIB) >= newest
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, variant: str | None = None, defines=()) -> str:
+    """Build the library; ``variant`` + ``defines`` (-DNAME...) make an A/B copy
+    libparalangevin_b200_<variant>.so (loaded when PL_LIB_VARIANT=<variant>)."""
+    lib_out = LIB if not variant else os.path.join(HERE, f"libparalangevin_b200_{variant}.so")
+    obj_dir = OBJ if not variant else os.path.join(OBJ, variant)
+    if not variant and not force and up_to_date():
         return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(obj_dir, exist_ok=True)
     cc = nvcc()
 
     def one(src):
-        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
-        cmd = [cc, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        cmd = [cc, *ARCH, *FLAGS, *defines, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
@@ -68,17 +72,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         for obj, log in results:
             sys.stderr.write(log)
-    with open(os.path.join(OBJ, "ptxas.log"), "w") as fh:
+    with open(os.path.join(obj_dir, "ptxas.log"), "w") as fh:
         for obj, log in results:
             fh.write(f"== {os.path.basename(obj)}\n{log}\n")
-    tmp = LIB + ".tmp"
+    tmp = lib_out + ".tmp"
     cmd = [cc, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    print(build(force="--force" in args, verbose="-v" in args, variant=var,
+                defines=[a for a in args if a.startswith("-D")]))

@@ -143,13 +143,10 @@ __device__ __forceinline__ void ptri(const PItem& A) {
   constexpr int FX = yib::foff(X), FY = yib::foff(Y);
   constexpr int AT = yib::ATOMS;
   Cx P[X + 1][Y + 1];
-#pragma unroll
-  for (int a = 0; a <= X; ++a)
-#pragma unroll
-    for (int b = 0; b <= Y; ++b) P[a][b] = Cx{0.0, 0.0};  // corners are never read: no registers
   const Cx* __restrict__ Ul = A.Ul;
-#pragma unroll 1
-  for (int mb1 = A.lo; mb1 <= A.hi; ++mb1) {
+  // one mb1 step; with PL_YI_PEEL the first one initialises P (P = ux uy exactly
+  // as fma(ux, uy, 0) rounds: no zero fill), else P starts from zeros
+  auto step = [&](const int mb1, const bool first) {
     const int mb2 = A.mb + SH - mb1;
     const double w = A.mid ? (2 * mb1 == X ? 0.5 : 1.0) : (A.swap ? (mb1 == mb2 ? 1.0 : 2.0) : 1.0);
     const double cbv = w * c_box[OFF + mb2 * (X + 1) + mb1];  // w C(mb; mb1), w exact
@@ -165,13 +162,31 @@ __device__ __forceinline__ void ptri(const PItem& A) {
 #pragma unroll
       for (int a = A0; a <= A1; ++a) {
         if (a + b < SH || a + b > SH + J) continue;  // outside the CG band (compile time)
-        P[a][b].re = fma(ux[a].re, uy.re, P[a][b].re);
-        P[a][b].im = fma(ux[a].re, uy.im, P[a][b].im);
+        if (first) {
+          P[a][b].re = ux[a].re * uy.re;
+          P[a][b].im = ux[a].re * uy.im;
+        } else {
+          P[a][b].re = fma(ux[a].re, uy.re, P[a][b].re);
+          P[a][b].im = fma(ux[a].re, uy.im, P[a][b].im);
+        }
         P[a][b].re = fma(-ux[a].im, uy.im, P[a][b].re);
         P[a][b].im = fma(ux[a].im, uy.re, P[a][b].im);
       }
     }
-  }
+  };
+#ifdef PL_YI_PEEL
+  if (A.lo > A.hi) return;  // no admissible mb1: no contribution
+  step(A.lo, true);
+#pragma unroll 1
+  for (int mb1 = A.lo + 1; mb1 <= A.hi; ++mb1) step(mb1, false);
+#else
+#pragma unroll
+  for (int a = 0; a <= X; ++a)
+#pragma unroll
+    for (int b = 0; b <= Y; ++b) P[a][b] = Cx{0.0, 0.0};  // corners are never read: no registers
+#pragma unroll 1
+  for (int mb1 = A.lo; mb1 <= A.hi; ++mb1) step(mb1, false);
+#endif
   // Z[ma] = sum_a C(ma; a) P[a][ma + SH - a], then Y[ma] += cy Z[ma] (the warp owns the row)
   Cx* yo = A.yrow;
 #pragma unroll

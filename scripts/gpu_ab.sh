@@ -1,5 +1,7 @@
-# A/B of SNAP kernel variants: GPU SNAP tests, then stage timings per env value
-# usage: bash scripts/gpu_ab.sh VAR v1 v2 ...
-V=${1:-PL_SNAP_PAIR}; shift
-python -m pytest tests/test_gpu_manybody.py -q -x > gpurun_out/pytest_mb.log 2>&1; tail -1 gpurun_out/pytest_mb.log
-for x in "$@"; do echo "== $V=$x"; env $V=$x python scripts/probe_snap.py 2>&1 | tail -2; done
+# A/B of library variants (build.py --variant NAME -D...): per-stage SNAP times at the larger config
+for v in "" peel; do for kb in 100 130; do
+  TAG="variant=${v:-base} kb=$kb" PL_LIB_VARIANT=$v PL_YI_PHASE_KB=$kb timeout 300 python scripts/probe_yi.py 2>&1 | tail -1
+done; done
+for v in "" peel; do
+  TAG="variant=${v:-base} PR1 batch" NCELL=4 BATCH=16 PL_LIB_VARIANT=$v timeout 300 python scripts/probe_yi.py 2>&1 | tail -1
+done

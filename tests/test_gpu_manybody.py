@@ -487,3 +487,31 @@ def test_heavy_system_sweeps_batch_equals_single(pl):
         assert one.slabs == batch[i].slabs
         assert one.error_history == batch[i].error_history
         assert one.trajectory.positions().tobytes() == batch[i].trajectory.positions().tobytes()
+
+
+@pytest.mark.parametrize("kind", ["eam", "snap"])
+def test_many_body_blow_up_substep_matches_oracle(pl, kind):
+    """The fused close kernels' trusted-range check on a many-body potential
+    (integrator.py:163-170): one atom placed beyond 1e12 A fails the check at the
+    first substep in the oracle's restatement of the reference window and on the
+    device (batched with a healthy window, in either order)."""
+    from oracle import integrator as oint, native, rng as orng
+    from paper_2212_10508_b200 import tungsten as W
+    L = 4
+    q_ok, box, n, mass, params, sched, _ = _w_pr1_setup(pl, L, 1)
+    q0 = q_ok.copy()
+    q0[0] = 2e12
+    p0 = np.zeros_like(q0)
+    pot = W.make_eam(n, box) if kind == "eam" else W.make_snap(n, box)
+    seed = pl.derive_seed(3, 1)
+    noise = orng.gaussian_stream(seed, (L + 1) * 3 * n)
+    grad = (lambda q: native.eam(q, box, W.eam_tables())[1]) if kind == "eam" else native.snap_fn(pot)
+    with pytest.raises(oint.OracleBlowUp) as oe:
+        oint.propagate_window(q0, p0, grad, params.gamma, params.inv_beta, params.dt, L, sched.coefficients, 0,
+                              mass=mass, noise=noise)
+    assert oe.value.substep == 1
+    good, bad = pl.PhaseState(q=q_ok, p=np.zeros_like(q0)), pl.PhaseState(q=q0, p=p0)
+    for states in ([good, bad], [bad, good]):
+        with pytest.raises(pl.BlowUpError) as ei:
+            pl.propagate_windows(states, pot, params, sched, [seed, seed], noise=np.stack([noise, noise]))
+        assert ei.value.substep == oe.value.substep
