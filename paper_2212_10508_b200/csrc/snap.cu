@@ -1066,14 +1066,72 @@ struct YPair {
   }
 };
 
+// Y_k^dagger staged in shared memory (k_snap_deidrj_tm): same layout as global
+struct YPairS {
+  const C2* y;   // Y_i, shared memory
+  const C2* yt;  // Y_k^dagger, shared memory (staged by a bulk copy per pair)
+  __device__ __forceinline__ C2 operator()(int J, int row, int x) const {
+    const C2 t = yt[c_hoff[J] + x * (J / 2 + 1) + row];
+    const C2 a = y[c_hoff[J] + row * (J + 1) + x];
+    return C2{a.re + t.re, a.im + t.im};
+  }
+};
+
+// forward-row history of the adjoint sweep: [slot][lane] in shared memory, or
+// the lane's own row of tensor memory (k_snap_deidrj_tm: TMEM holds it, freeing
+// the shared memory that stages Y_k^dagger).  tcgen05.ld/st are warp-collective
+// (.sync.aligned), so the TMEM policy stores and loads on every lane.
+struct HistSmem {
+  static constexpr bool kTmem = false;
+  C2* h;
+  int lane;
+  template <int J>
+  __device__ __forceinline__ void put(const C2 (&u)[9], bool active) const {
+    if (active)
+#pragma unroll
+      for (int ma = 0; ma <= J; ++ma) h[(J * (J + 1) / 2 + ma) * 32 + lane] = u[ma];
+  }
+  __device__ __forceinline__ C2 at(int slot, int dlane) const { return h[slot * 32 + lane + dlane]; }
+  __device__ __forceinline__ void sync() const {}
+};
+
+__device__ __forceinline__ void tm_st(uint32_t addr, const C2& v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+               "r"(__double2loint(v.re)), "r"(__double2hiint(v.re)), "r"(__double2loint(v.im)),
+               "r"(__double2hiint(v.im))
+               : "memory");
+}
+__device__ __forceinline__ C2 tm_ld(uint32_t addr) {
+  uint32_t a, b, c, d;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "r"(addr)
+               : "memory");
+  // the registers are valid only after wait::ld: tie them to it
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a), "+r"(b), "+r"(c), "+r"(d)::"memory");
+  return C2{__hiloint2double((int)b, (int)a), __hiloint2double((int)d, (int)c)};
+}
+
+struct HistTmem {
+  static constexpr bool kTmem = true;
+  uint32_t taddr;  // TMEM address of this warp's 32 lanes, column 0 (4 columns per slot)
+  template <int J>
+  __device__ __forceinline__ void put(const C2 (&u)[9], bool) const {
+#pragma unroll
+    for (int ma = 0; ma <= J; ++ma) tm_st(taddr + 4u * (J * (J + 1) / 2 + ma), u[ma]);
+  }
+  __device__ __forceinline__ C2 at(int slot) const { return tm_ld(taddr + 4u * slot); }
+  __device__ __forceinline__ void sync() const { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+};
+
 struct AdjR4 {
   static constexpr int TJ = 8;
   // forward: layer J from J-1 (in place), store rows of layers <= 7, accumulate F
-  template <int J, class YS, bool LAZY = false>
+  template <int J, class YS, bool LAZY = false, class H = HistSmem>
   __device__ __forceinline__ static void fwd(C2 (&u)[TJ + 1], C2 (&u4)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                             const YS& Y, C2* hist, int lane, double& F) {
+                                             const YS& Y, const H& hist, double& F) {
     if constexpr (J > 0) {
-      fwd<J - 1, YS, LAZY>(u, u4, g, mb, Y, hist, lane, F);
+      fwd<J - 1, YS, LAZY, H>(u, u4, g, mb, Y, hist, F);
       if constexpr (J == TJ) {
         // virtual row 4 of layer 7 = born image of this lane's row 3 of layer 7
 #pragma unroll
@@ -1087,10 +1145,10 @@ struct AdjR4 {
       row_step<TJ, J>(u, g, mb);  // rows 1..3 are born at J = 2, 4, 6 from the lane below
       if constexpr (J == TJ) row_update<TJ, TJ>(u4, g);
     }
+    if constexpr (J < TJ) hist.template put<J>(u, 2 * mb <= J);
     if (2 * mb <= J) {
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
-        if constexpr (J < TJ) hist[(J * (J + 1) / 2 + ma) * 32 + lane] = u[ma];
         if constexpr (!LAZY) {
           const C2 y = Y(J, mb, ma);
           F += half_w(J, mb, ma) * (u[ma].re * y.re + u[ma].im * y.im);
@@ -1137,21 +1195,36 @@ struct AdjR4 {
 
   // LAZY: F accumulates here from the history rows re-read for the adjoint and
   // the Y elements loaded for G (each Y element read once)
-  template <int J, class YS, bool LAZY = false>
+  template <int J, class YS, bool LAZY = false, class H = HistSmem>
   __device__ __forceinline__ static void bwd(C2 (&G)[TJ + 1], C2 (&G4)[TJ + 1], const RowGeom<TJ>& g, int mb,
-                                             const YS& Y, const C2* hist, int lane, C2& Sa, C2& Sb, double& F) {
+                                             const YS& Y, const H& hist, C2& Sa, C2& Sb, double& F) {
     if constexpr (J > 0) {
 
       const bool active = 2 * mb <= J;
       const bool born = (J % 2 == 0) && (J < TJ) && (2 * mb == J);  // rows 1..3: virtual in layer J-1
       C2 up[TJ + 1];
-      if (active) {
+      if constexpr (H::kTmem) {
+        // every lane loads its own row of layer J-1; born rows take the image of
+        // the lane below (row J/2-1 of layer J-1) by a shuffle
+        C2 L[TJ + 1];
+#pragma unroll
+        for (int x = 0; x < J; ++x) L[x] = hist.at((J - 1) * J / 2 + x);
+#pragma unroll
+        for (int x = 0; x < J; ++x) {
+          up[x] = L[x];
+          if constexpr (J % 2 == 0 && J < TJ) {
+            const C2 v = shfl_up_c2(L[J - 1 - x], 1);
+            if (born) up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+          }
+        }
+        if (active) row_adj<J>(G, up, g, Sa, Sb);
+      } else if (active) {
 #pragma unroll
         for (int x = 0; x < J; ++x) {
           if (!born) {
-            up[x] = hist[((J - 1) * J / 2 + x) * 32 + lane];
+            up[x] = hist.at((J - 1) * J / 2 + x, 0);
           } else {
-            const C2 v = hist[((J - 1) * J / 2 + (J - 1 - x)) * 32 + lane - 1];
+            const C2 v = hist.at((J - 1) * J / 2 + (J - 1 - x), -1);
             up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
           }
         }
@@ -1163,7 +1236,11 @@ struct AdjR4 {
           C2 up4[TJ + 1];
 #pragma unroll
           for (int x = 0; x < J; ++x) {
-            const C2 v = hist[((J - 1) * J / 2 + (J - 1 - x)) * 32 + lane];
+            C2 v;
+            if constexpr (H::kTmem)
+              v = up[J - 1 - x];  // this lane's own layer-7 row (not born at J = 8)
+            else
+              v = hist.at((J - 1) * J / 2 + (J - 1 - x), 0);
             up4[x] = ((x + TJ / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
           }
           row_adj<J>(G4, up4, g, Sa, Sb);
@@ -1204,7 +1281,7 @@ struct AdjR4 {
           G[x].im += w * y.im;
         }
       }
-      bwd<J - 1, YS, LAZY>(G, G4, g, mb, Y, hist, lane, Sa, Sb, F);
+      bwd<J - 1, YS, LAZY, H>(G, G4, g, mb, Y, hist, Sa, Sb, F);
     }
   }
 };
@@ -1388,7 +1465,7 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
     for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
     double F = 0.0;
-    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, Y, hist, lane, F);
+    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, Y, HistSmem{hist, lane}, F);
     __syncwarp();
     C2 G[TJ + 1], G4[TJ + 1];
     {
@@ -1407,7 +1484,7 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
       G4[x] = C2{w4 * G4[x].re, w4 * G4[x].im};
     }
     C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
-    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, Y, hist, lane, Sa, Sb, F);
+    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, Y, HistSmem{hist, lane}, Sa, Sb, F);
     __syncwarp();
 #pragma unroll
     for (int r = 1; r < R; ++r) {
@@ -1568,7 +1645,7 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
     for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
     double F = 0.0;
-    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, Y, hist, lane, F);
+    AdjR4::fwd<TJ, YPair, true>(u, u4, g, mb, Y, HistSmem{hist, lane}, F);
     asm volatile("cp.async.wait_all;\n" ::: "memory");  // ring refills issued after the last round
     __syncwarp();
     C2 G[TJ + 1], G4[TJ + 1];
@@ -1586,7 +1663,7 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
       G4[x] = C2{w4 * G4[x].re, w4 * G4[x].im};
     }
     C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
-    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, Y, hist, lane, Sa, Sb, F);
+    AdjR4::bwd<TJ, YPair, true>(G, G4, g, mb, Y, HistSmem{hist, lane}, Sa, Sb, F);
     __syncwarp();
 #pragma unroll
     for (int r = 1; r < R; ++r) {
@@ -1613,6 +1690,240 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
     }
     pos = end;
   }
+}
+
+// k_snap_deidrj_tm: the run kernel with the forward-row history in tensor
+// memory (each warp its 32 TMEM lanes, 36 slots x 4 columns) and the round's
+// Y_k^dagger staged in the shared memory that frees: one bulk copy (TMA engine)
+// per pair, issued when the round starts and landing behind its forward pass
+// (which reads no Y), so the adjoint sweep reads both Y terms from shared memory
+// instead of stalling on L2.  Same arithmetic as k_snap_deidrj_run (bitwise).
+// Pair form, one warp walking a run of CH consecutive atoms: the owned lists of
+// the run are concatenated, a round of 8 slots spans at most 2 atoms (a round
+// that would reach a third atom stops short), and Y_i of the live atoms sit in a
+// 2-slot ring (slot = local atom parity) refilled by cp.async as soon as an
+// atom's last pair is done, behind the next round's forward pass (which reads
+// no Y).  Slot fill ~98 % instead of 85 % for 2-atom warps.
+template <int CH, int NWB>
+__global__ void __launch_bounds__(NWB * 32)
+k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict__ q,
+                  const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
+                  const C2* __restrict__ ylist, const C2* __restrict__ ytlist, double* __restrict__ dedr) {
+  griddep_wait();
+  constexpr int TJ = 8, R = 4, P = 8;
+  extern __shared__ double smem[];
+  const int nh = D.nhalf;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int GB = 16;  // pairs per geometry batch (2 rounds; shared memory budget)
+  C2* base = reinterpret_cast<C2*>(smem);
+  C2* Yw = base + warp * 2 * nh;  // ring [2][nh]
+  C2* stg = base + NWB * 2 * nh + warp * P * nh;  // Y_k^dagger of the round's pairs [P][nh]
+  double* gb0 = reinterpret_cast<double*>(base + NWB * (2 * nh + P * nh));
+  double* gb = gb0 + warp * GB * PAIR_GEO;
+  int64_t* gk = reinterpret_cast<int64_t*>(gb0 + NWB * GB * PAIR_GEO) + warp * GB;
+  int16_t* oslot = reinterpret_cast<int16_t*>(reinterpret_cast<int64_t*>(gb0 + NWB * GB * PAIR_GEO) + NWB * GB) +
+                   warp * CH * SNAP_MAXN;
+  int32_t* cum = reinterpret_cast<int32_t*>(reinterpret_cast<int16_t*>(
+                     reinterpret_cast<int64_t*>(gb0 + NWB * GB * PAIR_GEO) + NWB * GB) + NWB * CH * SNAP_MAXN) +
+                 warp * (CH + 2);
+  __shared__ __align__(8) uint64_t s_mbar[NWB];
+  __shared__ uint32_t s_tmem;
+  // tensor memory: 256 columns per CTA (2 CTAs per SM), warp w uses lanes 32w..32w+31
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&s_tmem))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  const unsigned mbar = (unsigned)__cvta_generic_to_shared(&s_mbar[warp]);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const HistTmem hist{s_tmem + ((uint32_t)(32 * warp) << 16)};
+  unsigned phase = 0;
+  const int64_t a0 = ((int64_t)blockIdx.x * NWB + warp) * CH;
+  const int nrun = (int)max((int64_t)0, min((int64_t)CH, natoms - a0));
+  int tot = 0;
+  for (int c = 0; c < CH; ++c) {
+    if (lane == 0) cum[c] = tot;
+    const int base_c = tot;
+    if (c < nrun) {
+      const int64_t a = a0 + c;
+      const int i = (int)(a % N);
+      const int n = cnt[a];
+      for (int t0 = 0; t0 < n; t0 += 32) {
+        const bool own = t0 + lane < n && pair_owned(i, nbr[a * maxn + t0 + lane]);
+        const unsigned bal = __ballot_sync(0xffffffffu, own);
+        if (own) oslot[c * SNAP_MAXN + (tot - base_c) + __popc(bal & ((1u << lane) - 1u))] = (int16_t)(t0 + lane);
+        tot += __popc(bal);
+      }
+    }
+  }
+  if (lane == 0) {
+    cum[CH] = tot;
+    cum[CH + 1] = tot;
+  }
+  {  // Y of local atoms 0 and 1 (one contiguous range): loads in flight before the stores
+    constexpr int NL = (2 * 155 + 31) / 32;
+    const int nel = min(2, nrun) * nh;
+    C2 tmp[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (lane + 32 * j < nel) tmp[j] = ylist[a0 * nh + lane + 32 * j];
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (lane + 32 * j < nel) Yw[lane + 32 * j] = tmp[j];
+  }
+  __syncthreads();
+  const int p = lane / R, mb = lane - p * R;
+  int pos = 0, ca = 0, gbase = -64, next_load = 2;
+  while (nrun > 0 && pos < tot) {
+    while (cum[ca + 1] <= pos) ++ca;  // first atom of the round (skips atoms without owned pairs)
+    const int end = min(min(pos + P, tot), cum[ca + 2]);
+    // ring refill: every finished atom hands its slot to the atom two ahead (atoms
+    // already finished themselves are skipped, so a slot gets one copy at a time);
+    // the copies land behind this round's forward pass
+    while (next_load < nrun + 2 && cum[next_load - 1] <= pos) {
+      if (next_load < nrun && cum[next_load + 1] > pos) {
+        const C2* src = ylist + (a0 + next_load) * nh;
+        C2* dst = Yw + (next_load & 1) * nh;
+        for (int e = lane; e < nh; e += 32) {
+          const unsigned d = (unsigned)__cvta_generic_to_shared(dst + e);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + e) : "memory");
+        }
+      }
+      ++next_load;
+    }
+    if (pos + P > gbase + GB) {  // geometry of list positions pos .. pos + GB - 1
+      __syncwarp();
+      gbase = pos;
+      const int t = gbase + lane;
+      double* o = gb + (lane < GB ? lane : 0) * PAIR_GEO;
+      if (lane < GB && t < tot) {
+        int ct = ca;
+        while (cum[ct + 1] <= t) ++ct;
+        const int64_t at = a0 + ct;
+        const int64_t bt = at / N;
+        const int kk = nbr[at * maxn + oslot[ct * SNAP_MAXN + (t - cum[ct])]];
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ytlist + (bt * N + kk) * nh),
+                     "r"((unsigned)(nh * sizeof(C2)))
+                     : "memory");
+        double dx, dy, dz;
+        pair_vec(q + bt * (int64_t)N * 3, (int)(at - bt * N), kk, box, dx, dy, dz);
+        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+        const double inv = 1.0 / r;
+        const double u0 = dx * inv, u1 = dy * inv, u2 = dz * inv;
+        double sn, cs;
+        sincos(D.kappa * (r - D.rmin0), &sn, &cs);
+        double fc = 1.0, dfc = 0.0;
+        if (D.switchflag) {
+          double sa, ca2;
+          sincos(D.pi_span * (r - D.rmin0), &sa, &ca2);
+          fc = 0.5 * (ca2 + 1.0);
+          dfc = -D.half_pi_span * sa;
+        }
+        o[0] = cs; o[1] = -u2 * sn; o[2] = u1 * sn; o[3] = -u0 * sn;  // a, b
+        o[4] = fc; o[5] = dfc; o[6] = u0; o[7] = u1; o[8] = u2; o[9] = sn; o[10] = cs; o[11] = inv;
+        gk[lane] = bt * N + kk;
+      } else if (lane < GB) {
+        o[0] = 1.0; o[1] = 0.0; o[2] = 0.0; o[3] = 0.0;
+        gk[lane] = -1;
+      }
+      __syncwarp();
+    }
+    // stage the round's Y_k^dagger: one bulk copy per valid pair, completing on the
+    // warp's mbarrier; it lands while the forward pass (no Y) runs
+    {
+      const int nv = end - pos;
+      // the previous round's reads of the staging buffer (generic proxy) are done
+      // (consumed by its sweep); order them before the bulk writes (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
+                     "r"((unsigned)(nv * nh * sizeof(C2)))
+                     : "memory");
+      __syncwarp();
+      if (lane < nv)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                (unsigned)__cvta_generic_to_shared(stg + lane * nh)),
+            "l"(ytlist + gk[pos + lane - gbase] * nh), "r"((unsigned)(nh * sizeof(C2))), "r"(mbar)
+            : "memory");
+    }
+    const int pp = pos + p;
+    const bool valid = pp < end;
+    const int c = (valid && pp >= cum[ca + 1]) ? ca + 1 : ca;
+    const int64_t atom = a0 + c;
+    const int s = valid ? oslot[c * SNAP_MAXN + (pp - cum[c])] : 0;
+    const double* go = gb + (valid ? pp - gbase : 0) * PAIR_GEO;
+    const int64_t katom = valid ? gk[pp - gbase] : atom;  // invalid slots: own Y^dagger (weight 0)
+    (void)katom;
+    const YPairS Y{Yw + (c & 1) * nh, stg + p * nh};  // invalid slots read stale but finite data (weight 0)
+    RowGeom<TJ> g{valid ? C2{go[0], go[1]} : C2{1.0, 0.0}, valid ? C2{go[2], go[3]} : C2{0.0, 0.0}, C2{0.0, 0.0},
+                  C2{0.0, 0.0}};
+    C2 u[TJ + 1], u4[TJ + 1];
+#pragma unroll
+    for (int e = 0; e <= TJ; ++e) u[e] = u4[e] = C2{0.0, 0.0};
+    u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
+    double F = 0.0;
+    AdjR4::fwd<TJ, YPairS, true>(u, u4, g, mb, Y, hist, F);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");  // ring refills issued after the last round
+    asm volatile(
+        "{\n .reg .pred q;\n WT: mbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n @!q bra WT;\n}" ::"r"(mbar),
+        "r"(phase)
+        : "memory");
+    phase ^= 1u;
+    hist.sync();  // history stores complete before the sweep reads them
+    __syncwarp();
+    C2 G[TJ + 1], G4[TJ + 1];
+#pragma unroll
+    for (int x = 0; x <= TJ; ++x) {
+      G[x] = Y(TJ, mb, x);
+      G4[x] = (mb == TJ / 2 - 1) ? Y(TJ, TJ / 2, x) : C2{0.0, 0.0};
+    }
+#pragma unroll
+    for (int x = 0; x <= TJ; ++x) {  // layer-8 terms of F (row mb; row 4 on the row-3 lane)
+      const double w8 = half_w(TJ, mb, x), w4 = half_w(TJ, TJ / 2, x);
+      if (2 * mb <= TJ) F += w8 * (u[x].re * G[x].re + u[x].im * G[x].im);
+      if (mb == TJ / 2 - 1) F += w4 * (u4[x].re * G4[x].re + u4[x].im * G4[x].im);
+      G[x] = C2{w8 * G[x].re, w8 * G[x].im};
+      G4[x] = C2{w4 * G4[x].re, w4 * G4[x].im};
+    }
+    C2 Sa{0.0, 0.0}, Sb{0.0, 0.0};
+    AdjR4::bwd<TJ, YPairS, true>(G, G4, g, mb, Y, hist, Sa, Sb, F);
+    __syncwarp();
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double f = __shfl_down_sync(0xffffffffu, F, r);
+      const double ar = __shfl_down_sync(0xffffffffu, Sa.re, r), ai = __shfl_down_sync(0xffffffffu, Sa.im, r);
+      const double br = __shfl_down_sync(0xffffffffu, Sb.re, r), bi = __shfl_down_sync(0xffffffffu, Sb.im, r);
+      if (mb == 0) {
+        F += f;
+        Sa.re += ar; Sa.im += ai;
+        Sb.re += br; Sb.im += bi;
+      }
+    }
+    if (valid && mb == 0) {
+      const double uu[3] = {go[6], go[7], go[8]};
+      C2 da[3], db[3];
+      pair_deriv(D.kappa, uu, go[9], go[10], go[11], da, db);
+      const double fc = go[4], dfc = go[5];
+      double* o = dedr + (atom * maxn + s) * 3;
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) {
+        const double re = da[cc].re * Sa.re - da[cc].im * Sa.im + db[cc].re * Sb.re - db[cc].im * Sb.im;
+        o[cc] = dfc * uu[cc] * F + fc * re;
+      }
+    }
+    pos = end;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem) : "memory");
 }
 
 // gather of the pair form, one warp per atom (lanes over neighbour slots, the
@@ -1823,6 +2134,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_bispectrum, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_pair<2, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_run<8, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_tm<8, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_ui_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
   const bool special = S->tj == 8 && S->yi_reg && !snap_generic_forced();
@@ -1857,7 +2169,19 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
       return e ? atoi(e) : 1;  // 0: 2-atom warps only, 2: runs at every size (tests)
     }();
     constexpr int RUN = 8;
-    if (prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4)) {  // >= 4 waves of runs
+    static const bool tmem = [] {  // history in tensor memory + staged Y_k^dagger (PL_SNAP_TMEM=0: k_snap_deidrj_run)
+      const char* e = getenv("PL_SNAP_TMEM");
+      return !(e && e[0] == '0');
+    }();
+    if (tmem && (prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4))) {
+      constexpr int GB = 16;
+      const size_t sm = sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + 8 * D.nhalf) +
+                        (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * GB +
+                        sizeof(int16_t) * PAIR_WARPS * RUN * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (RUN + 2);
+      const unsigned grid = (unsigned)((na + PAIR_WARPS * RUN - 1) / (PAIR_WARPS * RUN));
+      PL_CUDA(launch_pdl(k_snap_deidrj_tm<RUN, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), sm, ctx->stream, D,
+                         na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
+    } else if (prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4)) {  // >= 4 waves of runs
       const size_t sm = sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
                         (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
                         sizeof(int16_t) * PAIR_WARPS * RUN * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (RUN + 2);

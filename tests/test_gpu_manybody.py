@@ -202,7 +202,7 @@ np.savez(sys.argv[1], E=E, G=G, V=V)
 
 def test_snap_specialised_matches_general_kernels(pl, tmp_path):
     """twojmax-8 kernels (k_snap_ui_r4, box-form Y, pair-symmetric reverse-mode forces
-    with 2-atom warps or 8-atom runs) against the general-twojmax kernels (k_snap_ui,
+    with 2-atom warps, 8-atom runs, or runs with the history in tensor memory) against the general-twojmax kernels (k_snap_ui,
     k_snap_yi, forward-mode k_snap_deidrj; PL_SNAP_GENERIC=1): energies, forces and
     virials to 1e-12; the two pair-kernel forms agree bit for bit."""
     import os
@@ -211,13 +211,14 @@ def test_snap_specialised_matches_general_kernels(pl, tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
     for mode, env_add in (("gen", {"PL_SNAP_GENERIC": "1"}), ("pair", {"PL_SNAP_PAIR_RUN": "0"}),
-                          ("run", {"PL_SNAP_PAIR_RUN": "2"})):
+                          ("run", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "0"}),
+                          ("tm", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "1"})):
         f = str(tmp_path / f"ab_{mode}.npz")
         env = dict(os.environ, **env_add)
         subprocess.run([sys.executable, "-c", _AB_SCRIPT, f], cwd=root, env=env, check=True)
         out[mode] = np.load(f)
     a = out["gen"]
-    for m in ("pair", "run"):
+    for m in ("pair", "run", "tm"):
         b = out[m]
         np.testing.assert_allclose(b["E"], a["E"], rtol=1e-12)
         np.testing.assert_allclose(b["G"], a["G"], rtol=1e-12, atol=1e-12 * np.abs(a["G"]).max())
@@ -225,6 +226,9 @@ def test_snap_specialised_matches_general_kernels(pl, tmp_path):
     # the pair gather sums each pair once, in list order: runs and 2-atom warps agree bit for bit
     np.testing.assert_array_equal(out["pair"]["G"], out["run"]["G"])
     np.testing.assert_array_equal(out["pair"]["E"], out["run"]["E"])
+    # history in tensor memory + staged Y_k^dagger: the same arithmetic, bit for bit
+    np.testing.assert_array_equal(out["tm"]["G"], out["run"]["G"])
+    np.testing.assert_array_equal(out["tm"]["V"], out["run"]["V"])
 
 
 @pytest.mark.parametrize("twojmax", [2, 4, 6])
