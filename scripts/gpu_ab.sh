@@ -1,7 +1,6 @@
-# A/B of library variants (build.py --variant NAME -D...): per-stage SNAP times at the larger config
-for v in "" peel; do for kb in 100 130; do
-  TAG="variant=${v:-base} kb=$kb" PL_LIB_VARIANT=$v PL_YI_PHASE_KB=$kb timeout 300 python scripts/probe_yi.py 2>&1 | tail -1
-done; done
-for v in "" peel; do
-  TAG="variant=${v:-base} PR1 batch" NCELL=4 BATCH=16 PL_LIB_VARIANT=$v timeout 300 python scripts/probe_yi.py 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_manybody.py tests/test_gpu_core.py -q -p no:cacheprovider -rf -x > gpurun_out/ab_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/ab_pytest.log
+for nw in 8 12; do
+  TAG="small nw=$nw PR1 batch" NCELL=4 BATCH=16 PL_YI_SMALL_NW=$nw timeout 300 python scripts/probe_yi.py 2>&1 | tail -1
+  TAG="small nw=$nw 4 windows larger" NCELL=8 BATCH=4 PL_YI_SMALL_NW=$nw timeout 300 python scripts/probe_yi.py 2>&1 | tail -1
 done
+TAG="large" timeout 300 python scripts/probe_yi.py 2>&1 | tail -1

@@ -156,10 +156,11 @@ def _snap_oracle_check(native, Q, box, pot, E, G, V, systems):
 def test_snap_production_batch_vs_oracle(pl):
     """150 x 129 atoms = 19,350 atoms (605 blocks of 32 atoms, > 148 SMs, >= 4 waves of
     8-atom runs): the batch sizes of the bench, force sweep and ensemble, which dispatch
-    the non-split Y kernel k_snap_yi_box<12,0,1> and the run force kernel
-    k_snap_deidrj_run<8,4> naturally.  Sampled systems vs the oracle (<= 1e-10), and
+    the non-split Y kernel k_snap_yi_p<8,0,1> and the run force kernel
+    (k_snap_deidrj_tm<8,4>) naturally.  Sampled systems vs the oracle (<= 1e-10), and
     each sampled system bitwise equal to its single-system evaluation (split Y
-    kernel <12,2,2> + 2-atom pair kernel): the batch never changes the arithmetic."""
+    kernel k_snap_yi_p<8,1,2> + 2-atom pair kernel): the batch never changes the
+    arithmetic."""
     from oracle import native
     from paper_2212_10508_b200 import tungsten as W
     Q, box = _configs(4, 150, seed=11)
