@@ -29,6 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import accounting, sia
+from .distributed import sharded_fine, world
 from .integrator import TemperatureSchedule, WindowKernel, _raise_first_blowup
 from .model import LangevinParams, PhaseState
 from .parareal import PararealConfig, parareal_adaptive_batch
@@ -45,6 +46,8 @@ def sequential_propagate_batch(initials, n_windows: int, pot, params: LangevinPa
     Member r's window m uses ``plans[r].seed_for(m + 1)`` exactly like
     ``sequential_propagate``; every window step is one batched launch over
     the members (independent chains), so each chain equals its single run.
+    Under torch.distributed the members of each step are sharded over the
+    ranks and all-gathered.
     """
     import torch
     R, d = len(initials), initials[0].dim
@@ -57,7 +60,16 @@ def sequential_propagate_batch(initials, n_windows: int, pot, params: LangevinPa
     P[0] = torch.from_numpy(np.stack([s.p for s in initials]))
     blow = torch.zeros((n_windows, R), dtype=torch.int32, device=k.device)
     for m in range(n_windows):
-        k.run(Q[m], P[m], noise[m], Q[m + 1], P[m + 1], blow[m])
+        if world()[1] == 1:
+            k.run(Q[m], P[m], noise[m], Q[m + 1], P[m + 1], blow[m])
+            continue
+
+        def run_block(lo, hi, m=m):  # members sharded over the ranks, gathered
+            return k.run(Q[m][lo:hi].contiguous(), P[m][lo:hi].contiguous(), noise[m][lo:hi].contiguous())
+        FQ, FP, b = sharded_fine(run_block, 0, R)
+        Q[m + 1].copy_(FQ)
+        P[m + 1].copy_(FP)
+        blow[m].copy_(b)
     b = blow.cpu().numpy()
     if b.any():
         m = int(np.nonzero(b.any(axis=1))[0][0])
