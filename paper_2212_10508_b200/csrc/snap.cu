@@ -2135,6 +2135,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_deidrj_pair<2, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_run<8, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_tm<8, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_tm<2, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_ui_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
   const bool special = S->tj == 8 && S->yi_reg && !snap_generic_forced();
@@ -2173,14 +2174,21 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
       const char* e = getenv("PL_SNAP_TMEM");
       return !(e && e[0] == '0');
     }();
-    if (tmem && (prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4))) {
+    const bool big = prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4);  // >= 4 waves of runs
+    auto tm_smem = [&](int ch) {
       constexpr int GB = 16;
-      const size_t sm = sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + 8 * D.nhalf) +
-                        (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * GB +
-                        sizeof(int16_t) * PAIR_WARPS * RUN * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (RUN + 2);
+      return sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + 8 * D.nhalf) +
+             (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * GB +
+             sizeof(int16_t) * PAIR_WARPS * ch * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (ch + 2);
+    };
+    if (tmem && big) {
       const unsigned grid = (unsigned)((na + PAIR_WARPS * RUN - 1) / (PAIR_WARPS * RUN));
-      PL_CUDA(launch_pdl(k_snap_deidrj_tm<RUN, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), sm, ctx->stream, D,
-                         na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
+      PL_CUDA(launch_pdl(k_snap_deidrj_tm<RUN, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), tm_smem(RUN),
+                         ctx->stream, D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
+    } else if (tmem) {  // small batches: 2-atom warps (the pair kernel's rounds) with the TMEM history
+      const unsigned grid = (unsigned)((na + PAIR_WARPS * 2 - 1) / (PAIR_WARPS * 2));
+      PL_CUDA(launch_pdl(k_snap_deidrj_tm<2, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), tm_smem(2), ctx->stream,
+                         D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
     } else if (prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4)) {  // >= 4 waves of runs
       const size_t sm = sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
                         (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
