@@ -234,6 +234,9 @@ int pl_fp64_peak(pl_ctx* ctx, double* h_tflops);
 /* FP64 tensor-core throughput (mma.sync m8n8k4 f64), measured (TFLOP/s): the
  * ceiling of a DMMA formulation of the Z/Y contraction. */
 int pl_dmma_peak(pl_ctx* ctx, double* h_tflops);
+/* Diagnostic build only (-DPL_YI_TIMING): per (block, phase, warp) cycles of the
+ * last Z/Y launch into h_out (4096 x 24 x 24 int64); returns 1 otherwise. */
+int pl_yi_timing(int64_t* h_out);
 
 #ifdef __cplusplus
 }

@@ -75,6 +75,7 @@ SIGNATURES = {
     "pl_sweep_path": (C.c_int, [vp]),
     "pl_pot_overflow_async": (C.c_int, [vp, vp, vp]),
     "pl_dmma_peak": (C.c_int, [vp, pd]),
+    "pl_yi_timing": (C.c_int, [vp]),
 }
 
 

@@ -216,6 +216,15 @@ __device__ __forceinline__ void ptri_dispatch(int tid, const PItem& A) {
   }
 }
 
+#ifdef PL_YI_TIMING
+// per (block, phase, warp): cycles from the phase start to the warp's arrival at the
+// phase barrier (diagnostic build, scripts/probe_yi_phases.py)
+constexpr int YT_BLOCKS = 4096;
+__device__ long long g_yi_timing[YT_BLOCKS][yib::NPH][P_MAX_VW];
+__device__ unsigned long long g_yi_item_cyc[yib::NT][5];  // per (triple, mb): summed cycles, and counts
+__device__ unsigned long long g_yi_item_cnt[yib::NT][5];
+#endif
+
 template <int NW, int V, int S>
 __global__ void __launch_bounds__(NW * 32, 1)
 k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const double* __restrict__ vs,
@@ -271,6 +280,9 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
   const int vw = split * NW + warp;  // virtual warp of the block's schedule
   const int nph = c_p_nph;
   for (int ph = 0; ph < nph; ++ph) {
+#ifdef PL_YI_TIMING
+    const long long t_ph = clock64();
+#endif
     for (int it = c_p_iseg[V][ph][vw]; it < c_p_iseg[V][ph][vw + 1]; ++it) {
       const int4 item = c_p_items[V][it];  // one constant load per item (host-decoded)
       const int tid = item.x;
@@ -283,8 +295,20 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
       A.mb = (item.z >> 16) & 0xff;
       A.mid = (item.z >> 24) & 1;
       A.swap = (item.z >> 25) & 1;
+#ifdef PL_YI_TIMING
+      const long long t_it = clock64();
+#endif
       ptri_dispatch<NW>(tid, A);
+#ifdef PL_YI_TIMING
+      if (lane == 0) {
+        atomicAdd(&g_yi_item_cyc[tid][A.mb], (unsigned long long)(clock64() - t_it));
+        atomicAdd(&g_yi_item_cnt[tid][A.mb], 1ull);
+      }
+#endif
     }
+#ifdef PL_YI_TIMING
+    if (lane == 0 && blockIdx.x < YT_BLOCKS) g_yi_timing[blockIdx.x][ph][vw] = clock64() - t_ph;
+#endif
     __syncthreads();  // next phase: rows change owners
   }
   // middle rows: Y[ma] += (-1)^(J/2+ma) conj(Y[J-ma]) for ma <= J/2 (the images of
@@ -387,7 +411,9 @@ int row_index(int J, int mb) { return yib::rowoff(J) + mb; }
 
 // cost of item (triple, mb) for the k_snap_yi_p body: per summed mb1, band
 // products (4 DFMA) + the C(mb; mb1) scaling + the column loads; epilogue per
-// band cell and per Y element
+// band cell and per Y element.  (Per-item cycles measured in a PL_YI_TIMING build
+// correlate at 0.88 with this model, but scheduling by them balanced the phases
+// worse, 0.921 vs 0.944: an item's cost depends on what runs beside it.)
 double item_cost(const Triple& t, int mb) {
   const int SH = (t.X + t.Y - t.J) / 2;
   const bool mid = 2 * mb == t.J, swap = (t.X == t.Y) && !mid;
@@ -640,3 +666,19 @@ cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const
 }
 
 }  // namespace pl
+
+// diagnostic: per (block, phase, warp) cycle counts of the last Y launch (only in a
+// build with -DPL_YI_TIMING; PL_EARG otherwise).  h_out: 4096 x 24 x 24 int64.
+extern "C" int pl_yi_timing(int64_t* h_out) {
+#ifdef PL_YI_TIMING
+  if (!h_out) return 1;
+  if (cudaMemcpyFromSymbol(h_out, pl::g_yi_timing, sizeof(pl::g_yi_timing)) != cudaSuccess) return 2;
+  // then per (triple, mb) summed item cycles and counts (125 x 5 each)
+  int64_t* p = h_out + sizeof(pl::g_yi_timing) / sizeof(int64_t);
+  if (cudaMemcpyFromSymbol(p, pl::g_yi_item_cyc, sizeof(pl::g_yi_item_cyc)) != cudaSuccess) return 2;
+  return cudaMemcpyFromSymbol(p + pl::yib::NT * 5, pl::g_yi_item_cnt, sizeof(pl::g_yi_item_cnt)) == cudaSuccess ? 0 : 2;
+#else
+  (void)h_out;
+  return 1;
+#endif
+}
