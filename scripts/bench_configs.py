@@ -147,7 +147,7 @@ def heavy(L=1000):
     peak = bench.ctypes_peak()
     per_kernel = {}
     for name, i, f in (("k_snap_ui_r4", 1, fl["ui"]), ("k_snap_yi_p", 2, fl["yi"]),
-                       ("k_snap_deidrj_pair", 3, fl["deidrj"])):
+                       ("k_snap_deidrj_tm", 3, fl["deidrj"])):
         t_launch = ms[i] / max(cnt[i], 1) * 1e-3
         tf = f / t_launch / 1e12
         per_kernel[name] = {"ms_per_launch": round(ms[i] / max(cnt[i], 1), 4), "tflops": round(tf, 3),
