@@ -1,5 +1,6 @@
 // extern "C" surface of paralangevin_b200 (declared in include/paralangevin_b200.h).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -266,6 +267,13 @@ int pl_pot_snap(pl_ctx* ctx, int n_atoms, const double* h_box, int twojmax, doub
   p->switchflag = switchflag;
   p->wself = wself;
   p->nbeta = nbeta;
+  // Verlet skin of the in-window lists (PL_SNAP_SKIN, A; 0 = exact lists every substep):
+  // 0.3 A keeps the BCC W lists below the fourth shell (5.25 A) at rcut 4.73 A
+  {
+    const char* e = std::getenv("PL_SNAP_SKIN");
+    p->skin = e ? std::atof(e) : 0.3;
+    if (!(p->skin >= 0.0 && p->skin < rcut)) p->skin = 0.0;
+  }
   int rc = snap_prepare(p, h_beta);
   if (rc != PL_OK) {
     delete p;

@@ -302,7 +302,21 @@ int propagate_windows(pl_ctx* ctx, pl_pot* pot, int64_t W, int64_t d, int L, con
     return lj_check(pot);
   }
 
-  // generic: batched force pipeline per substep
+  // generic: batched force pipeline per substep; SNAP keeps Verlet-skin lists over
+  // the window's substeps, rebuilt from the window's start state (so a window's
+  // result is a function of its start state alone)
+  struct SkinScope {
+    pl_pot* p;
+    SkinScope(pl_pot* p_) : p(p_) {
+      if (p && p->kind == POT_SNAP) {
+        p->skin_on = true;
+        p->skin_force = true;
+      }
+    }
+    ~SkinScope() {
+      if (p) p->skin_on = false;
+    }
+  } skin_scope(pot);
   size_t nd = (size_t)W * d;
   PL_TRY(w_grad.reserve(sizeof(double) * 2 * nd));
   double* grad = (double*)w_grad.ptr;

@@ -26,8 +26,10 @@ __device__ __forceinline__ int cell_of(double x, double L, double inv, int n) {
 }
 
 __global__ void k_cell_count(int64_t B, int N, Box box, CellGrid g, const double* __restrict__ q,
-                             int32_t* __restrict__ cell_of_atom, int32_t* __restrict__ ccount) {
+                             int32_t* __restrict__ cell_of_atom, int32_t* __restrict__ ccount,
+                             const int* __restrict__ go) {
   griddep_wait();
+  if (go && *go == 0) return;
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= B * N) return;
   int64_t b = t / N;
@@ -43,8 +45,10 @@ __global__ void k_cell_count(int64_t B, int N, Box box, CellGrid g, const double
 
 // exclusive scan of cell counts (single CTA, chunked)
 __global__ void __launch_bounds__(1024) k_cell_scan(int64_t ncell, const int32_t* __restrict__ ccount,
-                                                   int32_t* __restrict__ cstart, int32_t* __restrict__ cfill) {
+                                                   int32_t* __restrict__ cstart, int32_t* __restrict__ cfill,
+                                                   const int* __restrict__ go) {
   griddep_wait();
+  if (go && *go == 0) return;
   typedef cub::BlockScan<int32_t, 1024> S;
   __shared__ typename S::TempStorage tmp;
   __shared__ int32_t carry;
@@ -66,8 +70,9 @@ __global__ void __launch_bounds__(1024) k_cell_scan(int64_t ncell, const int32_t
 }
 
 __global__ void k_cell_fill(int64_t natoms, int N, const int32_t* __restrict__ cell_of_atom,
-                            int32_t* __restrict__ cfill, int32_t* __restrict__ catoms) {
+                            int32_t* __restrict__ cfill, int32_t* __restrict__ catoms, const int* __restrict__ go) {
   griddep_wait();
+  if (go && *go == 0) return;
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= natoms) return;
   int slot = atomicAdd(&cfill[cell_of_atom[t]], 1);
@@ -78,7 +83,8 @@ __global__ void __launch_bounds__(128)
 k_neigh_cell(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, const double* __restrict__ q,
              const int32_t* __restrict__ cell_of_atom, const int32_t* __restrict__ cstart,
              const int32_t* __restrict__ catoms, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
-             int* __restrict__ overflow) {
+             int* __restrict__ overflow, const int* __restrict__ go) {
+  if (go && *go == 0) return;
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= B * N) return;
   int64_t b = t / N;
@@ -133,8 +139,9 @@ __global__ void __launch_bounds__(NC_WARPS * 32)
 k_neigh_cell_w(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, const double* __restrict__ q,
                const int32_t* __restrict__ cell_of_atom, const int32_t* __restrict__ cstart,
                const int32_t* __restrict__ catoms, int32_t* __restrict__ nbr, int32_t* __restrict__ cnt,
-               int* __restrict__ overflow) {
+               int* __restrict__ overflow, const int* __restrict__ go) {
   griddep_wait();
+  if (go && *go == 0) return;
   __shared__ int32_t s_found[NC_WARPS][CELL_MAXN];
   __shared__ int32_t s_off[NC_WARPS][32], s_beg[NC_WARPS][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -208,7 +215,46 @@ k_neigh_cell_w(int64_t B, int N, Box box, CellGrid g, double rc2, int maxn, cons
 
 __global__ void k_or_flag(const int* __restrict__ src, int32_t* __restrict__ dst) { *dst |= *src; }
 
-int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out) {
+// Verlet skin: *flag = 1 when an atom moved more than skin/2 since the last build
+// (positions are unwrapped and continuous: no minimum image)
+__global__ void k_skin_check(int64_t n3, const double* __restrict__ q, const double* __restrict__ qref, double h2,
+                             int* __restrict__ flag) {
+  griddep_wait();
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (3 * t >= n3) return;
+  const double dx = q[3 * t] - qref[3 * t], dy = q[3 * t + 1] - qref[3 * t + 1], dz = q[3 * t + 2] - qref[3 * t + 2];
+  if (!(dx * dx + dy * dy + dz * dz <= h2)) *flag = 1;  // every writer stores 1 (non-finite moves rebuild too)
+}
+
+// the reference positions follow a rebuild
+__global__ void k_skin_ref(int64_t n3, const double* __restrict__ q, double* __restrict__ qref,
+                           const int* __restrict__ flag) {
+  griddep_wait();
+  if (*flag == 0) return;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n3; t += (int64_t)gridDim.x * blockDim.x)
+    qref[t] = q[t];
+}
+
+int skin_check(pl_pot* pot, int64_t na, const double* q, const double* qref, int* flag) {
+  cudaStream_t st = pot->ctx->stream;
+  PL_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  const double h = 0.5 * pot->skin;
+  PL_CUDA(launch_pdl(k_skin_check, dim3((unsigned)((na + 255) / 256)), dim3(256), 0, st, 3 * na, q, qref, h * h, flag));
+  PL_CHECK_LAUNCH();
+  return PL_OK;
+}
+
+int skin_ref(pl_pot* pot, int64_t na, const double* q, double* qref, const int* flag) {
+  cudaStream_t st = pot->ctx->stream;
+  int64_t blocks = (3 * na + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  PL_CUDA(launch_pdl(k_skin_ref, dim3((unsigned)blocks), dim3(256), 0, st, 3 * na, q, qref, flag));
+  PL_CHECK_LAUNCH();
+  return PL_OK;
+}
+
+int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out,
+                     const int* go) {
   int N = pot->n_atoms;
   size_t lists = sizeof(int32_t) * (size_t)B * N * maxn;
   size_t counts = sizeof(int32_t) * (size_t)B * N;
@@ -239,7 +285,7 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
   if (!cells_ok) {
     const int64_t warps = B * N;
     PL_CUDA(launch_pdl(k_neigh_brute_w, dim3((unsigned)((warps * 32 + NB_THREADS - 1) / NB_THREADS)), dim3(NB_THREADS),
-                       0, st, B, N, box, rc2, maxn, q, out->nbr, out->cnt, out->overflow));
+                       0, st, B, N, box, rc2, maxn, q, out->nbr, out->cnt, out->overflow, go));
     PL_CHECK_LAUNCH();
   } else {
     int64_t cells = (int64_t)g.n[0] * g.n[1] * g.n[2];
@@ -254,17 +300,18 @@ int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int m
     int32_t* catoms = cfill + (nc + 1);
     PL_CUDA(cudaMemsetAsync(ccount, 0, sizeof(int32_t) * nc, st));
     unsigned ga = (unsigned)((na + 255) / 256);
-    PL_CUDA(launch_pdl(k_cell_count, dim3(ga), dim3(256), 0, st, B, N, box, g, q, cell_of_atom, ccount));
-    PL_CUDA(launch_pdl(k_cell_scan, dim3(1), dim3(1024), 0, st, nc, ccount, cstart, cfill));
-    PL_CUDA(launch_pdl(k_cell_fill, dim3(ga), dim3(256), 0, st, na, N, cell_of_atom, cfill, catoms));
+    PL_CUDA(launch_pdl(k_cell_count, dim3(ga), dim3(256), 0, st, B, N, box, g, q, cell_of_atom, ccount, go));
+    PL_CUDA(launch_pdl(k_cell_scan, dim3(1), dim3(1024), 0, st, nc, ccount, cstart, cfill, go));
+    PL_CUDA(launch_pdl(k_cell_fill, dim3(ga), dim3(256), 0, st, na, N, cell_of_atom, cfill, catoms, go));
     static const bool warp_cells = !getenv("PL_NEIGH_THREAD");
     if (warp_cells)
       PL_CUDA(launch_pdl(k_neigh_cell_w, dim3((unsigned)((na + NC_WARPS - 1) / NC_WARPS)), dim3(NC_WARPS * 32), 0, st,
                          B, N, box, g, rc2, maxn, q, cell_of_atom, cstart, catoms, out->nbr, out->cnt,
-                         out->overflow));
+                         out->overflow, go));
     else
       k_neigh_cell<<<(unsigned)((na + 127) / 128), 128, 0, st>>>(B, N, box, g, rc2, maxn, q, cell_of_atom,
-                                                                cstart, catoms, out->nbr, out->cnt, out->overflow);
+                                                                cstart, catoms, out->nbr, out->cnt, out->overflow,
+                                                                go);
     PL_CHECK_LAUNCH();
   }
   prof_mark(st, ST_NEIGH, false);

@@ -90,8 +90,10 @@ k_neigh_brute(int64_t B, int N, Box box, double rc2, int maxn, const double* __r
 // systems where one thread per atom leaves the latency of N serial tests)
 static __global__ void __launch_bounds__(NB_THREADS)
 k_neigh_brute_w(int64_t B, int N, Box box, double rc2, int maxn, const double* __restrict__ q,
-                int32_t* __restrict__ nbr, int32_t* __restrict__ cnt, int* __restrict__ overflow) {
+                int32_t* __restrict__ nbr, int32_t* __restrict__ cnt, int* __restrict__ overflow,
+                const int* __restrict__ go) {
   griddep_wait();
+  if (go && *go == 0) return;
   const int64_t t = (blockIdx.x * (int64_t)NB_THREADS + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= B * N) return;
@@ -137,6 +139,21 @@ struct NeighList {
 };
 
 // builds into pot->work[0] (lists) / work[1] (counts + flag)
-int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out);
+// go (device flag, optional): every build kernel returns at entry when *go == 0
+// (Verlet-skin lists that are still valid; the lists are left as they are)
+int build_neighbours(pl_pot* pot, int64_t B, const double* q, double rcut, int maxn, NeighList* out,
+                     const int* go = nullptr);
+// Verlet skin (snap.cu): *flag = 1 when an atom moved more than skin/2 since qref;
+// qref = q where *flag (both on pot's stream, no host synchronisation)
+int skin_check(pl_pot* pot, int64_t na, const double* q, const double* qref, int* flag);
+int skin_ref(pl_pot* pot, int64_t na, const double* q, double* qref, const int* flag);
+// exact pair test of the list builders (r < rc on the minimum image)
+__device__ __forceinline__ bool pair_exact(const double* qb, int i, int j, const Box& box, double rc2);
+
+__device__ __forceinline__ bool pair_exact(const double* qb, int i, int j, const Box& box, double rc2) {
+  double dx, dy, dz;
+  pair_vec(qb, i, j, box, dx, dy, dz);
+  return r2_exact(dx, dy, dz) < rc2;
+}
 
 }  // namespace pl

@@ -155,6 +155,14 @@ struct pl_pot {
   double flops = 0.0;
   int* nb_overflow = nullptr;  // device flag: neighbour capacity exceeded since the last check (sticky)
   bool nb_armed = true;        // the next neighbour build clears the flag (set by every check)
+  // Verlet skin of the SNAP lists inside a window propagation (snap.cu): lists to
+  // rcut + skin, rebuilt on the device only when an atom moved more than skin/2
+  // since the last build; every SNAP kernel compacts the exact pairs (r < rcut)
+  // in list order, so the forces are bitwise those of exact lists
+  double skin = 0.0;
+  bool skin_on = false;     // set by propagate_windows for its duration
+  bool skin_force = false;  // next evaluation rebuilds unconditionally (window start)
+  int64_t skin_B = -1;      // batch size of the current skin lists
   // per-potential scratch (neighbour lists, per-atom buffers)
   pl::Scratch work[8];
 };

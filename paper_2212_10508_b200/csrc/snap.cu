@@ -92,6 +92,7 @@ struct SnapDev {  // POD view passed to kernels
   double beta0, rcut, rfac0, rmin0, wself;
   double kappa, pi_span, half_pi_span;  // rfac0*pi/(rcut-rmin0), pi/(rcut-rmin0), 0.5*pi/(rcut-rmin0)
   int switchflag;
+  int lists_exact;  // 1: the neighbour lists hold exactly the pairs r < rcut (no skin pairs to skip)
 };
 
 __constant__ double c_rootpq[SNAP_JMAX + 2][SNAP_JMAX + 2];  // sqrt(p/q)
@@ -454,6 +455,7 @@ static SnapDev snap_dev(const pl_pot* pot) {
   D.vs = S->yi_reg ? S->d_yi5 + 2 * 125 : nullptr;
   D.beta0 = S->beta0; D.rcut = pot->rcut; D.rfac0 = pot->rfac0; D.rmin0 = pot->rmin0;
   D.wself = pot->wself; D.switchflag = pot->switchflag;
+  D.lists_exact = 1;
   D.kappa = pot->rfac0 * M_PI / (pot->rcut - pot->rmin0);
   D.pi_span = M_PI / (pot->rcut - pot->rmin0);
   D.half_pi_span = 0.5 * M_PI / (pot->rcut - pot->rmin0);
@@ -971,7 +973,7 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   const int i = (int)(atom - b * N);
   const double* qb = q + b * (int64_t)N * 3;
   const int p = lane / R, mb = lane - p * R;
-  const int n = cnt[atom];
+  const int nl = cnt[atom];
   const int32_t* nb = nbr + atom * maxn;
   C2 acc[45];
 #pragma unroll
@@ -980,13 +982,26 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   if (mb == 3)
 #pragma unroll
     for (int k = 0; k <= TJ; ++k) row4[k] = C2{0.0, 0.0};
-  for (int j = lane; j < n; j += 32) {
-    double dx, dy, dz;
-    pair_vec(qb, i, nb[j], box, dx, dy, dz);
-    PairGeom pg;
-    pair_geom(D, dx, dy, dz, pg, false);
-    double* o = geo + 5 * j;
-    o[0] = pg.a.re; o[1] = pg.a.im; o[2] = pg.b.re; o[3] = pg.b.im; o[4] = pg.fc;
+  // exact pairs (r < rc) compacted in list order (a Verlet-skin list also holds
+  // pairs beyond rc): the slots are those of an exact list, bit for bit
+  int n = 0;
+  const double rc2 = D.rcut * D.rcut;
+  for (int j0 = 0; j0 < nl; j0 += 32) {
+    const int j = j0 + lane;
+    double dx = 0.0, dy = 0.0, dz = 0.0;
+    bool keep = false;
+    if (j < nl) {
+      pair_vec(qb, i, nb[j], box, dx, dy, dz);
+      keep = D.lists_exact || r2_exact(dx, dy, dz) < rc2;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      PairGeom pg;
+      pair_geom(D, dx, dy, dz, pg, false);
+      double* o = geo + 5 * (n + __popc(bal & ((1u << lane) - 1u)));
+      o[0] = pg.a.re; o[1] = pg.a.im; o[2] = pg.b.re; o[3] = pg.b.im; o[4] = pg.fc;
+    }
+    n += __popc(bal);
   }
   __syncwarp();
   for (int s0 = 0; s0 < n; s0 += P) {
@@ -1379,7 +1394,9 @@ k_snap_deidrj_pair(SnapDev D, int64_t natoms, int N, Box box, const double* __re
       const int c = cnt[a];
       int m = 0;
       for (int t0 = 0; t0 < c; t0 += 32) {  // compaction of the owned slots, list order
-        const bool own = t0 + lane < c && pair_owned(i, nbr[a * maxn + t0 + lane]);
+        const int kk = t0 + lane < c ? nbr[a * maxn + t0 + lane] : 0;
+        const bool own = t0 + lane < c && pair_owned(i, kk) &&
+                         (D.lists_exact || pair_exact(q + (a / N) * (int64_t)N * 3, i, kk, box, D.rcut * D.rcut));
         const unsigned bal = __ballot_sync(0xffffffffu, own);
         if (own) oslot[k * SNAP_MAXN + m + __popc(bal & ((1u << lane) - 1u))] = t0 + lane;
         m += __popc(bal);
@@ -1550,7 +1567,9 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
       const int i = (int)(a % N);
       const int n = cnt[a];
       for (int t0 = 0; t0 < n; t0 += 32) {
-        const bool own = t0 + lane < n && pair_owned(i, nbr[a * maxn + t0 + lane]);
+        const int kk = t0 + lane < n ? nbr[a * maxn + t0 + lane] : 0;
+        const bool own = t0 + lane < n && pair_owned(i, kk) &&
+                         (D.lists_exact || pair_exact(q + (a / N) * (int64_t)N * 3, i, kk, box, D.rcut * D.rcut));
         const unsigned bal = __ballot_sync(0xffffffffu, own);
         if (own) oslot[c * SNAP_MAXN + (tot - base_c) + __popc(bal & ((1u << lane) - 1u))] = (int16_t)(t0 + lane);
         tot += __popc(bal);
@@ -1756,7 +1775,9 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
       const int i = (int)(a % N);
       const int n = cnt[a];
       for (int t0 = 0; t0 < n; t0 += 32) {
-        const bool own = t0 + lane < n && pair_owned(i, nbr[a * maxn + t0 + lane]);
+        const int kk = t0 + lane < n ? nbr[a * maxn + t0 + lane] : 0;
+        const bool own = t0 + lane < n && pair_owned(i, kk) &&
+                         (D.lists_exact || pair_exact(q + (a / N) * (int64_t)N * 3, i, kk, box, D.rcut * D.rcut));
         const unsigned bal = __ballot_sync(0xffffffffu, own);
         if (own) oslot[c * SNAP_MAXN + (tot - base_c) + __popc(bal & ((1u << lane) - 1u))] = (int16_t)(t0 + lane);
         tot += __popc(bal);
@@ -1932,18 +1953,32 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
 __global__ void __launch_bounds__(128)
 k_snap_gather_pair_w(int64_t natoms, int N, Box box, const double* __restrict__ q,
                      const int32_t* __restrict__ nbr, const int32_t* __restrict__ cnt, int maxn,
-                     const double* __restrict__ dedr, double* __restrict__ grad, double* __restrict__ vatom) {
+                     const double* __restrict__ dedr, double* __restrict__ grad, double* __restrict__ vatom,
+                     double rc2, int lists_exact) {
   griddep_wait();
+  __shared__ int16_t s_slot[4][SNAP_MAXN];  // list slots of the exact pairs, in list order
   const int64_t atom = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = (threadIdx.x >> 5) & 3;
   if (atom >= natoms) return;
   const int64_t b = atom / N;
   const int a = (int)(atom - b * N);
-  const int n = cnt[atom];
+  const int nl = cnt[atom];
   const int32_t* nb = nbr + atom * maxn;
   const double* qb = q + b * (int64_t)N * 3;
+  // exact pairs (r < rc) compacted in list order: the e-th one is handled by lane
+  // e % 32 as in an exact list, whatever skin pairs the list also holds
+  int n = 0;
+  for (int s0 = 0; s0 < nl; s0 += 32) {
+    const int s = s0 + lane;
+    const bool keep = s < nl && (lists_exact || pair_exact(qb, a, nb[s], box, rc2));
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) s_slot[wib][n + __popc(bal & ((1u << lane) - 1u))] = (int16_t)s;
+    n += __popc(bal);
+  }
+  __syncwarp();
   double v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // g[3], vir[6]
-  for (int s = lane; s < n; s += 32) {
+  for (int e = lane; e < n; e += 32) {
+    const int s = s_slot[wib][e];
     const int k = nb[s];
     if (pair_owned(a, k)) {
       const double* h = dedr + (atom * maxn + s) * 3;
@@ -2073,6 +2108,7 @@ struct SnapBuffers {
   C2* y;
   C2* yt;     // Y^dagger (pair form only)
   bool pair;  // dedr holds h_ik on owned slots (k_snap_deidrj_pair) instead of dE_i/dr_ik
+  bool lists_exact = true;  // no Verlet-skin pairs in the lists
   double* eatom;
   double* dedr;
   double* vatom;
@@ -2112,7 +2148,32 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   int N = pot->n_atoms;
   int64_t na = B * N;
   if (na > 0x7fffffff) return fail(PL_EARG, "too many atoms in one batch");
-  PL_TRY(build_neighbours(pot, B, q, pot->rcut, SNAP_MAXN, &nl));
+  // Verlet skin inside a window propagation (twojmax-8 kernels only: they compact
+  // the exact pairs): lists to rcut + skin, rebuilt on the device when an atom
+  // moved more than skin/2 (no host synchronisation); forced at every window start
+  // (systems of >= 512 atoms, the cell-list builds; a brute-force build of a small
+  // system costs less than the check)
+  const bool skin = pot->skin_on && pot->skin > 0.0 && S->tj == 8 && S->yi_reg && !snap_generic_forced() &&
+                    N >= 512;
+  D.lists_exact = skin ? 0 : 1;
+  buf.lists_exact = !skin;
+  const int* go = nullptr;
+  double* qref = nullptr;
+  if (skin) {
+    PL_TRY(pot->work[4].reserve(sizeof(double) * 3 * na + 64));
+    qref = (double*)pot->work[4].ptr;
+    int* flag = (int*)(qref + 3 * na);
+    if (pot->skin_force || pot->skin_B != B) {
+      PL_CUDA(cudaMemcpyAsync(qref, q, sizeof(double) * 3 * na, cudaMemcpyDeviceToDevice, ctx->stream));
+      pot->skin_force = false;
+      pot->skin_B = B;
+    } else {
+      PL_TRY(skin_check(pot, na, q, qref, flag));
+      go = flag;
+    }
+  }
+  PL_TRY(build_neighbours(pot, B, q, pot->rcut + (skin ? pot->skin : 0.0), SNAP_MAXN, &nl, go));
+  if (go) PL_TRY(skin_ref(pot, na, q, qref, go));
   // + 25 x na doubles: per-row energies of the split Y kernel (small batches)
   // + na x nhalf C2: Y^dagger of the pair-symmetric force kernel
   size_t bytes = sizeof(C2) * 3 * na * S->nhalf + sizeof(double) * na * (1 + 3 * SNAP_MAXN + 6 + 25);
@@ -2225,7 +2286,8 @@ int compute_snap(pl_pot* pot, int64_t B, const double* q, double* energy, double
   prof_mark(ctx->stream, ST_GATHER, true);
   if (buf.pair)
     PL_CUDA(launch_pdl(k_snap_gather_pair_w, dim3((unsigned)((na * 32 + 127) / 128)), dim3(128), 0, ctx->stream, na,
-                       N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr));
+                       N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr,
+                       pot->rcut * pot->rcut, buf.lists_exact ? 1 : 0));
   else
     k_snap_gather<<<(unsigned)((na + 127) / 128), 128, 0, ctx->stream>>>(
         na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.dedr, grad, virial ? buf.vatom : nullptr);

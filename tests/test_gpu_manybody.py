@@ -520,3 +520,27 @@ def test_many_body_blow_up_substep_matches_oracle(pl, kind):
         with pytest.raises(pl.BlowUpError) as ei:
             pl.propagate_windows(states, pot, params, sched, [seed, seed], noise=np.stack([noise, noise]))
         assert ei.value.substep == oe.value.substep
+
+
+@pytest.mark.parametrize("ncell,W", [(4, 3), (8, 2)])
+def test_verlet_skin_lists_are_bitwise_neutral(pl, monkeypatch, ncell, W):
+    """SNAP windows keep Verlet-skin neighbour lists (rcut + 0.3 A, rebuilt on the
+    device when an atom moved more than half the skin); every SNAP kernel compacts
+    the exact pairs in list order, so trajectories equal the exact-list ones bit for
+    bit (PL_SNAP_SKIN=0), for brute-force (129 atoms) and cell lists (1025 atoms)."""
+    from paper_2212_10508_b200 import tungsten as W_
+    q0, box = W_.bcc_sia(ncell)
+    n = q0.shape[0] // 3
+    L = 40
+    params = pl.LangevinParams(1.0, W_.KB * 1500.0, 0.001, L, mass=np.full(3 * n, W_.MASS_W))
+    sched = pl.TemperatureSchedule.robust(L)
+    states = [pl.PhaseState(q=q0, p=W_.maxwell_boltzmann(n, 1500.0, s)) for s in range(1, W + 1)]
+    seeds = [pl.derive_seed(21, s) for s in range(1, W + 1)]
+    out = {}
+    for skin in ("0", "0.3"):
+        monkeypatch.setenv("PL_SNAP_SKIN", skin)
+        pot = W_.make_snap(n, box)
+        out[skin] = pl.propagate_windows(states, pot, params, sched, seeds)
+    for a, b in zip(out["0"], out["0.3"]):
+        assert a.q.tobytes() == b.q.tobytes()
+        assert a.p.tobytes() == b.p.tobytes()
