@@ -103,14 +103,36 @@ __host__ __device__ inline size_t cl_smem_bytes(int n, int own, int cache = 0) {
          sizeof(int32_t) * ((size_t)own * CL_MAXC + own + (size_t)own * CL_MAXN + own) + 64;
 }
 
+// Distributed shared memory through its own state space: mapa gives the peer's
+// shared::cluster address, st.shared::cluster writes it, and the cluster barrier
+// (release / acquire at cluster scope) orders those stores.  Generic pointers from
+// map_shared_rank made every exchange a generic store and the barrier a
+// GPU-scope membar (MEMBAR.ALL.GPU + ERRBAR in the SASS).
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_st(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// own slice [c0, c0 + cnt) of a shared array -> the same range of every peer:
+// one (peer, element) item per thread, so only threads with work run
+__device__ __forceinline__ void dsmem_push(const double* arr, int c0, int cnt, int C) {
+  for (int t = threadIdx.x; t < C * cnt; t += blockDim.x) {
+    const int pr = t / cnt, k = t - pr * cnt;
+    dsmem_st(dsmem_addr(arr + c0 + k, pr), arr[c0 + k]);
+  }
+}
+
 // fixed-order sum of one double per CTA over the cluster: every CTA pushes its
 // value to slot [rank] of every peer, then sums slots 0..C-1
 __device__ __forceinline__ double cluster_sum(cg::cluster_group& cl, double v, double* slots, int C, int rank) {
-  if (threadIdx.x < (unsigned)C) {
-    double* peer = cl.map_shared_rank(slots, (int)threadIdx.x);
-    peer[rank] = v;
-  }
-  cl.sync();
+  if (threadIdx.x < (unsigned)C) dsmem_st(dsmem_addr(slots + rank, (int)threadIdx.x), v);
+  cluster_barrier();
   double s = 0.0;
   for (int r = 0; r < C; ++r) s += slots[r];
   return s;
@@ -168,12 +190,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
   // so one cluster barrier per position exchange suffices
   double* q = M.q;
   double* qn = M.q2;
-  auto push_q_slice = [&]() {  // own positions -> every peer's current buffer
-    for (int pr = 0; pr < C; ++pr) {
-      double* dst = cl.map_shared_rank(q, pr);
-      for (int t = threadIdx.x; t < dn; t += blockDim.x) dst[c0 + t] = q[c0 + t];
-    }
-  };
+  auto push_q_slice = [&]() { dsmem_push(q, c0, dn, C); };  // own positions -> every peer's current buffer
 
   // ---------------------------------------------------------------- force
   auto eam_force = [&](bool any) {
@@ -282,11 +299,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
       }
     }
     __syncthreads();
-    for (int pr = 0; pr < C; ++pr) {  // own F' -> every peer
-      double* dst = cl.map_shared_rank(M.fp, pr);
-      for (int t = threadIdx.x; t < nown; t += blockDim.x) dst[a0 + t] = M.fp[a0 + t];
-    }
-    cl.sync();
+    dsmem_push(M.fp, a0, nown, C);  // own F' -> every peer
+    cluster_barrier();
     // force pass (eam_force_part semantics with cached r)
     for (int base = 0; base < nown; base += groups) {
       const int i = base + gi0;
@@ -376,8 +390,8 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
       }
       moved = __syncthreads_or(moved);
       push_q_slice();
-      if (threadIdx.x < (unsigned)C) cl.map_shared_rank(slots_c, (int)threadIdx.x)[rank] = moved ? 1.0 : 0.0;
-      cl.sync();
+      if (threadIdx.x < (unsigned)C) dsmem_st(dsmem_addr(slots_c + rank, (int)threadIdx.x), moved ? 1.0 : 0.0);
+      cluster_barrier();
       bool any = false;
       for (int rr_ = 0; rr_ < C; ++rr_) any = any || slots_c[rr_] > 0.0;
       eam_force(any);
@@ -403,10 +417,9 @@ __global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_co
       const double f = cluster_sum(cl, 0.0, slots_b, C, rank);  // barrier only
       (void)f;
       if (threadIdx.x < (unsigned)C) {
-        double* peer = cl.map_shared_rank(slots_a, (int)threadIdx.x);
-        peer[rank] = (double)s_fail;
+        dsmem_st(dsmem_addr(slots_a + rank, (int)threadIdx.x), (double)s_fail);
       }
-      cl.sync();
+      cluster_barrier();
       int mn = 0;
       for (int rr = 0; rr < C; ++rr) {
         const int v = (int)slots_a[rr];
