@@ -18,6 +18,8 @@
 #include <cooperative_groups.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 
 #include "eam.cuh"
 #include "neigh.cuh"
@@ -138,7 +140,13 @@ __device__ __forceinline__ double cluster_sum(cg::cluster_group& cl, double v, d
   return s;
 }
 
-__global__ void __launch_bounds__(CL_THREADS, 1) k_sweep_cluster(const __grid_constant__ ClArgs A) {
+// MAXT: launch bound of the instantiation.  The CTA runs only the threads its
+// atoms use (own x tpa, rounded to warps): the lane partition (tpa) is the
+// 1024-thread rule shared with the batched EAM kernels, and the per-CTA error
+// sums see the same per-thread terms (at most one component per thread) plus
+// zeros, so every result is bitwise that of a 1024-thread CTA
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_sweep_cluster(const __grid_constant__ ClArgs A) {
   extern __shared__ double sm[];
   __shared__ double red[33];
   __shared__ double slots_a[16], slots_b[16], slots_c[16];
@@ -571,12 +579,19 @@ int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N
   PL_CUDA(cudaMemcpyAsync(inc, h_inc, sizeof(int32_t) * R_act, cudaMemcpyHostToDevice, st));
   static std::atomic<uint64_t> attr_devs{0};
   if (first_on_device(attr_devs)) {
-    cudaFuncSetAttribute(k_sweep_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_sweep_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_sweep_cluster<CL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_sweep_cluster<CL_THREADS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_sweep_cluster<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_sweep_cluster<640>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(C * R_act));
-  cfg.blockDim = dim3(CL_THREADS);
+  // threads the atoms use (and >= the own components, so every thread holds at
+  // most one component in the error sums, as with 1024 threads)
+  int threads = std::max(own * tpa, 3 * own);
+  threads = std::min(CL_THREADS, (threads + 31) / 32 * 32);
+  if (getenv("PL_SWEEP_FULL")) threads = CL_THREADS;
+  cfg.blockDim = dim3((unsigned)threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -586,7 +601,10 @@ int sweep_cluster_batch(pl_ctx* ctx, pl_pot* coarse, int64_t d, int L, int64_t N
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  PL_CUDA(cudaLaunchKernelEx(&cfg, k_sweep_cluster, A));
+  if (threads <= 640)
+    PL_CUDA(cudaLaunchKernelEx(&cfg, k_sweep_cluster<640>, A));
+  else
+    PL_CUDA(cudaLaunchKernelEx(&cfg, k_sweep_cluster<CL_THREADS>, A));
   int hovf = 0;
   PL_CUDA(cudaMemcpyAsync(h_state, acc, sizeof(double) * 2 * R_act, cudaMemcpyDeviceToHost, st));
   PL_CUDA(cudaMemcpyAsync(h_out4, out, sizeof(int64_t) * 4 * R_act, cudaMemcpyDeviceToHost, st));

@@ -389,6 +389,28 @@ def test_speculative_pipeline_is_bitwise_neutral(pl, monkeypatch):
     assert spec["fine_windows_propagated"] < plain["fine_windows_propagated"]
 
 
+@pytest.mark.parametrize("ncell", [4, 8])
+def test_cluster_sweep_thread_count_is_bitwise_neutral(pl, monkeypatch, ncell):
+    """The cluster sweep runs only the threads its atoms use; with the full
+    1024-thread CTAs (PL_SWEEP_FULL=1) every node, slab record and error value is
+    the same bit for bit (129 atoms: 8 CTAs x 17 atoms; 1025 atoms: 16 x 65)."""
+    from paper_2212_10508_b200 import tungsten as W
+    q0, box = W.bcc_sia(ncell)
+    n = q0.shape[0] // 3
+    L, N = 10, 6
+    params = pl.LangevinParams(1.0, W.KB * 1000.0, 0.001, L, mass=np.full(3 * n, W.MASS_W))
+    sched = pl.TemperatureSchedule.robust(L)
+    init = pl.PhaseState(q=q0, p=W.maxwell_boltzmann(n, 1000.0, 3))
+    pair = pl.PropagatorPair(W.make_snap(n, box), W.make_eam(n, box), 100.0, 1.0)
+    plan = pl.NoisePlan.for_windows(17, N)
+    cfg = pl.PararealConfig(N, 1e-10, 0.35)
+    a = pl.parareal_adaptive(init, pair, params, sched, plan, cfg)
+    monkeypatch.setenv("PL_SWEEP_FULL", "1")
+    b = pl.parareal_adaptive(init, pair, params, sched, plan, cfg)
+    assert a.slabs == b.slabs and a.error_history == b.error_history
+    assert a.trajectory.positions().tobytes() == b.trajectory.positions().tobytes()
+
+
 def test_degenerate_pair_converges_in_one_iteration(pl):
     """coarse == fine: jumps are exactly zero, k_conv = 1 (acceptance criterion 5)."""
     from paper_2212_10508_b200 import tungsten as W
