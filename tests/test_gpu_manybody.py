@@ -211,15 +211,17 @@ def test_snap_specialised_matches_general_kernels(pl, tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    for mode, env_add in (("gen", {"PL_SNAP_GENERIC": "1"}), ("pair", {"PL_SNAP_PAIR_RUN": "0"}),
-                          ("run", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "0"}),
-                          ("tm", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "1"})):
+    for mode, env_add in (("gen", {"PL_SNAP_GENERIC": "1"}),
+                          ("pair", {"PL_SNAP_PAIR_RUN": "0", "PL_SNAP_TMEM": "0"}),   # k_snap_deidrj_pair
+                          ("tm2", {"PL_SNAP_PAIR_RUN": "0", "PL_SNAP_TMEM": "1"}),    # k_snap_deidrj_tm<2>
+                          ("run", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "0"}),    # k_snap_deidrj_run<8>
+                          ("tm", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "1"})):    # k_snap_deidrj_tm<8>
         f = str(tmp_path / f"ab_{mode}.npz")
         env = dict(os.environ, **env_add)
         subprocess.run([sys.executable, "-c", _AB_SCRIPT, f], cwd=root, env=env, check=True)
         out[mode] = np.load(f)
     a = out["gen"]
-    for m in ("pair", "run", "tm"):
+    for m in ("pair", "tm2", "run", "tm"):
         b = out[m]
         np.testing.assert_allclose(b["E"], a["E"], rtol=1e-12)
         np.testing.assert_allclose(b["G"], a["G"], rtol=1e-12, atol=1e-12 * np.abs(a["G"]).max())
@@ -230,6 +232,8 @@ def test_snap_specialised_matches_general_kernels(pl, tmp_path):
     # history in tensor memory + staged Y_k^dagger: the same arithmetic, bit for bit
     np.testing.assert_array_equal(out["tm"]["G"], out["run"]["G"])
     np.testing.assert_array_equal(out["tm"]["V"], out["run"]["V"])
+    np.testing.assert_array_equal(out["tm2"]["G"], out["pair"]["G"])
+    np.testing.assert_array_equal(out["tm2"]["V"], out["pair"]["V"])
 
 
 @pytest.mark.parametrize("twojmax", [2, 4, 6])
