@@ -252,6 +252,19 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+      // the block this SM most likely runs next (one CTA per SM, blocks dispatched in
+      // order): its U_tot towards L2 while this block computes
+      const int64_t nxt = blk + 148;
+#ifndef PL_NO_YI_PF
+      if (S == 1 && nxt * yib::ATOMS < natoms) {
+#else
+      if (false) {
+#endif
+        const int64_t nn = min((int64_t)yib::ATOMS, natoms - nxt * yib::ATOMS);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(utot + nxt * yib::ATOMS * yib::NHALF),
+                     "r"((unsigned)(sizeof(Cx) * yib::NHALF * nn))
+                     : "memory");
+      }
       const unsigned bytes = (unsigned)(sizeof(Cx) * yib::NHALF * na_blk);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
       asm volatile(
