@@ -16,6 +16,16 @@ namespace pl {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 
+// Device-side bounds checks (build.py --variant checks -DPL_CHECKS): the index
+// and capacity invariants of the hot kernels, trapping on violation.  The
+// compute-sanitizer stand-in on a pool where it is closed.
+#ifdef PL_CHECKS
+#include <cassert>
+#define PL_DASSERT(cond) assert(cond)
+#else
+#define PL_DASSERT(cond) ((void)0)
+#endif
+
 #define PL_CUDA(call)                                                              \
   do {                                                                             \
     cudaError_t _e = (call);                                                       \

@@ -998,6 +998,7 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
     if (keep) {
       PairGeom pg;
       pair_geom(D, dx, dy, dz, pg, false);
+      PL_DASSERT(n + __popc(bal & ((1u << lane) - 1u)) < SNAP_MAXN);
       double* o = geo + 5 * (n + __popc(bal & ((1u << lane) - 1u)));
       o[0] = pg.a.re; o[1] = pg.a.im; o[2] = pg.b.re; o[3] = pg.b.im; o[4] = pg.fc;
     }
@@ -1571,6 +1572,7 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
         const bool own = t0 + lane < n && pair_owned(i, kk) &&
                          (D.lists_exact || pair_exact(q + (a / N) * (int64_t)N * 3, i, kk, box, D.rcut * D.rcut));
         const unsigned bal = __ballot_sync(0xffffffffu, own);
+        PL_DASSERT(!own || (tot - base_c) + __popc(bal & ((1u << lane) - 1u)) < SNAP_MAXN);
         if (own) oslot[c * SNAP_MAXN + (tot - base_c) + __popc(bal & ((1u << lane) - 1u))] = (int16_t)(t0 + lane);
         tot += __popc(bal);
       }
@@ -1653,6 +1655,7 @@ k_snap_deidrj_run(SnapDev D, int64_t natoms, int N, Box box, const double* __res
     const bool valid = pp < end;
     const int c = (valid && pp >= cum[ca + 1]) ? ca + 1 : ca;
     const int64_t atom = a0 + c;
+    PL_DASSERT(!valid || (c < CH && pp - cum[c] < SNAP_MAXN));
     const int s = valid ? oslot[c * SNAP_MAXN + (pp - cum[c])] : 0;
     const double* go = gb + (valid ? pp - gbase : 0) * PAIR_GEO;
     const int64_t katom = valid ? gk[pp - gbase] : atom;  // invalid slots: own Y^dagger (weight 0)
@@ -1779,6 +1782,7 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
         const bool own = t0 + lane < n && pair_owned(i, kk) &&
                          (D.lists_exact || pair_exact(q + (a / N) * (int64_t)N * 3, i, kk, box, D.rcut * D.rcut));
         const unsigned bal = __ballot_sync(0xffffffffu, own);
+        PL_DASSERT(!own || (tot - base_c) + __popc(bal & ((1u << lane) - 1u)) < SNAP_MAXN);
         if (own) oslot[c * SNAP_MAXN + (tot - base_c) + __popc(bal & ((1u << lane) - 1u))] = (int16_t)(t0 + lane);
         tot += __popc(bal);
       }
@@ -1868,6 +1872,7 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
                      "r"((unsigned)(nv * nh * sizeof(C2)))
                      : "memory");
       __syncwarp();
+      PL_DASSERT(nv >= 1 && nv <= P && pos + nv - 1 - gbase < GB);
       if (lane < nv)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -1879,6 +1884,7 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
     const bool valid = pp < end;
     const int c = (valid && pp >= cum[ca + 1]) ? ca + 1 : ca;
     const int64_t atom = a0 + c;
+    PL_DASSERT(!valid || (c < CH && pp - cum[c] < SNAP_MAXN));
     const int s = valid ? oslot[c * SNAP_MAXN + (pp - cum[c])] : 0;
     const double* go = gb + (valid ? pp - gbase : 0) * PAIR_GEO;
     const int64_t katom = valid ? gk[pp - gbase] : atom;  // invalid slots: own Y^dagger (weight 0)
@@ -1972,7 +1978,10 @@ k_snap_gather_pair_w(int64_t natoms, int N, Box box, const double* __restrict__ 
     const int s = s0 + lane;
     const bool keep = s < nl && (lists_exact || pair_exact(qb, a, nb[s], box, rc2));
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (keep) s_slot[wib][n + __popc(bal & ((1u << lane) - 1u))] = (int16_t)s;
+    if (keep) {
+      PL_DASSERT(n + __popc(bal & ((1u << lane) - 1u)) < SNAP_MAXN);
+      s_slot[wib][n + __popc(bal & ((1u << lane) - 1u))] = (int16_t)s;
+    }
     n += __popc(bal);
   }
   __syncwarp();

@@ -36,6 +36,13 @@
 #include <utility>
 #include <vector>
 
+#ifdef PL_CHECKS
+#include <cassert>
+#define PL_DASSERT(cond) assert(cond)
+#else
+#define PL_DASSERT(cond) ((void)0)
+#endif
+
 namespace pl {
 
 double snap_clebsch(int j1, int m1, int j2, int m2, int J, int M);  // snap.cu
@@ -297,8 +304,10 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
     const long long t_ph = clock64();
 #endif
     for (int it = c_p_iseg[V][ph][vw]; it < c_p_iseg[V][ph][vw + 1]; ++it) {
+      PL_DASSERT(it < P_MAX_ITEMS);
       const int4 item = c_p_items[V][it];  // one constant load per item (host-decoded)
       const int tid = item.x;
+      PL_DASSERT(tid < yib::NT && item.y >= 0 && item.y < yib::NHALF);
       PItem A;
       A.Ul = Uf + lane;
       A.yrow = Ys + item.y * yib::ATOMS + lane;

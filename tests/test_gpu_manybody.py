@@ -280,6 +280,24 @@ def test_snap_deterministic_rerun(pl):
     assert a.tobytes() == b.tobytes()
 
 
+@pytest.mark.parametrize("ncell,B", [(4, 150), (8, 24)])
+def test_snap_repeated_evaluations_are_bitwise_stable(pl, ncell, B):
+    """Race detector stand-in (compute-sanitizer is closed on this pool): ten
+    evaluations of a production-size batch (150 x 129 atoms: non-split Y kernel,
+    TMEM run force kernel; 24 x 1025 atoms: cell lists) interleaved with other
+    batch shapes must give the same bits every time.  A missing barrier, a ring
+    or staging buffer overwritten early, or a TMEM/mbarrier ordering bug would
+    show up as run-to-run differences."""
+    from paper_2212_10508_b200 import tungsten as W
+    Q, box = _configs(ncell, B, seed=29)
+    pot = W.make_snap(Q.shape[1] // 3, box)
+    ref = [x.cpu().numpy().tobytes() for x in pot.evaluate(Q, True, True, True)]
+    for r in range(9):
+        pot.evaluate(Q[: 1 + r % 3], True, True, True)  # other shapes in between (buffers reused)
+        out = [x.cpu().numpy().tobytes() for x in pot.evaluate(Q, True, True, True)]
+        assert out == ref, f"repeat {r} differs"
+
+
 def test_snap_window_vs_oracle(pl):
     """20 BBK substeps of SNAP W+SIA at 1000 K: device vs oracle integrator + C SNAP."""
     from oracle import integrator as oint, native, rng as orng
