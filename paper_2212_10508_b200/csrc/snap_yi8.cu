@@ -118,10 +118,12 @@ __constant__ int c_box_code[yib::NT];  // X*100 + Y*10 + J
 // compiled variants: (warps per CTA, CTAs per 32-atom block).  A block's rows
 // are split over S CTAs when the batch has fewer blocks than SMs (latency of
 // small systems); a row stays with one CTA for the whole kernel.
-constexpr int P_NV = 2;
-constexpr int P_NW[P_NV] = {8, 8};   // 2 warps per SMSP, 255 registers (12 warps: 168, measured slower)
-constexpr int P_NS[P_NV] = {1, 2};
-constexpr int P_MAX_VW = 24;
+// (warps, CTAs per block): 1 CTA per block for large batches; a block's rows split
+// over 2 CTAs below 148 blocks, over 4 below 37 (one CTA per SM either way)
+constexpr int P_NV = 3;
+constexpr int P_NW[P_NV] = {8, 8, 8};   // 2 warps per SMSP, 255 registers (12 warps: 168, measured slower)
+constexpr int P_NS[P_NV] = {1, 2, 4};
+constexpr int P_MAX_VW = 32;
 constexpr int P_MAX_ITEMS = 400;  // (row, triple) items: 375 at twojmax 8
 __constant__ int c_p_iseg[P_NV][yib::NPH][P_MAX_VW + 1];  // items of virtual warp w in phase p
 // per item, decoded on the host: {tid, Y-row offset (elements), lo | hi << 8 | mb << 16 | mid << 24 | swap << 25, 0}
@@ -683,6 +685,12 @@ cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const
                             const void* utot, void* ylist, double* eatom, double* erow_g) {
   const int64_t blocks = (natoms + yib::ATOMS - 1) / yib::ATOMS;
   const bool split = blocks < 148 && erow_g;
+  static const int max_split = [] {  // PL_YI_SPLIT_MAX=2: no 4-way split (A/B)
+    const char* e = getenv("PL_YI_SPLIT_MAX");
+    return e ? atoi(e) : 4;
+  }();
+  if (split && max_split >= 4 && 4 * blocks <= 148)
+    return p_launch<8, 2, 4>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g);
   return split ? p_launch<8, 1, 2>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g)
                : p_launch<8, 0, 1>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g);
 }
