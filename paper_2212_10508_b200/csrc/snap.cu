@@ -918,19 +918,19 @@ __device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g
 // store per element into its pair slot, then a fixed-order sum over 8 slots.
 constexpr int UI4_WARPS = 4;
 
+// Row 4 of layer 8 is born from row 3 of layer 7, which the row-3 lane parks in
+// shared memory (sv: [8][pair slot], its own 8 slots) while its u registers
+// advance row 3 to layer 8; the same registers then carry row 4 (no second row
+// array: 18 fewer live doubles, no spills).
 template <int J>
-__device__ __forceinline__ void ui4_layers(C2 (&u)[9], C2 (&u4)[9], const RowGeom<8>& g, int mb, bool on,
-                                           double fc, C2 (&acc)[45], C2* row4) {
+__device__ __forceinline__ void ui4_layers(C2 (&u)[9], const RowGeom<8>& g, int mb, bool on, double fc,
+                                           C2 (&acc)[45], C2* row4, C2* sv) {
   if constexpr (J > 0) {
-    ui4_layers<J - 1>(u, u4, g, mb, on, fc, acc, row4);
+    ui4_layers<J - 1>(u, g, mb, on, fc, acc, row4, sv);
     if constexpr (J == 8) {
+      if (mb == 3)
 #pragma unroll
-      for (int i = 0; i < J; ++i) {
-        const int x = J - 1 - i;
-        const C2 v = u[i];
-        u4[x] = ((x + J / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
-      }
-      u4[J] = C2{0.0, 0.0};
+        for (int i = 0; i < J; ++i) sv[i * 8] = u[i];
     }
     row_step<8, J>(u, g, mb);
     if (on && 2 * mb <= J) {
@@ -942,12 +942,21 @@ __device__ __forceinline__ void ui4_layers(C2 (&u)[9], C2 (&u4)[9], const RowGeo
       }
     }
     if constexpr (J == 8) {
-      row_update<8, 8>(u4, g);
+      if (mb == 3) {
+#pragma unroll
+        for (int i = 0; i < J; ++i) {
+          const int x = J - 1 - i;
+          const C2 v = sv[i * 8];
+          u[x] = ((x + J / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+        }
+        u[J] = C2{0.0, 0.0};
+      }
+      row_update<8, 8>(u, g);
       if (on && mb == 3) {  // row 4 accumulates in the lane's own slot (shared memory)
 #pragma unroll
         for (int ma = 0; ma <= 8; ++ma) {
-          row4[ma].re = fma(fc, u4[ma].re, row4[ma].re);
-          row4[ma].im = fma(fc, u4[ma].im, row4[ma].im);
+          row4[ma].re = fma(fc, u[ma].re, row4[ma].re);
+          row4[ma].im = fma(fc, u[ma].im, row4[ma].im);
         }
       }
     }
@@ -967,6 +976,9 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   // per-pair (a, b, fc) of the whole list, one lane per pair (instead of the 4 row
   // lanes of a slot recomputing it every round)
   double* geo = reinterpret_cast<double*>(reinterpret_cast<C2*>(smem) + UI4_WARPS * P * ps) + warp * SNAP_MAXN * 5;
+  C2* sv = reinterpret_cast<C2*>(reinterpret_cast<double*>(reinterpret_cast<C2*>(smem) + UI4_WARPS * P * ps) +
+                                 UI4_WARPS * SNAP_MAXN * 5) +
+           warp * 8 * P + lane / 4;  // row-3 lanes: layer 7 parked for the row-4 birth
   const int64_t atom = (int64_t)blockIdx.x * UI4_WARPS + warp;
   if (atom >= natoms) return;
   const int64_t b = atom / N;
@@ -1019,12 +1031,12 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
       g.a = C2{1.0, 0.0};
       g.b = C2{0.0, 0.0};
     }
-    C2 u[TJ + 1], u4[TJ + 1];
+    C2 u[TJ + 1];
 #pragma unroll
-    for (int k = 0; k <= TJ; ++k) u[k] = u4[k] = C2{0.0, 0.0};
+    for (int k = 0; k <= TJ; ++k) u[k] = C2{0.0, 0.0};
     u[0] = C2{mb == 0 ? 1.0 : 0.0, 0.0};
     if (valid && mb == 0) acc[0].re += fc;  // J = 0
-    ui4_layers<TJ>(u, u4, g, mb, valid, fc, acc, row4);
+    ui4_layers<TJ>(u, g, mb, valid, fc, acc, row4, sv);
   }
   {  // each lane owns its (pair slot, rows): plain stores (every element of every slot is written)
     C2* mypart = part + p * ps;
@@ -2211,7 +2223,8 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   const bool special = S->tj == 8 && S->yi_reg && !snap_generic_forced();
   prof_mark(ctx->stream, ST_UI, true);
   if (special) {
-    const size_t sm4 = sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2) + sizeof(double) * UI4_WARPS * SNAP_MAXN * 5;
+    const size_t sm4 = sizeof(C2) * UI4_WARPS * 8 * (D.nhalf + 2) + sizeof(double) * UI4_WARPS * SNAP_MAXN * 5 +
+                       sizeof(C2) * UI4_WARPS * 8 * 8;
     PL_CUDA(launch_pdl(k_snap_ui_r4, dim3((unsigned)((na + UI4_WARPS - 1) / UI4_WARPS)), dim3(UI4_WARPS * 32), sm4,
                        ctx->stream, D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.utot));
   } else {
