@@ -878,7 +878,9 @@ __device__ __forceinline__ C2 vstep(const C2& a, const C2& b, const C2& u, const
 // even J the middle row mb = J/2 is born from row J/2-1 of layer J-1 (lane - 1)
 template <int TJ, int J>
 __device__ __forceinline__ void row_step(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb) {
-  if (J % 2 == 0) {
+  // (the callers run 4 lanes per pair, mb <= 3 = TJ/2 - 1: no lane is born at J = TJ, the
+  // row-3 lane builds row TJ/2 itself, so the layer-TJ shuffles would be dead work)
+  if (J % 2 == 0 && J < TJ) {
     // lane mb = J/2 receives row J/2-1 of layer J-1 from lane-1 (all lanes shuffle)
 #pragma unroll
     for (int i = 0; i < J; ++i) {
@@ -1123,21 +1125,42 @@ struct HistSmem {
   __device__ __forceinline__ void sync() const {}
 };
 
+// A complex as two .x2 stores: a double already sits in an aligned register pair, so
+// no operand moves (the .x4 form needs 4 consecutive registers and cost ~150 MOVs per
+// round; the kernel is bound by instruction fetch, so every instruction counts).
 __device__ __forceinline__ void tm_st(uint32_t addr, const C2& v) {
+#ifndef PL_TM_ST4
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(__double2loint(v.re)),
+               "r"(__double2hiint(v.re))
+               : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr + 2u), "r"(__double2loint(v.im)),
+               "r"(__double2hiint(v.im))
+               : "memory");
+#else
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
                "r"(__double2loint(v.re)), "r"(__double2hiint(v.re)), "r"(__double2loint(v.im)),
                "r"(__double2hiint(v.im))
                : "memory");
+#endif
 }
-__device__ __forceinline__ C2 tm_ld(uint32_t addr) {
+// issue one load (no wait): the registers are valid only after tm_ld_wait + tm_ld_tie
+struct TmRaw {
   uint32_t a, b, c, d;
+};
+__device__ __forceinline__ TmRaw tm_ld_issue(uint32_t addr) {
+  TmRaw r;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "=r"(r.a), "=r"(r.b), "=r"(r.c), "=r"(r.d)
                : "r"(addr)
                : "memory");
-  // the registers are valid only after wait::ld: tie them to it
-  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a), "+r"(b), "+r"(c), "+r"(d)::"memory");
-  return C2{__hiloint2double((int)b, (int)a), __hiloint2double((int)d, (int)c)};
+  return r;
+}
+__device__ __forceinline__ void tm_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// orders every use of the loaded registers after the wait (volatile statements keep
+// their order; no instruction is emitted)
+__device__ __forceinline__ C2 tm_ld_tie(TmRaw r) {
+  asm volatile("" : "+r"(r.a), "+r"(r.b), "+r"(r.c), "+r"(r.d)::"memory");
+  return C2{__hiloint2double((int)r.b, (int)r.a), __hiloint2double((int)r.d, (int)r.c)};
 }
 
 struct HistTmem {
@@ -1148,7 +1171,16 @@ struct HistTmem {
 #pragma unroll
     for (int ma = 0; ma <= J; ++ma) tm_st(taddr + 4u * (J * (J + 1) / 2 + ma), u[ma]);
   }
-  __device__ __forceinline__ C2 at(int slot) const { return tm_ld(taddr + 4u * slot); }
+  // the lane's row of layer J - 1 (J elements): all loads in flight, one wait
+  template <int J>
+  __device__ __forceinline__ void row(C2 (&L)[9]) const {
+    TmRaw r[J];
+#pragma unroll
+    for (int x = 0; x < J; ++x) r[x] = tm_ld_issue(taddr + 4u * ((J - 1) * J / 2 + x));
+    tm_ld_wait();
+#pragma unroll
+    for (int x = 0; x < J; ++x) L[x] = tm_ld_tie(r[x]);
+  }
   __device__ __forceinline__ void sync() const { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 };
 
@@ -1235,14 +1267,14 @@ struct AdjR4 {
         // every lane loads its own row of layer J-1; born rows take the image of
         // the lane below (row J/2-1 of layer J-1) by a shuffle
         C2 L[TJ + 1];
-#pragma unroll
-        for (int x = 0; x < J; ++x) L[x] = hist.at((J - 1) * J / 2 + x);
+        hist.template row<J>(L);
 #pragma unroll
         for (int x = 0; x < J; ++x) {
           up[x] = L[x];
           if constexpr (J % 2 == 0 && J < TJ) {
             const C2 v = shfl_up_c2(L[J - 1 - x], 1);
-            if (born) up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+            // born: mb = J/2, so the parity (x + mb) & 1 is a compile-time constant
+            if (born) up[x] = ((x + J / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
           }
         }
         if (active) row_adj<J>(G, up, g, Sa, Sb);
@@ -1253,7 +1285,7 @@ struct AdjR4 {
             up[x] = hist.at((J - 1) * J / 2 + x, 0);
           } else {
             const C2 v = hist.at((J - 1) * J / 2 + (J - 1 - x), -1);
-            up[x] = ((x + mb) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
+            up[x] = ((x + J / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};  // born: mb = J/2
           }
         }
         row_adj<J>(G, up, g, Sa, Sb);
@@ -1289,7 +1321,8 @@ struct AdjR4 {
           const C2 v = C2{__shfl_down_sync(0xffffffffu, G[x].re, 1), __shfl_down_sync(0xffffffffu, G[x].im, 1)};
           if (2 * (mb + 1) == J) {
             const int xs = J - 1 - x;
-            const bool neg = ((x + mb + 1) & 1) != 0;
+            constexpr int MBB = J / 2;  // = mb + 1 on the receiving lane: compile-time parity
+            const bool neg = ((x + MBB) & 1) != 0;
             G[xs].re += neg ? -v.re : v.re;
             G[xs].im += neg ? v.im : -v.im;
           }
