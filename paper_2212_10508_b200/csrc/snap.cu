@@ -1795,10 +1795,12 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
                  warp * (CH + 2);
   __shared__ __align__(8) uint64_t s_mbar[NWB];
   __shared__ uint32_t s_tmem;
-  // tensor memory: 256 columns per CTA (2 CTAs per SM), warp w uses lanes 32w..32w+31
+  // tensor memory: 256 columns per 4 warps (2 CTAs of 4 warps per SM, or one of 8), warp w
+  // uses the lanes of its sub-partition (w % 4) and the column half w / 4
+  constexpr unsigned TCOLS = NWB > 4 ? 512u : 256u;
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(&s_tmem))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&s_tmem)), "n"(TCOLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -1810,7 +1812,7 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const HistTmem hist{s_tmem + ((uint32_t)(32 * warp) << 16)};
+  const HistTmem hist{s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2)};
   unsigned phase = 0;
   const int64_t a0 = ((int64_t)blockIdx.x * NWB + warp) * CH;
   const int nrun = (int)max((int64_t)0, min((int64_t)CH, natoms - a0));
@@ -1995,7 +1997,7 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem) : "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(TCOLS) : "memory");
 }
 
 // gather of the pair form, one warp per atom (lanes over neighbour slots, the
@@ -2251,6 +2253,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     cudaFuncSetAttribute(k_snap_deidrj_run<8, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_tm<8, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_snap_deidrj_tm<2, PAIR_WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_snap_deidrj_tm<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
     cudaFuncSetAttribute(k_snap_ui_r4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
   const bool special = S->tj == 8 && S->yi_reg && !snap_generic_forced();
@@ -2291,13 +2294,27 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
       return !(e && e[0] == '0');
     }();
     const bool big = prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4);  // >= 4 waves of runs
-    auto tm_smem = [&](int ch) {
+    auto tm_smem = [&](int ch, int nwb = PAIR_WARPS) {
       constexpr int GB = 16;
-      return sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + 8 * D.nhalf) +
-             (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * GB +
-             sizeof(int16_t) * PAIR_WARPS * ch * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (ch + 2);
+      return sizeof(C2) * nwb * (2 * D.nhalf + 8 * D.nhalf) + (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * nwb * GB +
+             sizeof(int16_t) * nwb * ch * SNAP_MAXN + sizeof(int32_t) * nwb * (ch + 2);
     };
-    if (tmem && big) {
+    // large batches: one CTA of 8 warps per SM instead of two of 4.  The round's code
+    // (~75 KB) exceeds the SM's 32 KB instruction cache and the kernel is bound by
+    // instruction fetches from the GPC-level cache (ncu: gcc instruction requests 91 % of
+    // peak); 8 warps launched together walk the code closer to each other and share more
+    // of the fetched lines: 0.912 -> 0.868 ms at the larger config.  (A barrier per round,
+    // full lockstep, costs more than it saves: 0.94 ms.)  PL_SNAP_TM8=0: 4-warp CTAs.
+    static const bool tm8 = [] {
+      const char* e = getenv("PL_SNAP_TM8");
+      return !(e && e[0] == '0');
+    }();
+    if (tmem && big && tm8) {
+      constexpr int NWB8 = 8;
+      const unsigned grid = (unsigned)((na + NWB8 * RUN - 1) / (NWB8 * RUN));
+      PL_CUDA(launch_pdl(k_snap_deidrj_tm<RUN, NWB8>, dim3(grid), dim3(NWB8 * 32), tm_smem(RUN, NWB8), ctx->stream, D,
+                         na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
+    } else if (tmem && big) {
       const unsigned grid = (unsigned)((na + PAIR_WARPS * RUN - 1) / (PAIR_WARPS * RUN));
       PL_CUDA(launch_pdl(k_snap_deidrj_tm<RUN, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), tm_smem(RUN),
                          ctx->stream, D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));

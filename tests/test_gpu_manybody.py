@@ -157,7 +157,7 @@ def test_snap_production_batch_vs_oracle(pl):
     """150 x 129 atoms = 19,350 atoms (605 blocks of 32 atoms, > 148 SMs, >= 4 waves of
     8-atom runs): the batch sizes of the bench, force sweep and ensemble, which dispatch
     the non-split Y kernel k_snap_yi_p<8,0,1> and the run force kernel
-    (k_snap_deidrj_tm<8,4>) naturally.  Sampled systems vs the oracle (<= 1e-10), and
+    (k_snap_deidrj_tm<8,8>) naturally.  Sampled systems vs the oracle (<= 1e-10), and
     each sampled system bitwise equal to its single-system evaluation (split Y
     kernel k_snap_yi_p<8,1,2> + 2-atom pair kernel): the batch never changes the
     arithmetic."""
@@ -215,13 +215,15 @@ def test_snap_specialised_matches_general_kernels(pl, tmp_path):
                           ("pair", {"PL_SNAP_PAIR_RUN": "0", "PL_SNAP_TMEM": "0"}),   # k_snap_deidrj_pair
                           ("tm2", {"PL_SNAP_PAIR_RUN": "0", "PL_SNAP_TMEM": "1"}),    # k_snap_deidrj_tm<2>
                           ("run", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "0"}),    # k_snap_deidrj_run<8>
-                          ("tm", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "1"})):    # k_snap_deidrj_tm<8>
+                          ("tm", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "1"}),     # k_snap_deidrj_tm<8, 8>
+                          ("tm4", {"PL_SNAP_PAIR_RUN": "2", "PL_SNAP_TMEM": "1",      # k_snap_deidrj_tm<8, 4>
+                                   "PL_SNAP_TM8": "0"})):
         f = str(tmp_path / f"ab_{mode}.npz")
         env = dict(os.environ, **env_add)
         subprocess.run([sys.executable, "-c", _AB_SCRIPT, f], cwd=root, env=env, check=True)
         out[mode] = np.load(f)
     a = out["gen"]
-    for m in ("pair", "tm2", "run", "tm"):
+    for m in ("pair", "tm2", "run", "tm", "tm4"):
         b = out[m]
         np.testing.assert_allclose(b["E"], a["E"], rtol=1e-12)
         np.testing.assert_allclose(b["G"], a["G"], rtol=1e-12, atol=1e-12 * np.abs(a["G"]).max())
@@ -232,6 +234,8 @@ def test_snap_specialised_matches_general_kernels(pl, tmp_path):
     # history in tensor memory + staged Y_k^dagger: the same arithmetic, bit for bit
     np.testing.assert_array_equal(out["tm"]["G"], out["run"]["G"])
     np.testing.assert_array_equal(out["tm"]["V"], out["run"]["V"])
+    np.testing.assert_array_equal(out["tm4"]["G"], out["run"]["G"])  # one 8-warp CTA per SM or two of 4
+    np.testing.assert_array_equal(out["tm4"]["V"], out["run"]["V"])
     np.testing.assert_array_equal(out["tm2"]["G"], out["pair"]["G"])
     np.testing.assert_array_equal(out["tm2"]["V"], out["pair"]["V"])
 
