@@ -877,6 +877,21 @@ __device__ __forceinline__ C2 vstep(const C2& a, const C2& b, const C2& u, const
 // advance row mb of V from layer J-1 to layer J (in place, descending ma); at
 // even J the middle row mb = J/2 is born from row J/2-1 of layer J-1 (lane - 1)
 template <int TJ, int J>
+__device__ __forceinline__ void row_born(C2 (&u)[TJ + 1], int mb) {
+  if (J % 2 == 0 && J < TJ) {
+#pragma unroll
+    for (int i = 0; i < J; ++i) {
+      C2 v = shfl_up_c2(u[i], 1);
+      if (2 * mb == J) {
+        const int x = J - 1 - i;  // destination index in row J/2 of layer J-1
+        const bool neg = ((x + J / 2) & 1) != 0;
+        u[x] = neg ? C2{-v.re, v.im} : C2{v.re, -v.im};
+      }
+    }
+  }
+}
+
+template <int TJ, int J>
 __device__ __forceinline__ void row_step(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb) {
   // (the callers run 4 lanes per pair, mb <= 3 = TJ/2 - 1: no lane is born at J = TJ, the
   // row-3 lane builds row TJ/2 itself, so the layer-TJ shuffles would be dead work)
@@ -912,6 +927,12 @@ template <int TJ, int J>
 __device__ __forceinline__ void row_update(C2 (&u)[TJ + 1], const RowGeom<TJ>& g) {
 #pragma unroll
   for (int ma = J; ma >= 0; --ma) u[ma] = vstep(g.a, g.b, u[ma], u[ma > 0 ? ma - 1 : 0], ma < J, ma > 0);
+}
+
+template <int TJ, int J>
+__device__ __forceinline__ void row_update_active(C2 (&u)[TJ + 1], const RowGeom<TJ>& g, int mb) {
+  if (2 * mb > J) return;
+  row_update<TJ, J>(u, g);
 }
 
 // U_tot with 4 lanes per pair (twojmax 8; see k_snap_deidrj_adj4): lanes own
@@ -1202,10 +1223,20 @@ struct AdjR4 {
         }
         u4[J] = C2{0.0, 0.0};
       }
-      row_step<TJ, J>(u, g, mb);  // rows 1..3 are born at J = 2, 4, 6 from the lane below
+      // rows 1..3 are born at J = 2, 4, 6 from the lane below.  The history of layer J-1
+      // is stored after the born lane received its (virtual) row of layer J-1, so with the
+      // history in tensor memory (every lane stores and loads its own row) the adjoint
+      // sweep finds the born row's upstream values in its own slots: no second shuffle
+      if constexpr (H::kTmem) {
+        row_born<TJ, J>(u, mb);
+        hist.template put<J - 1>(u, true);
+        row_update_active<TJ, J>(u, g, mb);
+      } else {
+        hist.template put<J - 1>(u, 2 * mb <= J - 1);
+        row_step<TJ, J>(u, g, mb);
+      }
       if constexpr (J == TJ) row_update<TJ, TJ>(u4, g);
     }
-    if constexpr (J < TJ) hist.template put<J>(u, 2 * mb <= J);
     if (2 * mb <= J) {
 #pragma unroll
       for (int ma = 0; ma <= J; ++ma) {
@@ -1264,19 +1295,9 @@ struct AdjR4 {
       const bool born = (J % 2 == 0) && (J < TJ) && (2 * mb == J);  // rows 1..3: virtual in layer J-1
       C2 up[TJ + 1];
       if constexpr (H::kTmem) {
-        // every lane loads its own row of layer J-1; born rows take the image of
-        // the lane below (row J/2-1 of layer J-1) by a shuffle
-        C2 L[TJ + 1];
-        hist.template row<J>(L);
-#pragma unroll
-        for (int x = 0; x < J; ++x) {
-          up[x] = L[x];
-          if constexpr (J % 2 == 0 && J < TJ) {
-            const C2 v = shfl_up_c2(L[J - 1 - x], 1);
-            // born: mb = J/2, so the parity (x + mb) & 1 is a compile-time constant
-            if (born) up[x] = ((x + J / 2) & 1) ? C2{-v.re, v.im} : C2{v.re, -v.im};
-          }
-        }
+        // every lane loads its own row of layer J-1 (born rows stored their image of the
+        // lane below in the forward pass)
+        hist.template row<J>(up);
         if (active) row_adj<J>(G, up, g, Sa, Sb);
       } else if (active) {
 #pragma unroll
@@ -1812,7 +1833,9 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const HistTmem hist{s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2)};
+  // broadcast from lane 0: the compiler then knows the address is warp-uniform and keeps
+  // it in a uniform register (otherwise one R2UR per tcgen05.ld/st, ~100 per round)
+  const HistTmem hist{__shfl_sync(0xffffffffu, s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 256u * (uint32_t)(warp >> 2), 0)};
   unsigned phase = 0;
   const int64_t a0 = ((int64_t)blockIdx.x * NWB + warp) * CH;
   const int nrun = (int)max((int64_t)0, min((int64_t)CH, natoms - a0));
