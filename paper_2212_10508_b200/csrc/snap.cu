@@ -121,7 +121,8 @@ __constant__ int c_foff[SNAP_JMAX + 2];
 // box-form Z/Y kernel (snap_yi8.cu, own constant bank)
 cudaError_t snap_yi8_setup(double* balance_out);
 cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const double* vs,
-                            const void* utot, void* ylist, double* eatom, double* erow_g);
+                            const void* utot, void* ylist, double* eatom, double* erow_g, void* ytlist,
+                            bool* yt_done);
 
 // ------------------------------------------------------------------ host setup
 static double fact(int n) {
@@ -2293,8 +2294,9 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   PL_CHECK_LAUNCH();
   prof_mark(ctx->stream, ST_UI, false);
   prof_mark(ctx->stream, ST_YI, true);
+  bool yt_done = false;  // the unsplit Y kernel also writes S (.) Y^dagger
   if (special) {
-    PL_CUDA(snap_box_launch(ctx->stream, na, D.beta0, D.yi5, D.vs, buf.utot, buf.y, buf.eatom, erow));
+    PL_CUDA(snap_box_launch(ctx->stream, na, D.beta0, D.yi5, D.vs, buf.utot, buf.y, buf.eatom, erow, buf.yt, &yt_done));
   } else {
     k_snap_yi<<<(unsigned)((na + YI_ATOMS - 1) / YI_ATOMS), YI_THREADS, yi_smem(D), ctx->stream>>>(D, na, buf.utot,
                                                                                                  buf.y, buf.eatom);
@@ -2304,9 +2306,11 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
   prof_mark(ctx->stream, ST_DE, true);
   if (special) {
     const int64_t nel = na * D.nhalf;
-    PL_CUDA(launch_pdl(k_snap_ytrans, dim3((unsigned)((nel + 255) / 256)), dim3(256), 0, ctx->stream, na, D.nhalf,
-                       D.vs + D.nhalf, buf.y, buf.yt));
-    PL_CHECK_LAUNCH();
+    if (!yt_done) {
+      PL_CUDA(launch_pdl(k_snap_ytrans, dim3((unsigned)((nel + 255) / 256)), dim3(256), 0, ctx->stream, na, D.nhalf,
+                         D.vs + D.nhalf, buf.y, buf.yt));
+      PL_CHECK_LAUNCH();
+    }
     static const int prun = [] {
       const char* e = getenv("PL_SNAP_PAIR_RUN");
       return e ? atoi(e) : 1;  // 0: 2-atom warps only, 2: runs at every size (tests)

@@ -114,6 +114,23 @@ struct BoxExpand {
   }
 };
 __constant__ BoxExpand c_box_exp = BoxExpand();
+// Y^dagger element o = hoff(J) + ma (J/2 + 1) + mb (column-interleaved half rows) ->
+// (source half element << 12) | (half element of (mb, ma) << 2) | (mirrored << 1) | (odd ma + mb)
+struct YtMap {
+  int e[yib::NHALF];
+  constexpr YtMap() : e() {
+    for (int J = 0; J <= yib::TJ; ++J)
+      for (int ma = 0; ma <= J; ++ma)
+        for (int mb = 0; 2 * mb <= J; ++mb) {
+          const int base = yib::hoff(J);
+          const bool mir = 2 * ma > J;  // element (row ma, column mb) of the full matrix
+          const int src = mir ? base + (J - ma) * (J + 1) + (J - mb) : base + ma * (J + 1) + mb;
+          e[base + ma * (J / 2 + 1) + mb] =
+              (src << 12) | ((base + mb * (J + 1) + ma) << 2) | (mir ? 2 : 0) | ((ma + mb) & 1);
+        }
+  }
+};
+__constant__ YtMap c_yt_map = YtMap();
 __constant__ int c_box_code[yib::NT];  // X*100 + Y*10 + J
 // compiled variants: (warps per CTA, CTAs per 32-atom block).  A block's rows
 // are split over S CTAs when the batch has fewer blocks than SMs (latency of
@@ -238,7 +255,7 @@ template <int NW, int V, int S>
 __global__ void __launch_bounds__(NW * 32, 1)
 k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const double* __restrict__ vs,
             const Cx* __restrict__ utot, Cx* __restrict__ ylist, double* __restrict__ eatom,
-            double* __restrict__ erow_g) {
+            double* __restrict__ erow_g, Cx* __restrict__ ytlist) {
   griddep_wait_yi();
   extern __shared__ double smem[];
   Cx* Uf = reinterpret_cast<Cx*>(smem);                 // [NFULL][32] full U matrices
@@ -376,20 +393,67 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
   // rows owned by this CTA -> global (all rows when S = 1), as S (.) Y: the force
   // kernels propagate the coefficient-free V = U / S (snap.cu, vstep), and
   // Re<U, Y> = Re<V, S (.) Y>
-  // 8 consecutive threads take 8 consecutive atoms of one element h: conflict-free
-  // shared-memory reads ([h][atom] layout), 16-byte global stores
-  for (int t = threadIdx.x; t < yib::ATOMS * yib::NHALF; t += blockDim.x) {
-    const int rest = t >> 3, h = rest % yib::NHALF, at = (rest / yib::NHALF) * 8 + (t & 7);
-    if (at >= na_blk) continue;
-    if (S > 1) {
+  if constexpr (S == 1) {
+    // The block's Y is one contiguous range of ylist ([atom][h]).  It is transposed into
+    // that layout in shared memory (the U area is dead after the energy pass; [h][atom]
+    // reads and [atom][h] writes are both conflict-free: 155 x 16 B per atom puts the 32
+    // lanes on 8 x 4 distinct banks) and leaves as ONE bulk async store (TMA engine),
+    // instead of 16-byte stores to 8 atoms' rows per warp.  S (.) Y^dagger for the pair
+    // force kernel (k_snap_ytrans' arithmetic, bit for bit: the stored S (.) Y element,
+    // mirrored through the inversion symmetry for ma > J/2, times vs2 = S^2, conjugated;
+    // column-interleaved [J][ma][mb <= J/2]) is built from the transposed copy into the Y
+    // area and leaves the same way: no k_snap_ytrans launch re-reading Y from HBM.
+    double2* T = reinterpret_cast<double2*>(Uf);
+    const double2* Y2 = reinterpret_cast<const double2*>(Ys);
+#pragma unroll 5
+    for (int h = warp; h < yib::NHALF; h += NW) {
+      const double sc = __ldg(vs + h);
+      const double2 y = Y2[h * yib::ATOMS + lane];
+      T[lane * yib::NHALF + h] = make_double2(y.x * sc, y.y * sc);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    const unsigned bytes = (unsigned)(sizeof(Cx) * yib::NHALF * na_blk);
+    if (threadIdx.x == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(ylist + a0 * yib::NHALF),
+                   "r"((unsigned)__cvta_generic_to_shared(T)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (ytlist) {
+      const double* vs2 = vs + yib::NHALF;
+      double2* T2 = reinterpret_cast<double2*>(Ys);  // Y fully consumed above
+#pragma unroll 5
+      for (int o = warp; o < yib::NHALF; o += NW) {
+        const int code = c_yt_map.e[o];
+        double2 v = T[lane * yib::NHALF + (code >> 12)];
+        if (code & 2) v = (code & 1) ? make_double2(-v.x, v.y) : make_double2(v.x, -v.y);
+        const double f = __ldg(vs2 + ((code >> 2) & 0x3ff));
+        T2[lane * yib::NHALF + o] = make_double2(f * v.x, -(f * v.y));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(ytlist + a0 * yib::NHALF),
+                     "r"((unsigned)__cvta_generic_to_shared(T2)), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+  } else {
+    // 8 consecutive threads take 8 consecutive atoms of one element h: conflict-free
+    // shared-memory reads ([h][atom] layout), 16-byte global stores
+    for (int t = threadIdx.x; t < yib::ATOMS * yib::NHALF; t += blockDim.x) {
+      const int rest = t >> 3, h = rest % yib::NHALF, at = (rest / yib::NHALF) * 8 + (t & 7);
+      if (at >= na_blk) continue;
       int J = 0;
       while (J < yib::TJ && h >= yib::hoff(J + 1)) ++J;
       const int r = yib::rowoff(J) + (h - yib::hoff(J)) / (J + 1);
       if (c_p_rowsplit[V][r] != split) continue;
+      const Cx y = Ys[h * yib::ATOMS + at];
+      const double sc = __ldg(vs + h);
+      ylist[(a0 + at) * yib::NHALF + h] = Cx{y.re * sc, y.im * sc};
     }
-    const Cx y = Ys[h * yib::ATOMS + at];
-    const double sc = __ldg(vs + h);
-    ylist[(a0 + at) * yib::NHALF + h] = Cx{y.re * sc, y.im * sc};
   }
   if (S == 1) {
     if (warp == 0 && lane < na_blk) {
@@ -397,6 +461,8 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
       for (int r = 0; r < yib::ROWS; ++r) e += erow[r * yib::ATOMS + lane];
       eatom[a0 + lane] = e;
     }
+    // the staging areas stay valid until the bulk stores have read them
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else {
     for (int t = threadIdx.x; t < yib::ROWS * na_blk; t += blockDim.x) {
       const int r = t / na_blk, at = t - r * na_blk;
@@ -657,7 +723,7 @@ cudaError_t snap_yi8_setup(double* balance_out) {
 
 template <int NW, int V, int S>
 static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const double* vs,
-                            const void* utot, void* ylist, double* eatom, double* erow_g) {
+                            const void* utot, void* ylist, double* eatom, double* erow_g, void* ytlist) {
   const size_t sm = sizeof(Cx) * (yib::NFULL + yib::NHALF) * yib::ATOMS + sizeof(double) * yib::ROWS * yib::ATOMS;
   static std::atomic<uint64_t> attr_devs{0};
   int dev = 0;
@@ -670,7 +736,7 @@ static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const
   }
   const unsigned grid = (unsigned)(S * ((natoms + yib::ATOMS - 1) / yib::ATOMS));
   cudaError_t e = launch_pdl_yi(k_snap_yi_p<NW, V, S>, dim3(grid), dim3(NW * 32), sm, st, natoms, beta0, coef,
-                                vs, (const Cx*)utot, (Cx*)ylist, eatom, erow_g);
+                                vs, (const Cx*)utot, (Cx*)ylist, eatom, erow_g, (Cx*)ytlist);
   if (e != cudaSuccess) return e;
   if (S > 1)
     e = launch_pdl_yi(k_box_energy, dim3((unsigned)((natoms + 255) / 256)), dim3(256), 0, st, natoms, beta0,
@@ -680,19 +746,28 @@ static cudaError_t p_launch(cudaStream_t st, int64_t natoms, double beta0, const
 }
 
 // split rows over 2 CTAs per block when the batch has fewer blocks than SMs
-// (erow_g: 25 x natoms doubles of scratch)
+// (erow_g: 25 x natoms doubles of scratch).  ytlist (optional): S (.) Y^dagger, written
+// by the unsplit kernel; *yt_done tells the caller whether it was (else k_snap_ytrans).
 cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const double* vs,
-                            const void* utot, void* ylist, double* eatom, double* erow_g) {
+                            const void* utot, void* ylist, double* eatom, double* erow_g, void* ytlist,
+                            bool* yt_done) {
   const int64_t blocks = (natoms + yib::ATOMS - 1) / yib::ATOMS;
   const bool split = blocks < 148 && erow_g;
   static const int max_split = [] {  // PL_YI_SPLIT_MAX=2: no 4-way split (A/B)
     const char* e = getenv("PL_YI_SPLIT_MAX");
     return e ? atoi(e) : 4;
   }();
+  static const bool fuse_yt = [] {  // PL_YI_YT=0: separate k_snap_ytrans at every size (A/B, tests)
+    const char* e = getenv("PL_YI_YT");
+    return !(e && e[0] == '0');
+  }();
+  if (yt_done) *yt_done = false;
   if (split && max_split >= 4 && 4 * blocks <= 148)
-    return p_launch<8, 2, 4>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g);
-  return split ? p_launch<8, 1, 2>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g)
-               : p_launch<8, 0, 1>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g);
+    return p_launch<8, 2, 4>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g, nullptr);
+  if (split) return p_launch<8, 1, 2>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g, nullptr);
+  void* yt = fuse_yt ? ytlist : nullptr;
+  if (yt_done) *yt_done = yt != nullptr;
+  return p_launch<8, 0, 1>(st, natoms, beta0, coef, vs, utot, ylist, eatom, erow_g, yt);
 }
 
 }  // namespace pl

@@ -195,7 +195,8 @@ sys.path.insert(0, '.')
 from paper_2212_10508_b200 import tungsten as W
 q0, box = W.bcc_sia(4)
 rs = np.random.default_rng(5)
-Q = torch.from_numpy(q0[None] + 0.1 * rs.normal(size=(6, q0.shape[0]))).cuda()
+import os
+Q = torch.from_numpy(q0[None] + 0.1 * rs.normal(size=(int(os.environ.get('AB_BATCH', 6)), q0.shape[0]))).cuda()
 E, G, V = (x.cpu().numpy() for x in W.make_snap(q0.shape[0] // 3, box).evaluate(Q, True, True, True))
 np.savez(sys.argv[1], E=E, G=G, V=V)
 """
@@ -238,6 +239,23 @@ def test_snap_specialised_matches_general_kernels(pl, tmp_path):
     np.testing.assert_array_equal(out["tm4"]["V"], out["run"]["V"])
     np.testing.assert_array_equal(out["tm2"]["G"], out["pair"]["G"])
     np.testing.assert_array_equal(out["tm2"]["V"], out["pair"]["V"])
+
+
+def test_snap_fused_ydagger_store_is_bitwise_ytrans(pl, tmp_path):
+    """At >= 148 blocks the unsplit Y kernel writes S (.) Y^dagger itself (no k_snap_ytrans
+    launch); PL_YI_YT=0 keeps the separate kernel.  Same bits in E, forces and virials."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode, env_add in (("fused", {}), ("separate", {"PL_YI_YT": "0"})):
+        f = str(tmp_path / f"yt_{mode}.npz")
+        env = dict(os.environ, AB_BATCH="40", **env_add)   # 5160 atoms = 162 blocks
+        subprocess.run([sys.executable, "-c", _AB_SCRIPT, f], cwd=root, env=env, check=True)
+        out[mode] = np.load(f)
+    for k in ("E", "G", "V"):
+        np.testing.assert_array_equal(out["fused"][k], out["separate"][k])
 
 
 @pytest.mark.parametrize("twojmax", [2, 4, 6])
