@@ -352,12 +352,12 @@ def run_ours(args, rank, world, local_rank):
         # per substep: neighbours (cell lists at >= 512 atoms and >= 3 cells per axis: count,
         # scan, fill, list; else one brute-force kernel; at >= 512 atoms also the skin check
         # and reference update), ui, yi (+ k_box_energy when the batch has fewer 32-atom
-        # blocks than SMs), ytrans, deidrj, gather, one integrator kernel; + the opening
-        # gradient and k_open
+        # blocks than SMs; the unsplit Y kernel also writes Y^dagger, else k_snap_ytrans),
+        # deidrj, gather, one integrator kernel; + the opening gradient and k_open
         cells = n >= 512 and min(inp["box"]) / (4.73 + 0.3) >= 3
         skin = n >= 512  # Verlet-skin check + reference update kernels (the builds are gated on the device)
         split = (slices * n + 31) // 32 < 148
-        per_eval = (4 if cells else 1) + (2 if skin else 0) + 5 + (1 if split else 0)
+        per_eval = (4 if cells else 1) + (2 if skin else 0) + 4 + (2 if split else 0)
         launches_per_step = (L + 1) * per_eval + (L + 1)
         line = {
             "metric": METRIC,
