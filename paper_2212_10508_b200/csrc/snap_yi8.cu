@@ -435,6 +435,7 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
 #pragma unroll 5
       for (int o = warp; o < yib::NHALF; o += NW) {
         const int code = c_yt_map.e[o];
+        PL_DASSERT((code >> 12) >= 0 && (code >> 12) < yib::NHALF && ((code >> 2) & 0x3ff) < yib::NHALF);
         double2 v = T[lane * yib::NHALF + (code >> 12)];
         if (code & 2) v = (code & 1) ? make_double2(-v.x, v.y) : make_double2(v.x, -v.y);
         const double f = __ldg(vs2 + ((code >> 2) & 0x3ff));
