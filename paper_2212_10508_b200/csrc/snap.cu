@@ -2320,7 +2320,15 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
       const char* e = getenv("PL_SNAP_TMEM");
       return !(e && e[0] == '0');
     }();
-    const bool big = prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4);  // >= 4 waves of runs
+    // runs (8 atoms per warp, one 8-warp CTA per SM) when their waves are well filled: a
+    // wave of run CTAs takes ~0.117 ms whatever its fill, the 2-atom form ~0.0148 ms per
+    // 1000 atoms (measured, 8,200-65,600 atoms), so runs win at a fill >= 0.84
+    // (8,200 atoms: 0.122 -> 0.117 ms; 16,001: 0.229 -> 0.218; 19,350: three waves at 0.68 lose)
+    bool big = prun == 2;
+    if (prun == 1) {
+      const int64_t ctas = (na + 8 * RUN - 1) / (8 * RUN), waves = (ctas + 147) / 148;
+      big = (double)na >= 0.84 * (double)(waves * 148 * 8 * RUN);
+    }
     auto tm_smem = [&](int ch, int nwb = PAIR_WARPS) {
       constexpr int GB = 16;
       return sizeof(C2) * nwb * (2 * D.nhalf + 8 * D.nhalf) + (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * nwb * GB +
@@ -2349,7 +2357,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
       const unsigned grid = (unsigned)((na + PAIR_WARPS * 2 - 1) / (PAIR_WARPS * 2));
       PL_CUDA(launch_pdl(k_snap_deidrj_tm<2, PAIR_WARPS>, dim3(grid), dim3(PAIR_WARPS * 32), tm_smem(2), ctx->stream,
                          D, na, N, box, q, nl.nbr, nl.cnt, nl.maxn, buf.y, buf.yt, buf.dedr));
-    } else if (prun == 2 || (prun == 1 && na >= (int64_t)RUN * PAIR_WARPS * 148 * 4)) {  // >= 4 waves of runs
+    } else if (big) {  // PL_SNAP_TMEM=0: the run kernel with the history in shared memory
       const size_t sm = sizeof(C2) * PAIR_WARPS * (2 * D.nhalf + ADJ4_SLOTS * 32) +
                         (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * PAIR_WARPS * 32 +
                         sizeof(int16_t) * PAIR_WARPS * RUN * SNAP_MAXN + sizeof(int32_t) * PAIR_WARPS * (RUN + 2);

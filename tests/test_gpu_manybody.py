@@ -154,20 +154,20 @@ def _snap_oracle_check(native, Q, box, pot, E, G, V, systems):
 
 
 def test_snap_production_batch_vs_oracle(pl):
-    """150 x 129 atoms = 19,350 atoms (605 blocks of 32 atoms, > 148 SMs, >= 4 waves of
-    8-atom runs): the batch sizes of the bench, force sweep and ensemble, which dispatch
-    the non-split Y kernel k_snap_yi_p<8,0,1> and the run force kernel
-    (k_snap_deidrj_tm<8,8>) naturally.  Sampled systems vs the oracle (<= 1e-10), and
+    """220 x 129 atoms = 28,380 atoms (887 blocks of 32 atoms, > 148 SMs; 444 run CTAs =
+    three full waves): the batch sizes of the bench, force sweep and ensemble, which
+    dispatch the non-split Y kernel k_snap_yi_p<8,0,1> and the run force kernel
+    (k_snap_deidrj_tm<8,8>, chosen when its waves are >= 84 % full) naturally.  Sampled systems vs the oracle (<= 1e-10), and
     each sampled system bitwise equal to its single-system evaluation (split Y
     kernel k_snap_yi_p<8,1,2> + 2-atom pair kernel): the batch never changes the
     arithmetic."""
     from oracle import native
     from paper_2212_10508_b200 import tungsten as W
-    Q, box = _configs(4, 150, seed=11)
+    Q, box = _configs(4, 220, seed=11)
     n = Q.shape[1] // 3
     pot = W.make_snap(n, box)
     E, G, V = (x.cpu().numpy() for x in pot.evaluate(Q, True, True, True))
-    sample = (0, 1, 74, 75, 148, 149)
+    sample = (0, 1, 109, 110, 218, 219)
     _snap_oracle_check(native, Q, box, pot, E, G, V, sample)
     for b in sample:
         e1, g1, v1 = (x.cpu().numpy() for x in pot.evaluate(Q[b:b + 1], True, True, True))
@@ -178,7 +178,8 @@ def test_snap_production_batch_vs_oracle(pl):
 
 def test_snap_heavy_system_vs_oracle(pl):
     """Two 16,001-atom systems (BASELINE configs[4] cell; cell-list neighbours,
-    32,002 atoms dispatch the run force kernel): system 0 vs the oracle <= 1e-10."""
+    32,002 atoms = four run-kernel waves at 84.5 % fill dispatch the run force kernel):
+    system 0 vs the oracle <= 1e-10."""
     from oracle import native
     from paper_2212_10508_b200 import tungsten as W
     Q, box = _configs(20, 2, sigma=0.08, seed=13)
