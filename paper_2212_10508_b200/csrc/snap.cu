@@ -1806,8 +1806,12 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
   constexpr int GB = 16;  // pairs per geometry batch (2 rounds; shared memory budget)
   C2* base = reinterpret_cast<C2*>(smem);
   C2* Yw = base + warp * 2 * nh;  // ring [2][nh]
-  C2* stg = base + NWB * 2 * nh + warp * P * nh;  // Y_k^dagger of the round's pairs [P][nh]
-  double* gb0 = reinterpret_cast<double*>(base + NWB * (2 * nh + P * nh));
+  // Y_k^dagger of the round's pairs [P][nh + 1]: the slot stride of 156 complex = 624
+  // words = 16 mod 32 puts the 64-byte reads of the two pairs of a quarter warp on
+  // disjoint bank halves (155: 12 mod 32, they overlap)
+  const int sts = nh + 1;
+  C2* stg = base + NWB * 2 * nh + warp * P * sts;
+  double* gb0 = reinterpret_cast<double*>(base + NWB * (2 * nh + P * (nh + 1)));
   double* gb = gb0 + warp * GB * PAIR_GEO;
   int64_t* gk = reinterpret_cast<int64_t*>(gb0 + NWB * GB * PAIR_GEO) + warp * GB;
   int16_t* oslot = reinterpret_cast<int16_t*>(reinterpret_cast<int64_t*>(gb0 + NWB * GB * PAIR_GEO) + NWB * GB) +
@@ -1947,7 +1951,7 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
       if (lane < nv)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                (unsigned)__cvta_generic_to_shared(stg + lane * nh)),
+                (unsigned)__cvta_generic_to_shared(stg + lane * sts)),
             "l"(ytlist + gk[pos + lane - gbase] * nh), "r"((unsigned)(nh * sizeof(C2))), "r"(mbar)
             : "memory");
     }
@@ -1960,7 +1964,7 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
     const double* go = gb + (valid ? pp - gbase : 0) * PAIR_GEO;
     const int64_t katom = valid ? gk[pp - gbase] : atom;  // invalid slots: own Y^dagger (weight 0)
     (void)katom;
-    const YPairS Y{Yw + (c & 1) * nh, stg + p * nh};  // invalid slots read stale but finite data (weight 0)
+    const YPairS Y{Yw + (c & 1) * nh, stg + p * sts};  // invalid slots read stale but finite data (weight 0)
     RowGeom<TJ> g{valid ? C2{go[0], go[1]} : C2{1.0, 0.0}, valid ? C2{go[2], go[3]} : C2{0.0, 0.0}, C2{0.0, 0.0},
                   C2{0.0, 0.0}};
     C2 u[TJ + 1], u4[TJ + 1];
@@ -2331,7 +2335,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     }
     auto tm_smem = [&](int ch, int nwb = PAIR_WARPS) {
       constexpr int GB = 16;
-      return sizeof(C2) * nwb * (2 * D.nhalf + 8 * D.nhalf) + (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * nwb * GB +
+      return sizeof(C2) * nwb * (2 * D.nhalf + 8 * (D.nhalf + 1)) + (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * nwb * GB +
              sizeof(int16_t) * nwb * ch * SNAP_MAXN + sizeof(int32_t) * nwb * (ch + 2);
     };
     // large batches: one CTA of 8 warps per SM instead of two of 4.  The round's code
