@@ -1119,12 +1119,18 @@ struct YPair {
 };
 
 // Y_k^dagger staged in shared memory (k_snap_deidrj_tm): same layout as global
+// Y_i rows of layer 7 are padded to 9 elements (ypad7): 8 complex = 32 words put the 4
+// row lanes of a pair on the same banks (a 4-way conflict on every layer-7 read)
+__device__ __forceinline__ int ypad7(int e) {  // shift of half element e in the padded copy
+  constexpr int H7 = hoff8(7);
+  return e < H7 ? 0 : (e < H7 + 32 ? (e - H7) >> 3 : 4);
+}
 struct YPairS {
-  const C2* y;   // Y_i, shared memory
+  const C2* y;   // Y_i, shared memory, layer-7 rows padded (ypad7)
   const C2* yt;  // Y_k^dagger, shared memory (staged by a bulk copy per pair)
   __device__ __forceinline__ C2 operator()(int J, int row, int x) const {
     const C2 t = yt[c_hoff[J] + x * (J / 2 + 1) + row];
-    const C2 a = y[c_hoff[J] + row * (J + 1) + x];
+    const C2 a = y[c_hoff[J] + (J == 7 ? row * 9 : row * (J + 1)) + (J == 8 ? 4 : 0) + x];
     return C2{a.re + t.re, a.im + t.im};
   }
 };
@@ -1805,13 +1811,14 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int GB = 16;  // pairs per geometry batch (2 rounds; shared memory budget)
   C2* base = reinterpret_cast<C2*>(smem);
-  C2* Yw = base + warp * 2 * nh;  // ring [2][nh]
+  const int nhp = nh + 4;           // Y_i slot with the layer-7 rows padded (ypad7)
+  C2* Yw = base + warp * 2 * nhp;  // ring [2][nhp]
   // Y_k^dagger of the round's pairs [P][nh + 1]: the slot stride of 156 complex = 624
   // words = 16 mod 32 puts the 64-byte reads of the two pairs of a quarter warp on
   // disjoint bank halves (155: 12 mod 32, they overlap)
   const int sts = nh + 1;
-  C2* stg = base + NWB * 2 * nh + warp * P * sts;
-  double* gb0 = reinterpret_cast<double*>(base + NWB * (2 * nh + P * (nh + 1)));
+  C2* stg = base + NWB * 2 * nhp + warp * P * sts;
+  double* gb0 = reinterpret_cast<double*>(base + NWB * (2 * nhp + P * (nh + 1)));
   double* gb = gb0 + warp * GB * PAIR_GEO;
   int64_t* gk = reinterpret_cast<int64_t*>(gb0 + NWB * GB * PAIR_GEO) + warp * GB;
   int16_t* oslot = reinterpret_cast<int16_t*>(reinterpret_cast<int64_t*>(gb0 + NWB * GB * PAIR_GEO) + NWB * GB) +
@@ -1876,7 +1883,10 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
       if (lane + 32 * j < nel) tmp[j] = ylist[a0 * nh + lane + 32 * j];
 #pragma unroll
     for (int j = 0; j < NL; ++j)
-      if (lane + 32 * j < nel) Yw[lane + 32 * j] = tmp[j];
+      if (lane + 32 * j < nel) {
+        const int g = lane + 32 * j, w = g >= nh ? 1 : 0, e = g - w * nh;
+        Yw[w * nhp + e + ypad7(e)] = tmp[j];
+      }
   }
   __syncthreads();
   const int p = lane / R, mb = lane - p * R;
@@ -1890,9 +1900,9 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
     while (next_load < nrun + 2 && cum[next_load - 1] <= pos) {
       if (next_load < nrun && cum[next_load + 1] > pos) {
         const C2* src = ylist + (a0 + next_load) * nh;
-        C2* dst = Yw + (next_load & 1) * nh;
+        C2* dst = Yw + (next_load & 1) * nhp;
         for (int e = lane; e < nh; e += 32) {
-          const unsigned d = (unsigned)__cvta_generic_to_shared(dst + e);
+          const unsigned d = (unsigned)__cvta_generic_to_shared(dst + e + ypad7(e));
           asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + e) : "memory");
         }
       }
@@ -1964,7 +1974,7 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
     const double* go = gb + (valid ? pp - gbase : 0) * PAIR_GEO;
     const int64_t katom = valid ? gk[pp - gbase] : atom;  // invalid slots: own Y^dagger (weight 0)
     (void)katom;
-    const YPairS Y{Yw + (c & 1) * nh, stg + p * sts};  // invalid slots read stale but finite data (weight 0)
+    const YPairS Y{Yw + (c & 1) * nhp, stg + p * sts};  // invalid slots read stale but finite data (weight 0)
     RowGeom<TJ> g{valid ? C2{go[0], go[1]} : C2{1.0, 0.0}, valid ? C2{go[2], go[3]} : C2{0.0, 0.0}, C2{0.0, 0.0},
                   C2{0.0, 0.0}};
     C2 u[TJ + 1], u4[TJ + 1];
@@ -2335,7 +2345,7 @@ static int snap_stages(pl_pot* pot, int64_t B, const double* q, SnapBuffers& buf
     }
     auto tm_smem = [&](int ch, int nwb = PAIR_WARPS) {
       constexpr int GB = 16;
-      return sizeof(C2) * nwb * (2 * D.nhalf + 8 * (D.nhalf + 1)) + (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * nwb * GB +
+      return sizeof(C2) * nwb * (2 * (D.nhalf + 4) + 8 * (D.nhalf + 1)) + (sizeof(double) * PAIR_GEO + sizeof(int64_t)) * nwb * GB +
              sizeof(int16_t) * nwb * ch * SNAP_MAXN + sizeof(int32_t) * nwb * (ch + 2);
     };
     // large batches: one CTA of 8 warps per SM instead of two of 4.  The round's code
