@@ -1009,8 +1009,9 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
   const int i = (int)(atom - b * N);
   const double* qb = q + b * (int64_t)N * 3;
   const int p = lane / R, mb = lane - p * R;
-  const int nl = cnt[atom];
   const int32_t* nb = nbr + atom * maxn;
+  const int nl = cnt[atom];
+  const int k_first = nb[lane];  // with the count, not after it (maxn >= 32; entries past the count are not used)
   C2 acc[45];
 #pragma unroll
   for (int k = 0; k < 45; ++k) acc[k] = C2{0.0, 0.0};
@@ -1027,7 +1028,7 @@ k_snap_ui_r4(SnapDev D, int64_t natoms, int N, Box box, const double* __restrict
     double dx = 0.0, dy = 0.0, dz = 0.0;
     bool keep = false;
     if (j < nl) {
-      pair_vec(qb, i, nb[j], box, dx, dy, dz);
+      pair_vec(qb, i, j0 == 0 ? k_first : nb[j], box, dx, dy, dz);
       keep = D.lists_exact || r2_exact(dx, dy, dz) < rc2;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
