@@ -1853,17 +1853,47 @@ k_snap_deidrj_tm(SnapDev D, int64_t natoms, int N, Box box, const double* __rest
   const int64_t a0 = ((int64_t)blockIdx.x * NWB + warp) * CH;
   const int nrun = (int)max((int64_t)0, min((int64_t)CH, natoms - a0));
   int tot = 0;
+  // the run's counts, list entries and exact-pair tests are loaded up front, all in
+  // flight together (three dependent global loads per atom, one atom after the other,
+  // were ~3 % of the kernel's samples); the lists hold SNAP_MAXN = 2 x 32 entries
+  const int cn_l = lane < nrun ? cnt[a0 + lane] : 0;
+  int kk_r[CH][2];
+  bool own_r[CH][2];
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+      kk_r[c][hf] = (c < nrun && maxn == SNAP_MAXN) ? nbr[(a0 + c) * maxn + 32 * hf + lane] : 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int n = __shfl_sync(0xffffffffu, cn_l, c);
+    const int64_t a = a0 + c;
+    const int i = (int)(a % N);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int kk = kk_r[c][hf];
+      own_r[c][hf] = maxn == SNAP_MAXN && c < nrun && 32 * hf + lane < n && pair_owned(i, kk) &&
+                     (D.lists_exact || pair_exact(q + (a / N) * (int64_t)N * 3, i, kk, box, D.rcut * D.rcut));
+    }
+  }
+#pragma unroll
   for (int c = 0; c < CH; ++c) {
     if (lane == 0) cum[c] = tot;
     const int base_c = tot;
     if (c < nrun) {
       const int64_t a = a0 + c;
       const int i = (int)(a % N);
-      const int n = cnt[a];
+      const int n = __shfl_sync(0xffffffffu, cn_l, c);
+#pragma unroll 1
       for (int t0 = 0; t0 < n; t0 += 32) {
-        const int kk = t0 + lane < n ? nbr[a * maxn + t0 + lane] : 0;
-        const bool own = t0 + lane < n && pair_owned(i, kk) &&
-                         (D.lists_exact || pair_exact(q + (a / N) * (int64_t)N * 3, i, kk, box, D.rcut * D.rcut));
+        bool own;
+        if (maxn == SNAP_MAXN) {
+          own = t0 == 0 ? own_r[c][0] : own_r[c][1];
+        } else {
+          const int kk = t0 + lane < n ? nbr[a * maxn + t0 + lane] : 0;
+          own = t0 + lane < n && pair_owned(i, kk) &&
+                (D.lists_exact || pair_exact(q + (a / N) * (int64_t)N * 3, i, kk, box, D.rcut * D.rcut));
+        }
         const unsigned bal = __ballot_sync(0xffffffffu, own);
         PL_DASSERT(!own || (tot - base_c) + __popc(bal & ((1u << lane) - 1u)) < SNAP_MAXN);
         if (own) oslot[c * SNAP_MAXN + (tot - base_c) + __popc(bal & ((1u << lane) - 1u))] = (int16_t)(t0 + lane);
