@@ -471,8 +471,9 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
       for (int r = 0; r < yib::ROWS; ++r) e += erow[r * yib::ATOMS + lane];
       eatom[a0 + lane] = e;
     }
-    // the staging areas stay valid until the bulk stores have read them
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // the staging areas stay valid until the bulk stores have read them (.read: the writes
+    // complete with the grid; a full wait_group costs a CCTL.IVALL and the drain, ~1 us per CTA)
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   } else {
     for (int t = threadIdx.x; t < yib::ROWS * na_blk; t += blockDim.x) {
       const int r = t / na_blk, at = t - r * na_blk;
