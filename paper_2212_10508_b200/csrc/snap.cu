@@ -120,6 +120,7 @@ __device__ __forceinline__ void half_layer8(int t, int& J, int& base) {
 __constant__ int c_foff[SNAP_JMAX + 2];
 // box-form Z/Y kernel (snap_yi8.cu, own constant bank)
 cudaError_t snap_yi8_setup(double* balance_out);
+bool snap_yi8_append_records(const double* coef, std::vector<double>& out);  // snap_yi8.cu
 cudaError_t snap_box_launch(cudaStream_t st, int64_t natoms, double beta0, const double* coef, const double* vs,
                             const void* utot, void* ylist, double* eatom, double* erow_g, void* ytlist,
                             bool* yt_done);
@@ -239,6 +240,10 @@ int snap_prepare(pl_pot* pot, const double* beta) {
     }
     cb2.insert(cb2.end(), vs.begin(), vs.end());
     cb2.insert(cb2.end(), vs2.begin(), vs2.end());
+    if (!snap_yi8_append_records(cy.data(), cb2)) {  // the Y kernel's item records with cy folded in
+      delete S;
+      return fail(PL_EARG, "twojmax-8 item records");
+    }
     PL_CUDA(cudaMalloc(&S->d_yi5, sizeof(double) * cb2.size()));
     PL_CUDA(cudaMemcpy(S->d_yi5, cb2.data(), sizeof(double) * cb2.size(), cudaMemcpyHostToDevice));
     S->yi_reg = true;

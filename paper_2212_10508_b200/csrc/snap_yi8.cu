@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <atomic>
 #include <utility>
 #include <vector>
@@ -144,7 +145,13 @@ constexpr int P_MAX_VW = 32;
 constexpr int P_MAX_ITEMS = 400;  // (row, triple) items: 375 at twojmax 8
 __constant__ int c_p_iseg[P_NV][yib::NPH][P_MAX_VW + 1];  // items of virtual warp w in phase p
 // per item, decoded on the host: {tid, Y-row offset (elements), lo | hi << 8 | mb << 16 | mid << 24 | swap << 25, 0}
-__constant__ int4 c_p_items[P_NV][P_MAX_ITEMS];
+// The items live in global memory next to the potential's coefficients, 32 bytes each:
+// the descriptor above and cy = coef[tid], so an item costs two independent 16-byte
+// loads through L1 instead of an indexed constant load followed by a dependent global
+// load (the per-item dispatch was 8.6 % of the kernel's stall samples, and the constant
+// cache shares the GPC-level cache with the instruction fetches)
+constexpr int P_REC_OFF = 2 * yib::NT + 2 * yib::NHALF;  // doubles before the records in the coefficient buffer
+static std::vector<int4> g_items4;  // host copy of the schedule (device independent)
 __constant__ int c_p_rowsplit[P_NV][yib::ROWS];          // CTA of the block that owns row r
 __constant__ int c_p_nph;                                // phases in use
 
@@ -332,13 +339,15 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
 #endif
     for (int it = c_p_iseg[V][ph][vw]; it < c_p_iseg[V][ph][vw + 1]; ++it) {
       PL_DASSERT(it < P_MAX_ITEMS);
-      const int4 item = c_p_items[V][it];  // one constant load per item (host-decoded)
+      const double* rec = coef + P_REC_OFF + 4 * (V * P_MAX_ITEMS + it);
+      const int4 item = __ldg(reinterpret_cast<const int4*>(rec));  // host-decoded descriptor
+      const double cy = __ldg(rec + 2);
       const int tid = item.x;
       PL_DASSERT(tid < yib::NT && item.y >= 0 && item.y < yib::NHALF);
       PItem A;
       A.Ul = Uf + lane;
       A.yrow = Ys + item.y * yib::ATOMS + lane;
-      A.cy = coef[tid];
+      A.cy = cy;
       A.zaddr = (unsigned)__cvta_generic_to_shared(erow);  // zero until the energy pass
       A.lo = item.z & 0xff;
       A.hi = (item.z >> 8) & 0xff;
@@ -726,10 +735,24 @@ cudaError_t snap_yi8_setup(double* balance_out) {
     items4[i] = make_int4(tid, yib::hoff(J) + mb * (J + 1),
                           lo | (hi << 8) | (mb << 16) | ((mid ? 1 : 0) << 24) | ((swap ? 1 : 0) << 25), 0);
   }
-  if ((e = cudaMemcpyToSymbol(c_p_items, items4.data(), sizeof(int4) * items4.size())) != cudaSuccess) return e;
+  g_items4 = items4;
   if ((e = cudaMemcpyToSymbol(c_p_rowsplit, rowsplit.data(), sizeof(int) * rowsplit.size())) != cudaSuccess)
     return e;
   return cudaSuccess;
+}
+
+// item records {descriptor, cy = coef[tid], 0} of the three variants, appended to the
+// potential's coefficient buffer (after coef, beta, vs, vs2: P_REC_OFF doubles)
+bool snap_yi8_append_records(const double* coef, std::vector<double>& out) {
+  if ((int)out.size() != P_REC_OFF || g_items4.size() != (size_t)P_NV * P_MAX_ITEMS) return false;
+  for (const int4& it : g_items4) {
+    double d[4] = {0.0, 0.0, 0.0, 0.0};
+    static_assert(sizeof(int4) == 2 * sizeof(double), "record layout");
+    memcpy(d, &it, sizeof(int4));
+    d[2] = (it.x >= 0 && it.x < yib::NT) ? coef[it.x] : 0.0;
+    out.insert(out.end(), d, d + 4);
+  }
+  return true;
 }
 
 template <int NW, int V, int S>
