@@ -337,7 +337,10 @@ k_snap_yi_p(int64_t natoms, double beta0, const double* __restrict__ coef, const
 #ifdef PL_YI_TIMING
     const long long t_ph = clock64();
 #endif
-    for (int it = c_p_iseg[V][ph][vw]; it < c_p_iseg[V][ph][vw + 1]; ++it) {
+    // (the bound in a register: read from constant memory in the loop condition it was
+    // re-loaded after every body, whose asm statements clobber memory)
+    const int it_end = c_p_iseg[V][ph][vw + 1];
+    for (int it = c_p_iseg[V][ph][vw]; it < it_end; ++it) {
       PL_DASSERT(it < P_MAX_ITEMS);
       const double* rec = coef + P_REC_OFF + 4 * (V * P_MAX_ITEMS + it);
       const int4 item = __ldg(reinterpret_cast<const int4*>(rec));  // host-decoded descriptor
