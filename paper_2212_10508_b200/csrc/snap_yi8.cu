@@ -623,9 +623,12 @@ cudaError_t snap_yi8_setup(double* balance_out) {
     code.push_back(t.X * 100 + t.Y * 10 + t.J);
   }
   // phases: consecutive triples (code order, ascending X) whose bodies fit the
-  // budget (estimated SASS bytes; PL_YI_PHASE_KB, default 100 KB: measured
+  // budget (estimated SASS bytes; PL_YI_PHASE_KB, default 90 KB; round 2 first measured
   // 1.70 ms at 100-140 KB vs 1.79 at 60 and 2.5-2.6 at 170 KB-1 phase, larger config)
-  double budget = 100.0 * 1024.0;
+  // (re-scanned on the final kernel, larger config: 70-128 KB give 1.58, 1.56, 1.52 (80),
+  // 1.55 (84), 1.517 (88), 1.491 (90, 91), 1.555 (92), 1.516 (94), 1.518 (100), 1.508 (110),
+  // 1.53-1.55 (120-128) ms: the budget decides which triples share a phase, hence the balance)
+  double budget = 90.0 * 1024.0;
   if (const char* e = getenv("PL_YI_PHASE_KB")) budget = atof(e) * 1024.0;
   std::vector<int> tphase(yib::NT, 0);
   int nph = 1;
